@@ -1,0 +1,266 @@
+// K2: FP64 GEMM on the sm_100a FP64 tensor path.
+//
+// Replaces Matrix::multiply (proj/src/matrix.cpp:86-102, the naive i-k-j A*G) and
+// every dense contraction of the path: A*G, the blocked-GENP TRSM/Schur updates,
+// A*H, Q^T*A, G*Y.  On sm_100a FP64 tensor math exists only as DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; tcgen05 has no .kind::f64, SURVEY.md
+// §0 item 6), measured at 37.1 TFLOP/s vs 36.6 for DFMA (profiles/r01_peaks.txt).
+//
+// Structure: CTA tile BM x BN, K-tile 16, NSTAGE-deep cp.async ring (global ->
+// shared, 16-byte copies, zero-fill at the edges), 8 warps each owning a
+// (BM/WM) x (BN/WN) accumulator tile in registers.  Shared tiles are padded so the
+// m8n8k4 fragment reads (8 rows x 4 k) hit 4 distinct 32-byte bank groups per
+// half-warp: no bank conflicts for either operand majorness.
+#include <algorithm>
+
+#include "rl_internal.cuh"
+
+namespace rl {
+
+namespace {
+
+constexpr int BK = 16;
+constexpr int PAD = 4; // doubles; row pitch = 32 B mod 128
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    int bytes = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    int bytes = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Shared-tile geometry for one operand.  KMAJOR: tile stored [rows=MN][BK+PAD];
+// otherwise [BK][MN+PAD].
+template <int MN, bool KMAJOR>
+struct Tile {
+    static constexpr int kPitch = KMAJOR ? (BK + PAD) : (MN + PAD);
+    static constexpr int kElems = KMAJOR ? MN * kPitch : BK * kPitch;
+    // element (mn, k) of the tile
+    __device__ __forceinline__ static int at(int mn, int k) {
+        return KMAJOR ? mn * kPitch + k : k * kPitch + mn;
+    }
+};
+
+// Load one BK-slice of an operand tile.  KMAJOR global layout: g[(mn0+r)*ld + k0 + c];
+// else g[(k0+r)*ld + mn0 + c].  dims: MNdim (rows along mn), Kdim.
+template <int MN, bool KMAJOR, int VEC, int NT>
+__device__ __forceinline__ void load_tile(double* s, const double* g, uint64_t ld, uint64_t mn0,
+                                          uint64_t k0, uint64_t MNdim, uint64_t Kdim, int tid) {
+    using T = Tile<MN, KMAJOR>;
+    constexpr int ROWS = KMAJOR ? MN : BK;  // rows of the tile in memory order
+    constexpr int COLS = KMAJOR ? BK : MN;  // contiguous extent
+    constexpr int CPR = COLS / VEC;         // copies per row
+    constexpr int TOTAL = ROWS * CPR;
+#pragma unroll
+    for (int it = 0; it < (TOTAL + NT - 1) / NT; ++it) {
+        int idx = it * NT + tid;
+        if (TOTAL % NT != 0 && idx >= TOTAL)
+            break;
+        int r = idx / CPR, c = (idx % CPR) * VEC;
+        uint64_t grow, gcol;
+        bool ok;
+        if (KMAJOR) {
+            grow = mn0 + r;
+            gcol = k0 + c;
+            ok = grow < MNdim && gcol < Kdim;
+        } else {
+            grow = k0 + r;
+            gcol = mn0 + c;
+            ok = grow < Kdim && gcol < MNdim;
+        }
+        const double* src = ok ? g + grow * ld + gcol : g;
+        double* dst = s + r * T::kPitch + c;
+        if (VEC == 2)
+            cp_async16(dst, src, ok);
+        else
+            cp_async8(dst, src, ok);
+    }
+}
+
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE>
+struct Cfg {
+    static constexpr int NT = WM * WN * 32;
+    static constexpr int WTM = BM / WM, WTN = BN / WN;
+    static constexpr int MF = WTM / 8, NF = WTN / 8;
+    using TA = Tile<BM, AK>;
+    using TB = Tile<BN, BKM>;
+    static constexpr int kStageElems = TA::kElems + TB::kElems;
+    static constexpr size_t kSmem = static_cast<size_t>(NSTAGE) * kStageElems * sizeof(double);
+};
+
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE>
+__global__ void __launch_bounds__(WM* WN * 32, 1)
+    k_dgemm(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* __restrict__ A,
+            uint64_t lda, const double* __restrict__ B, uint64_t ldb, double beta,
+            double* __restrict__ C, uint64_t ldc) {
+    using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE>;
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int g = lane >> 2, t = lane & 3;
+    const uint64_t m0 = static_cast<uint64_t>(blockIdx.y) * BM, n0 = static_cast<uint64_t>(blockIdx.x) * BN;
+    const int ktiles = static_cast<int>((K + BK - 1) / BK);
+
+    double acc[G::MF][G::NF][2];
+#pragma unroll
+    for (int i = 0; i < G::MF; ++i)
+#pragma unroll
+        for (int j = 0; j < G::NF; ++j)
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    auto sA = [&](int s) { return smem + s * G::kStageElems; };
+    auto sB = [&](int s) { return smem + s * G::kStageElems + G::TA::kElems; };
+
+#pragma unroll
+    for (int s = 0; s < NSTAGE - 1; ++s) {
+        if (s < ktiles) {
+            load_tile<BM, AK, VEC, G::NT>(sA(s), A, lda, m0, static_cast<uint64_t>(s) * BK, M, K, tid);
+            load_tile<BN, BKM, VEC, G::NT>(sB(s), B, ldb, n0, static_cast<uint64_t>(s) * BK, N, K, tid);
+        }
+        cp_commit();
+    }
+
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_wait<NSTAGE - 2>();
+        __syncthreads();
+        const int nk = kt + NSTAGE - 1;
+        if (nk < ktiles) {
+            int s = nk % NSTAGE;
+            load_tile<BM, AK, VEC, G::NT>(sA(s), A, lda, m0, static_cast<uint64_t>(nk) * BK, M, K, tid);
+            load_tile<BN, BKM, VEC, G::NT>(sB(s), B, ldb, n0, static_cast<uint64_t>(nk) * BK, N, K, tid);
+        }
+        cp_commit();
+        const double* a_s = sA(kt % NSTAGE);
+        const double* b_s = sB(kt % NSTAGE);
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[G::MF], bf[G::NF];
+#pragma unroll
+            for (int i = 0; i < G::MF; ++i)
+                af[i] = a_s[G::TA::at(wm * G::WTM + i * 8 + g, kk + t)];
+#pragma unroll
+            for (int j = 0; j < G::NF; ++j)
+                bf[j] = b_s[G::TB::at(wn * G::WTN + j * 8 + g, kk + t)];
+#pragma unroll
+            for (int i = 0; i < G::MF; ++i)
+#pragma unroll
+                for (int j = 0; j < G::NF; ++j)
+                    dmma(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+
+    // epilogue: C = alpha acc + beta C
+#pragma unroll
+    for (int i = 0; i < G::MF; ++i) {
+        uint64_t row = m0 + wm * G::WTM + i * 8 + g;
+        if (row >= M)
+            continue;
+#pragma unroll
+        for (int j = 0; j < G::NF; ++j) {
+            uint64_t col = n0 + wn * G::WTN + j * 8 + 2 * t;
+            double* cp = C + row * ldc + col;
+            double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+            if (VEC == 2 && col + 1 < N) {
+                if (beta != 0.0) {
+                    double2 o = *reinterpret_cast<const double2*>(cp);
+                    v0 = fma(beta, o.x, v0);
+                    v1 = fma(beta, o.y, v1);
+                }
+                *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+            } else {
+                if (col < N) {
+                    if (beta != 0.0)
+                        v0 = fma(beta, cp[0], v0);
+                    cp[0] = v0;
+                }
+                if (col + 1 < N) {
+                    if (beta != 0.0)
+                        v1 = fma(beta, cp[1], v1);
+                    cp[1] = v1;
+                }
+            }
+        }
+    }
+}
+
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE>
+void launch(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda,
+            const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
+    using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE>;
+    auto kern = k_dgemm<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE>;
+    static bool configured[16] = {};
+    int dev = ctx().device & 15;
+    if (!configured[dev]) {
+        RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(G::kSmem)));
+        configured[dev] = true;
+    }
+    dim3 grid(cdiv(N, BN), cdiv(M, BM));
+    kern<<<grid, G::NT, G::kSmem, stream()>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    RL_LAUNCHED();
+}
+
+template <bool AK, bool BKM, int VEC>
+void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda,
+                    const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
+    const int sms = ctx().sms;
+    uint64_t big_tiles = static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 128);
+    if (N > 64 && big_tiles >= static_cast<uint64_t>(sms))
+        launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else if (N > 32)
+        launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else
+        launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+} // namespace
+
+void gemm(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double alpha, const double* a,
+          uint64_t lda, const double* b, uint64_t ldb, double beta, double* c, uint64_t ldc) {
+    if (m == 0 || n == 0)
+        return;
+    if (k == 0) {
+        // C = beta C
+        gemm(false, false, m, n, 1, 0.0, c, ldc, c, ldc, beta, c, ldc);
+        return;
+    }
+    // operand contiguous extents must be even and 16-byte aligned for 16-byte copies
+    bool aligned = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                     reinterpret_cast<uintptr_t>(c)) & 15) == 0 &&
+                   lda % 2 == 0 && ldb % 2 == 0 && ldc % 2 == 0 && (ta ? m : k) % 2 == 0 &&
+                   (tb ? k : n) % 2 == 0;
+    // AK = A is K-major (row-major m x k, not transposed); BKM = B is K-major (tb)
+#define RL_GEMM_CASE(AK_, BK_)                                                          \
+    if (aligned)                                                                        \
+        dispatch_shape<AK_, BK_, 2>(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);     \
+    else                                                                                \
+        dispatch_shape<AK_, BK_, 1>(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+    if (!ta && !tb) {
+        RL_GEMM_CASE(true, false)
+    } else if (!ta && tb) {
+        RL_GEMM_CASE(true, true)
+    } else if (ta && !tb) {
+        RL_GEMM_CASE(false, false)
+    } else {
+        RL_GEMM_CASE(false, true)
+    }
+#undef RL_GEMM_CASE
+}
+
+} // namespace rl

@@ -1,0 +1,372 @@
+// Host orchestration of genp::randomized_genp on device data
+// (proj/src/genp.cpp:207-291): raw-GENP contrast arm, up to 8 multiplier draws on
+// stream id + 7919*attempt (left multiplier from that stream, right from
+// stream ^ 0x5000000000000000), system M A / A N / M A N, blocked GENP with pivot
+// floor 1e-300, solves, y = N z, refinement, residual-gated acceptance at 1e-7,
+// best-attempt fallback, PivotBreakdown rethrown only when the last attempt breaks
+// down with no best.  Every FLOP runs on the GPU; the host only reads back the
+// scalars the protocol branches on (breakdown flag, residuals, pivots).
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "rl_internal.cuh"
+
+namespace rl {
+
+// genp.cu
+void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor, double* d_pivots,
+                         unsigned long long* d_breakdown, double* aux);
+void genp_solve_blocked(uint64_t n, uint64_t nrhs, const double* lu, uint64_t lda, const double* aux,
+                        double* b, uint64_t ldb);
+void copy2d_dev(uint64_t rows, uint64_t cols, const double* src, uint64_t lds, double* dst, uint64_t ldd);
+void axpy_dev(uint64_t count, double alpha, const double* x, double* y);
+// structured.cu
+void circulant_dense_dev(uint64_t n, const double* c, double* out);
+void rank1_dense_dev(uint64_t n, const double* u, const double* v, double inv_uv, double* out);
+void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
+                         double s12, double* out, uint64_t ldo);
+void hh2_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* u1, const double* u2, const double* y,
+                       double* x);
+void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs,
+                            const double* a, uint64_t lda, double* out, uint64_t ldo);
+struct SparseT {
+    int32_t* row_ptr;
+    int32_t* col_j;
+    double* col_s;
+};
+SparseT sparse_transpose_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs);
+void sparse_apply_vec_dev(uint64_t n, uint64_t nrhs, const SparseT& s, const double* y, double* x);
+void circ_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* c, const double* z, double* y);
+// genp_batched.cu
+rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int refine, uint64_t seed,
+                         const uint64_t* d_sids, double* dX, rl_precond_report* d_rep);
+
+namespace {
+
+constexpr int NB = 128;
+
+struct Mult {
+    int tag = 0;
+    uint64_t n = 0;
+    double* dense = nullptr; // n x n (dense kinds; circulant densified for the left product)
+    double* c = nullptr;     // circulant first column
+    double* u1 = nullptr;
+    double* u2 = nullptr;
+    double s12 = 0.0;
+    int32_t* rows = nullptr;
+    double* signs = nullptr;
+    SparseT st{};
+};
+
+std::vector<double> to_host(const double* d, uint64_t count) {
+    std::vector<double> h(count);
+    RL_CUDA(cudaMemcpyAsync(h.data(), d, count * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+    return h;
+}
+
+// draw_multiplier (genp.cpp:183-203) on the GPU; `slot_dense` / `slot_vec` are scratch slots.
+void draw(Mult& m, int tag, double mu, double sigma, uint64_t n, uint64_t seed, uint64_t sid,
+          int slot_dense, int slot_vec, bool want_dense) {
+    m.tag = tag;
+    m.n = n;
+    switch (tag) {
+    case RL_GAUSSIAN:
+        if (!(sigma > 0.0))
+            fail(RL_INVALID_ARGUMENT, "gaussian_matrix: sigma must be positive");
+        m.dense = ws<double>(slot_dense, n * n);
+        rng_generate(seed, sid, Draw::Gaussian, n * n, mu, sigma, m.dense);
+        break;
+    case RL_UNIFORM_PM1:
+        m.dense = ws<double>(slot_dense, n * n);
+        rng_generate(seed, sid, Draw::UniformPm1, n * n, 0.0, 1.0, m.dense);
+        break;
+    case RL_CIRCULANT_SIGN:
+    case RL_CIRCULANT_GAUSSIAN:
+        m.c = ws<double>(slot_vec, n);
+        if (tag == RL_CIRCULANT_SIGN)
+            rng_generate(seed, sid, Draw::Sign, n, 0.0, 1.0, m.c);
+        else
+            rng_generate(seed, sid, Draw::Gaussian, n, mu, sigma, m.c);
+        if (want_dense) {
+            m.dense = ws<double>(slot_dense, n * n);
+            circulant_dense_dev(n, m.c, m.dense);
+        }
+        break;
+    case RL_HOUSEHOLDER_SIGN: {
+        // random_gen.cpp:125-143: u, v signs; resample while u^T v == 0 (<= 64)
+        double* uv = ws<double>(slot_vec, 2 * n * 64);
+        rng_generate(seed, sid, Draw::Sign, 2 * n * 64, 0.0, 1.0, uv);
+        std::vector<double> h = to_host(uv, 2 * n * 64);
+        int found = -1;
+        double dotv = 0.0;
+        for (int r = 0; r < 64 && found < 0; ++r) {
+            double s = 0.0;
+            for (uint64_t i = 0; i < n; ++i)
+                s += h[2 * n * r + i] * h[2 * n * r + n + i];
+            if (s != 0.0) {
+                found = r;
+                dotv = s;
+            }
+        }
+        if (found < 0)
+            fail(RL_DEGENERATE, "householder_sign: u^T v == 0 after 64 resamples");
+        m.dense = ws<double>(slot_dense, n * n);
+        rank1_dense_dev(n, uv + 2 * n * found, uv + 2 * n * found + n, 1.0 / dotv, m.dense);
+        break;
+    }
+    case RL_HOUSEHOLDER_PAIR: {
+        double* u = ws<double>(slot_vec, 2 * n);
+        rng_generate(seed, sid, Draw::Sign, 2 * n, 0.0, 1.0, u);
+        m.u1 = u;
+        m.u2 = u + n;
+        std::vector<double> h = to_host(u, 2 * n);
+        double s = 0.0;
+        for (uint64_t i = 0; i < n; ++i)
+            s += h[i] * h[n + i];
+        m.s12 = s;
+        break;
+    }
+    case RL_SPARSE_SIGN: {
+        const int nnz = 4;
+        if (n < 4)
+            fail(RL_INVALID_ARGUMENT, "sparse multiplier needs n >= 4");
+        char* base = ws<char>(slot_vec, n * nnz * 12 + 64);
+        m.signs = reinterpret_cast<double*>(base);
+        m.rows = reinterpret_cast<int32_t*>(base + n * nnz * 8);
+        rng_sparse_sign(seed, sid, n, nnz, m.rows, m.signs);
+        m.st = sparse_transpose_dev(n, nnz, m.rows, m.signs);
+        break;
+    }
+    default:
+        fail(RL_INVALID_ARGUMENT, "randomized_genp: unsupported multiplier kind");
+    }
+}
+
+// out = sys * M  (out != sys)
+void apply_right(const Mult& m, const double* sys, double* out) {
+    const uint64_t n = m.n;
+    switch (m.tag) {
+    case RL_HOUSEHOLDER_PAIR:
+        hh2_apply_right_dev(n, sys, n, m.u1, m.u2, m.s12, out, n);
+        return;
+    case RL_SPARSE_SIGN:
+        sparse_apply_right_dev(n, 4, m.rows, m.signs, sys, n, out, n);
+        return;
+    default:
+        gemm(false, false, n, n, n, 1.0, sys, n, m.dense, n, 0.0, out, n);
+    }
+}
+
+// out = M * sys (out != sys)
+void apply_left(const Mult& m, const double* sys, uint64_t cols, double* out) {
+    const uint64_t n = m.n;
+    gemm(false, false, n, cols, n, 1.0, m.dense, n, sys, cols, 0.0, out, cols);
+}
+
+// out = M * v  (v n x nrhs)
+void apply_vec(const Mult& m, const double* v, uint64_t nrhs, double* out) {
+    const uint64_t n = m.n;
+    switch (m.tag) {
+    case RL_CIRCULANT_SIGN:
+    case RL_CIRCULANT_GAUSSIAN:
+        circ_apply_vec_dev(n, nrhs, m.c, v, out);
+        return;
+    case RL_HOUSEHOLDER_PAIR:
+        hh2_apply_vec_dev(n, nrhs, m.u1, m.u2, v, out);
+        return;
+    case RL_SPARSE_SIGN:
+        sparse_apply_vec_dev(n, nrhs, m.st, v, out);
+        return;
+    default:
+        gemm(false, false, n, nrhs, n, 1.0, m.dense, n, v, nrhs, 0.0, out, nrhs);
+    }
+}
+
+void minmax_fold(const std::vector<double>& p, double* mn, double* mx) {
+    double a = p.empty() ? 0.0 : p[0], b = a;
+    for (double v : p) {
+        a = (v < a) ? v : a;
+        b = (b < v) ? v : b;
+    }
+    *mn = a;
+    *mx = b;
+}
+
+// max over columns of per-column relative residuals (nrhs = 1: the reference metric);
+// non-finite columns count as +inf when check_finite.
+double residual_max(uint64_t n, uint64_t nrhs, const double* a, const double* x, const double* b,
+                    bool check_finite) {
+    double* tmp = ws<double>(WS_RESID, n * nrhs + nrhs);
+    double* out = tmp + n * nrhs;
+    residuals_dev(n, nrhs, a, x, b, tmp, out);
+    std::vector<double> r = to_host(out, nrhs);
+    double worst = 0.0;
+    std::vector<double> xs;
+    if (check_finite)
+        xs = to_host(x, n * nrhs);
+    for (uint64_t j = 0; j < nrhs; ++j) {
+        double v = r[j];
+        if (check_finite)
+            for (uint64_t i = 0; i < n; ++i)
+                if (!std::isfinite(xs[i * nrhs + j])) {
+                    v = std::numeric_limits<double>::infinity();
+                    break;
+                }
+        if (j == 0 || v > worst || std::isnan(v))
+            worst = v;
+    }
+    return worst;
+}
+
+} // namespace
+
+rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const double* B, int tag,
+                              double mu, double sigma, int side, int refine, uint64_t seed, uint64_t sid,
+                              double* X, rl_precond_report* report, uint32_t flags) {
+    if (refine < 0 || refine > 2)
+        fail(RL_INVALID_ARGUMENT, "randomized_genp: refine must be in {0, 1, 2}");
+    if (side < 0 || side > 2)
+        fail(RL_INVALID_ARGUMENT, "randomized_genp: bad side");
+    if (tag == RL_TOEPLITZ_GAUSSIAN)
+        fail(RL_INVALID_ARGUMENT, "randomized_genp: ToeplitzGaussian needs m x n specs (not a square multiplier)");
+    if ((tag == RL_HOUSEHOLDER_PAIR || tag == RL_SPARSE_SIGN) && side != RL_RIGHT)
+        fail(RL_INVALID_ARGUMENT, "randomized_genp: the new multiplier kinds are applied on the right");
+    const bool use_left = side == RL_LEFT || side == RL_BOTH;
+    const bool use_right = side == RL_RIGHT || side == RL_BOTH;
+    const uint64_t nblk = (n + NB - 1) / NB;
+    double* sys = ws<double>(WS_SYS, n * n);
+    double* tmp = ws<double>(WS_OUT, n * n);
+    double* aux = ws<double>(WS_LU_AUX, nblk * 2 * NB * NB);
+    double* vecs = ws<double>(WS_RHS, 4 * n * nrhs + n + 8);
+    double* Z = vecs;
+    double* Y = Z + n * nrhs;
+    double* R = Y + n * nrhs;
+    double* D = R + n * nrhs;
+    double* piv = D + n * nrhs;
+    unsigned long long* brk = reinterpret_cast<unsigned long long*>(piv + n);
+    cudaStream_t st = stream();
+
+    rl_precond_report rep{};
+    rep.attempt = -1;
+    if (!(flags & 1u)) {
+        // raw-GENP contrast arm (genp.cpp:222-234)
+        copy2d_dev(n, n, A, n, sys, n);
+        RL_CUDA(cudaMemsetAsync(brk, 0xff, 8, st));
+        genp_factor_blocked(n, sys, n, 0.0, piv, brk, aux);
+        copy2d_dev(n, nrhs, B, nrhs, Z, nrhs);
+        genp_solve_blocked(n, nrhs, sys, n, aux, Z, nrhs);
+        rep.raw_residual = residual_max(n, nrhs, A, Z, B, true);
+        minmax_fold(to_host(piv, n), &rep.raw_pivot_min, &rep.raw_pivot_max);
+    }
+    rl_precond_report best = rep;
+    bool have_best = false;
+    rl_status status = RL_OK;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        const uint64_t ds = sid + 7919ULL * static_cast<uint64_t>(attempt);
+        rep.attempts_drawn = attempt + 1;
+        Mult left, right;
+        if (use_left)
+            draw(left, tag, mu, sigma, n, seed, ds, WS_MULT, WS_LVEC, true);
+        if (use_right)
+            draw(right, tag, mu, sigma, n, seed, ds ^ 0x5000000000000000ULL, use_left ? WS_RF1 : WS_MULT,
+                 WS_RF2, true);
+        const double* src = A;
+        if (use_left) {
+            apply_left(left, src, n, tmp);
+            std::swap(sys, tmp);
+            src = sys;
+        }
+        if (use_right) {
+            apply_right(right, src, tmp);
+            std::swap(sys, tmp);
+        }
+        if (!use_left && !use_right)
+            copy2d_dev(n, n, A, n, sys, n);
+        if (use_left)
+            apply_vec(left, B, nrhs, Z);
+        else
+            copy2d_dev(n, nrhs, B, nrhs, Z, nrhs);
+        RL_CUDA(cudaMemsetAsync(brk, 0xff, 8, st));
+        genp_factor_blocked(n, sys, n, 1e-300, piv, brk, aux);
+        long long hb = -1;
+        RL_CUDA(cudaMemcpyAsync(&hb, brk, 8, cudaMemcpyDeviceToHost, st));
+        RL_CUDA(cudaStreamSynchronize(st));
+        if (hb >= 0) { // PivotBreakdown (genp.cpp:285-288)
+            if (attempt + 1 >= 8 && !have_best) {
+                status = RL_PIVOT_BREAKDOWN;
+                set_error("genp_factor: pivot below floor at step " + std::to_string(hb));
+            }
+            continue;
+        }
+        genp_solve_blocked(n, nrhs, sys, n, aux, Z, nrhs);
+        if (use_right)
+            apply_vec(right, Z, nrhs, Y);
+        else
+            copy2d_dev(n, nrhs, Z, nrhs, Y, nrhs);
+        for (int s = 0; s < refine; ++s) {
+            copy2d_dev(n, nrhs, B, nrhs, R, nrhs);
+            gemm(false, false, n, nrhs, n, -1.0, A, n, Y, nrhs, 1.0, R, nrhs); // r = b - A y
+            if (use_left) {
+                apply_vec(left, R, nrhs, D);
+                copy2d_dev(n, nrhs, D, nrhs, R, nrhs);
+            }
+            genp_solve_blocked(n, nrhs, sys, n, aux, R, nrhs);
+            if (use_right)
+                apply_vec(right, R, nrhs, D);
+            else
+                copy2d_dev(n, nrhs, R, nrhs, D, nrhs);
+            axpy_dev(n * nrhs, 1.0, D, Y); // y += d
+        }
+        rep.residual = residual_max(n, nrhs, A, Y, B, false);
+        minmax_fold(to_host(piv, n), &rep.pivot_min, &rep.pivot_max);
+        rep.attempt = attempt;
+        if (rep.residual <= 1e-7) {
+            copy2d_dev(n, nrhs, Y, nrhs, X, nrhs);
+            if (report)
+                *report = rep;
+            RL_CUDA(cudaStreamSynchronize(st));
+            return RL_OK;
+        }
+        if (!have_best || rep.residual < best.residual) {
+            copy2d_dev(n, nrhs, Y, nrhs, X, nrhs);
+            best = rep;
+            have_best = true;
+        }
+    }
+    if (status == RL_OK && report) {
+        best.attempts_drawn = 8;
+        *report = best;
+    }
+    RL_CUDA(cudaStreamSynchronize(st));
+    return status;
+}
+
+rl_status randomized_genp_batched_dev(uint64_t batch, uint64_t n, const double* dA, const double* dB,
+                                      int tag, double mu, double sigma, int side, int refine,
+                                      uint64_t seed, const uint64_t* d_sids, double* dX,
+                                      rl_precond_report* d_rep) {
+    if (refine < 0 || refine > 2)
+        fail(RL_INVALID_ARGUMENT, "randomized_genp: refine must be in {0, 1, 2}");
+    if (tag == RL_CIRCULANT_SIGN && side == RL_RIGHT && n == 64)
+        return batched_circ64(batch, dA, dB, refine, seed, d_sids, dX, d_rep);
+    // general kinds / sizes: one system at a time through the blocked path
+    std::vector<uint64_t> sids(batch);
+    RL_CUDA(cudaMemcpyAsync(sids.data(), d_sids, batch * 8, cudaMemcpyDeviceToHost, stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+    std::vector<rl_precond_report> reps(batch);
+    for (uint64_t t = 0; t < batch; ++t) {
+        rl_status s = randomized_genp_dev(n, 1, dA + t * n * n, dB + t * n, tag, mu, sigma, side, refine,
+                                          seed, sids[t], dX + t * n, &reps[t], 0);
+        if (s != RL_OK)
+            return s;
+    }
+    RL_CUDA(cudaMemcpyAsync(d_rep, reps.data(), batch * sizeof(rl_precond_report), cudaMemcpyHostToDevice,
+                            stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+    return RL_OK;
+}
+
+} // namespace rl

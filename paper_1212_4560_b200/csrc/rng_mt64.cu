@@ -1,0 +1,501 @@
+// K1: the reference's random streams on the GPU, bit-exact.
+//
+// Reference: rnd::Rng (proj/src/random_gen.cpp:13-70) = splitmix64-mixed seed ->
+// std::mt19937_64 -> discard(8), one SEQUENTIAL stream per generated matrix
+// (gaussian_matrix random_gen.cpp:72-80 fills row-major entries in draw order).
+//
+// B200 design: a stream of N outputs is cut into chunks of J = 2^15 engine steps,
+// one warp per chunk.  The engine state at the start of chunk c is
+//     s_{8 + cJ} = p(T) s_0,   p = x^(8 + cJ) mod phi
+// (phi = characteristic polynomial of the mt19937_64 transition, table built at
+// build time by mt64_jumpgen.cpp).  Applying p is a GF(2) correlation of the
+// polynomial's set bits with the word sequence (k_jump).  Two levels keep the
+// table small: level-1 windows every 2^21 steps from s_0, level-2 windows every
+// 2^15 steps from each level-1 window.  The warp then twists its 312-word window
+// in shared memory and tempers / transforms 312 outputs per twist.
+#include <dlfcn.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "dd_math.cuh"
+#include "rl_internal.cuh"
+
+namespace rl {
+
+namespace {
+
+constexpr int kN = 312, kM = 156;
+constexpr uint64_t kUpper = 0xFFFFFFFF80000000ULL, kLower = 0x7FFFFFFFULL,
+                   kMatA = 0xB5026F5AA96619E9ULL;
+constexpr int kLog2J = 15;
+constexpr uint64_t kJ = 1ULL << kLog2J;
+constexpr int kSeqWords = 19937 + kN - 1; // words x_t .. x_{t+20247} feed a jump
+constexpr uint64_t kSmallMax = 1ULL << 16; // streams this short run on one warp
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// random_gen.cpp:22-29: the engine seed of stream (seed, sid)
+__host__ __device__ __forceinline__ uint64_t engine_seed(uint64_t seed, uint64_t sid) {
+    uint64_t s = seed;
+    uint64_t a = splitmix64(s);
+    s ^= sid * 0xda942042e4dd58b5ULL + 0x2545f4914f6cdd1dULL;
+    uint64_t b = splitmix64(s);
+    return a ^ (b << 1);
+}
+
+__device__ __forceinline__ uint64_t temper(uint64_t z) {
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    return z;
+}
+
+__device__ __forceinline__ uint64_t twist_word(uint64_t xi, uint64_t xi1, uint64_t xim) {
+    uint64_t y = (xi & kUpper) | (xi1 & kLower);
+    return xim ^ (y >> 1) ^ ((y & 1ULL) ? kMatA : 0ULL);
+}
+
+// mt19937_64::seed(v) by lane 0 (sequential recurrence), window = x_0..x_311
+__device__ void warp_seed_window(uint64_t* w, uint64_t v, int lane) {
+    if (lane == 0) {
+        w[0] = v;
+        for (int i = 1; i < kN; ++i) {
+            v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
+            w[i] = v;
+        }
+    }
+    __syncwarp();
+}
+
+// In-place twist of a 312-word window held in shared memory by one warp.
+// Same recurrence as libstdc++'s mersenne_twister_engine::_M_gen_rand.
+__device__ void warp_twist(uint64_t* w, int lane) {
+#pragma unroll 1
+    for (int base = 0; base < kN - kM; base += 32) {
+        int i = base + lane;
+        uint64_t v = 0;
+        if (i < kN - kM)
+            v = twist_word(w[i], w[i + 1], w[i + kM]);
+        __syncwarp();
+        if (i < kN - kM)
+            w[i] = v;
+        __syncwarp();
+    }
+#pragma unroll 1
+    for (int base = kN - kM; base < kN; base += 32) {
+        int i = base + lane;
+        uint64_t v = 0;
+        if (i < kN)
+            v = twist_word(w[i], w[(i + 1) % kN], w[i - (kN - kM)]);
+        __syncwarp();
+        if (i < kN)
+            w[i] = v;
+        __syncwarp();
+    }
+}
+
+struct GenParams {
+    int kind;        // Draw
+    double mu, sigma;
+    uint64_t count;  // number of transformed values (Gaussian: entries)
+    void* out;
+};
+
+// Box-Muller pair of random_gen.cpp:46-52 from two raw draws; returns (cos, sin) entries.
+__device__ __forceinline__ void box_muller(uint64_t r1, uint64_t r2, double mu, double sigma,
+                                           double* g0, double* g1) {
+    double u1 = __dsub_rn(1.0, __dmul_rn(static_cast<double>(r1 >> 11), 0x1.0p-53));
+    double u2 = __dmul_rn(static_cast<double>(r2 >> 11), 0x1.0p-53);
+    double lg = cr_log_unit(u1);
+    double r = __dsqrt_rn(__dmul_rn(-2.0, lg));
+    double a = __dmul_rn(2.0 * 3.14159265358979323846, u2);
+    double s, c;
+    cr_sincos(a, &s, &c);
+    *g0 = __dadd_rn(mu, __dmul_rn(sigma, __dmul_rn(r, c)));
+    *g1 = __dadd_rn(mu, __dmul_rn(sigma, __dmul_rn(r, s)));
+}
+
+// Emit the outputs carried by one freshly twisted window whose word 0 is stream
+// output index o0 (may be negative during the constructor's discard), limited to
+// outputs [lo, hi).
+__device__ __forceinline__ void emit_block(const uint64_t* w, int64_t o0, int64_t lo, int64_t hi,
+                                           const GenParams& p, int lane) {
+    if (p.kind == static_cast<int>(Draw::Gaussian)) {
+        // pairs (o, o+1) with o even: entries o (cos) and o+1 (sin)
+        for (int q = lane; q < kN / 2; q += 32) {
+            int64_t o = o0 + 2 * q;
+            if (o < lo || o >= hi)
+                continue;
+            double g0, g1;
+            box_muller(temper(w[2 * q]), temper(w[2 * q + 1]), p.mu, p.sigma, &g0, &g1);
+            double* out = static_cast<double*>(p.out);
+            if (static_cast<uint64_t>(o) + 1 < p.count) {
+                *reinterpret_cast<double2*>(out + o) = make_double2(g0, g1);
+            } else {
+                out[o] = g0;
+            }
+        }
+        return;
+    }
+    for (int i = lane; i < kN; i += 32) {
+        int64_t o = o0 + i;
+        if (o < lo || o >= hi)
+            continue;
+        uint64_t z = temper(w[i]);
+        switch (p.kind) {
+        case static_cast<int>(Draw::RawU64):
+            static_cast<uint64_t*>(p.out)[o] = z;
+            break;
+        case static_cast<int>(Draw::Uniform01):
+            static_cast<double*>(p.out)[o] = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+            break;
+        case static_cast<int>(Draw::UniformPm1):
+            static_cast<double*>(p.out)[o] =
+                __dsub_rn(__dmul_rn(2.0, __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53)), 1.0);
+            break;
+        default: // Sign
+            static_cast<double*>(p.out)[o] = (z & 1ULL) ? 1.0 : -1.0;
+            break;
+        }
+    }
+}
+
+// Short streams: one warp from the seed; outputs [0, nout).
+__global__ void k_gen_small(uint64_t eseed, uint64_t nout, GenParams p) {
+    __shared__ uint64_t w[kN];
+    int lane = threadIdx.x;
+    warp_seed_window(w, eseed, lane);
+    // window at time 0; after each twist word 0 is stream position 312k -> output 312k - 320
+    for (int64_t pos = 0; pos < static_cast<int64_t>(nout) + 8; pos += kN) {
+        warp_twist(w, lane);
+        emit_block(w, pos - 8, 0, static_cast<int64_t>(nout), p, lane);
+    }
+}
+
+// Word sequence x_0 .. x_{kSeqWords-1} of a seeded engine (the base for level-1 jumps).
+__global__ void k_base_sequence(uint64_t eseed, uint64_t* seq) {
+    __shared__ uint64_t w[kN];
+    int lane = threadIdx.x;
+    warp_seed_window(w, eseed, lane);
+    for (int base = 0; base < kSeqWords; base += kN) {
+        for (int i = lane; i < kN; i += 32)
+            if (base + i < kSeqWords)
+                seq[base + i] = w[i];
+        __syncwarp();
+        warp_twist(w, lane);
+    }
+}
+
+// Word sequences continuing each window: seq[k][0..kSeqWords) from windows[k].
+__global__ void k_window_sequence(const uint64_t* windows, uint64_t* seqs) {
+    __shared__ uint64_t w[kN];
+    int lane = threadIdx.x;
+    const uint64_t* src = windows + static_cast<size_t>(blockIdx.x) * kN;
+    uint64_t* seq = seqs + static_cast<size_t>(blockIdx.x) * kSeqWords;
+    for (int i = lane; i < kN; i += 32)
+        w[i] = src[i];
+    __syncwarp();
+    for (int base = 0; base < kSeqWords; base += kN) {
+        for (int i = lane; i < kN; i += 32)
+            if (base + i < kSeqWords)
+                seq[base + i] = w[i];
+        __syncwarp();
+        warp_twist(w, lane);
+    }
+}
+
+// Jump: out window t = XOR_{i : poly[i]} seq[i + j], j = 0..311.
+// Target b of block uses poly polys[(first_poly + b) % poly_mod] and base sequence
+// seqs[(b / seq_div)].
+constexpr int kJumpThreads = 320;
+__global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, int first_poly,
+                                                       int poly_mod, const uint64_t* seqs,
+                                                       int seq_div, int ntargets,
+                                                       uint64_t* out) {
+    extern __shared__ __align__(16) uint64_t sm[];
+    uint64_t* x = sm;                                              // kSeqWords
+    uint16_t* list = reinterpret_cast<uint16_t*>(sm + kSeqWords);  // up to 19937 offsets
+    __shared__ int wcount[kN];
+    __shared__ int total;
+    const int tgt = blockIdx.x;
+    if (tgt >= ntargets)
+        return;
+    const uint64_t* poly = polys + static_cast<size_t>((first_poly + tgt) % poly_mod) * kN;
+    const uint64_t* seq = seqs + static_cast<size_t>(tgt / seq_div) * kSeqWords;
+    const int t = threadIdx.x;
+    for (int i = t; i < kSeqWords; i += kJumpThreads)
+        x[i] = seq[i];
+    uint64_t pw = 0;
+    if (t < kN) {
+        pw = poly[t];
+        wcount[t] = __popcll(pw);
+    }
+    __syncthreads();
+    if (t == 0) { // exclusive scan of 312 counts (tiny)
+        int acc = 0;
+        for (int i = 0; i < kN; ++i) {
+            int c = wcount[i];
+            wcount[i] = acc;
+            acc += c;
+        }
+        total = acc;
+    }
+    __syncthreads();
+    if (t < kN) {
+        int pos = wcount[t];
+        while (pw) {
+            int b = __ffsll(static_cast<long long>(pw)) - 1;
+            pw &= pw - 1;
+            list[pos++] = static_cast<uint16_t>(64 * t + b);
+        }
+    }
+    __syncthreads();
+    if (t < kN) {
+        uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        const int n = total;
+        const uint64_t* xj = x + t;
+        int k = 0;
+        for (; k + 4 <= n; k += 4) {
+            uint2 ids = *reinterpret_cast<const uint2*>(list + k); // 4 x u16, 8B aligned
+            a0 ^= xj[ids.x & 0xffffu];
+            a1 ^= xj[ids.x >> 16];
+            a2 ^= xj[ids.y & 0xffffu];
+            a3 ^= xj[ids.y >> 16];
+        }
+        for (; k < n; ++k)
+            a0 ^= xj[list[k]];
+        out[static_cast<size_t>(tgt) * kN + t] = a0 ^ a1 ^ a2 ^ a3;
+    }
+}
+
+// One warp per chunk: window at stream position 8 + cJ -> outputs [cJ, cJ + J).
+constexpr int kGenWarps = 4;
+__global__ void __launch_bounds__(32 * kGenWarps) k_gen_chunks(const uint64_t* windows,
+                                                               uint64_t nchunks, uint64_t nout,
+                                                               GenParams p) {
+    __shared__ uint64_t wbuf[kGenWarps][kN];
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t c = static_cast<uint64_t>(blockIdx.x) * kGenWarps + wid;
+    if (c >= nchunks)
+        return;
+    uint64_t* w = wbuf[wid];
+    for (int i = lane; i < kN; i += 32)
+        w[i] = windows[c * kN + i];
+    __syncwarp();
+    const int64_t lo = static_cast<int64_t>(c * kJ);
+    const int64_t hi = static_cast<int64_t>(min(nout, (c + 1) * kJ));
+    for (int64_t o0 = lo; o0 < hi; o0 += kN) {
+        warp_twist(w, lane);
+        emit_block(w, o0, lo, hi, p, lane);
+    }
+}
+
+// Per-thread streams, n <= 148 sign draws each (only the first twist's phase 1 is
+// needed: new[i] = x[i+156] ^ tw(x[i], x[i+1]) for i < 8 + n <= 156).
+__global__ void k_sign_batched(uint64_t seed, const uint64_t* sids, uint64_t add, uint64_t xor_mask,
+                               uint64_t batch, int n, double* out) {
+    uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= batch)
+        return;
+    uint64_t v = engine_seed(seed, (sids[t] + add) ^ xor_mask);
+    const int need = 8 + n; // new words 0 .. need-1
+    uint64_t lo[157], hi[157];
+    lo[0] = v;
+    for (int i = 1; i < kN; ++i) {
+        v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
+        if (i <= need)
+            lo[i] = v;
+        if (i >= kM && i < kM + need)
+            hi[i - kM] = v;
+        if (i >= kM + need)
+            break;
+    }
+    for (int i = 8; i < need; ++i) {
+        uint64_t z = temper(twist_word(lo[i], lo[i + 1], hi[i]));
+        out[t * n + (i - 8)] = (z & 1ULL) ? 1.0 : -1.0;
+    }
+}
+
+// ---------------------------------------------------------------- tables --
+struct JumpTable {
+    uint64_t* d_l1 = nullptr;
+    uint64_t* d_l2 = nullptr;
+    int n_l1 = 0, n_l2 = 0;
+};
+
+std::mutex g_jt_mu;
+JumpTable g_jt[16];
+
+std::string lib_dir() {
+    Dl_info info;
+    if (dladdr(reinterpret_cast<void*>(&lib_dir), &info) && info.dli_fname) {
+        std::string p(info.dli_fname);
+        auto s = p.rfind('/');
+        return s == std::string::npos ? std::string(".") : p.substr(0, s);
+    }
+    return ".";
+}
+
+const JumpTable& jump_table() {
+    int dev = ctx().device;
+    std::lock_guard<std::mutex> lk(g_jt_mu);
+    JumpTable& jt = g_jt[dev & 15];
+    if (jt.d_l1)
+        return jt;
+    std::string path = lib_dir() + "/mt64_jump.bin";
+    FILE* fh = std::fopen(path.c_str(), "rb");
+    if (!fh)
+        fail(RL_ERROR, "mt19937_64 jump table missing: " + path + " (run __graft_entry__.build())");
+    uint64_t magic = 0;
+    uint32_t hdr[4] = {0, 0, 0, 0};
+    bool ok = std::fread(&magic, 8, 1, fh) == 1 && std::fread(hdr, 4, 4, fh) == 4 &&
+              magic == 0x314A3436544D4C52ULL && hdr[0] == kN && hdr[1] == kLog2J;
+    std::vector<uint64_t> buf;
+    if (ok) {
+        buf.resize(static_cast<size_t>(hdr[2] + hdr[3]) * kN);
+        ok = std::fread(buf.data(), 8, buf.size(), fh) == buf.size();
+    }
+    std::fclose(fh);
+    if (!ok)
+        fail(RL_ERROR, "mt19937_64 jump table corrupt: " + path);
+    uint64_t* d = nullptr;
+    RL_CUDA(cudaMalloc(&d, buf.size() * 8));
+    RL_CUDA(cudaMemcpy(d, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice));
+    jt.d_l1 = d;
+    jt.d_l2 = d + static_cast<size_t>(hdr[2]) * kN;
+    jt.n_l1 = static_cast<int>(hdr[2]);
+    jt.n_l2 = static_cast<int>(hdr[3]);
+    return jt;
+}
+
+constexpr size_t kJumpSmem = kSeqWords * 8 + 19968 * 2 + 16;
+
+} // namespace
+
+void rng_generate(uint64_t seed, uint64_t sid, Draw kind, uint64_t count, double mu, double sigma,
+                  void* d_out) {
+    if (count == 0)
+        return;
+    GenParams p{static_cast<int>(kind), mu, sigma, count, d_out};
+    uint64_t nout = (kind == Draw::Gaussian) ? ((count + 1) & ~1ULL) : count;
+    uint64_t eseed = engine_seed(seed, sid);
+    cudaStream_t st = stream();
+    if (nout <= kSmallMax) {
+        k_gen_small<<<1, 32, 0, st>>>(eseed, count, p);
+        RL_LAUNCHED();
+        return;
+    }
+    const JumpTable& jt = jump_table();
+    uint64_t nchunks = (nout + kJ - 1) / kJ;
+    uint64_t nl1 = (nchunks + jt.n_l2 - 1) / jt.n_l2;
+    if (nl1 > static_cast<uint64_t>(jt.n_l1))
+        fail(RL_TOO_LARGE, "rng: stream longer than 2^30 draws");
+    static bool attr_set[16] = {};
+    if (!attr_set[ctx().device & 15]) {
+        RL_CUDA(cudaFuncSetAttribute(k_jump, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kJumpSmem)));
+        attr_set[ctx().device & 15] = true;
+    }
+    uint64_t* base = ws<uint64_t>(WS_RNG, kSeqWords + nl1 * kN + nl1 * kSeqWords);
+    uint64_t* l1w = base + kSeqWords;
+    uint64_t* l1s = l1w + nl1 * kN;
+    uint64_t* cw = ws<uint64_t>(WS_RNG2, nchunks * kN);
+    k_base_sequence<<<1, 32, 0, st>>>(eseed, base);
+    RL_LAUNCHED();
+    k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(jt.d_l1, 0, jt.n_l1, base,
+                                                                          1 << 30, static_cast<int>(nl1), l1w);
+    RL_LAUNCHED();
+    k_window_sequence<<<static_cast<unsigned>(nl1), 32, 0, st>>>(l1w, l1s);
+    RL_LAUNCHED();
+    k_jump<<<static_cast<unsigned>(nchunks), kJumpThreads, kJumpSmem, st>>>(
+        jt.d_l2, 0, jt.n_l2, l1s, jt.n_l2, static_cast<int>(nchunks), cw);
+    RL_LAUNCHED();
+    k_gen_chunks<<<cdiv(nchunks, kGenWarps), 32 * kGenWarps, 0, st>>>(cw, nchunks, count, p);
+    RL_LAUNCHED();
+}
+
+void rng_sign_vectors_batched(uint64_t seed, const uint64_t* d_sids, uint64_t add, uint64_t xor_mask,
+                              uint64_t batch, uint64_t n, double* d_out) {
+    if (batch == 0)
+        return;
+    if (n > 148)
+        fail(RL_INVALID_ARGUMENT, "batched sign vectors: n > 148");
+    k_sign_batched<<<cdiv(batch, 128), 128, 0, stream()>>>(seed, d_sids, add, xor_mask, batch,
+                                                           static_cast<int>(n), d_out);
+    RL_LAUNCHED();
+}
+
+// ------------------------------------------------------ sparse +-1 (NEW) --
+namespace {
+// Serial consumption of a raw pool: per column nnz distinct rows by
+// uniform_int(0, n-1) (random_gen.cpp:59-70 rejection) then nnz signs.
+__global__ void k_sparse_consume(const uint64_t* pool, uint64_t pool_len, uint64_t n, int nnz,
+                                 int32_t* rows, double* signs, int* status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0)
+        return;
+    const uint64_t span = n;
+    const uint64_t limit = (~0ULL) / span * span;
+    uint64_t k = 0;
+    for (uint64_t j = 0; j < n; ++j) {
+        int32_t* rj = rows + j * nnz;
+        for (int t = 0; t < nnz; ++t) {
+            for (;;) {
+                if (k >= pool_len) {
+                    *status = 1;
+                    return;
+                }
+                uint64_t v = pool[k++];
+                if (v >= limit)
+                    continue;
+                int32_t r = static_cast<int32_t>(v % span);
+                bool dup = false;
+                for (int s = 0; s < t; ++s)
+                    dup |= (rj[s] == r);
+                if (!dup) {
+                    rj[t] = r;
+                    break;
+                }
+            }
+        }
+        for (int t = 0; t < nnz; ++t) {
+            if (k >= pool_len) {
+                *status = 1;
+                return;
+            }
+            signs[j * nnz + t] = (pool[k++] & 1ULL) ? 1.0 : -1.0;
+        }
+    }
+    *status = 0;
+}
+} // namespace
+
+void rng_sparse_sign(uint64_t seed, uint64_t sid, uint64_t n, int nnz, int32_t* d_rows,
+                     double* d_signs) {
+    // 2 nnz draws per column + slack for (rare) rejections; retried with a larger pool.
+    uint64_t slack = 1024 + n / 8;
+    for (int tries = 0; tries < 4; ++tries, slack *= 8) {
+        uint64_t len = 2ULL * nnz * n + slack;
+        uint64_t* pool = ws<uint64_t>(WS_TMP2, len + 1);
+        int* d_status = reinterpret_cast<int*>(pool + len);
+        rng_generate(seed, sid, Draw::RawU64, len, 0.0, 1.0, pool);
+        k_sparse_consume<<<1, 32, 0, stream()>>>(pool, len, n, nnz, d_rows, d_signs, d_status);
+        RL_LAUNCHED();
+        int h = 0;
+        RL_CUDA(cudaMemcpyAsync(&h, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+        RL_CUDA(cudaStreamSynchronize(stream()));
+        if (h == 0)
+            return;
+    }
+    fail(RL_ERROR, "sparse_sign: draw pool exhausted");
+}
+
+} // namespace rl
