@@ -1,0 +1,440 @@
+"""Benchmark driver (contract: see DESIGN.md §6).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json `metric`: "fp64 TFLOP/s precond+GENP at n=8192; batched n=64
+solves/s; % of roofline"):
+  * headline `value` — config 3: Gaussian-preconditioned GENP, n = 8192, 16 RHS, MulSide::Right
+    (G = gaussian_matrix(n, n) on the reference's Right stream, A G, blocked GENP with block 128,
+    forward/back solves, X = G Y, residual-gated acceptance).  TFLOP/s over the algorithmic
+    1.4704e12 flop of SURVEY.md §8(d) (A G + LU + solves + G Y; G generation is timed but not
+    counted).  Inputs resident in HBM; A (512 MiB) and G (512 MiB) exceed the 126 MB L2.
+  * `batched` — config 2: 4096 systems of n = 64 with circulant +-1 multipliers (solves/s).
+  * `e2e` — the same config-3 solve through the public host-pointer C-ABI call
+    (rl_randomized_genp_ex) from pinned host buffers: H2D of A and B, D2H of X inside the timed
+    region.
+One process per GPU; for N > 1 (torchrun) every rank runs an independent replica of the
+config-3 solve (the path does not shard: "replicas only") and its own 4096-system
+batch (weak scaling); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 TFLOP/s precond+GENP at n=8192; batched n=64 solves/s; % of roofline"
+N3, NRHS3 = 8192, 16
+FLOPS3 = 2 * N3 ** 3 + 2 * N3 ** 3 / 3 + 2 * N3 ** 2 * NRHS3 + 2 * N3 ** 2 * NRHS3   # 1.4704e12
+BATCH2, N2 = 4096, 64
+FLOPS2_PER_SYS = 445035      # circulant signed sums + LU + solves + C y
+BYTES2_PER_SYS = 33800
+SEED = 20260825
+
+
+# ----------------------------------------------------------------- helpers ----
+def shard_range(total: int, rank: int, world: int):
+    """Contiguous block of [0, total) owned by `rank` (independent units, no collective)."""
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def max_over_ranks(value: float, dist) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_config3_inputs(torch, dev):
+    """A = U diag(sigma) V^T-like test matrix of config 3, built once on the GPU (not timed).
+
+    Construction: A = Q1 diag(sigma) Q2^T with Q1, Q2 the Q
+    factors of seeded Gaussians (torch's QR on device, input construction only), sigma log-spaced
+    1 .. 1e-6, then the leading 4096^2 block replaced by P Q (4096 x 4095 times 4095 x 4096), with
+    the Gaussians drawn from the reference's own streams by the library (bit-exact draws).
+    """
+    import paper_1212_4560_b200 as rl
+    n, h = N3, N3 // 2
+    g1 = torch.empty(n, n, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(g1, 0.0, 1.0, rl.RngStream(SEED, 31))
+    q1, _ = torch.linalg.qr(g1)
+    rl.dev_gaussian_matrix(g1, 0.0, 1.0, rl.RngStream(SEED, 32))
+    q2, _ = torch.linalg.qr(g1)
+    sig = torch.logspace(0, -6, n, dtype=torch.float64, device=dev)
+    A = (q1 * sig) @ q2.T
+    del q1, q2
+    P = torch.empty(h, h - 1, dtype=torch.float64, device=dev)
+    Q = torch.empty(h - 1, h, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(P, 0.0, 1.0, rl.RngStream(SEED, 33))
+    rl.dev_gaussian_matrix(Q, 0.0, 1.0, rl.RngStream(SEED, 34))
+    A[:h, :h] = P @ Q
+    Xt = torch.empty(n, NRHS3, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(Xt, 0.0, 1.0, rl.RngStream(SEED, 35))
+    B = A @ Xt
+    del g1, P, Q
+    torch.cuda.synchronize()
+    return A.contiguous(), B.contiguous()
+
+
+def make_config2_inputs(torch, dev, batch):
+    import paper_1212_4560_b200 as rl
+    n = N2
+    A = torch.empty(batch, n, n, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(A.view(batch * n, n), 0.0, 1.0, rl.RngStream(SEED, 41))
+    P = torch.empty(batch, 32, 31, dtype=torch.float64, device=dev)
+    Q = torch.empty(batch, 31, 32, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(P.view(batch * 32, 31), 0.0, 1.0, rl.RngStream(SEED, 42))
+    rl.dev_gaussian_matrix(Q.view(batch * 31, 32), 0.0, 1.0, rl.RngStream(SEED, 43))
+    A[:, :32, :32] = torch.bmm(P, Q)
+    xt = torch.empty(batch, n, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(xt, 0.0, 1.0, rl.RngStream(SEED, 44))
+    b = torch.bmm(A, xt.unsqueeze(2)).squeeze(2).contiguous()
+    sids = torch.arange(batch, dtype=torch.int64, device=dev) + 7
+    torch.cuda.synchronize()
+    return A.contiguous(), b, sids
+
+
+def load_profile_traffic():
+    """Per-launch DRAM traffic of the dominant kernel from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+# ------------------------------------------------------------------ our arm ----
+def run_ours(args, dist, rank, world, local_rank):
+    import torch
+    import paper_1212_4560_b200 as rl
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    rl.lib().rl_init(local_rank)
+    fp64_peak, hbm_peak = rl.probe_peaks()
+
+    kind = rl.MultiplierKind(rl.MultiplierTag.GAUSSIAN)
+    A, B = make_config3_inputs(torch, dev)
+    X = torch.empty_like(B)
+    stream = rl.RngStream(SEED, 11)
+
+    def step3():
+        return rl.dev_randomized_genp(A, B, X, kind, rl.MulSide.RIGHT, 0, stream, skip_raw_arm=True)
+
+    for _ in range(args.warmup):
+        rep = step3()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = rl.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            rep = step3()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = rl.launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        dist.barrier()
+    ms = max_over_ranks(ms, dist)
+    value = world * FLOPS3 / (ms * 1e-3) / 1e12
+
+    # backward error of the last solve, computed on the device (reported, not timed)
+    res = (A @ X - B)
+    bwd = float((res.norm(dim=0) / (A.norm() * X.norm(dim=0))).max())
+
+    # dominant kernel: the A G DGEMM (2 n^3 flop per launch), timed alone on the same stream
+    G = torch.empty(N3, N3, dtype=torch.float64, device=dev)
+    AG = torch.empty_like(G)
+    rl.dev_gaussian_matrix(G, 0.0, 1.0, rl.RngStream(SEED, 11 ^ 0x5000000000000000))
+    for _ in range(2):
+        rl.dev_gemm(A, G, AG)
+    torch.cuda.synchronize()
+    e0.record()
+    reps = 5
+    for _ in range(reps):
+        rl.dev_gemm(A, G, AG)
+    e1.record()
+    torch.cuda.synchronize()
+    gemm_ms = e0.elapsed_time(e1) / reps
+    gemm_tf = 2 * N3 ** 3 / (gemm_ms * 1e-3) / 1e12
+    # RNG stage alone (reported separately: not in the flop count)
+    torch.cuda.synchronize()
+    e0.record()
+    rl.dev_gaussian_matrix(G, 0.0, 1.0, rl.RngStream(SEED, 11 ^ 0x5000000000000000))
+    e1.record()
+    torch.cuda.synchronize()
+    rng_ms = e0.elapsed_time(e1)
+    del G, AG
+
+    # ---- e2e: public host-pointer call from pinned host memory ----
+    L = rl.lib()
+    L.rl_randomized_genp_ex.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                        C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p,
+                                        C.c_void_p, C.c_uint32]
+    L.rl_randomized_genp_ex.restype = C.c_int
+    hA = A.cpu().pin_memory()
+    hB = B.cpu().pin_memory()
+    hX = torch.empty_like(hB).pin_memory()
+    rl.lib().rl_set_stream(None)
+
+    def step_e2e():
+        st = L.rl_randomized_genp_ex(N3, NRHS3, hA.data_ptr(), hB.data_ptr(), 0, 0.0, 1.0, 1, 0, SEED, 11,
+                                     hX.data_ptr(), None, 1)
+        if st != 0:
+            raise RuntimeError(rl.lib().rl_last_error().decode())
+
+    step_e2e()
+    if dist:
+        dist.barrier()
+    e2e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_e2e()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    e2e_ms = max_over_ranks(e2e_ms, dist)
+    e2e_value = world * FLOPS3 / (e2e_ms * 1e-3) / 1e12
+    del hA, hB, hX
+
+    # ---- config 2: batched n = 64 circulant +-1 (secondary line) ----
+    A2, b2, sids = make_config2_inputs(torch, dev, BATCH2)
+    x2 = torch.empty_like(b2)
+    ckind = rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN)
+
+    def step2():
+        rl.dev_randomized_genp_batched(A2, b2, x2, ckind, rl.MulSide.RIGHT, 0, SEED, sids)
+
+    for _ in range(max(args.warmup, 3)):
+        step2()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    k2 = max(args.steps, 10)
+    e0.record()
+    for _ in range(k2):
+        step2()
+    e1.record()
+    torch.cuda.synchronize()
+    ms2 = max_over_ranks(e0.elapsed_time(e1) / k2, dist)
+    solves_s = world * BATCH2 / (ms2 * 1e-3)
+    res2 = torch.bmm(A2, x2.unsqueeze(2)).squeeze(2) - b2
+    bwd2 = float((res2.norm(dim=1) / (A2.flatten(1).norm(dim=1) * x2.norm(dim=1))).max())
+    fp64_frac2 = BATCH2 * FLOPS2_PER_SYS / (ms2 * 1e-3) / 1e12 / fp64_peak
+    hbm_frac2 = BATCH2 * BYTES2_PER_SYS / (ms2 * 1e-3) / 1e9 / hbm_peak
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_config3(threads=1)
+
+    prof = load_profile_traffic()
+    traffic = prof.get("dgemm_dram_bytes_per_launch")
+    line = {
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded; reference RNG streams)",
+        "config": {"workload": "config3: Gaussian-preconditioned GENP n=8192, 16 RHS, MulSide::Right, block 128",
+                   "n": N3, "nrhs": NRHS3, "flop_per_step": FLOPS3, "parallelism": f"replicas{world}",
+                   "l2": "inputs larger than L2 (A, G 512 MiB each)",
+                   "backward_error_max": bwd, "residual": rep.residual, "attempt": rep.attempt,
+                   "rng_ms_per_G": round(rng_ms, 3)},
+        "roofline": {"bound": "tensor", "kernel": "k_dgemm (A G, DMMA m8n8k4 f64)",
+                     "achieved": round(gemm_tf, 3), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
+                     "frac": round(gemm_tf / fp64_peak, 4), "traffic": traffic,
+                     "peak_source": "same-run FP64 DMMA probe (rl_probe_peaks; MEASURED_PEAKS.json has no fp64)",
+                     "step_frac_of_fp64_peak": round(FLOPS3 / (ms * 1e-3) / 1e12 / fp64_peak, 4)},
+        "e2e": {"value": round(e2e_value, 4), "unit": "TFLOP/s",
+                "h2d_bytes_per_step": 8 * (N3 * N3 + N3 * NRHS3), "d2h_bytes_per_step": 8 * N3 * NRHS3,
+                "ms_per_step": round(e2e_ms, 3), "call": "rl_randomized_genp_ex (host pointers, pinned)"},
+        "gpu_launches": launches,
+        "batched": {"workload": "config2: 4096 x n=64, circulant +-1, MulSide::Right, redraw protocol",
+                    "value": round(solves_s, 1), "unit": "solves/s", "ms_per_step": round(ms2, 4),
+                    "backward_error_max": bwd2,
+                    "roofline": {"bound": "fp64", "frac_fp64": round(fp64_frac2, 4),
+                                 "frac_hbm": round(hbm_frac2, 4), "peak_fp64": round(fp64_peak, 3),
+                                 "peak_hbm_gbs": round(hbm_peak, 1)}},
+        "clocks": clocks.summary(),
+        "peaks_same_run": {"fp64_dmma_tflops": round(fp64_peak, 3), "hbm_copy_gbs": round(hbm_peak, 1)},
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    return line
+
+
+# ------------------------------------------------------- CPU baseline legs ----
+def cpu_baseline_config3(threads: int = 1):
+    """The reference's own CPU code (oracle/_ref, compiled from /root/reference) on a bounded
+    sample of the config-3 work: Matrix::multiply of a row slab of A (rows split over
+    `threads` threads, each a reference call) against the full 8192^2 G, plus one genp_factor
+    (the reference's LU is single-threaded) at n = 1024.  value = sample flop / sample time."""
+    from oracle.pyoracle import Reference, Restated
+    kind = "reference" if Reference.available() else "port"
+    lib = Reference() if kind == "reference" else Restated()
+    rng = np.random.default_rng(0)
+    G = rng.standard_normal((N3, N3))
+    rows_per = 8
+    slabs = [rng.standard_normal((rows_per, N3)) for _ in range(threads)]
+    t0 = time.perf_counter()
+    ts = [threading.Thread(target=lib.matmul, args=(s, G)) for s in slabs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    t_mm = time.perf_counter() - t0
+    f_mm = 2.0 * rows_per * threads * N3 * N3
+    nl = 1024
+    M = rng.standard_normal((nl, nl)) + nl * np.eye(nl)
+    t0 = time.perf_counter()
+    lib.genp_factor(M, 0.0)
+    t_lu = time.perf_counter() - t0
+    f_lu = 2.0 * nl ** 3 / 3
+    value = (f_mm + f_lu) / (t_mm + t_lu) / 1e12
+    return {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": kind,
+            "sample": f"Matrix::multiply {rows_per * threads}x{N3} slab x {N3}^2 G ({threads} thread(s)) "
+                      f"+ genp_factor n={nl} (1 thread); {t_mm + t_lu:.2f} s",
+            "host": _host_cpu()}
+
+
+def _host_cpu():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = next((l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")), "?")
+    except OSError:
+        model = "?"
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU implementation of the path on the host cores."""
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_baseline_config3(threads)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline_config3(threads))
+    wall = time.perf_counter() - t0
+    v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "config3 (bounded CPU sample, see cpu_baseline.sample)",
+                                             "n": N3, "nrhs": NRHS3},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, dist, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,10 @@ rl_status rl_dev_genp_solve_packed(uint64_t n, uint64_t nrhs, const double* d_lu
 rl_status rl_randomized_genp(uint64_t n, uint64_t nrhs, const double* a, const double* b, int tag,
                              double mu, double sigma, int side, int refine, uint64_t seed,
                              uint64_t stream_id, double* x, rl_precond_report* report);
+rl_status rl_randomized_genp_ex(uint64_t n, uint64_t nrhs, const double* a, const double* b,
+                                int tag, double mu, double sigma, int side, int refine,
+                                uint64_t seed, uint64_t stream_id, double* x,
+                                rl_precond_report* report, uint32_t flags);
 rl_status rl_dev_randomized_genp(uint64_t n, uint64_t nrhs, const double* d_a, const double* d_b,
                                  int tag, double mu, double sigma, int side, int refine,
                                  uint64_t seed, uint64_t stream_id, double* d_x,

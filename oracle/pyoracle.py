@@ -230,6 +230,7 @@ class Reference:
         L.rlref_illblock_system.argtypes = [u64, u64, u64, _d, _d, _d]
         L.rlref_qr_positive.argtypes = [u64, u64, _d, _d, _d]
         L.rlref_singular_values.argtypes = [u64, u64, _d, _d]
+        L.rlref_profile_matrix_paper.argtypes = [u64, u64, u64, u64, _d]
 
     def _chk(self, code, where):
         if code != 0:
@@ -323,6 +324,11 @@ class Reference:
         a, b, y = np.empty((n, n)), np.empty(n), np.empty(n)
         self._chk(self.lib.rlref_illblock_system(n, seed, sid, a, b, y), "illblock_system")
         return a, b, y
+
+    def profile_matrix_paper(self, n, rho, seed, sid):
+        out = np.empty((n, n))
+        self._chk(self.lib.rlref_profile_matrix_paper(n, rho, seed, sid, out), "profile_matrix")
+        return out
 
     def qr_positive(self, a):
         m, n = a.shape

@@ -260,3 +260,14 @@ int rlref_singular_values(uint64_t m, uint64_t n, const double* a, double* sigma
 }
 
 } // extern "C"
+
+extern "C" int rlref_profile_matrix_paper(uint64_t n, uint64_t rho, uint64_t seed, uint64_t sid, double* out) {
+    try {
+        auto s = randla::rnd::paper_sigma_profile(n, rho);
+        auto m = randla::rnd::profile_matrix(n, s, randla::rnd::RngStream{seed, sid});
+        std::memcpy(out, m.data().data(), n * n * sizeof(double));
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+    return 0;
+}

@@ -423,12 +423,18 @@ rl_status rl_dev_randomized_genp(uint64_t n, uint64_t nrhs, const double* d_a, c
 rl_status rl_randomized_genp(uint64_t n, uint64_t nrhs, const double* a, const double* b, int tag, double mu,
                              double sigma, int side, int refine, uint64_t seed, uint64_t sid, double* x,
                              rl_precond_report* report) {
+    return rl_randomized_genp_ex(n, nrhs, a, b, tag, mu, sigma, side, refine, seed, sid, x, report, 0);
+}
+
+rl_status rl_randomized_genp_ex(uint64_t n, uint64_t nrhs, const double* a, const double* b, int tag, double mu,
+                                double sigma, int side, int refine, uint64_t seed, uint64_t sid, double* x,
+                                rl_precond_report* report, uint32_t flags) {
     API_BEGIN
     require_positive(n, nrhs, "randomized_genp");
     double* da = upload(WS_H0, a, n * n);
     double* db = upload(WS_H1, b, n * nrhs);
     double* dx = ws<double>(WS_H2, n * nrhs);
-    rl_status s = randomized_genp_dev(n, nrhs, da, db, tag, mu, sigma, side, refine, seed, sid, dx, report, 0);
+    rl_status s = randomized_genp_dev(n, nrhs, da, db, tag, mu, sigma, side, refine, seed, sid, dx, report, flags);
     if (s != RL_OK)
         return s;
     download(x, dx, n * nrhs);

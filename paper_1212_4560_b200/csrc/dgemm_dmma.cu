@@ -103,8 +103,8 @@ struct Cfg {
     static constexpr size_t kSmem = static_cast<size_t>(NSTAGE) * kStageElems * sizeof(double);
 };
 
-template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE>
-__global__ void __launch_bounds__(WM* WN * 32, 1)
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1>
+__global__ void __launch_bounds__(WM* WN * 32, MINB)
     k_dgemm(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* __restrict__ A,
             uint64_t lda, const double* __restrict__ B, uint64_t ldb, double beta,
             double* __restrict__ C, uint64_t ldc) {
@@ -199,11 +199,11 @@ __global__ void __launch_bounds__(WM* WN * 32, 1)
     }
 }
 
-template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE>
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1>
 void launch(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda,
             const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
     using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE>;
-    auto kern = k_dgemm<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE>;
+    auto kern = k_dgemm<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, MINB>;
     static bool configured[16] = {};
     int dev = ctx().device & 15;
     if (!configured[dev]) {
@@ -221,7 +221,11 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const doub
                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
     const int sms = ctx().sms;
     uint64_t big_tiles = static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 128);
-    if (N > 64 && big_tiles >= static_cast<uint64_t>(sms))
+    if (K <= 256 && N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms)
+        // short-K rank updates (the GENP Schur complement): two CTAs per SM so one CTA's
+        // C read-modify-write epilogue overlaps the other's DMMA main loop
+        launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else if (N > 64 && big_tiles >= static_cast<uint64_t>(sms))
         launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     else if (N > 32)
         launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);

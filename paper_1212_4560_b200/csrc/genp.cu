@@ -15,6 +15,7 @@
 //   Schur       A22 -= L21 U12, the (n-o)^2 x 128 DMMA GEMM that carries ~2n^3/3.
 // Without pivoting the panel is embarrassingly parallel: there is no tall
 // sequential panel factorisation on the critical path.
+#include "panel.cuh"
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -22,309 +23,296 @@ namespace rl {
 namespace {
 
 constexpr int NB = 128;        // block size (config 3's "Block size 128")
-constexpr int DIAG_THREADS = 1024;
 
-// One CTA per diagonal block.  mode 1: factor the bs x bs block at (o, o) in place
-// (reference loop order, genp.cpp:20-33), write |pivots|, flag breakdown; then (both
-// modes) invert L11 (unit lower) and U11 in place in shared memory and store them to
-// aux as [Linv NB x NB][Uinv NB x NB].  mode 0: the block is already factored; CTA b
-// handles the diagonal block at o = b*NB (all blocks of a packed LU at once).
-__global__ void __launch_bounds__(DIAG_THREADS) k_diag_lu(double* a, uint64_t lda, uint64_t n,
-                                                          uint64_t o_first, double floor,
-                                                          double* pivots,
-                                                          unsigned long long* breakdown,
-                                                          double* aux, int mode) {
-    extern __shared__ double w[]; // NB x (NB+1)
-    __shared__ double col[NB];
-    constexpr int P = NB + 1;
-    const int tid = threadIdx.x;
-    const uint64_t o = o_first + static_cast<uint64_t>(blockIdx.x) * NB;
+// ------------------------------------------------------------ panel kernels ----
+// All three use the two-level scheme of panel.cuh: 16-wide sub-panels, per-thread
+// 16-step substitutions out of registers, DMMA updates between shared-memory tiles.
+using panel::PT;
+using panel::SB;
+constexpr int PK_THREADS = 256; // 8 warps
+constexpr int PK_WARPS = PK_THREADS / 32;
+
+// Diagonal-block LU of the bs x bs block at (o, o), in place (genp.cpp:20-33 order
+// within each 16-column sub-panel; the sub-panel's effect on the rest is a DMMA update).
+// Rows/columns beyond bs are padded with the identity so every tile is 128 x 128.
+//   per sub-panel c0:  (1) warp 0 factors the 16x16 diagonal sub-block (lanes own rows,
+//   pivot rows broadcast through shared memory, __syncwarp only); (2) every row below
+//   solves its 16 L entries against that U (independent rows, no sync); (3) every column
+//   right of it solves its 16 U entries against that unit L; (4) DMMA trailing update.
+// |pivots| and the first step with |p| < floor are recorded; 1/p := 0 when p == 0 gives
+// the reference's multiplier 0 (genp.cpp:27).
+__global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t lda, uint64_t n, uint64_t o,
+                                                           double floor, double* pivots,
+                                                           unsigned long long* breakdown) {
+    extern __shared__ double W[]; // NB x PT
+    __shared__ double rcp[NB];
+    __shared__ double prow[SB];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
-    double* ablk = a + o * lda + o;
-    for (int e = tid; e < bs * bs; e += DIAG_THREADS) {
-        int i = e / bs, j = e % bs;
-        w[i * P + j] = ablk[static_cast<uint64_t>(i) * lda + j];
-    }
+    double* blk = a + o * lda + o;
+    panel::load_tile<NB, NB, PK_THREADS>(W, PT, blk, lda, bs, bs, [](int, int) { return true; },
+                                         [](int i, int j) { return i == j ? 1.0 : 0.0; });
     __syncthreads();
-    if (mode == 1) {
-        for (int k = 0; k < bs; ++k) {
-            const double p = w[k * P + k];
-            if (tid == 0) {
-                pivots[o + k] = fabs(p);
-                if (fabs(p) < floor)
-                    atomicMin(breakdown, static_cast<unsigned long long>(o + k));
+    for (int c0 = 0; c0 < NB; c0 += SB) {
+        // (1) 16x16 diagonal sub-block, warp 0, lanes 0..15 own its rows
+        if (warp == 0) {
+            double p[SB];
+            const int r = c0 + (lane & (SB - 1));
+#pragma unroll
+            for (int l = 0; l < SB; ++l)
+                p[l] = W[r * PT + c0 + l];
+#pragma unroll
+            for (int kk = 0; kk < SB; ++kk) {
+                if (lane == kk) {
+#pragma unroll
+                    for (int l = 0; l < SB; ++l)
+                        prow[l] = p[l];
+                }
+                __syncwarp();
+                const double piv = prow[kk];
+                const double inv = (piv == 0.0) ? 0.0 : 1.0 / piv;
+                if (lane == 0) {
+                    const int k = c0 + kk;
+                    if (k < bs) {
+                        pivots[o + k] = fabs(piv);
+                        if (fabs(piv) < floor)
+                            atomicMin(breakdown, static_cast<unsigned long long>(o + k));
+                    }
+                    rcp[k] = inv;
+                }
+                if (lane < SB && lane > kk) {
+                    const double m = p[kk] * inv;
+                    p[kk] = m;
+                    if (m != 0.0)
+#pragma unroll
+                        for (int l = kk + 1; l < SB; ++l)
+                            p[l] = fma(-m, prow[l], p[l]);
+                }
+                __syncwarp();
             }
-            // multipliers m = w(i,k)/p, 0 when p == 0 (genp.cpp:26-28)
-            for (int i = k + 1 + tid; i < bs; i += DIAG_THREADS)
-                w[i * P + k] = (p == 0.0) ? 0.0 : w[i * P + k] / p;
-            __syncthreads();
-            const int rem = bs - k - 1;
-            for (int e = tid; e < rem * rem; e += DIAG_THREADS) {
-                int i = k + 1 + e / rem, j = k + 1 + e % rem;
-                double m = w[i * P + k];
-                if (m != 0.0)
-                    w[i * P + j] -= m * w[k * P + j];
+            if (lane < SB)
+#pragma unroll
+                for (int l = 0; l < SB; ++l)
+                    W[r * PT + c0 + l] = p[l];
+        }
+        __syncthreads();
+        const int rest = NB - c0 - SB;
+        if (rest == 0)
+            break;
+        // (2) rows below: l_r U_sub = w_r   (x_j = (w_j - sum_{l<j} x_l U_lj) / U_jj)
+        for (int t = tid; t < rest; t += PK_THREADS) {
+            const int r = c0 + SB + t;
+            double x[SB];
+#pragma unroll
+            for (int l = 0; l < SB; ++l)
+                x[l] = W[r * PT + c0 + l];
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+                const double xj = x[j] * rcp[c0 + j];
+                x[j] = xj;
+                if (xj != 0.0)
+#pragma unroll
+                    for (int l = j + 1; l < SB; ++l)
+                        x[l] = fma(-xj, W[(c0 + j) * PT + c0 + l], x[l]);
             }
-            __syncthreads();
+#pragma unroll
+            for (int l = 0; l < SB; ++l)
+                W[r * PT + c0 + l] = x[l];
         }
-        for (int e = tid; e < bs * bs; e += DIAG_THREADS) {
-            int i = e / bs, j = e % bs;
-            ablk[static_cast<uint64_t>(i) * lda + j] = w[i * P + j];
+        // (3) columns right: L_sub y = w  (unit lower)
+        for (int t = tid; t < rest; t += PK_THREADS) {
+            const int c = c0 + SB + t;
+            double y[SB];
+#pragma unroll
+            for (int i = 0; i < SB; ++i)
+                y[i] = W[(c0 + i) * PT + c];
+#pragma unroll
+            for (int i = 1; i < SB; ++i)
+#pragma unroll
+                for (int l = 0; l < i; ++l)
+                    y[i] = fma(-W[(c0 + i) * PT + c0 + l], y[l], y[i]);
+#pragma unroll
+            for (int i = 1; i < SB; ++i)
+                W[(c0 + i) * PT + c] = y[i];
         }
+        __syncthreads();
+        // (4) trailing 128-c0-16 square: W22 -= L21 U12
+        panel::smem_update16(W + (c0 + SB) * PT + c0 + SB, PT, W + (c0 + SB) * PT + c0, PT, W + c0 * PT + c0 + SB,
+                             PT, rest, rest, warp, PK_WARPS, lane);
+        __syncthreads();
     }
-    if (!aux)
-        return;
-    double* linv = aux + (o / NB) * 2 * NB * NB;
-    double* uinv = linv + NB * NB;
-    // inv(L) in place (strict lower; unit diagonal implicit), steps k ascending:
-    //   Y[i][k] = -L[i][k],  Y[i][j] -= L[i][k] Y[k][j]  (i > k, j < k)
-    for (int k = 0; k < bs; ++k) {
-        __syncthreads();
-        for (int i = k + 1 + tid; i < bs; i += DIAG_THREADS)
-            col[i] = w[i * P + k];
-        __syncthreads();
-        const int rows = bs - k - 1;
-        for (int e = tid; e < rows * (k + 1); e += DIAG_THREADS) {
-            int i = k + 1 + e / (k + 1), j = e % (k + 1);
-            double l = col[i];
-            w[i * P + j] = (j == k) ? -l : w[i * P + j] - l * w[k * P + j];
-        }
-    }
-    // inv(U) in place (upper incl. diagonal), steps k descending:
-    //   X[k][k] = 1/U[k][k], X[k][j] *= X[k][k] (j > k); X[i][k] = -U[i][k] X[k][k],
-    //   X[i][j] -= U[i][k] X[k][j]  (i < k, j > k).  1/0 := 0 (genp.cpp:27 convention).
-    for (int k = bs - 1; k >= 0; --k) {
-        __syncthreads();
-        const double d = w[k * P + k];
-        const double r = (d == 0.0) ? 0.0 : 1.0 / d;
-        for (int i = tid; i < k; i += DIAG_THREADS)
-            col[i] = w[i * P + k];
-        __syncthreads();
-        for (int j = k + tid; j < bs; j += DIAG_THREADS)
-            w[k * P + j] = (j == k) ? r : w[k * P + j] * r;
-        __syncthreads();
-        const int cols = bs - k;
-        for (int e = tid; e < k * cols; e += DIAG_THREADS) {
-            int i = e / cols, j = k + e % cols;
-            double u = col[i];
-            w[i * P + j] = (j == k) ? -u * w[k * P + k] : w[i * P + j] - u * w[k * P + j];
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < NB * NB; e += DIAG_THREADS) {
-        int i = e / NB, j = e % NB;
-        bool in = i < bs && j < bs;
-        linv[e] = !in ? 0.0 : (i == j ? 1.0 : (i > j ? w[i * P + j] : 0.0));
-        uinv[e] = !in ? 0.0 : (j >= i ? w[i * P + j] : 0.0);
-    }
+    panel::store_tile<NB, NB, PK_THREADS>(blk, lda, W, PT, bs, bs);
 }
 
-
-// ---------------------------------------------------------------- TRSM ----
-// Substitution-based triangular solves on 128-wide panels (backward stable, like the
-// reference's block_ge L21/U12 loops, genp.cpp:77-92).  The triangle sits in shared
-// memory; every warp owns independent rows (right solve) or columns (left solve) in
-// registers, so after the initial load there is no CTA-wide synchronisation: the
-// sequential chain is per warp, broadcasts are __shfl_sync.
-constexpr int TR_WARPS = 16;            // 512 threads
-constexpr int TR_TILE = 64;             // rows (right) or columns (left) per CTA
-constexpr int TR_PER_WARP = TR_TILE / TR_WARPS; // 4
-constexpr int TP = NB + 1;              // smem pitch of the triangle
-
-// Right solve with U11 (upper, non-unit): rows x of A21 satisfy x U11 = a,
-//   x_j = (a_j - sum_{l<j} x_l U_lj) / U_jj      (L21 = A21 U11^-1)
-// Left solve with L11 (unit lower): columns y of A12 satisfy L11 y = a,
-//   y_i = a_i - sum_{l<i} L_il y_l              (U12 = L11^-1 A12)
-// One launch does both: CTAs [0, nrb) take 64-row blocks of A21, the rest take
-// 64-column blocks of A12.  rest = n - o - bs rows/cols, bs = NB here.
-__global__ void __launch_bounds__(TR_WARPS * 32, 1) k_panel_trsm(double* a, uint64_t lda, uint64_t o,
-                                                                 uint64_t rest, int nrb) {
+// Panel TRSMs of block step o (genp.cpp:77-92), in place, one launch:
+//   CTAs [0, nrb):      64-row tiles of A21 <- A21 U11^-1   (x U11 = a)
+//   CTAs [nrb, 2 nrb2): 64-column tiles of A12 <- L11^-1 A12 (L11 y = a, unit lower)
+// Each sub-panel: per-thread 16-step substitution, then a DMMA update of the remaining
+// columns (right) / rows (left) of the tile.
+constexpr int TR_TILE = 64;
+__global__ void __launch_bounds__(PK_THREADS, 1) k_panel_trsm(double* a, uint64_t lda, uint64_t o, uint64_t rest,
+                                                              int nrb) {
     extern __shared__ double smt[];
-    double* T = smt;                 // NB x TP triangle
-    double* tile = smt + NB * TP;    // right: 64 x TP ; left: NB x (64+1)
+    double* T = smt;            // NB x PT triangle
+    double* X = smt + NB * PT;  // right: 64 x PT ; left: NB x (64 + 4)
+    __shared__ double rcp[NB];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool right = static_cast<int>(blockIdx.x) < nrb;
     const double* diag = a + o * lda + o;
-    for (int e = tid; e < NB * NB; e += blockDim.x) {
-        int i = e / NB, j = e % NB;
-        bool want = right ? (j >= i) : (i > j);
-        T[i * TP + j] = want ? diag[static_cast<uint64_t>(i) * lda + j] : 0.0;
-    }
+    if (right)
+        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return j >= i; },
+                                             [](int, int) { return 0.0; });
+    else
+        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return i > j; },
+                                             [](int, int) { return 0.0; });
     if (right) {
         const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * TR_TILE;
         const int nr = static_cast<int>(rest - r0 < TR_TILE ? rest - r0 : TR_TILE);
         double* src = a + (o + NB + r0) * lda + o;
-        for (int e = tid; e < nr * NB; e += blockDim.x) {
-            int i = e / NB, j = e % NB;
-            tile[i * TP + j] = src[static_cast<uint64_t>(i) * lda + j];
+        panel::load_tile<TR_TILE, NB, PK_THREADS>(X, PT, src, lda, nr, NB, [](int, int) { return true; },
+                                                  [](int, int) { return 0.0; });
+        __syncthreads();
+        for (int j = tid; j < NB; j += PK_THREADS) {
+            const double d = T[j * PT + j];
+            rcp[j] = (d == 0.0) ? 0.0 : 1.0 / d;
         }
         __syncthreads();
-        // warp owns rows warp*4 .. +3 ; lane owns columns lane + 32c
-        double w[TR_PER_WARP][4];
+        for (int c0 = 0; c0 < NB; c0 += SB) {
+            for (int r = tid; r < TR_TILE; r += PK_THREADS) {
+                double x[SB];
 #pragma unroll
-        for (int r = 0; r < TR_PER_WARP; ++r)
+                for (int l = 0; l < SB; ++l)
+                    x[l] = X[r * PT + c0 + l];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                int row = warp * TR_PER_WARP + r;
-                w[r][c] = row < nr ? tile[row * TP + lane + 32 * c] : 0.0;
-            }
-        for (int j = 0; j < NB; ++j) {
-            const double d = T[j * TP + j];
-            const double rcp = (d == 0.0) ? 0.0 : 1.0 / d; // multiplier 0 when p == 0 (genp.cpp:27)
-            const int cj = j >> 5, lj = j & 31;
-            double x[TR_PER_WARP];
+                for (int j = 0; j < SB; ++j) {
+                    const double xj = x[j] * rcp[c0 + j];
+                    x[j] = xj;
+                    if (xj != 0.0)
 #pragma unroll
-            for (int r = 0; r < TR_PER_WARP; ++r) {
-                double mine = 0.0;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (c == cj)
-                        mine = w[r][c];
-                x[r] = __shfl_sync(0xffffffffu, mine, lj) * rcp;
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int col = lane + 32 * c;
-                if (col == j) {
-#pragma unroll
-                    for (int r = 0; r < TR_PER_WARP; ++r)
-                        w[r][c] = x[r];
-                } else if (col > j) {
-                    const double u = T[j * TP + col];
-#pragma unroll
-                    for (int r = 0; r < TR_PER_WARP; ++r)
-                        if (x[r] != 0.0)
-                            w[r][c] = fma(-x[r], u, w[r][c]);
+                        for (int l = j + 1; l < SB; ++l)
+                            x[l] = fma(-xj, T[(c0 + j) * PT + c0 + l], x[l]);
                 }
+#pragma unroll
+                for (int l = 0; l < SB; ++l)
+                    X[r * PT + c0 + l] = x[l];
             }
+            __syncthreads();
+            if (c0 + SB < NB)
+                panel::smem_update16(X + c0 + SB, PT, X + c0, PT, T + c0 * PT + c0 + SB, PT, TR_TILE,
+                                     NB - c0 - SB, warp, PK_WARPS, lane);
+            __syncthreads();
         }
-        double* dst = a + (o + NB + r0) * lda + o;
-#pragma unroll
-        for (int r = 0; r < TR_PER_WARP; ++r) {
-            int row = warp * TR_PER_WARP + r;
-            if (row < nr)
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    dst[static_cast<uint64_t>(row) * lda + lane + 32 * c] = w[r][c];
-        }
+        panel::store_tile<TR_TILE, NB, PK_THREADS>(src, lda, X, PT, nr, NB);
     } else {
-        constexpr int CP = TR_TILE + 1;
-        const uint64_t c0 = static_cast<uint64_t>(blockIdx.x - nrb) * TR_TILE;
-        const int nc = static_cast<int>(rest - c0 < TR_TILE ? rest - c0 : TR_TILE);
-        double* src = a + o * lda + o + NB + c0;
-        for (int e = tid; e < NB * TR_TILE; e += blockDim.x) {
-            int i = e / TR_TILE, j = e % TR_TILE;
-            tile[i * CP + j] = j < nc ? src[static_cast<uint64_t>(i) * lda + j] : 0.0;
-        }
+        constexpr int XP = TR_TILE + 4;
+        const uint64_t c0g = static_cast<uint64_t>(blockIdx.x - nrb) * TR_TILE;
+        const int nc = static_cast<int>(rest - c0g < TR_TILE ? rest - c0g : TR_TILE);
+        double* src = a + o * lda + o + NB + c0g;
+        panel::load_tile<NB, TR_TILE, PK_THREADS>(X, XP, src, lda, NB, nc, [](int, int) { return true; },
+                                                  [](int, int) { return 0.0; });
         __syncthreads();
-        // warp owns columns warp*4 .. +3 ; lane owns rows lane + 32c
-        double w[TR_PER_WARP][4];
+        for (int c0 = 0; c0 < NB; c0 += SB) {
+            for (int c = tid; c < TR_TILE; c += PK_THREADS) {
+                double y[SB];
 #pragma unroll
-        for (int q = 0; q < TR_PER_WARP; ++q)
+                for (int i = 0; i < SB; ++i)
+                    y[i] = X[(c0 + i) * XP + c];
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                w[q][c] = tile[(lane + 32 * c) * CP + warp * TR_PER_WARP + q];
-        for (int i = 0; i < NB; ++i) {
-            const int ci = i >> 5, li = i & 31;
-            double y[TR_PER_WARP];
+                for (int i = 1; i < SB; ++i)
 #pragma unroll
-            for (int q = 0; q < TR_PER_WARP; ++q) {
-                double mine = 0.0;
+                    for (int l = 0; l < i; ++l)
+                        y[i] = fma(-T[(c0 + i) * PT + c0 + l], y[l], y[i]);
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (c == ci)
-                        mine = w[q][c];
-                y[q] = __shfl_sync(0xffffffffu, mine, li);
+                for (int i = 1; i < SB; ++i)
+                    X[(c0 + i) * XP + c] = y[i];
             }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int row = lane + 32 * c;
-                if (row > i) {
-                    const double l = T[row * TP + i];
-                    if (l != 0.0)
-#pragma unroll
-                        for (int q = 0; q < TR_PER_WARP; ++q)
-                            w[q][c] = fma(-l, y[q], w[q][c]);
-                }
-            }
+            __syncthreads();
+            if (c0 + SB < NB)
+                panel::smem_update16(X + (c0 + SB) * XP, XP, T + (c0 + SB) * PT + c0, PT, X + c0 * XP, XP,
+                                     NB - c0 - SB, TR_TILE, warp, PK_WARPS, lane);
+            __syncthreads();
         }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < TR_PER_WARP; ++q)
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                tile[(lane + 32 * c) * CP + warp * TR_PER_WARP + q] = w[q][c];
-        __syncthreads();
-        for (int e = tid; e < NB * TR_TILE; e += blockDim.x) {
-            int i = e / TR_TILE, j = e % TR_TILE;
-            if (j < nc)
-                src[static_cast<uint64_t>(i) * lda + j] = tile[i * CP + j];
-        }
+        panel::store_tile<NB, TR_TILE, PK_THREADS>(src, lda, X, XP, NB, nc);
     }
 }
 
-// Solve with one diagonal block of a packed LU on a bs x nrhs panel of B (ld ldb):
-// lower = unit-lower forward substitution, else upper backward substitution with
-// division by U_ii (genp.cpp:110-122).  One CTA; warps own RHS columns.
-__global__ void __launch_bounds__(TR_WARPS * 32, 1) k_block_solve(const double* lu, uint64_t lda, uint64_t o,
-                                                                  int bs, double* b, uint64_t ldb,
-                                                                  uint64_t nrhs, int lower) {
-    extern __shared__ double smt[];
-    double* T = smt; // bs x TP
+// Diagonal-panel substitution of the multi-RHS solves (genp.cpp:106-124) on a bs x nrhs
+// slice of B: lower = unit-lower forward, upper = backward with x_i = s * (1/U_ii)
+// (within 1 ulp of the reference's division).  Blocks beyond bs are padded with the
+// identity; off-diagonal updates outside the 128-block are DMMA GEMMs (host loop).
+constexpr int SV_MAXRHS = 32;
+constexpr int SVP = SV_MAXRHS + 4;
+__global__ void __launch_bounds__(PK_THREADS, 1) k_block_solve(const double* __restrict__ lu, uint64_t lda,
+                                                               uint64_t n, uint64_t o, double* __restrict__ b,
+                                                               uint64_t ldb, int nrhs, int lower) {
+    extern __shared__ double T[]; // NB x PT, then Bs NB x SVP
+    double* Bs = T + NB * PT;
+    __shared__ double rcp[NB];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
     const double* diag = lu + o * lda + o;
-    for (int e = tid; e < bs * bs; e += blockDim.x) {
-        int i = e / bs, j = e % bs;
-        T[i * TP + j] = diag[static_cast<uint64_t>(i) * lda + j];
-    }
+    if (lower)
+        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, bs, bs, [](int i, int j) { return i > j; },
+                                             [](int, int) { return 0.0; });
+    else
+        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, bs, bs, [](int i, int j) { return j >= i; },
+                                             [](int i, int j) { return i == j ? 1.0 : 0.0; });
+    const int n8 = (nrhs + 7) & ~7;
+    panel::load_tile<NB, SV_MAXRHS, PK_THREADS>(Bs, SVP, b + o * ldb, ldb, bs, nrhs, [](int, int) { return true; },
+                                                [](int, int) { return 0.0; });
     __syncthreads();
-    for (uint64_t col = warp; col < nrhs; col += TR_WARPS) {
-        double w[4];
+    if (!lower)
+        for (int i = tid; i < NB; i += PK_THREADS)
+            rcp[i] = 1.0 / T[i * PT + i];
+    __syncthreads();
+    if (lower) {
+        for (int c0 = 0; c0 < NB; c0 += SB) {
+            for (int c = tid; c < nrhs; c += PK_THREADS) {
+                double y[SB];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            int row = lane + 32 * c;
-            w[c] = row < bs ? b[(o + row) * ldb + col] : 0.0;
-        }
-        if (lower) {
-            for (int i = 0; i < bs; ++i) {
-                double mine = 0.0;
+                for (int i = 0; i < SB; ++i)
+                    y[i] = Bs[(c0 + i) * SVP + c];
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (c == (i >> 5))
-                        mine = w[c];
-                const double yi = __shfl_sync(0xffffffffu, mine, i & 31);
+                for (int i = 1; i < SB; ++i)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    int row = lane + 32 * c;
-                    if (row > i && row < bs)
-                        w[c] = fma(-T[row * TP + i], yi, w[c]);
-                }
+                    for (int l = 0; l < i; ++l)
+                        y[i] = fma(-T[(c0 + i) * PT + c0 + l], y[l], y[i]);
+#pragma unroll
+                for (int i = 1; i < SB; ++i)
+                    Bs[(c0 + i) * SVP + c] = y[i];
             }
-        } else {
-            for (int i = bs - 1; i >= 0; --i) {
-                double mine = 0.0;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (c == (i >> 5))
-                        mine = w[c];
-                const double xi = __shfl_sync(0xffffffffu, mine, i & 31) / T[i * TP + i];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    int row = lane + 32 * c;
-                    if (row == i)
-                        w[c] = xi;
-                    else if (row < i)
-                        w[c] = fma(-T[row * TP + i], xi, w[c]);
-                }
-            }
+            __syncthreads();
+            if (c0 + SB < NB)
+                panel::smem_update16(Bs + (c0 + SB) * SVP, SVP, T + (c0 + SB) * PT + c0, PT, Bs + c0 * SVP, SVP,
+                                     NB - c0 - SB, n8, warp, PK_WARPS, lane);
+            __syncthreads();
         }
+    } else {
+        for (int c0 = NB - SB; c0 >= 0; c0 -= SB) {
+            for (int c = tid; c < nrhs; c += PK_THREADS) {
+                double y[SB];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            int row = lane + 32 * c;
-            if (row < bs)
-                b[(o + row) * ldb + col] = w[c];
+                for (int i = 0; i < SB; ++i)
+                    y[i] = Bs[(c0 + i) * SVP + c];
+#pragma unroll
+                for (int i = SB - 1; i >= 0; --i) {
+                    const double xi = y[i] * rcp[c0 + i];
+                    y[i] = xi;
+#pragma unroll
+                    for (int l = 0; l < i; ++l)
+                        y[l] = fma(-T[(c0 + l) * PT + c0 + i], xi, y[l]);
+                }
+#pragma unroll
+                for (int i = 0; i < SB; ++i)
+                    Bs[(c0 + i) * SVP + c] = y[i];
+            }
+            __syncthreads();
+            if (c0 > 0)
+                panel::smem_update16(Bs, SVP, T + c0, PT, Bs + c0 * SVP, SVP, c0, n8, warp, PK_WARPS, lane);
+            __syncthreads();
         }
     }
+    panel::store_tile<NB, SV_MAXRHS, PK_THREADS>(b + o * ldb, ldb, Bs, SVP, bs, nrhs);
 }
 
 __global__ void k_copy2d(uint64_t rows, uint64_t cols, const double* src, uint64_t lds, double* dst,
@@ -391,16 +379,42 @@ __global__ void k_colnorm_ratio(uint64_t n, uint64_t nrhs, const double* r, cons
     }
 }
 
-size_t diag_smem() { return static_cast<size_t>(NB) * (NB + 1) * sizeof(double); }
+size_t trsm_smem() { return (static_cast<size_t>(NB) * PT + static_cast<size_t>(NB) * (TR_TILE + 4)) * sizeof(double); }
+size_t diag_smem() { return static_cast<size_t>(NB) * PT * sizeof(double); }
+size_t solve_smem() { return static_cast<size_t>(NB) * (PT + SVP) * sizeof(double); }
 
-void prep_diag_attr() {
+void prep_attrs() {
     static bool done[16] = {};
     int dev = ctx().device & 15;
     if (!done[dev]) {
+        RL_CUDA(cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(trsm_smem())));
         RL_CUDA(cudaFuncSetAttribute(k_diag_lu, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(diag_smem())));
+        RL_CUDA(cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(solve_smem())));
         done[dev] = true;
     }
+}
+
+// Per-thread helper stream (high priority) and events for the panel lookahead.
+struct Lookahead {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int device = -1;
+};
+
+Lookahead& lookahead() {
+    static thread_local Lookahead la;
+    if (la.device != ctx().device) {
+        int lo = 0, hi = 0;
+        RL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        RL_CUDA(cudaStreamCreateWithPriority(&la.s2, cudaStreamNonBlocking, hi));
+        for (auto& e : la.ev)
+            RL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        la.device = ctx().device;
+    }
+    return la;
 }
 
 } // namespace
@@ -428,43 +442,55 @@ void transpose_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, double
     RL_LAUNCHED();
 }
 
-size_t trsm_smem() { return (static_cast<size_t>(NB) * TP + static_cast<size_t>(NB) * (TR_TILE + 1)) * sizeof(double); }
-
-void prep_trsm_attr() {
-    static bool done[16] = {};
-    int dev = ctx().device & 15;
-    if (!done[dev]) {
-        RL_CUDA(cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(trsm_smem())));
-        RL_CUDA(cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(NB * TP * sizeof(double))));
-        done[dev] = true;
-    }
-}
-
-// Blocked right-looking GENP in place (packed LU).  aux is unused (kept for the
-// signature); pivots / first breakdown step go to d_pivots / d_breakdown.
+// Blocked right-looking GENP in place (packed LU) with one-panel lookahead:
+//   main stream : Schur update of step k split into the next panel's strips (first) and
+//                 the remaining trailing block (the big DMMA GEMM)
+//   panel stream: diagonal LU + both TRSMs of step k+1, started as soon as the strips
+//                 of step k are done, so they run under the trailing GEMM of step k.
+// The regions written concurrently are disjoint.  aux is unused.
 void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor, double* d_pivots,
                          unsigned long long* d_breakdown, double* aux) {
     (void)aux;
-    prep_diag_attr();
-    prep_trsm_attr();
-    cudaStream_t st = stream();
-    for (uint64_t o = 0; o < n; o += NB) {
-        const int bs = static_cast<int>(std::min<uint64_t>(NB, n - o));
-        k_diag_lu<<<1, DIAG_THREADS, diag_smem(), st>>>(a, lda, n, o, pivot_floor, d_pivots, d_breakdown,
-                                                        nullptr, 1);
+    prep_attrs();
+    cudaStream_t s1 = stream();
+    Lookahead& la = lookahead();
+    cudaStream_t s2 = la.s2;
+    auto at = [&](uint64_t i, uint64_t j) { return a + i * lda + j; };
+    auto panel = [&](uint64_t o, cudaStream_t st) {
+        k_diag_lu<<<1, PK_THREADS, diag_smem(), st>>>(a, lda, n, o, pivot_floor, d_pivots, d_breakdown);
         RL_LAUNCHED();
-        const uint64_t rest = n - o - bs;
-        if (rest == 0)
-            break;
-        // L21 = A21 U11^-1 and U12 = L11^-1 A12 by substitution, in place (bs == NB here)
-        const int nrb = static_cast<int>((rest + TR_TILE - 1) / TR_TILE);
-        k_panel_trsm<<<2 * nrb, TR_WARPS * 32, trsm_smem(), st>>>(a, lda, o, rest, nrb);
-        RL_LAUNCHED();
-        // Schur: A22 -= L21 U12  (the DMMA GEMM carrying ~2n^3/3)
-        gemm(false, false, rest, rest, bs, -1.0, a + (o + bs) * lda + o, lda, a + o * lda + o + bs, lda, 1.0,
-             a + (o + bs) * lda + o + bs, lda);
+        const uint64_t rest = n - o - std::min<uint64_t>(NB, n - o);
+        if (rest) {
+            const int nrb = static_cast<int>((rest + TR_TILE - 1) / TR_TILE);
+            k_panel_trsm<<<2 * nrb, PK_THREADS, trsm_smem(), st>>>(a, lda, o, rest, nrb);
+            RL_LAUNCHED();
+        }
+    };
+    // panel 0 on the main stream
+    panel(0, s1);
+    for (uint64_t o = 0; o + NB < n; o += NB) {
+        const uint64_t rest = n - o - NB;        // trailing size after this step
+        const uint64_t nb2 = std::min<uint64_t>(NB, rest); // width of the next panel
+        const double* L21 = at(o + NB, o);
+        const double* U12 = at(o, o + NB);
+        // (i) next panel's column strip and row strip
+        gemm(false, false, rest, nb2, NB, -1.0, L21, lda, U12, lda, 1.0, at(o + NB, o + NB), lda);
+        if (rest > nb2)
+            gemm(false, false, nb2, rest - nb2, NB, -1.0, L21, lda, at(o, o + NB + nb2), lda, 1.0,
+                 at(o + NB, o + NB + nb2), lda);
+        // hand the next panel to the panel stream
+        cudaEvent_t strips = la.ev[0], done = la.ev[1];
+        RL_CUDA(cudaEventRecord(strips, s1));
+        RL_CUDA(cudaStreamWaitEvent(s2, strips, 0));
+        ctx().stream = s2;
+        panel(o + NB, s2);
+        ctx().stream = s1;
+        RL_CUDA(cudaEventRecord(done, s2));
+        // (ii) remaining trailing block on the main stream
+        if (rest > nb2)
+            gemm(false, false, rest - nb2, rest - nb2, NB, -1.0, at(o + NB + nb2, o), lda,
+                 at(o, o + NB + nb2), lda, 1.0, at(o + NB + nb2, o + NB + nb2), lda);
+        RL_CUDA(cudaStreamWaitEvent(s1, done, 0));
     }
 }
 
@@ -475,39 +501,38 @@ void genp_factor_dev(uint64_t n, double* a, uint64_t lda, double pivot_floor, do
                         reinterpret_cast<unsigned long long*>(d_breakdown), nullptr);
 }
 
-// Kept for the C-ABI signature (block inverses are no longer needed by the solves).
-void genp_block_inverses(uint64_t n, const double* lu, uint64_t lda, double* aux) {
-    (void)n;
-    (void)lu;
-    (void)lda;
-    (void)aux;
-}
+// Kept for the C-ABI signature (the solves need no precomputed block inverses).
+void genp_block_inverses(uint64_t, const double*, uint64_t, double*) {}
 
-// Forward (unit L) then backward (U) substitution, blocked, nrhs columns; b (n x nrhs,
-// ldb) is overwritten by the solution (genp.cpp:106-124).
+// Forward (unit L) then backward (U) substitution, blocked: per 128-block a one-CTA
+// substitution on the diagonal panel + a DMMA GEMM update of the remaining rows;
+// b (n x nrhs, ldb) is overwritten by the solution (genp.cpp:106-124).
 void genp_solve_blocked(uint64_t n, uint64_t nrhs, const double* lu, uint64_t lda, const double* aux,
                         double* b, uint64_t ldb) {
     (void)aux;
-    prep_trsm_attr();
+    prep_attrs();
     cudaStream_t st = stream();
-    const size_t sm = NB * TP * sizeof(double);
-    for (uint64_t o = 0; o < n; o += NB) {
-        const int bs = static_cast<int>(std::min<uint64_t>(NB, n - o));
-        k_block_solve<<<1, TR_WARPS * 32, sm, st>>>(lu, lda, o, bs, b, ldb, nrhs, 1);
-        RL_LAUNCHED();
-        const uint64_t rest = n - o - bs;
-        if (rest)
-            gemm(false, false, rest, nrhs, bs, -1.0, lu + (o + bs) * lda + o, lda, b + o * ldb, ldb, 1.0,
-                 b + (o + bs) * ldb, ldb);
-    }
-    const uint64_t nblk = (n + NB - 1) / NB;
-    for (uint64_t bi = nblk; bi-- > 0;) {
-        const uint64_t o = bi * NB;
-        const int bs = static_cast<int>(std::min<uint64_t>(NB, n - o));
-        k_block_solve<<<1, TR_WARPS * 32, sm, st>>>(lu, lda, o, bs, b, ldb, nrhs, 0);
-        RL_LAUNCHED();
-        if (o)
-            gemm(false, false, o, nrhs, bs, -1.0, lu + o, lda, b + o * ldb, ldb, 1.0, b, ldb);
+    const size_t sm = solve_smem();
+    for (uint64_t c0 = 0; c0 < nrhs; c0 += SV_MAXRHS) { // RHS in slices of <= 32 columns
+        const int nc = static_cast<int>(std::min<uint64_t>(SV_MAXRHS, nrhs - c0));
+        double* bc = b + c0;
+        for (uint64_t o = 0; o < n; o += NB) {
+            const uint64_t bs = std::min<uint64_t>(NB, n - o);
+            k_block_solve<<<1, PK_THREADS, sm, st>>>(lu, lda, n, o, bc, ldb, nc, 1);
+            RL_LAUNCHED();
+            const uint64_t rest = n - o - bs;
+            if (rest)
+                gemm(false, false, rest, nc, bs, -1.0, lu + (o + bs) * lda + o, lda, bc + o * ldb, ldb, 1.0,
+                     bc + (o + bs) * ldb, ldb);
+        }
+        const uint64_t nblk = (n + NB - 1) / NB;
+        for (uint64_t bi = nblk; bi-- > 0;) {
+            const uint64_t o = bi * NB, bs = std::min<uint64_t>(NB, n - o);
+            k_block_solve<<<1, PK_THREADS, sm, st>>>(lu, lda, n, o, bc, ldb, nc, 0);
+            RL_LAUNCHED();
+            if (o)
+                gemm(false, false, o, nc, bs, -1.0, lu + o, lda, bc + o * ldb, ldb, 1.0, bc, ldb);
+        }
     }
 }
 

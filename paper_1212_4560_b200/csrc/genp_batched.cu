@@ -18,6 +18,8 @@
 // (SURVEY.md §0 item 4): such attempts are pre-screened and skipped; if a system
 // ever exhausts its attempts, it is recomputed without the pre-screen so the
 // returned "best" attempt is exactly the reference's choice.
+#include <cmath>
+
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -221,20 +223,23 @@ __device__ bool all_finite64(const double* v, int tid, int* flag) {
     return *flag != 0;
 }
 
-// exact singularity pre-screen: min_k |DFT(c)_k| < 1e-9
+// DFT twiddles of the 64-point transform: (cos, sin)(2 pi m / 64)
+__constant__ double2 kTw[64];
+
+// exact singularity pre-screen: min_k |DFT(c)_k| < 1e-9 (k = 0..32 by conjugate symmetry)
 __device__ bool circ_singular(uint64_t mask, int tid, int* flag) {
     if (tid == 0)
         *flag = 0;
     __syncthreads();
-    if (tid <= 32) { // k = 0..32 (conjugate symmetry)
+    if (tid <= 32) {
         const int k = tid;
         double re = 0.0, im = 0.0;
+#pragma unroll 8
         for (int j = 0; j < N; ++j) {
-            double s, c;
-            sincospi(static_cast<double>((j * k) & 63) / 32.0, &s, &c);
-            double v = sgn(mask, j);
-            re = fma(v, c, re);
-            im = fma(-v, s, im);
+            const double2 w = kTw[(j * k) & 63];
+            const double v = sgn(mask, j);
+            re = fma(v, w.x, re);
+            im = fma(-v, w.y, im);
         }
         if (sqrt(re * re + im * im) < 1e-9)
             atomicOr(flag, 1);
@@ -243,108 +248,68 @@ __device__ bool circ_singular(uint64_t mask, int tid, int* flag) {
     return *flag != 0;
 }
 
-__global__ void __launch_bounds__(THREADS) k_batched_circ64(
-    const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs,
-    const int* __restrict__ active, int nactive, int attempt, int refine, int prescreen, int do_raw,
-    double* __restrict__ X, rl_precond_report* __restrict__ rep, SysState* __restrict__ state,
-    int* __restrict__ pending) {
-    extern __shared__ double dsm[];
-    double* As = dsm;          // N x P
-    double* Ws = dsm + N * P;  // N x P
-    __shared__ double rowbuf[2 * N];
-    __shared__ double bv[N], yv[N], zv[N], rv[N], red[2];
-    __shared__ int flag;
-    if (static_cast<int>(blockIdx.x) >= nactive)
-        return;
-    const int sys = active ? active[blockIdx.x] : blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-    const double* Ag = A + static_cast<size_t>(sys) * N * N;
-    for (int e = tid; e < N * N / 2; e += THREADS) {
-        double2 v = reinterpret_cast<const double2*>(Ag)[e];
-        int i = (2 * e) / N, j = (2 * e) % N;
-        As[i * P + j] = v.x;
-        As[i * P + j + 1] = v.y;
+// mt19937_64 stream (seed, sid): 64 sign draws after discard(8) as a bitmask
+// (bit j set <=> c_j = -1), random_gen.cpp:22-31,55-57.  One thread; only the first
+// phase of the first twist is needed (new[i] for i < 72 < 156).
+__device__ uint64_t sign_mask_stream(uint64_t seed, uint64_t sid) {
+    auto splitmix = [](uint64_t& st) {
+        uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    };
+    uint64_t st = seed;
+    uint64_t a = splitmix(st);
+    st ^= sid * 0xda942042e4dd58b5ULL + 0x2545f4914f6cdd1dULL;
+    uint64_t bb = splitmix(st);
+    uint64_t v = a ^ (bb << 1);
+    uint64_t lo[73], hi[72];
+    lo[0] = v;
+    for (int i = 1; i < 156 + 72; ++i) {
+        v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
+        if (i <= 72)
+            lo[i] = v;
+        if (i >= 156)
+            hi[i - 156] = v;
     }
-    if (tid < N)
-        bv[tid] = B[static_cast<size_t>(sys) * N + tid];
     uint64_t mask = 0;
-    {
-        // sign vector of this attempt -> bitmask (bit j set <=> c_j = -1)
-        const double* sg = signs + static_cast<size_t>(blockIdx.x) * N;
-        double v0 = sg[lane], v1 = sg[lane + 32];
-        unsigned lo = __ballot_sync(0xffffffffu, v0 < 0.0), hi = __ballot_sync(0xffffffffu, v1 < 0.0);
-        mask = (static_cast<uint64_t>(hi) << 32) | lo;
+    for (int i = 8; i < 72; ++i) {
+        uint64_t y = (lo[i] & 0xFFFFFFFF80000000ULL) | (lo[i + 1] & 0x7FFFFFFFULL);
+        uint64_t z = hi[i] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+        z ^= (z >> 29) & 0x5555555555555555ULL;
+        z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+        z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+        z ^= z >> 43;
+        if (!(z & 1ULL))
+            mask |= 1ULL << (i - 8);
     }
-    __syncthreads();
-    rl_precond_report* r = rep + sys;
-    SysState* stt = state + sys;
-    Regs W;
+    return mask;
+}
 
-    if (do_raw) {
-        // raw-GENP contrast arm on A (genp.cpp:222-234), pivot floor 0
-#pragma unroll
-        for (int jb = 0; jb < 8; ++jb) {
-            W.v[jb][0] = As[(8 * warp + g) * P + 8 * jb + 2 * t];
-            W.v[jb][1] = As[(8 * warp + g) * P + 8 * jb + 2 * t + 1];
-        }
-        double pmn, pmx;
-        lu_regs(W, 0.0, rowbuf, warp, g, t, lane, &pmn, &pmx);
-        regs_to_smem(W, Ws, warp, g, t);
-        if (tid < N)
-            zv[tid] = bv[tid];
-        __syncthreads();
-        if (warp == 0)
-            lu_solve_warp(Ws, zv, lane);
-        __syncthreads();
-        bool fin = all_finite64(zv, tid, &flag);
-        double rr = fin ? rel_residual(As, zv, bv, red, rv, tid) : INFINITY;
-        if (tid == 0) {
-            r->raw_residual = rr;
-            r->raw_pivot_min = pmn;
-            r->raw_pivot_max = pmx;
-            r->residual = 0.0;
-            r->pivot_min = 0.0;
-            r->pivot_max = 0.0;
-            r->attempt = -1;
-            r->attempts_drawn = 0;
-            stt->best_res = 0.0;
-            stt->have_best = 0;
-            stt->accepted = -1;
-            stt->skipped = 0;
-            stt->status = 0;
-        }
-        __syncthreads();
-    }
-    if (tid == 0)
-        r->attempts_drawn = attempt + 1;
-    if (prescreen && circ_singular(mask, tid, &flag)) {
-        if (tid == 0) {
-            stt->skipped += 1;
-            if (attempt < 7)
-                atomicAdd(pending, 1);
-        }
-        return;
-    }
+struct Smem {
+    double rowbuf[2 * N];
+    double bv[N], yv[N], zv[N], rv[N], red[2];
+    uint64_t mask;
+    int flag;
+};
+
+// One preconditioned attempt (genp.cpp:250-281) with circulant mask on the system in
+// As: returns 0 = solved (residual in *res), 1 = PivotBreakdown.  y left in S.yv.
+__device__ int attempt(const double* As, double* Ws, Smem& S, uint64_t mask, int refine, int tid,
+                       double* res, double* pmn, double* pmx) {
+    const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    Regs W;
     circ_right_dmma(As, mask, warp, g, t, W);
-    double pmn, pmx;
-    bool brk = lu_regs(W, 1e-300, rowbuf, warp, g, t, lane, &pmn, &pmx);
-    if (brk) { // PivotBreakdown: next attempt (genp.cpp:285-288)
-        if (tid == 0) {
-            if (attempt < 7)
-                atomicAdd(pending, 1);
-            else if (!stt->have_best)
-                stt->status = RL_PIVOT_BREAKDOWN;
-        }
-        return;
-    }
+    if (lu_regs(W, 1e-300, S.rowbuf, warp, g, t, lane, pmn, pmx))
+        return 1;
     regs_to_smem(W, Ws, warp, g, t);
     if (tid < N)
-        zv[tid] = bv[tid];
+        S.zv[tid] = S.bv[tid];
     __syncthreads();
     if (warp == 0) {
-        lu_solve_warp(Ws, zv, lane);
+        lu_solve_warp(Ws, S.zv, lane);
         __syncwarp();
-        circ_vec_warp(mask, zv, yv, lane);
+        circ_vec_warp(mask, S.zv, S.yv, lane);
     }
     __syncthreads();
     for (int s = 0; s < refine; ++s) {
@@ -354,68 +319,151 @@ __global__ void __launch_bounds__(THREADS) k_batched_circ64(
             double acc = 0.0;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                acc = fma(As[i * P + q * 16 + j], yv[q * 16 + j], acc);
+                acc = fma(As[i * P + q * 16 + j], S.yv[q * 16 + j], acc);
             acc += __shfl_xor_sync(0xffffffffu, acc, 1);
             acc += __shfl_xor_sync(0xffffffffu, acc, 2);
             if (q == 0)
-                zv[i] = bv[i] - acc;
+                S.zv[i] = S.bv[i] - acc;
         }
         __syncthreads();
         if (warp == 0) {
-            lu_solve_warp(Ws, zv, lane);
+            lu_solve_warp(Ws, S.zv, lane);
             __syncwarp();
-            circ_vec_warp(mask, zv, rv, lane);
+            circ_vec_warp(mask, S.zv, S.rv, lane);
             __syncwarp();
-            yv[lane] += rv[lane];
-            yv[lane + 32] += rv[lane + 32];
+            S.yv[lane] += S.rv[lane];
+            S.yv[lane + 32] += S.rv[lane + 32];
         }
         __syncthreads();
     }
-    double res = rel_residual(As, yv, bv, red, rv, tid);
-    bool accept = res <= 1e-7;
-    bool better = !stt->have_best || res < stt->best_res;
+    *res = rel_residual(As, S.yv, S.bv, S.red, S.rv, tid);
+    return 0;
+}
+
+// One CTA per system; the whole redraw protocol (8 attempts on stream
+// sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) runs in-kernel.
+// Pass 0 skips attempts whose circulant is exactly singular (DFT pre-screen); if a
+// system accepts no attempt in pass 0 while some were skipped, pass 1 reruns the exact
+// reference protocol without the pre-screen so the kept "best" attempt is identical.
+__global__ void __launch_bounds__(THREADS) k_batched_circ64(
+    const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs0,
+    uint64_t seed, const uint64_t* __restrict__ sids, int refine, double* __restrict__ X,
+    rl_precond_report* __restrict__ rep, int* __restrict__ status) {
+    extern __shared__ double dsm[];
+    double* As = dsm;         // N x P
+    double* Ws = dsm + N * P; // N x P
+    __shared__ Smem S;
+    const int sys = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const double* Ag = A + static_cast<size_t>(sys) * N * N;
+    for (int e = tid; e < N * N / 2; e += THREADS) {
+        double2 v = reinterpret_cast<const double2*>(Ag)[e];
+        int i = (2 * e) / N, j = (2 * e) % N;
+        As[i * P + j] = v.x;
+        As[i * P + j + 1] = v.y;
+    }
+    if (tid < N)
+        S.bv[tid] = B[static_cast<size_t>(sys) * N + tid];
+    if (warp == 0) {
+        const double* sg = signs0 + static_cast<size_t>(sys) * N;
+        unsigned lo = __ballot_sync(0xffffffffu, sg[lane] < 0.0);
+        unsigned hi = __ballot_sync(0xffffffffu, sg[lane + 32] < 0.0);
+        if (lane == 0)
+            S.mask = (static_cast<uint64_t>(hi) << 32) | lo;
+    }
     __syncthreads();
-    if (accept || better) {
-        if (tid < N)
-            X[static_cast<size_t>(sys) * N + tid] = yv[tid];
-        if (tid == 0) {
-            r->residual = res;
-            r->pivot_min = pmn;
-            r->pivot_max = pmx;
-            r->attempt = attempt;
-            stt->best_res = res;
-            stt->have_best = 1;
+    rl_precond_report r{};
+    // raw-GENP contrast arm on A (genp.cpp:222-234), pivot floor 0
+    {
+        Regs W;
+#pragma unroll
+        for (int jb = 0; jb < 8; ++jb) {
+            W.v[jb][0] = As[(8 * warp + g) * P + 8 * jb + 2 * t];
+            W.v[jb][1] = As[(8 * warp + g) * P + 8 * jb + 2 * t + 1];
         }
+        lu_regs(W, 0.0, S.rowbuf, warp, g, t, lane, &r.raw_pivot_min, &r.raw_pivot_max);
+        regs_to_smem(W, Ws, warp, g, t);
+        if (tid < N)
+            S.zv[tid] = S.bv[tid];
+        __syncthreads();
+        if (warp == 0)
+            lu_solve_warp(Ws, S.zv, lane);
+        __syncthreads();
+        bool fin = all_finite64(S.zv, tid, &S.flag);
+        r.raw_residual = fin ? rel_residual(As, S.zv, S.bv, S.red, S.rv, tid) : INFINITY;
+    }
+    const uint64_t sid = sids[sys];
+    double* xg = X + static_cast<size_t>(sys) * N;
+    int st = RL_PIVOT_BREAKDOWN;
+    for (int pass = 0; pass < 2; ++pass) {
+        bool have_best = false, skipped = false, accepted = false;
+        double best_res = 0.0;
+        for (int a = 0; a < 8; ++a) {
+            if (a > 0 || pass > 0) { // redraw: signs of stream (sid + 7919 a) ^ 0x5000...
+                if (tid == 0)
+                    S.mask = (a == 0) ? S.mask : sign_mask_stream(seed, (sid + 7919ULL * a) ^ 0x5000000000000000ULL);
+                __syncthreads();
+            }
+            const uint64_t mask = S.mask;
+            if (pass == 0 && circ_singular(mask, tid, &S.flag)) {
+                skipped = true;
+                continue;
+            }
+            double res, pmn, pmx;
+            if (attempt(As, Ws, S, mask, refine, tid, &res, &pmn, &pmx) != 0)
+                continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
+            const bool acc = res <= 1e-7;
+            if (acc || !have_best || res < best_res) {
+                if (tid < N)
+                    xg[tid] = S.yv[tid];
+                r.residual = res;
+                r.pivot_min = pmn;
+                r.pivot_max = pmx;
+                r.attempt = a;
+                best_res = res;
+                have_best = true;
+            }
+            r.attempts_drawn = a + 1;
+            if (acc) {
+                accepted = true;
+                break;
+            }
+        }
+        if (accepted || have_best)
+            st = 0;
+        if (accepted || !skipped)
+            break;
+        // pass 1: the exact protocol from attempt 0 (restore the attempt-0 mask)
+        if (warp == 0) {
+            const double* sg = signs0 + static_cast<size_t>(sys) * N;
+            unsigned lo = __ballot_sync(0xffffffffu, sg[lane] < 0.0);
+            unsigned hi = __ballot_sync(0xffffffffu, sg[lane + 32] < 0.0);
+            if (lane == 0)
+                S.mask = (static_cast<uint64_t>(hi) << 32) | lo;
+        }
+        __syncthreads();
     }
     if (tid == 0) {
-        if (accept)
-            stt->accepted = attempt;
-        else if (attempt < 7)
-            atomicAdd(pending, 1);
+        if (r.attempts_drawn == 0)
+            r.attempts_drawn = 8;
+        rep[sys] = r;
+        if (st != 0)
+            atomicExch(status, st);
     }
 }
 
-__global__ void k_collect_pending(const SysState* state, uint64_t batch, int* active, int* count) {
-    uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (s < batch && state[s].accepted < 0 && state[s].status == 0) {
-        int pos = atomicAdd(count, 1);
-        active[pos] = static_cast<int>(s);
+void init_twiddles() {
+    static bool done[16] = {};
+    int dev = ctx().device & 15;
+    if (done[dev])
+        return;
+    double2 tw[64];
+    for (int m = 0; m < 64; ++m) {
+        const double ang = 3.14159265358979323846 * static_cast<double>(m) / 32.0;
+        tw[m] = make_double2(std::cos(ang), std::sin(ang));
     }
-}
-
-// systems that never accepted but skipped attempts: need the full protocol rerun
-__global__ void k_collect_exhausted(const SysState* state, uint64_t batch, int* active, int* count) {
-    uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (s < batch && state[s].accepted < 0 && state[s].skipped > 0) {
-        int pos = atomicAdd(count, 1);
-        active[pos] = static_cast<int>(s);
-    }
-}
-
-__global__ void k_gather_sids(const uint64_t* sids, const int* active, int n, uint64_t* out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n)
-        out[i] = sids[active[i]];
+    RL_CUDA(cudaMemcpyToSymbol(kTw, tw, sizeof(tw)));
+    done[dev] = true;
 }
 
 } // namespace
@@ -431,54 +479,18 @@ rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int
                                      static_cast<int>(kDynSmem)));
         attr[ctx().device & 15] = true;
     }
-    SysState* state = ws<SysState>(WS_BATCH, batch);
-    double* signs = ws<double>(WS_TMP1, batch * N);
-    int* active = ws<int>(WS_TMP2, batch + 4);
-    int* counter = active + batch;
-    uint64_t* sids_act = ws<uint64_t>(WS_SMALL, batch);
-    int h_count = 0;
-    auto run_protocol = [&](int prescreen, int nact, bool first) {
-        for (int attempt = 0; attempt < 8 && nact > 0; ++attempt) {
-            const uint64_t* sid_src = d_sids;
-            if (!first || attempt > 0) {
-                k_gather_sids<<<cdiv(nact, 256), 256, 0, st>>>(d_sids, active, nact, sids_act);
-                RL_LAUNCHED();
-                sid_src = sids_act;
-            }
-            rng_sign_vectors_batched(seed, sid_src, 7919ULL * attempt, 0x5000000000000000ULL, nact, N,
-                                     signs);
-            RL_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-            const int* act = (first && attempt == 0) ? nullptr : active;
-            k_batched_circ64<<<nact, THREADS, kDynSmem, st>>>(dA, dB, signs, act, nact, attempt, refine,
-                                                       prescreen, attempt == 0 ? 1 : 0, dX, d_rep,
-                                                       state, counter);
-            RL_LAUNCHED();
-            RL_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-            k_collect_pending<<<cdiv(batch, 256), 256, 0, st>>>(state, batch, active, counter);
-            RL_LAUNCHED();
-            RL_CUDA(cudaMemcpyAsync(&h_count, counter, sizeof(int), cudaMemcpyDeviceToHost, st));
-            RL_CUDA(cudaStreamSynchronize(st));
-            nact = (attempt < 7) ? h_count : 0;
-            first = false;
-        }
-    };
-    run_protocol(1, static_cast<int>(batch), true);
-    // exhausted systems with pre-screened attempts: rerun the exact protocol
-    RL_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    k_collect_exhausted<<<cdiv(batch, 256), 256, 0, st>>>(state, batch, active, counter);
+    init_twiddles();
+    double* signs = ws<double>(WS_TMP1, batch * N + 1);
+    int* d_status = reinterpret_cast<int*>(signs + batch * N);
+    rng_sign_vectors_batched(seed, d_sids, 0, 0x5000000000000000ULL, batch, N, signs);
+    RL_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), st));
+    k_batched_circ64<<<static_cast<unsigned>(batch), THREADS, kDynSmem, st>>>(dA, dB, signs, seed, d_sids,
+                                                                            refine, dX, d_rep, d_status);
     RL_LAUNCHED();
-    RL_CUDA(cudaMemcpyAsync(&h_count, counter, sizeof(int), cudaMemcpyDeviceToHost, st));
+    int h = 0;
+    RL_CUDA(cudaMemcpyAsync(&h, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
     RL_CUDA(cudaStreamSynchronize(st));
-    if (h_count > 0)
-        run_protocol(0, h_count, false);
-    // any system still with status != 0?
-    std::vector<SysState> hs(batch);
-    RL_CUDA(cudaMemcpyAsync(hs.data(), state, batch * sizeof(SysState), cudaMemcpyDeviceToHost, st));
-    RL_CUDA(cudaStreamSynchronize(st));
-    for (auto& s : hs)
-        if (s.status != 0)
-            return RL_PIVOT_BREAKDOWN;
-    return RL_OK;
+    return h == 0 ? RL_OK : RL_PIVOT_BREAKDOWN;
 }
 
 } // namespace rl

@@ -317,7 +317,7 @@ bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r) {
     double* tmpq = ws<double>(WS_RF5, m * k + KMAX);
     const int sp = splits_for(k, k, m);
     // ||Y||_F^2 for the shift (Fukaya et al.: s = 11 (m k + k(k+1)) u ||Y||_2^2, F-norm bound)
-    double* part = tmpq; // reuse as scratch for the norm partials
+    double* part = ws<double>(WS_RESID, 256);
     k_sumsq_partial<<<256, 256, 0, stream()>>>(m * k, y, part);
     RL_LAUNCHED();
     std::vector<double> hp = to_host(part, 256);

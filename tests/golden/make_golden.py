@@ -1,0 +1,102 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference compiled by oracle/Makefile
+(oracle/_ref/librandla_ref.so, built from /root/reference/proj/src).  Run here, where
+/root/reference exists:
+
+    make -C oracle ref && python tests/golden/make_golden.py
+
+The fixtures are small (a few MB) and committed; the GPU box never needs the reference.
+Inputs for the configuration-shaped cases are built with the reference's own RNG
+(gaussian_matrix) and Matrix::multiply, so the bytes are exactly what the reference sees.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), "..", ".."))
+sys.path.insert(0, ROOT)
+from oracle.pyoracle import Reference  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(__file__))
+R = Reference()
+g = {}
+
+# --- RNG streams (random_gen.cpp:22-70) -------------------------------------------
+streams = [(1, 0), (7, 3), (7, 4), (11, 0), (20260825, 0x2000000000000), (31, 5)]
+for seed, sid in streams:
+    key = f"{seed}_{sid}"
+    g[f"rng/uniform01/{key}"] = R.draws(seed, sid, "uniform01", 64)
+    g[f"rng/uniform_pm1/{key}"] = R.draws(seed, sid, "uniform_pm1", 64)
+    g[f"rng/gaussian/{key}"] = R.draws(seed, sid, "gaussian", 257)
+    g[f"rng/sign/{key}"] = R.draws(seed, sid, "sign", 128)
+    g[f"rng/uniform_int/{key}"] = R.uniform_int(seed, sid, 64, 0, 16383).astype(np.int64)
+g["rng/uniform_int_dice"] = R.uniform_int(7, 5, 1000, 1, 6)
+g["gaussian_matrix/4x5/11_0"] = R.gaussian_matrix(4, 5, 11, 0)
+g["gaussian_matrix/33x31/mu_sigma"] = R.gaussian_matrix(33, 31, 3, 9, mu=0.5, sigma=2.0)
+g["uniform_matrix/20x17/11_1"] = R.uniform_matrix(20, 17, 11, 1)
+g["circulant_sign/64/9_1"] = R.circulant_sign(64, 9, 1)
+g["circulant_sign/8/1_0"] = R.circulant_sign(8, 1, 0)
+g["householder_sign/16/5_5"] = R.householder_sign(16, 5, 5)
+
+# --- GENP KATs (tests/test_genp.cpp) -----------------------------------------------
+dd = R.uniform_matrix(8, 8, 31, 0)
+np.fill_diagonal(dd, 9.0)  # diag_dominant(8, {31, 0}) (test_genp.cpp:25-30)
+L, U, piv, mm = R.genp_factor(dd)
+g["genp/diag_dominant8/A"], g["genp/diag_dominant8/L"], g["genp/diag_dominant8/U"] = dd, L, U
+g["genp/diag_dominant8/pivots"] = piv
+a = R.gaussian_matrix(150, 150, 5, 5) + 150 * np.eye(150)
+L, U, piv, mm = R.genp_factor(a)
+g["genp/gauss150/A"], g["genp/gauss150/L"], g["genp/gauss150/U"], g["genp/gauss150/pivots"] = a, L, U, piv
+bb = R.gaussian_matrix(150, 1, 5, 6).ravel()
+g["genp/gauss150/b"], g["genp/gauss150/y"] = bb, R.genp_solve(L, U, bb)
+
+# --- config 1 (n = 256, Gaussian, Right) ------------------------
+n, seed = 256, 20260825
+A = R.gaussian_matrix(n, n, seed, 1)
+P = R.gaussian_matrix(128, 127, seed, 2)
+Q = R.gaussian_matrix(127, 128, seed, 3)
+A[:128, :128] = R.matmul(P, Q)
+xt = R.gaussian_matrix(n, 1, seed, 4).ravel()
+b = R.matvec(A, xt)
+g["c1/A"], g["c1/b"], g["c1/x_true"] = A, b, xt
+for kind in ("gaussian", "circulant_sign", "uniform_pm1"):
+    for refine in (0, 1):
+        y, rep = R.randomized_genp(A, b, kind, "right", refine, seed=seed, sid=11)
+        g[f"c1/{kind}/r{refine}/y"], g[f"c1/{kind}/r{refine}/report"] = y, rep
+y, rep = R.randomized_genp(A, b, "gaussian", "left", 0, seed=seed, sid=11)
+g["c1/gaussian/left/y"], g["c1/gaussian/left/report"] = y, rep
+y, rep = R.randomized_genp(A, b, "circulant_sign", "both", 1, seed=seed, sid=11)
+g["c1/circulant_sign/both/y"], g["c1/circulant_sign/both/report"] = y, rep
+
+# --- config 2 shape (n = 64 systems, circulant sign, Right) --------------------------
+batch, n2, seed2 = 48, 64, 4096
+As, bs, ys, reps = [], [], [], []
+for t in range(batch):
+    At = R.gaussian_matrix(n2, n2, seed2, 10 * t + 1)
+    Pt = R.gaussian_matrix(32, 31, seed2, 10 * t + 2)
+    Qt = R.gaussian_matrix(31, 32, seed2, 10 * t + 3)
+    At[:32, :32] = R.matmul(Pt, Qt)
+    xt = R.gaussian_matrix(n2, 1, seed2, 10 * t + 4).ravel()
+    bt = R.matvec(At, xt)
+    y, rep = R.randomized_genp(At, bt, "circulant_sign", "right", 0, seed=seed2, sid=1000 + t)
+    As.append(At), bs.append(bt), ys.append(y), reps.append(rep)
+g["c2/A"], g["c2/b"], g["c2/y"], g["c2/report"] = np.array(As), np.array(bs), np.array(ys), np.array(reps)
+g["c2/sids"] = np.arange(1000, 1000 + batch, dtype=np.uint64)
+g["c2/seed"] = np.array([seed2], dtype=np.uint64)
+
+# --- Table-1 shaped systems (illblock_system, test_genp.cpp:136-161) -----------------
+for t in range(4):
+    Ai, bi, yi = R.illblock_system(64, 32, t)
+    g[f"illblock64/{t}/A"], g[f"illblock64/{t}/b"] = Ai, bi
+    for refine in (0, 1):
+        y, rep = R.randomized_genp(Ai, bi, "circulant_sign", "left", refine, seed=33, sid=t)
+        g[f"illblock64/{t}/r{refine}/y"], g[f"illblock64/{t}/r{refine}/report"] = y, rep
+
+# --- dense core ------------------------------------------------------------------------
+M = R.gaussian_matrix(40, 12, 8, 8)
+qq, rr = R.qr_positive(M)
+g["qr/40x12/A"], g["qr/40x12/Q"], g["qr/40x12/R"] = M, qq, rr
+g["nrank/profile64"] = R.profile_matrix_paper(64, 8, 42, 90)
+
+np.savez_compressed(os.path.join(OUT, "golden.npz"), **g)
+print("wrote", os.path.join(OUT, "golden.npz"), len(g), "arrays")

@@ -1,0 +1,67 @@
+"""GPU: batched randomized GENP (config 2 shape, K6) against the reference's per-system
+randomized_genp (golden fixtures) and the restated oracle: same accepted attempt for every
+system, solutions within tolerance, deterministic bits, pre-screen == full protocol."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config2_golden(rl, golden):
+    A, b, y_ref, rep_ref = golden["c2/A"], golden["c2/b"], golden["c2/y"], golden["c2/report"]
+    seed = int(golden["c2/seed"][0])
+    x, reps = rl.randomized_genp_batched(A, b, rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN),
+                                         rl.MulSide.RIGHT, 0, seed, golden["c2/sids"])
+    worst, worst_ref = 0.0, 0.0
+    for t in range(A.shape[0]):
+        assert np.abs(x[t] - y_ref[t]).max() / np.abs(y_ref[t]).max() < 1e-8, t
+        be = np.linalg.norm(A[t] @ x[t] - b[t]) / (np.linalg.norm(A[t]) * np.linalg.norm(x[t]))
+        be_ref = np.linalg.norm(A[t] @ y_ref[t] - b[t]) / (np.linalg.norm(A[t]) * np.linalg.norm(y_ref[t]))
+        worst, worst_ref = max(worst, be), max(worst_ref, be_ref)
+        assert be <= 4 * be_ref + 16 * 2.2e-16, t  # per system: eps-level noise floor
+        assert reps[t].attempt == int(rep_ref[t][6]) if rep_ref.shape[1] > 6 else True
+        assert reps[t].residual <= 1e-7 and rep_ref[t][0] <= 1e-7
+    assert worst <= 2 * worst_ref  # config 2 reports the worst backward error
+
+
+def test_redraw_protocol_matches_oracle(rl, oracle):
+    batch, n, seed = 256, 64, 7
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((batch, n, n))
+    A[:, :32, :32] = rng.standard_normal((batch, 32, 31)) @ rng.standard_normal((batch, 31, 32))
+    b = np.einsum("bij,bj->bi", A, rng.standard_normal((batch, n)))
+    sids = np.arange(batch, dtype=np.uint64) * 3 + 1
+    kind = rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN)
+    x, reps = rl.randomized_genp_batched(A, b, kind, rl.MulSide.RIGHT, 0, seed, sids)
+    redrawn = 0
+    for t in range(batch):
+        xo, ro, eo = oracle.randomized_genp(A[t], b[t], "circulant_sign", "right", 0, seed=seed, sid=int(sids[t]))
+        assert reps[t].attempt == eo[0], t
+        redrawn += eo[0] > 0
+        assert np.abs(x[t] - xo).max() / np.abs(xo).max() < 1e-7
+    assert redrawn > 10  # ~18% of circulant +-1 draws are exactly singular at n = 64
+    x2, _ = rl.randomized_genp_batched(A, b, kind, rl.MulSide.RIGHT, 0, seed, sids)
+    assert np.array_equal(x, x2)  # deterministic
+
+
+def test_refinement_in_batch(rl, oracle):
+    batch, n = 32, 64
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((batch, n, n))
+    b = rng.standard_normal((batch, n))
+    sids = np.arange(batch, dtype=np.uint64)
+    kind = rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN)
+    x0, r0 = rl.randomized_genp_batched(A, b, kind, rl.MulSide.RIGHT, 0, 5, sids)
+    x1, r1 = rl.randomized_genp_batched(A, b, kind, rl.MulSide.RIGHT, 1, 5, sids)
+    assert sum(r1[t].residual <= r0[t].residual * 1.01 for t in range(batch)) >= 28
+
+
+def test_batched_general_kind_fallback_path(rl, oracle):
+    batch, n = 3, 40
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((batch, n, n))
+    b = rng.standard_normal((batch, n))
+    x, reps = rl.randomized_genp_batched(A, b, rl.MultiplierKind(), rl.MulSide.RIGHT, 0, 3, [5, 6, 7])
+    for t in range(batch):
+        xo, ro, _ = oracle.randomized_genp(A[t], b[t], "gaussian", "right", 0, seed=3, sid=5 + t)
+        assert np.abs(x[t] - xo).max() / np.abs(xo).max() < 1e-9

@@ -1,0 +1,100 @@
+"""GPU: DGEMM, qr_positive, project_onto_basis, numerical_rank and the fused range finder
+against numpy / the restated oracle / the reference's dense-core tests
+(proj/tests/test_dense_core.cpp, test_lowrank.cpp)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,k,n", [(1, 1, 1), (5, 7, 3), (128, 128, 128), (300, 257, 129), (1000, 64, 72),
+                                   (64, 4096, 72), (129, 1, 33)])
+def test_gemm_vs_numpy(rl, m, k, n):
+    rng = np.random.default_rng(m * 7 + n)
+    a, b = rng.standard_normal((m, k)), rng.standard_normal((k, n))
+    ref = a @ b
+    assert np.abs(rl.multiply(a, b) - ref).max() <= 1e-13 * np.abs(a).max() * np.abs(b).max() * k
+
+
+def test_gemm_transposes_device(rl):
+    import torch
+    for ta in (False, True):
+        for tb in (False, True):
+            m, n, k = 333, 222, 190
+            A = torch.randn(k if ta else m, m if ta else k, dtype=torch.float64, device="cuda")
+            B = torch.randn(n if tb else k, k if tb else n, dtype=torch.float64, device="cuda")
+            C = torch.randn(m, n, dtype=torch.float64, device="cuda")
+            ref = 2.0 * ((A.T if ta else A) @ (B.T if tb else B)) - 0.5 * C
+            rl.dev_gemm(A, B, C, alpha=2.0, beta=-0.5, trans_a=ta, trans_b=tb)
+            torch.cuda.synchronize()
+            assert ((C - ref).abs().max() / ref.abs().max()).item() < 1e-14
+
+
+def test_qr_known_answers(rl):
+    q, r = rl.qr_positive(np.array([[2.0, 0.0], [0.0, 3.0]]))
+    assert np.abs(q - np.eye(2)).max() < 1e-14 and np.abs(r - np.diag([2.0, 3.0])).max() < 1e-14
+    p = np.array([[0.0, 1.0], [1.0, 0.0]])
+    q, r = rl.qr_positive(p)
+    assert np.abs(q - p).max() < 1e-14 and np.abs(r - np.eye(2)).max() < 1e-14
+    s = np.sqrt(2.0)
+    q, r = rl.qr_positive(np.array([[1.0, 1.0], [1.0, -1.0], [0.0, 0.0]]))
+    assert np.linalg.norm(r - np.array([[s, 0], [0, s]])) < 1e-13
+    assert np.linalg.norm(q - np.array([[1 / s, 1 / s], [1 / s, -1 / s], [0, 0]])) < 1e-13
+
+
+def test_qr_vs_reference_and_rank_deficient(rl, golden):
+    q, r = rl.qr_positive(golden["qr/40x12/A"])
+    assert np.abs(q - golden["qr/40x12/Q"]).max() < 1e-12 and np.abs(r - golden["qr/40x12/R"]).max() < 1e-12
+    a = np.array([[i + 1.0, 2.0 * (i + 1)] for i in range(4)])
+    with pytest.raises(rl.RankDeficient):
+        rl.qr_positive(a)
+    with pytest.raises(rl.InvalidArgument):
+        rl.qr_positive(np.ones((2, 3)))
+
+
+def test_numerical_rank_kat(rl, golden):
+    assert rl.numerical_rank(np.diag([1.0, 0.5, 1e-10]), 1e-6)[0] == 2
+    assert rl.numerical_rank(np.eye(5), 1e-6)[0] == 5
+    assert rl.numerical_rank(golden["nrank/profile64"], 1e-6)[0] == 8
+    with pytest.raises(rl.InvalidArgument):
+        rl.numerical_rank(np.eye(3), 0.0)
+    r, s = rl.numerical_rank(np.zeros((200, 20)), 1e-6)
+    assert r == 0
+
+
+def test_projection_and_basis(rl, oracle):
+    rng = np.random.default_rng(4)
+    m, n, k = 600, 300, 10
+    U, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    A = U @ rng.standard_normal((k, n))
+    with pytest.raises(rl.RankDeficient):  # rho+ > rank(A): the sketch is rank deficient
+        rl.qr_positive(rl.approx_basis(A, k + 2, rl.MultiplierKind(), 0, rl.RngStream(1, 1)))
+    y = rl.approx_basis(A, k, rl.MultiplierKind(), 0, rl.RngStream(1, 1))
+    H = oracle.gaussian_matrix(n, k, 1, 1)
+    assert np.abs(y - A @ H).max() <= 1e-12 * np.abs(A @ H).max()
+    q, _ = rl.qr_positive(y)
+    out, sta = rl.project_onto_basis(A, q)
+    assert np.abs(out - A).max() < 1e-11 * np.abs(A).max()
+    assert np.abs(sta - q.T @ A).max() < 1e-12 * np.abs(A).max()
+
+
+def test_range_finder_vs_oracle(rl, oracle):
+    import torch
+    m, n, r, k = 2048, 512, 16, 24
+    rng = np.random.default_rng(5)
+    U, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    A = (U * np.logspace(0, -2, r)) @ V.T + 1e-10 * rng.standard_normal((m, n))
+    Ad = torch.tensor(A, device="cuda")
+    Q = torch.empty(m, k, dtype=torch.float64, device="cuda")
+    B = torch.empty(k, n, dtype=torch.float64, device="cuda")
+    sg, rank, res = rl.dev_range_finder(Ad, k, rl.RngStream(9, 9), 1e-8, Q, B)
+    Y = A @ oracle.gaussian_matrix(n, k, 9, 9)
+    qo, ro = oracle.qr_positive(Y)
+    so = oracle.singular_values(qo.T @ A)
+    res_o = np.linalg.norm(A - qo @ (qo.T @ A)) / np.linalg.norm(A)
+    assert rank == oracle.numerical_rank(so, 1e-8)
+    assert res <= 2 * res_o
+    assert np.abs(sg - so).max() <= 1e-12
+    Qh = Q.cpu().numpy()
+    assert np.abs(Qh.T @ Qh - np.eye(k)).max() < 1e-13
