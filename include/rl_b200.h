@@ -200,6 +200,20 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
                               uint64_t seed, uint64_t stream_id, double rank_tol, double* d_q,
                               double* d_b, double* sigma_host, uint64_t* rank, double* resid_fro);
 
+/* ------------------------------------------ support for the C++ drop-in ---- */
+/* Raw draws [offset, offset+count) of stream (seed, stream_id) (rnd::Rng's engine outputs
+ * after discard(8)); lets the C++ Rng buffer its sequential draws from the GPU. */
+rl_status rl_rng_block(uint64_t seed, uint64_t stream_id, uint64_t offset, uint64_t count,
+                       uint64_t* raw);
+/* Box-Muller of npairs consecutive raw pairs (random_gen.cpp:46-52): out[2q] = r cos a,
+ * out[2q+1] = r sin a. */
+rl_status rl_box_muller(uint64_t npairs, const uint64_t* raw, double* out);
+/* structured::fft (structured.cpp:96-130): complex interleaved (re, im), n a power of two,
+ * inverse scaled by 1/n. */
+rl_status rl_dft(uint64_t n, const double* in, int inverse, double* out);
+/* dense::norm (dense_core.cpp:48-84): kind 0 One, 1 Two, 2 Inf, 3 Frobenius. */
+rl_status rl_norm(uint64_t m, uint64_t n, const double* a, int kind, double* out);
+
 /* -------------------------------------------------------- probes (K12) ---- */
 /* Measured peaks on the current device: FP64 DMMA TFLOP/s and HBM copy GB/s. */
 rl_status rl_probe_peaks(double* fp64_tflops, double* hbm_gbs);

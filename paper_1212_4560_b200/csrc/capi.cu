@@ -40,6 +40,8 @@ void uniform_int_dev(uint64_t seed, uint64_t sid, uint64_t count, int64_t lo, in
 void unpack_lu_dev(uint64_t n, const double* lu, double* l, double* u);
 void pack_lu_dev(uint64_t n, const double* l, const double* u, double* lu);
 rl_status probe_peaks(double* fp64, double* hbm);
+void dft_dev(uint64_t n, const double* in, int inverse, double* out);
+void abs_sums_dev(uint64_t m, uint64_t n, const double* a, int rows, double* out);
 } // namespace rl
 
 using namespace rl;
@@ -640,6 +642,61 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
         *resid_fro = std::sqrt(sumsq_dev(m * n, e) / sumsq_dev(m * n, d_a));
     }
     RL_CUDA(cudaStreamSynchronize(stream()));
+    API_END
+}
+
+rl_status rl_rng_block(uint64_t seed, uint64_t sid, uint64_t offset, uint64_t count, uint64_t* raw) {
+    API_BEGIN
+    uint64_t* d = ws<uint64_t>(WS_H0, count);
+    rng_generate_at(seed, sid, Draw::RawU64, offset, count, 0.0, 1.0, d);
+    download(raw, d, count);
+    API_END
+}
+
+rl_status rl_box_muller(uint64_t npairs, const uint64_t* raw, double* out) {
+    API_BEGIN
+    uint64_t* d = upload(WS_H0, raw, 2 * npairs);
+    double* o = ws<double>(WS_H1, 2 * npairs);
+    box_muller_pairs_dev(d, npairs, o);
+    download(out, o, 2 * npairs);
+    API_END
+}
+
+rl_status rl_dft(uint64_t n, const double* in, int inverse, double* out) {
+    API_BEGIN
+    if (n == 0 || (n & (n - 1)))
+        fail(RL_LENGTH_NOT_POW2, "fft: length must be a power of two");
+    double* d = upload(WS_H0, in, 2 * n);
+    double* o = ws<double>(WS_H1, 2 * n);
+    dft_dev(n, d, inverse, o);
+    download(out, o, 2 * n);
+    API_END
+}
+
+rl_status rl_norm(uint64_t m, uint64_t n, const double* a, int kind, double* out) {
+    API_BEGIN
+    require_positive(m, n, "norm");
+    double* d = upload(WS_H0, a, m * n);
+    if (kind == 3) {
+        *out = std::sqrt(sumsq_dev(m * n, d));
+    } else if (kind == 0 || kind == 2) {
+        const uint64_t cnt = kind == 2 ? m : n;
+        double* v = ws<double>(WS_H1, cnt);
+        abs_sums_dev(m, n, d, kind == 2, v);
+        std::vector<double> h(cnt);
+        download(h.data(), v, cnt);
+        double best = 0.0;
+        for (double x : h)
+            best = std::max(best, x);
+        *out = best;
+    } else {
+        uint64_t r = 0;
+        std::vector<double> sg(std::min(m, n));
+        rl_status st = rl_numerical_rank(m, n, a, 0.5, &r, sg.data());
+        if (st != RL_OK)
+            return st;
+        *out = sg.empty() ? 0.0 : sg[0];
+    }
     API_END
 }
 

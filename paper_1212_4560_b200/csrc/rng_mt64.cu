@@ -108,6 +108,7 @@ struct GenParams {
     double mu, sigma;
     uint64_t count;  // number of transformed values (Gaussian: entries)
     void* out;
+    int64_t base;    // output index of out[0] (stream offset of a partial block)
 };
 
 // Box-Muller pair of random_gen.cpp:46-52 from two raw draws; returns (cos, sin) entries.
@@ -137,7 +138,7 @@ __device__ __forceinline__ void emit_block(const uint64_t* w, int64_t o0, int64_
                 continue;
             double g0, g1;
             box_muller(temper(w[2 * q]), temper(w[2 * q + 1]), p.mu, p.sigma, &g0, &g1);
-            double* out = static_cast<double*>(p.out);
+            double* out = static_cast<double*>(p.out) - p.base;
             if (static_cast<uint64_t>(o) + 1 < p.count) {
                 *reinterpret_cast<double2*>(out + o) = make_double2(g0, g1);
             } else {
@@ -151,33 +152,35 @@ __device__ __forceinline__ void emit_block(const uint64_t* w, int64_t o0, int64_
         if (o < lo || o >= hi)
             continue;
         uint64_t z = temper(w[i]);
+        const int64_t oi = o - p.base;
         switch (p.kind) {
         case static_cast<int>(Draw::RawU64):
-            static_cast<uint64_t*>(p.out)[o] = z;
+            static_cast<uint64_t*>(p.out)[oi] = z;
             break;
         case static_cast<int>(Draw::Uniform01):
-            static_cast<double*>(p.out)[o] = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+            static_cast<double*>(p.out)[oi] = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
             break;
         case static_cast<int>(Draw::UniformPm1):
-            static_cast<double*>(p.out)[o] =
+            static_cast<double*>(p.out)[oi] =
                 __dsub_rn(__dmul_rn(2.0, __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53)), 1.0);
             break;
         default: // Sign
-            static_cast<double*>(p.out)[o] = (z & 1ULL) ? 1.0 : -1.0;
+            static_cast<double*>(p.out)[oi] = (z & 1ULL) ? 1.0 : -1.0;
             break;
         }
     }
 }
 
-// Short streams: one warp from the seed; outputs [0, nout).
+// Short streams: one warp from the seed; outputs [p.base, nout).
 __global__ void k_gen_small(uint64_t eseed, uint64_t nout, GenParams p) {
     __shared__ uint64_t w[kN];
     int lane = threadIdx.x;
     warp_seed_window(w, eseed, lane);
-    // window at time 0; after each twist word 0 is stream position 312k -> output 312k - 320
+    // window at time 0; after each twist word 0 is stream position 312k -> output 312k - 8
     for (int64_t pos = 0; pos < static_cast<int64_t>(nout) + 8; pos += kN) {
         warp_twist(w, lane);
-        emit_block(w, pos - 8, 0, static_cast<int64_t>(nout), p, lane);
+        if (pos + kN - 8 > p.base)
+            emit_block(w, pos - 8, p.base, static_cast<int64_t>(nout), p, lane);
     }
 }
 
@@ -219,7 +222,7 @@ __global__ void k_window_sequence(const uint64_t* windows, uint64_t* seqs) {
 constexpr int kJumpThreads = 320;
 __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, int first_poly,
                                                        int poly_mod, const uint64_t* seqs,
-                                                       int seq_div, int ntargets,
+                                                       int seq_div, int ntargets, int tgt_off,
                                                        uint64_t* out) {
     extern __shared__ __align__(16) uint64_t sm[];
     uint64_t* x = sm;                                              // kSeqWords
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, in
     if (tgt >= ntargets)
         return;
     const uint64_t* poly = polys + static_cast<size_t>((first_poly + tgt) % poly_mod) * kN;
-    const uint64_t* seq = seqs + static_cast<size_t>(tgt / seq_div) * kSeqWords;
+    const uint64_t* seq = seqs + static_cast<size_t>((tgt + tgt_off) / seq_div) * kSeqWords;
     const int t = threadIdx.x;
     for (int i = t; i < kSeqWords; i += kJumpThreads)
         x[i] = seq[i];
@@ -279,23 +282,26 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, in
 
 // One warp per chunk: window at stream position 8 + cJ -> outputs [cJ, cJ + J).
 constexpr int kGenWarps = 4;
-__global__ void __launch_bounds__(32 * kGenWarps) k_gen_chunks(const uint64_t* windows,
+__global__ void __launch_bounds__(32 * kGenWarps) k_gen_chunks(const uint64_t* windows, uint64_t c_first,
                                                                uint64_t nchunks, uint64_t nout,
                                                                GenParams p) {
     __shared__ uint64_t wbuf[kGenWarps][kN];
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint64_t c = static_cast<uint64_t>(blockIdx.x) * kGenWarps + wid;
-    if (c >= nchunks)
+    uint64_t ci = static_cast<uint64_t>(blockIdx.x) * kGenWarps + wid;
+    if (ci >= nchunks)
         return;
+    const uint64_t c = c_first + ci;
     uint64_t* w = wbuf[wid];
     for (int i = lane; i < kN; i += 32)
-        w[i] = windows[c * kN + i];
+        w[i] = windows[ci * kN + i];
     __syncwarp();
-    const int64_t lo = static_cast<int64_t>(c * kJ);
+    const int64_t clo = static_cast<int64_t>(c * kJ);
+    const int64_t lo = max(clo, p.base);
     const int64_t hi = static_cast<int64_t>(min(nout, (c + 1) * kJ));
-    for (int64_t o0 = lo; o0 < hi; o0 += kN) {
+    for (int64_t o0 = clo; o0 < hi; o0 += kN) {
         warp_twist(w, lane);
-        emit_block(w, o0, lo, hi, p, lane);
+        if (o0 + kN > lo)
+            emit_block(w, o0, lo, hi, p, lane);
     }
 }
 
@@ -381,23 +387,29 @@ constexpr size_t kJumpSmem = kSeqWords * 8 + 19968 * 2 + 16;
 
 } // namespace
 
-void rng_generate(uint64_t seed, uint64_t sid, Draw kind, uint64_t count, double mu, double sigma,
-                  void* d_out) {
+// Outputs [offset, offset + count) of stream (seed, sid) (offset must be even for Gaussians).
+void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, uint64_t count, double mu,
+                     double sigma, void* d_out) {
     if (count == 0)
         return;
-    GenParams p{static_cast<int>(kind), mu, sigma, count, d_out};
-    uint64_t nout = (kind == Draw::Gaussian) ? ((count + 1) & ~1ULL) : count;
+    if (kind == Draw::Gaussian && (offset & 1ULL))
+        fail(RL_INVALID_ARGUMENT, "rng: Gaussian blocks start at an even stream offset");
+    const uint64_t end = offset + count;
+    GenParams p{static_cast<int>(kind), mu, sigma, end, d_out, static_cast<int64_t>(offset)};
+    uint64_t nend = (kind == Draw::Gaussian) ? ((end + 1) & ~1ULL) : end;
     uint64_t eseed = engine_seed(seed, sid);
     cudaStream_t st = stream();
-    if (nout <= kSmallMax) {
-        k_gen_small<<<1, 32, 0, st>>>(eseed, count, p);
+    if (nend <= kSmallMax) {
+        k_gen_small<<<1, 32, 0, st>>>(eseed, end, p);
         RL_LAUNCHED();
         return;
     }
     const JumpTable& jt = jump_table();
-    uint64_t nchunks = (nout + kJ - 1) / kJ;
-    uint64_t nl1 = (nchunks + jt.n_l2 - 1) / jt.n_l2;
-    if (nl1 > static_cast<uint64_t>(jt.n_l1))
+    const uint64_t c_first = offset / kJ, c_last = (nend - 1) / kJ;
+    const uint64_t nchunks = c_last - c_first + 1;
+    const uint64_t a_first = c_first / jt.n_l2, a_last = c_last / jt.n_l2;
+    const uint64_t nl1 = a_last - a_first + 1;
+    if (a_last >= static_cast<uint64_t>(jt.n_l1))
         fail(RL_TOO_LARGE, "rng: stream longer than 2^30 draws");
     static bool attr_set[16] = {};
     if (!attr_set[ctx().device & 15]) {
@@ -411,15 +423,41 @@ void rng_generate(uint64_t seed, uint64_t sid, Draw kind, uint64_t count, double
     uint64_t* cw = ws<uint64_t>(WS_RNG2, nchunks * kN);
     k_base_sequence<<<1, 32, 0, st>>>(eseed, base);
     RL_LAUNCHED();
-    k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(jt.d_l1, 0, jt.n_l1, base,
-                                                                          1 << 30, static_cast<int>(nl1), l1w);
+    k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(
+        jt.d_l1, static_cast<int>(a_first), jt.n_l1, base, 1 << 30, static_cast<int>(nl1), 0, l1w);
     RL_LAUNCHED();
     k_window_sequence<<<static_cast<unsigned>(nl1), 32, 0, st>>>(l1w, l1s);
     RL_LAUNCHED();
     k_jump<<<static_cast<unsigned>(nchunks), kJumpThreads, kJumpSmem, st>>>(
-        jt.d_l2, 0, jt.n_l2, l1s, jt.n_l2, static_cast<int>(nchunks), cw);
+        jt.d_l2, static_cast<int>(c_first % jt.n_l2), jt.n_l2, l1s, jt.n_l2, static_cast<int>(nchunks),
+        static_cast<int>(c_first % jt.n_l2), cw);
     RL_LAUNCHED();
-    k_gen_chunks<<<cdiv(nchunks, kGenWarps), 32 * kGenWarps, 0, st>>>(cw, nchunks, count, p);
+    k_gen_chunks<<<cdiv(nchunks, kGenWarps), 32 * kGenWarps, 0, st>>>(cw, c_first, nchunks, end, p);
+    RL_LAUNCHED();
+}
+
+void rng_generate(uint64_t seed, uint64_t sid, Draw kind, uint64_t count, double mu, double sigma,
+                  void* d_out) {
+    rng_generate_at(seed, sid, kind, 0, count, mu, sigma, d_out);
+}
+
+namespace {
+__global__ void k_box_muller_pairs(const uint64_t* raw, uint64_t npairs, double* out) {
+    uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (q >= npairs)
+        return;
+    double g0, g1;
+    box_muller(raw[2 * q], raw[2 * q + 1], 0.0, 1.0, &g0, &g1);
+    out[2 * q] = g0;
+    out[2 * q + 1] = g1;
+}
+} // namespace
+
+// Box-Muller (random_gen.cpp:46-52) of consecutive raw pairs: out[2q] = r cos a, out[2q+1] = r sin a.
+void box_muller_pairs_dev(const uint64_t* d_raw, uint64_t npairs, double* d_out) {
+    if (npairs == 0)
+        return;
+    k_box_muller_pairs<<<cdiv(npairs, 128), 128, 0, stream()>>>(d_raw, npairs, d_out);
     RL_LAUNCHED();
 }
 
