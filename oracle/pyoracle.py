@@ -48,11 +48,14 @@ def _chk(code: int, where: str) -> None:
 
 
 class Restated:
-    """The C restatement (oracle/rl_oracle.c)."""
+    """The C restatement (oracle/rl_oracle.c).  threads > 1 enables its row-parallel
+    loops (bit-identical results; used by the full-size parity runs)."""
 
-    def __init__(self) -> None:
+    def __init__(self, threads: int = 1) -> None:
         _ensure_built("restated")
         L = C.CDLL(RESTATED_SO)
+        L.rlo_set_threads.argtypes = [cint]
+        L.rlo_set_threads(threads)
         self.lib = L
         L.rlo_raw_u64.argtypes = [u64, u64, u64, _u64p]
         L.rlo_gaussian_matrix.argtypes = [u64, u64, dbl, dbl, u64, u64, _d]

@@ -7,6 +7,7 @@
  * are bit-identical to oracle/_ref/librandla_ref.so on the same inputs
  * (tests/test_oracle.py checks this).
  */
+#define _POSIX_C_SOURCE 200809L
 #include "rl_oracle.h"
 
 #include <math.h>
@@ -14,6 +15,101 @@
 #include <string.h>
 
 static const double kPi = 3.14159265358979323846;
+
+/* Optional row-parallelism for the full-size parity runs (tools/fullsize_parity.py):
+ * rows of the product and of each elimination step are independent, so the threaded
+ * results are bit-identical to the sequential ones. */
+#include <pthread.h>
+static int g_threads = 1;
+void rlo_set_threads(int t) { g_threads = t < 1 ? 1 : (t > 256 ? 256 : t); }
+
+typedef void (*row_fn)(uint64_t lo, uint64_t hi, void* arg);
+struct par_job {
+    row_fn fn;
+    void* arg;
+    uint64_t lo, hi;
+};
+static void* par_entry(void* p) {
+    struct par_job* j = (struct par_job*)p;
+    j->fn(j->lo, j->hi, j->arg);
+    return NULL;
+}
+static void par_rows(uint64_t m, row_fn fn, void* arg) {
+    pthread_t th[256];
+    struct par_job jobs[256];
+    int t = g_threads;
+    for (int i = 0; i < t; ++i) {
+        jobs[i].fn = fn;
+        jobs[i].arg = arg;
+        jobs[i].lo = m * (uint64_t)i / (uint64_t)t;
+        jobs[i].hi = m * (uint64_t)(i + 1) / (uint64_t)t;
+        pthread_create(&th[i], NULL, par_entry, &jobs[i]);
+    }
+    for (int i = 0; i < t; ++i)
+        pthread_join(th[i], NULL);
+}
+
+struct mm_args {
+    uint64_t k, n;
+    const double *a, *b;
+    double* c;
+};
+static void matmul_rows(uint64_t lo, uint64_t hi, void* p) {
+    struct mm_args* g = (struct mm_args*)p;
+    for (uint64_t i = lo; i < hi; ++i)
+        for (uint64_t kk = 0; kk < g->k; ++kk) {
+            double av = g->a[i * g->k + kk];
+            if (av == 0.0)
+                continue;
+            const double* rr = g->b + kk * g->n;
+            double* orow = g->c + i * g->n;
+            for (uint64_t j = 0; j < g->n; ++j)
+                orow[j] += av * rr[j];
+        }
+}
+
+/* threaded elimination: each worker owns the rows i == tid (mod t); two barriers per step */
+struct ge_shared {
+    uint64_t n;
+    double* w;
+    double floor;
+    double* pivots;
+    pthread_barrier_t bar;
+    volatile int stop;
+    int t;
+};
+struct ge_job {
+    struct ge_shared* s;
+    int tid;
+};
+static void* ge_worker(void* p) {
+    struct ge_job* j = (struct ge_job*)p;
+    struct ge_shared* s = j->s;
+    const uint64_t n = s->n;
+    double* w = s->w;
+    for (uint64_t k = 0; k < n; ++k) {
+        double pv = w[k * n + k];
+        if (j->tid == 0) {
+            if (s->pivots)
+                s->pivots[k] = fabs(pv);
+            if (fabs(pv) < s->floor)
+                s->stop = (int)(k + 1);
+        }
+        pthread_barrier_wait(&s->bar);
+        if (s->stop)
+            return NULL;
+        uint64_t first = k + 1 + (uint64_t)((j->tid - (int)((k + 1) % (uint64_t)s->t) + s->t) % s->t);
+        for (uint64_t i = first; i < n; i += (uint64_t)s->t) {
+            double mlt = (pv == 0.0) ? 0.0 : w[i * n + k] / pv;
+            w[i * n + k] = mlt;
+            if (mlt != 0.0)
+                for (uint64_t jj = k + 1; jj < n; ++jj)
+                    w[i * n + jj] -= mlt * w[k * n + jj];
+        }
+        pthread_barrier_wait(&s->bar);
+    }
+    return NULL;
+}
 
 /* ---------------------------------------------------------------- RNG ---- */
 
@@ -180,6 +276,10 @@ int rlo_sparse_pm1(uint64_t n, int nnz, uint64_t seed, uint64_t sid, int32_t* ro
 /* matrix.cpp:86-102: i-k-j, ascending k, skip zero a(i,k). */
 void rlo_matmul(uint64_t m, uint64_t k, uint64_t n, const double* a, const double* b, double* c) {
     memset(c, 0, m * n * sizeof(double));
+    if (g_threads > 1 && m >= 64) { /* rows are independent: bit-identical when threaded */
+        par_rows(m, matmul_rows, &(struct mm_args){k, n, a, b, c});
+        return;
+    }
     for (uint64_t i = 0; i < m; ++i)
         for (uint64_t kk = 0; kk < k; ++kk) {
             double av = a[i * k + kk];
@@ -211,6 +311,27 @@ void rlo_transpose(uint64_t m, uint64_t n, const double* a, double* t) {
 
 /* genp.cpp:11-41, packed: the multiplier l(i,k) is stored in w(i,k). */
 int rlo_genp_factor(uint64_t n, double* w, double pivot_floor, double* pivots) {
+    if (g_threads > 1 && n >= 512) {
+        struct ge_shared s;
+        memset(&s, 0, sizeof(s));
+        s.n = n;
+        s.w = w;
+        s.floor = pivot_floor;
+        s.pivots = pivots;
+        s.t = g_threads;
+        pthread_barrier_init(&s.bar, NULL, (unsigned)g_threads);
+        pthread_t th[256];
+        struct ge_job jobs[256];
+        for (int i = 0; i < g_threads; ++i) {
+            jobs[i].s = &s;
+            jobs[i].tid = i;
+            pthread_create(&th[i], NULL, ge_worker, &jobs[i]);
+        }
+        for (int i = 0; i < g_threads; ++i)
+            pthread_join(th[i], NULL);
+        pthread_barrier_destroy(&s.bar);
+        return s.stop ? -s.stop : 0;
+    }
     for (uint64_t k = 0; k < n; ++k) {
         double p = w[k * n + k];
         if (pivots)

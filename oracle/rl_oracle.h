@@ -25,6 +25,9 @@ typedef struct {
     double cached;
 } rlo_rng;
 
+/* Row-parallel worker threads for the full-size parity runs (default 1; bit-identical). */
+void rlo_set_threads(int t);
+
 void rlo_rng_init(rlo_rng* r, uint64_t seed, uint64_t sid);
 uint64_t rlo_next_u64(rlo_rng* r);
 double rlo_uniform01(rlo_rng* r);
