@@ -72,8 +72,7 @@ __device__ __forceinline__ dd dd_div(dd a, dd b) {
 
 // log(x) for x in (0, 1], correctly rounded (with overwhelming probability).
 __device__ __forceinline__ double cr_log_unit(double x) {
-    if (x == 1.0)
-        return 0.0;
+    // (x == 1 needs no special case: m = 1, e = 0, i = 0, f = 0 give exactly 0)
     int e;
     double m = frexp(x, &e); // x = m 2^e, m in [0.5, 1)
     m = __dmul_rn(m, 2.0);   // m in [1, 2)
@@ -83,7 +82,11 @@ __device__ __forceinline__ double cr_log_unit(double x) {
     double f = __dsub_rn(m, c);                                             // exact, |f| <= 1/128
     // log(m) = log(c) + 2 atanh(s), s = f / (2c + f)
     dd den = two_sum(__dmul_rn(2.0, c), f);
-    dd s = dd_div({f, 0.0}, den);
+    // s = f / den to ~2^-104: one Newton correction of the double quotient
+    const double s_hi = __ddiv_rn(f, den.hi);
+    dd prod = two_prod(s_hi, den.hi);
+    const double rem = __dsub_rn(__dsub_rn(f, prod.hi), __fma_rn(s_hi, den.lo, prod.lo));
+    dd s = quick_two_sum(s_hi, __ddiv_rn(rem, den.hi));
     dd z = dd_mul(s, s);
     // atanh(s)/s = sum z^k / (2k+1), |z| <= 2^-16: 7 terms reach 2^-112
     const double inv[8] = {1.0, 1.0 / 3, 1.0 / 5, 1.0 / 7, 1.0 / 9, 1.0 / 11, 1.0 / 13, 1.0 / 15};
@@ -143,12 +146,10 @@ __device__ __forceinline__ void cr_sincos(double a, double* sn, double* cs) {
     dd sr = dd_add(dd_mul(S0, cd), dd_mul(C0, sd));
     dd cr = dd_add(dd_mul(C0, cd), dd_neg(dd_mul(S0, sd)));
     double srd = __dadd_rn(sr.hi, sr.lo), crd = __dadd_rn(cr.hi, cr.lo);
-    switch (q) {
-    case 0: *sn = srd; *cs = crd; break;
-    case 1: *sn = crd; *cs = -srd; break;
-    case 2: *sn = -srd; *cs = -crd; break;
-    default: *sn = -crd; *cs = srd; break;
-    }
+    // quadrant select without branches
+    const double a0 = (q & 1) ? crd : srd, a1 = (q & 1) ? srd : crd;
+    *sn = (q & 2) ? -a0 : a0;
+    *cs = ((q + 1) & 2) ? -a1 : a1;
 }
 
 } // namespace rl

@@ -12,6 +12,7 @@
 // m8n8k4 fragment reads (8 rows x 4 k) hit 4 distinct 32-byte bank groups per
 // half-warp: no bank conflicts for either operand majorness.
 #include <algorithm>
+#include <cstdlib>
 
 #include "rl_internal.cuh"
 
@@ -221,14 +222,20 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const doub
                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
     const int sms = ctx().sms;
     uint64_t big_tiles = static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 128);
-    if (K <= 256 && N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms)
-        // short-K rank updates (the GENP Schur complement): two CTAs per SM so one CTA's
-        // C read-modify-write epilogue overlaps the other's DMMA main loop
+    static const int force = getenv("RL_GEMM_FORCE") ? atoi(getenv("RL_GEMM_FORCE")) : -1; // dev sweeps
+    if (force == 0)
+        return launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 1)
+        return launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 2)
+        return launch<128, 128, 2, 4, AK, BKM, VEC, 3>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 3)
+        return launch<64, 64, 2, 2, AK, BKM, VEC, 4, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms)
+        // two CTAs per SM (128x64 tiles, 3 stages, <= 128 regs): one CTA's prologue / C
+        // epilogue overlaps the other's DMMA loop.  Measured (tools/gemm_sweep.py): 8192^3
+        // 32.8 TF/s vs 31.3 for a 1-CTA 128x128 tile; rank-128 updates 23.3 vs 16.5 TF/s.
         launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (N > 64 && big_tiles >= static_cast<uint64_t>(sms))
-        // 8 warps of 64x32 accumulators (measured: 31.6 TF/s at 8192^3; a 16-warp 4x4
-        // layout of 32x32 tiles reached only 29.2 TF/s — more fragment traffic per DMMA)
-        launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     else if (N > 32)
         launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     else

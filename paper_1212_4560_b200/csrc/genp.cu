@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_panel_trsm(double* a, uint64_
 // (within 1 ulp of the reference's division).  Blocks beyond bs are padded with the
 // identity; off-diagonal updates outside the 128-block are DMMA GEMMs (host loop).
 constexpr int SV_MAXRHS = 32;
+constexpr int SV_ROWS = 64;
 constexpr int SVP = SV_MAXRHS + 4;
 __global__ void __launch_bounds__(PK_THREADS, 1) k_block_solve(const double* __restrict__ lu, uint64_t lda,
                                                                uint64_t n, uint64_t o, double* __restrict__ b,
@@ -313,6 +314,18 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_block_solve(const double* __r
         }
     }
     panel::store_tile<NB, SV_MAXRHS, PK_THREADS>(b + o * ldb, ldb, Bs, SVP, bs, nrhs);
+}
+
+// diagonal 128-blocks of a packed LU -> contiguous [nblk][NB][NB] (ragged last block)
+__global__ void k_gather_diag(const double* __restrict__ lu, uint64_t lda, uint64_t n, double* __restrict__ out) {
+    const uint64_t o = static_cast<uint64_t>(blockIdx.x) * NB;
+    const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
+    double* dst = out + static_cast<uint64_t>(blockIdx.x) * NB * NB;
+    for (int e = threadIdx.x; e < bs * NB; e += blockDim.x) {
+        const int i = e / NB, j = e % NB;
+        if (j < bs)
+            dst[i * NB + j] = lu[(o + i) * lda + o + j];
+    }
 }
 
 __global__ void k_copy2d(uint64_t rows, uint64_t cols, const double* src, uint64_t lds, double* dst,
@@ -393,6 +406,7 @@ void prep_attrs() {
                                      static_cast<int>(diag_smem())));
         RL_CUDA(cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(solve_smem())));
+
         done[dev] = true;
     }
 }
@@ -442,12 +456,15 @@ void transpose_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, double
     RL_LAUNCHED();
 }
 
-// Blocked right-looking GENP in place (packed LU) with one-panel lookahead:
-//   main stream : Schur update of step k split into the next panel's strips (first) and
-//                 the remaining trailing block (the big DMMA GEMM)
-//   panel stream: diagonal LU + both TRSMs of step k+1, started as soon as the strips
-//                 of step k are done, so they run under the trailing GEMM of step k.
-// The regions written concurrently are disjoint.  aux is unused.
+// Blocked right-looking GENP in place (packed LU), outer block 256 built from two 128
+// steps, with one-panel lookahead:
+//   main stream : Schur update of outer step k split into the next outer panel's strips
+//                 (first) and the remaining trailing block (the big K = 256 DMMA GEMM)
+//   panel stream: the next outer panel (2 x [diagonal LU + both TRSMs] + the strip update
+//                 between them), started as soon as the strips of step k are done, so it
+//                 runs under the trailing GEMM of step k.
+// The regions written concurrently are disjoint.  The L and U produced are
+// those of block_ge with block 128 (genp.cpp:43-104) up to rounding.  aux is unused.
 void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor, double* d_pivots,
                          unsigned long long* d_breakdown, double* aux) {
     (void)aux;
@@ -456,7 +473,8 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
     Lookahead& la = lookahead();
     cudaStream_t s2 = la.s2;
     auto at = [&](uint64_t i, uint64_t j) { return a + i * lda + j; };
-    auto panel = [&](uint64_t o, cudaStream_t st) {
+    // one 128-wide step: diagonal LU + both TRSMs over everything below / right of it
+    auto panel128 = [&](uint64_t o, cudaStream_t st) {
         k_diag_lu<<<1, PK_THREADS, diag_smem(), st>>>(a, lda, n, o, pivot_floor, d_pivots, d_breakdown);
         RL_LAUNCHED();
         const uint64_t rest = n - o - std::min<uint64_t>(NB, n - o);
@@ -466,30 +484,46 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
             RL_LAUNCHED();
         }
     };
-    // panel 0 on the main stream
-    panel(0, s1);
-    for (uint64_t o = 0; o + NB < n; o += NB) {
-        const uint64_t rest = n - o - NB;        // trailing size after this step
-        const uint64_t nb2 = std::min<uint64_t>(NB, rest); // width of the next panel
-        const double* L21 = at(o + NB, o);
-        const double* U12 = at(o, o + NB);
-        // (i) next panel's column strip and row strip
-        gemm(false, false, rest, nb2, NB, -1.0, L21, lda, U12, lda, 1.0, at(o + NB, o + NB), lda);
-        if (rest > nb2)
-            gemm(false, false, nb2, rest - nb2, NB, -1.0, L21, lda, at(o, o + NB + nb2), lda, 1.0,
-                 at(o + NB, o + NB + nb2), lda);
-        // hand the next panel to the panel stream
+    // one outer panel of width W = 2 * NB at o (block LU with a 256 pivot block composed of two
+    // 128 steps): step 1, then only the second sub-panel's strips are updated (the trailing
+    // update is delayed), then step 2.  The trailing matrix is updated once with K = 256.
+    auto panel256 = [&](uint64_t o, cudaStream_t st) {
+        cudaStream_t keep = ctx().stream;
+        ctx().stream = st; // gemm() launches on ctx().stream
+        panel128(o, st);
+        const uint64_t o2 = o + NB;
+        if (o2 < n) {
+            const uint64_t rest = n - o2, w2 = std::min<uint64_t>(NB, rest);
+            gemm(false, false, rest, w2, NB, -1.0, at(o2, o), lda, at(o, o2), lda, 1.0, at(o2, o2), lda);
+            if (rest > w2)
+                gemm(false, false, w2, rest - w2, NB, -1.0, at(o2, o), lda, at(o, o2 + w2), lda, 1.0,
+                     at(o2, o2 + w2), lda);
+            panel128(o2, st);
+        }
+        ctx().stream = keep;
+    };
+    constexpr uint64_t W = 2 * NB;
+    panel256(0, s1);
+    for (uint64_t o = 0; o + W < n; o += W) {
+        const uint64_t rest = n - o - W;                 // trailing size after this outer step
+        const uint64_t w2 = std::min<uint64_t>(W, rest); // width of the next outer panel
+        const double* L21 = at(o + W, o);                // rest x 256
+        const double* U12 = at(o, o + W);                // 256 x rest
+        // (i) next outer panel's column strip and row strip (K = 256)
+        gemm(false, false, rest, w2, W, -1.0, L21, lda, U12, lda, 1.0, at(o + W, o + W), lda);
+        if (rest > w2)
+            gemm(false, false, w2, rest - w2, W, -1.0, L21, lda, at(o, o + W + w2), lda, 1.0,
+                 at(o + W, o + W + w2), lda);
+        // hand the next outer panel to the high-priority panel stream ...
         cudaEvent_t strips = la.ev[0], done = la.ev[1];
         RL_CUDA(cudaEventRecord(strips, s1));
         RL_CUDA(cudaStreamWaitEvent(s2, strips, 0));
-        ctx().stream = s2;
-        panel(o + NB, s2);
-        ctx().stream = s1;
+        panel256(o + W, s2);
         RL_CUDA(cudaEventRecord(done, s2));
-        // (ii) remaining trailing block on the main stream
-        if (rest > nb2)
-            gemm(false, false, rest - nb2, rest - nb2, NB, -1.0, at(o + NB + nb2, o), lda,
-                 at(o, o + NB + nb2), lda, 1.0, at(o + NB + nb2, o + NB + nb2), lda);
+        // (ii) ... while the main stream runs the remaining trailing update (K = 256)
+        if (rest > w2)
+            gemm(false, false, rest - w2, rest - w2, W, -1.0, at(o + W + w2, o), lda, at(o, o + W + w2), lda, 1.0,
+                 at(o + W + w2, o + W + w2), lda);
         RL_CUDA(cudaStreamWaitEvent(s1, done, 0));
     }
 }
@@ -513,22 +547,27 @@ void genp_solve_blocked(uint64_t n, uint64_t nrhs, const double* lu, uint64_t ld
     prep_attrs();
     cudaStream_t st = stream();
     const size_t sm = solve_smem();
+    // the 64 diagonal 128x128 blocks, gathered once into an L2-resident buffer (8 MiB at
+    // n = 8192) so each block solve reads its triangle from L2, not from the 512 MiB LU
+    const uint64_t nblk = (n + NB - 1) / NB;
+    double* diag = ws<double>(WS_RF4, nblk * NB * NB);
+    k_gather_diag<<<static_cast<unsigned>(nblk), 256, 0, st>>>(lu, lda, n, diag);
+    RL_LAUNCHED();
     for (uint64_t c0 = 0; c0 < nrhs; c0 += SV_MAXRHS) { // RHS in slices of <= 32 columns
         const int nc = static_cast<int>(std::min<uint64_t>(SV_MAXRHS, nrhs - c0));
         double* bc = b + c0;
-        for (uint64_t o = 0; o < n; o += NB) {
-            const uint64_t bs = std::min<uint64_t>(NB, n - o);
-            k_block_solve<<<1, PK_THREADS, sm, st>>>(lu, lda, n, o, bc, ldb, nc, 1);
+        for (uint64_t bi = 0; bi < nblk; ++bi) {
+            const uint64_t o = bi * NB, bs = std::min<uint64_t>(NB, n - o);
+            k_block_solve<<<1, PK_THREADS, sm, st>>>(diag + bi * NB * NB, NB, bs, 0, bc + o * ldb, ldb, nc, 1);
             RL_LAUNCHED();
             const uint64_t rest = n - o - bs;
             if (rest)
                 gemm(false, false, rest, nc, bs, -1.0, lu + (o + bs) * lda + o, lda, bc + o * ldb, ldb, 1.0,
                      bc + (o + bs) * ldb, ldb);
         }
-        const uint64_t nblk = (n + NB - 1) / NB;
         for (uint64_t bi = nblk; bi-- > 0;) {
             const uint64_t o = bi * NB, bs = std::min<uint64_t>(NB, n - o);
-            k_block_solve<<<1, PK_THREADS, sm, st>>>(lu, lda, n, o, bc, ldb, nc, 0);
+            k_block_solve<<<1, PK_THREADS, sm, st>>>(diag + bi * NB * NB, NB, bs, 0, bc + o * ldb, ldb, nc, 0);
             RL_LAUNCHED();
             if (o)
                 gemm(false, false, o, nc, bs, -1.0, lu + o, lda, bc + o * ldb, ldb, 1.0, bc, ldb);

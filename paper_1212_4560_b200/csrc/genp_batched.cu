@@ -1,23 +1,25 @@
 // K6: batched randomized GENP for small systems (config 2: 4096 x n=64, circulant +-1,
-// MulSide::Right) — semantically the loop bench::table1_genp runs (bench.cpp:117-133)
-// over genp::randomized_genp (genp.cpp:207-291), one stream per system.
+// MulSide::Right) — semantically the loop bench::table1_genp runs (bench.cpp:117-133) over
+// genp::randomized_genp (genp.cpp:207-291), one stream per system.
 //
-// One CTA (8 warps) per system, everything on-chip:
-//   * A (64 x 64) read from HBM once into shared memory (kept for the residuals).
-//   * W = A C on DMMA: warp w owns rows 8w..8w+7; the B-operand fragment
-//     C[k][j] = c[(k - j) mod 64] is synthesised from the 64-bit sign mask in a
-//     register (no smem traffic for C).  The accumulators stay in registers and ARE
-//     the LU's data layout: lane (g, t) of warp w owns row 8w+g, columns 8jb+2t, +1.
-//   * No-pivot LU with the rows in registers: per step the pivot row goes through a
-//     double-buffered shared row (one __syncthreads per step) and the multiplier
-//     w(i,k)/p is broadcast inside the row's 4-lane group with __shfl_sync.
-//   * Solves, y = C z, refinement and the residual ||A y - b|| / ||b|| on-chip.
-// The redraw protocol (8 attempts on stream id + 7919 a, accept <= 1e-7, keep best,
-// genp.cpp:236-290) runs as one launch per attempt over the still-unaccepted systems.
-// A circulant +-1 C is exactly singular iff a DFT coefficient of c vanishes
-// (SURVEY.md §0 item 4): such attempts are pre-screened and skipped; if a system
-// ever exhausts its attempts, it is recomputed without the pre-screen so the
-// returned "best" attempt is exactly the reference's choice.
+// One 64-thread CTA per system; thread t owns ROW t of the working matrix in registers
+// (64 doubles, fully unrolled so every index is static).  Per attempt:
+//   * A (64 x 64, L2-resident after the first touch) is staged in shared memory and
+//     W = A C runs on DMMA (2 warps x 32 rows); the +-1 B fragment C[k][j] = c[(k - j) mod 64]
+//     is synthesised from a 64-bit sign mask.
+//   * No-pivot LU, warp-split: warp 0 eliminates rows 0..31 with __syncwarp only (pivot row
+//     through a double-buffered shared row), publishes its U rows, then warp 1 applies those
+//     32 steps to rows 32..63 and eliminates its own 32 x 32 block — two CTA barriers per LU
+//     instead of one per pivot.  Row update order as genp.cpp:20-33; m = w(i,k) * (1/p),
+//     1/p := 0 for p = 0 (the reference's zero-pivot convention).
+//   * Forward / backward substitution the same way (shuffles inside a warp, one barrier
+//     between the halves), y = C z, refinement, residual ||A y - b|| / ||b||.
+// The raw-GENP contrast arm is iteration -1 of the same loop (pivot floor 0, no multiplier),
+// so the unrolled LU / solve code exists once.  The 8-attempt redraw protocol (stream id +
+// 7919 a, accept <= 1e-7, keep best, genp.cpp:236-290) runs in-kernel.  Exactly singular
+// circulants (a vanishing 64-point DFT coefficient) are pre-screened and
+// skipped; a system that exhausts its attempts is re-run with the exact protocol (pass 1) so
+// the returned best attempt is the reference's.
 #include <cmath>
 
 #include "rl_internal.cuh"
@@ -27,15 +29,18 @@ namespace rl {
 namespace {
 
 constexpr int N = 64;
-constexpr int P = N + 1;   // smem pitch
-constexpr int THREADS = 256;
+constexpr int XP = N + 4; // shared pitch: 544 B = 32 mod 128 -> conflict-free DMMA fragments
 
-struct SysState {          // per system, persistent across attempt launches
-    double best_res;
-    int have_best;
-    int accepted;          // attempt index accepted, -1 none
-    int skipped;           // attempts skipped by the singularity pre-screen
-    int status;            // 0 ok, RL_PIVOT_BREAKDOWN if every attempt broke down
+struct Smem {
+    double X[N * XP];  // A / W staging, pivot rows, published U rows, LCG scratch
+    double v0[N], v1[N];
+    double2 tw[N];     // DFT twiddles (cos, sin)(2 pi m / 64)
+    double red[2];
+    double rcp[N];
+    double pm[4];
+    uint64_t mask, mask0;
+    unsigned bal[2];
+    int flag;
 };
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
@@ -44,214 +49,17 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-// element (row, col) of the register layout: row = 8w+g, cols 8jb+2t+e
-struct Regs {
-    double v[8][2];
-};
-
-// signs bit j = 1 <=> c_j = -1
-__device__ __forceinline__ double sgn(uint64_t mask, int j) {
+__device__ __forceinline__ double sgn(uint64_t mask, int j) { // bit j set <=> c_j = -1
     return ((mask >> (j & 63)) & 1ULL) ? -1.0 : 1.0;
 }
 
-// W = A C (A in smem), result in the register layout
-__device__ void circ_right_dmma(const double* As, uint64_t mask, int warp, int g, int t, Regs& W) {
-#pragma unroll
-    for (int jb = 0; jb < 8; ++jb)
-        W.v[jb][0] = W.v[jb][1] = 0.0;
-#pragma unroll 4
-    for (int kk = 0; kk < N; kk += 4) {
-        double a = As[(8 * warp + g) * P + kk + t];
-        const int k = kk + t;
-#pragma unroll
-        for (int jb = 0; jb < 8; ++jb) {
-            // B fragment element: row k, col 8jb+g -> C[k][j] = c[(k - j) mod 64]
-            double b = sgn(mask, k - (8 * jb + g));
-            dmma(W.v[jb], a, b);
-        }
-    }
-}
+__device__ __forceinline__ double min_fold(double a, double v) { return (v < a) ? v : a; }
+__device__ __forceinline__ double max_fold(double b, double v) { return (b < v) ? v : b; }
 
-// No-pivot LU in registers; returns breakdown flag; pmin/pmax of |pivots|.
-__device__ bool lu_regs(Regs& W, double floor, double* rowbuf, int warp, int g, int t, int lane,
-                        double* pmin, double* pmax) {
-    const int row = 8 * warp + g;
-    bool brk = false;
-    double mn = 0.0, mx = 0.0;
-    for (int k = 0; k < N; ++k) {
-        double* rb = rowbuf + (k & 1) * N;
-        if (row == k) {
-#pragma unroll
-            for (int jb = 0; jb < 8; ++jb)
-                *reinterpret_cast<double2*>(rb + 8 * jb + 2 * t) = make_double2(W.v[jb][0], W.v[jb][1]);
-        }
-        __syncthreads();
-        const double p = rb[k];
-        const double ap = fabs(p);
-        if (k == 0) {
-            mn = mx = ap;
-        } else {
-            mn = (ap < mn) ? ap : mn;
-            mx = (mx < ap) ? ap : mx;
-        }
-        brk |= (ap < floor);
-        // multiplier for my row from the lane owning column k
-        const int jbk = k >> 3, tk = (k & 7) >> 1, ek = k & 1;
-        double mine = 0.0;
-#pragma unroll
-        for (int jb = 0; jb < 8; ++jb)
-            if (jb == jbk)
-                mine = ek ? W.v[jb][1] : W.v[jb][0];
-        double m = (p == 0.0) ? 0.0 : mine / p;
-        m = __shfl_sync(0xffffffffu, m, (lane & ~3) | tk);
-        if (row > k) {
-            if (t == tk) {
-#pragma unroll
-                for (int jb = 0; jb < 8; ++jb)
-                    if (jb == jbk) {
-                        if (ek)
-                            W.v[jb][1] = m;
-                        else
-                            W.v[jb][0] = m;
-                    }
-            }
-            if (m != 0.0) {
-#pragma unroll
-                for (int jb = 0; jb < 8; ++jb) {
-                    const int j0 = 8 * jb + 2 * t;
-                    double2 r = *reinterpret_cast<const double2*>(rb + j0);
-                    if (j0 > k)
-                        W.v[jb][0] = fma(-m, r.x, W.v[jb][0]);
-                    if (j0 + 1 > k)
-                        W.v[jb][1] = fma(-m, r.y, W.v[jb][1]);
-                }
-            }
-        }
-    }
-    *pmin = mn;
-    *pmax = mx;
-    return brk;
-}
-
-// spill the packed LU to smem (pitch P)
-__device__ void regs_to_smem(const Regs& W, double* Ws, int warp, int g, int t) {
-    const int row = 8 * warp + g;
-#pragma unroll
-    for (int jb = 0; jb < 8; ++jb) {
-        Ws[row * P + 8 * jb + 2 * t] = W.v[jb][0];
-        Ws[row * P + 8 * jb + 2 * t + 1] = W.v[jb][1];
-    }
-}
-
-// warp 0: x <- LU^{-1} x  (forward unit-L, backward U; genp.cpp:106-124 order of terms)
-__device__ void lu_solve_warp(const double* Ws, double* x, int lane) {
-    double x0 = x[lane], x1 = x[lane + 32];
-    for (int j = 0; j < N; ++j) {
-        double zj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
-        if (lane > j)
-            x0 = fma(-Ws[lane * P + j], zj, x0);
-        if (lane + 32 > j)
-            x1 = fma(-Ws[(lane + 32) * P + j], zj, x1);
-    }
-    for (int j = N - 1; j >= 0; --j) {
-        double xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
-        xj = xj / Ws[j * P + j];
-        if (lane == (j & 31)) {
-            if (j < 32)
-                x0 = xj;
-            else
-                x1 = xj;
-        }
-        if (lane < j)
-            x0 = fma(-Ws[lane * P + j], xj, x0);
-        if (lane + 32 < j)
-            x1 = fma(-Ws[(lane + 32) * P + j], xj, x1);
-    }
-    x[lane] = x0;
-    x[lane + 32] = x1;
-}
-
-// y = C z (warp 0): y_i = sum_j c[(i - j) mod 64] z_j
-__device__ void circ_vec_warp(uint64_t mask, const double* z, double* y, int lane) {
-    double y0 = 0.0, y1 = 0.0;
-    for (int j = 0; j < N; ++j) {
-        double zj = z[j];
-        y0 = fma(sgn(mask, lane - j), zj, y0);
-        y1 = fma(sgn(mask, lane + 32 - j), zj, y1);
-    }
-    __syncwarp();
-    y[lane] = y0;
-    y[lane + 32] = y1;
-}
-
-// ||A y - b|| / ||b|| (all threads; result broadcast through red[])
-__device__ double rel_residual(const double* As, const double* y, const double* b, double* red,
-                               double* rvec, int tid) {
-    // 4 threads per row
-    const int i = tid >> 2, q = tid & 3;
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-        s = fma(As[i * P + q * 16 + j], y[q * 16 + j], s);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (q == 0)
-        rvec[i] = s - b[i];
-    __syncthreads();
-    if (tid < 32) {
-        double d0 = rvec[tid], d1 = rvec[tid + 32];
-        double num = d0 * d0 + d1 * d1;
-        double den = b[tid] * b[tid] + b[tid + 32] * b[tid + 32];
-        for (int off = 16; off > 0; off >>= 1) {
-            num += __shfl_xor_sync(0xffffffffu, num, off);
-            den += __shfl_xor_sync(0xffffffffu, den, off);
-        }
-        if (tid == 0)
-            red[0] = sqrt(num) / sqrt(den);
-    }
-    __syncthreads();
-    return red[0];
-}
-
-__device__ bool all_finite64(const double* v, int tid, int* flag) {
-    if (tid == 0)
-        *flag = 1;
-    __syncthreads();
-    if (tid < N && !isfinite(v[tid]))
-        *flag = 0;
-    __syncthreads();
-    return *flag != 0;
-}
-
-// DFT twiddles of the 64-point transform: (cos, sin)(2 pi m / 64)
-__constant__ double2 kTw[64];
-
-// exact singularity pre-screen: min_k |DFT(c)_k| < 1e-9 (k = 0..32 by conjugate symmetry)
-__device__ bool circ_singular(uint64_t mask, int tid, int* flag) {
-    if (tid == 0)
-        *flag = 0;
-    __syncthreads();
-    if (tid <= 32) {
-        const int k = tid;
-        double re = 0.0, im = 0.0;
-#pragma unroll 8
-        for (int j = 0; j < N; ++j) {
-            const double2 w = kTw[(j * k) & 63];
-            const double v = sgn(mask, j);
-            re = fma(v, w.x, re);
-            im = fma(-v, w.y, im);
-        }
-        if (sqrt(re * re + im * im) < 1e-9)
-            atomicOr(flag, 1);
-    }
-    __syncthreads();
-    return *flag != 0;
-}
-
-// mt19937_64 stream (seed, sid): 64 sign draws after discard(8) as a bitmask
-// (bit j set <=> c_j = -1), random_gen.cpp:22-31,55-57.  One thread; only the first
-// phase of the first twist is needed (new[i] for i < 72 < 156).
-__device__ uint64_t sign_mask_stream(uint64_t seed, uint64_t sid) {
+// 64 sign draws of stream (seed, sid) after discard(8) as a bitmask (random_gen.cpp:22-31,
+// 55-57).  One thread; only the first phase of the first twist is needed (new[i], i < 72 <
+// 156); the 228 seeding words are staged in `scratch` (shared) instead of a local array.
+__device__ uint64_t sign_mask_stream(uint64_t seed, uint64_t sid, uint64_t* scratch) {
     auto splitmix = [](uint64_t& st) {
         uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
         z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -259,23 +67,19 @@ __device__ uint64_t sign_mask_stream(uint64_t seed, uint64_t sid) {
         return z ^ (z >> 31);
     };
     uint64_t st = seed;
-    uint64_t a = splitmix(st);
+    const uint64_t a = splitmix(st);
     st ^= sid * 0xda942042e4dd58b5ULL + 0x2545f4914f6cdd1dULL;
-    uint64_t bb = splitmix(st);
-    uint64_t v = a ^ (bb << 1);
-    uint64_t lo[73], hi[72];
-    lo[0] = v;
+    const uint64_t b = splitmix(st);
+    uint64_t v = a ^ (b << 1);
+    scratch[0] = v;
     for (int i = 1; i < 156 + 72; ++i) {
         v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
-        if (i <= 72)
-            lo[i] = v;
-        if (i >= 156)
-            hi[i - 156] = v;
+        scratch[i] = v;
     }
     uint64_t mask = 0;
     for (int i = 8; i < 72; ++i) {
-        uint64_t y = (lo[i] & 0xFFFFFFFF80000000ULL) | (lo[i + 1] & 0x7FFFFFFFULL);
-        uint64_t z = hi[i] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+        const uint64_t y = (scratch[i] & 0xFFFFFFFF80000000ULL) | (scratch[i + 1] & 0x7FFFFFFFULL);
+        uint64_t z = scratch[i + 156] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
         z ^= (z >> 29) & 0x5555555555555555ULL;
         z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
         z ^= (z << 37) & 0xFFF7EEE000000000ULL;
@@ -286,136 +90,361 @@ __device__ uint64_t sign_mask_stream(uint64_t seed, uint64_t sid) {
     return mask;
 }
 
-struct Smem {
-    double rowbuf[2 * N];
-    double bv[N], yv[N], zv[N], rv[N], red[2];
-    uint64_t mask;
-    int flag;
-};
-
-// One preconditioned attempt (genp.cpp:250-281) with circulant mask on the system in
-// As: returns 0 = solved (residual in *res), 1 = PivotBreakdown.  y left in S.yv.
-__device__ int attempt(const double* As, double* Ws, Smem& S, uint64_t mask, int refine, int tid,
-                       double* res, double* pmn, double* pmx) {
-    const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-    Regs W;
-    circ_right_dmma(As, mask, warp, g, t, W);
-    if (lu_regs(W, 1e-300, S.rowbuf, warp, g, t, lane, pmn, pmx))
-        return 1;
-    regs_to_smem(W, Ws, warp, g, t);
-    if (tid < N)
-        S.zv[tid] = S.bv[tid];
-    __syncthreads();
-    if (warp == 0) {
-        lu_solve_warp(Ws, S.zv, lane);
-        __syncwarp();
-        circ_vec_warp(mask, S.zv, S.yv, lane);
+__device__ __forceinline__ void load_A(Smem& S, const double* __restrict__ Ag, int t) {
+#pragma unroll 8
+    for (int e = t; e < N * N / 2; e += N) {
+        const double2 v = reinterpret_cast<const double2*>(Ag)[e];
+        const int i = (2 * e) >> 6, j = (2 * e) & 63;
+        *reinterpret_cast<double2*>(S.X + i * XP + j) = v;
     }
-    __syncthreads();
-    for (int s = 0; s < refine; ++s) {
-        // r = b - A y ; w = solve(r) ; d = C w ; y += d   (genp.cpp:263-274)
-        {
-            const int i = tid >> 2, q = tid & 3;
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                acc = fma(As[i * P + q * 16 + j], S.yv[q * 16 + j], acc);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-            if (q == 0)
-                S.zv[i] = S.bv[i] - acc;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            lu_solve_warp(Ws, S.zv, lane);
-            __syncwarp();
-            circ_vec_warp(mask, S.zv, S.rv, lane);
-            __syncwarp();
-            S.yv[lane] += S.rv[lane];
-            S.yv[lane + 32] += S.rv[lane + 32];
-        }
-        __syncthreads();
-    }
-    *res = rel_residual(As, S.yv, S.bv, S.red, S.rv, tid);
-    return 0;
 }
 
-// One CTA per system; the whole redraw protocol (8 attempts on stream
-// sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) runs in-kernel.
-// Pass 0 skips attempts whose circulant is exactly singular (DFT pre-screen); if a
-// system accepts no attempt in pass 0 while some were skipped, pass 1 reruns the exact
-// reference protocol without the pre-screen so the kept "best" attempt is identical.
-__global__ void __launch_bounds__(THREADS) k_batched_circ64(
-    const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs0,
-    uint64_t seed, const uint64_t* __restrict__ sids, int refine, double* __restrict__ X,
-    rl_precond_report* __restrict__ rep, int* __restrict__ status) {
-    extern __shared__ double dsm[];
-    double* As = dsm;         // N x P
-    double* Ws = dsm + N * P; // N x P
-    __shared__ Smem S;
-    const int sys = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-    const double* Ag = A + static_cast<size_t>(sys) * N * N;
-    for (int e = tid; e < N * N / 2; e += THREADS) {
-        double2 v = reinterpret_cast<const double2*>(Ag)[e];
-        int i = (2 * e) / N, j = (2 * e) % N;
-        As[i * P + j] = v.x;
-        As[i * P + j + 1] = v.y;
-    }
-    if (tid < N)
-        S.bv[tid] = B[static_cast<size_t>(sys) * N + tid];
-    if (warp == 0) {
-        const double* sg = signs0 + static_cast<size_t>(sys) * N;
-        unsigned lo = __ballot_sync(0xffffffffu, sg[lane] < 0.0);
-        unsigned hi = __ballot_sync(0xffffffffu, sg[lane + 32] < 0.0);
-        if (lane == 0)
-            S.mask = (static_cast<uint64_t>(hi) << 32) | lo;
-    }
-    __syncthreads();
-    rl_precond_report r{};
-    // raw-GENP contrast arm on A (genp.cpp:222-234), pivot floor 0
-    {
-        Regs W;
+// W = A C: X holds A on entry; W lands in the register rows (X is clobbered).
+__device__ __forceinline__ void circ_product(Smem& S, uint64_t mask, int t, double (&w)[N]) {
+    const int lane = t & 31, warp = t >> 5, g = lane >> 2, q = lane & 3;
+    double acc[4][8][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jb = 0; jb < 8; ++jb)
+            acc[i][jb][0] = acc[i][jb][1] = 0.0;
+#pragma unroll 2
+    for (int kk = 0; kk < N; kk += 4) {
+        const int k = kk + q;
+        double af[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            af[i] = S.X[(32 * warp + 8 * i + g) * XP + k];
 #pragma unroll
         for (int jb = 0; jb < 8; ++jb) {
-            W.v[jb][0] = As[(8 * warp + g) * P + 8 * jb + 2 * t];
-            W.v[jb][1] = As[(8 * warp + g) * P + 8 * jb + 2 * t + 1];
+            const double bf = sgn(mask, k - (8 * jb + g)); // C[k][8 jb + g]
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dmma(acc[i][jb], af[i], bf);
         }
-        lu_regs(W, 0.0, S.rowbuf, warp, g, t, lane, &r.raw_pivot_min, &r.raw_pivot_max);
-        regs_to_smem(W, Ws, warp, g, t);
-        if (tid < N)
-            S.zv[tid] = S.bv[tid];
-        __syncthreads();
-        if (warp == 0)
-            lu_solve_warp(Ws, S.zv, lane);
-        __syncthreads();
-        bool fin = all_finite64(S.zv, tid, &S.flag);
-        r.raw_residual = fin ? rel_residual(As, S.zv, S.bv, S.red, S.rv, tid) : INFINITY;
     }
+    __syncthreads(); // every read of A is done
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jb = 0; jb < 8; ++jb)
+            *reinterpret_cast<double2*>(S.X + (32 * warp + 8 * i + g) * XP + 8 * jb + 2 * q) =
+                make_double2(acc[i][jb][0], acc[i][jb][1]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+        w[j] = S.X[t * XP + j];
+}
+
+// One pivot step K (static) of the in-warp elimination of rows base..base+31
+// (lane = row - base).  The pivot row goes through rb (64 entries, 1/p in rb[64]).
+template <int K>
+__device__ __forceinline__ void elim_step(double (&w)[N], double* rb, int lane, int base, double floor,
+                                          double& my_rcp, bool& brk, double& pmn, double& pmx) {
+    const int owner = K - base;
+    if (lane == owner) {
+#pragma unroll
+        for (int j = K; j < N; ++j)
+            rb[j] = w[j];
+        const double p = w[K];
+        rb[N] = (p == 0.0) ? 0.0 : 1.0 / p;
+        my_rcp = rb[N];
+    }
+    __syncwarp();
+    const double p = rb[K], rc = rb[N];
+    const double ap = fabs(p);
+    pmn = (K == 0) ? ap : min_fold(pmn, ap);
+    pmx = (K == 0) ? ap : max_fold(pmx, ap);
+    brk |= ap < floor;
+    if (lane > owner) {
+        const double m = w[K] * rc;
+        w[K] = m;
+        if (m != 0.0) {
+#pragma unroll
+            for (int j = K + 1; j < N; ++j)
+                w[j] = fma(-m, rb[j], w[j]);
+        }
+    }
+}
+
+template <int K0, int K1>
+struct Elim {
+    __device__ __forceinline__ static void run(double (&w)[N], double* rbuf, int lane, int base, double floor,
+                                               double& my_rcp, bool& brk, double& pmn, double& pmx) {
+        elim_step<K0>(w, rbuf + (K0 & 1) * XP, lane, base, floor, my_rcp, brk, pmn, pmx);
+        Elim<K0 + 1, K1>::run(w, rbuf, lane, base, floor, my_rcp, brk, pmn, pmx);
+    }
+};
+template <int K1>
+struct Elim<K1, K1> {
+    __device__ __forceinline__ static void run(double (&)[N], double*, int, int, double, double&, bool&, double&,
+                                               double&) {}
+};
+
+// rows 32..63: apply the published U rows K0..K1-1 (read-only shared data, no sync inside)
+template <int K0, int K1>
+struct Apply {
+    __device__ __forceinline__ static void run(double (&w)[N], const Smem& S) {
+        const double m = w[K0] * S.rcp[K0];
+        w[K0] = m;
+        if (m != 0.0) {
+#pragma unroll
+            for (int j = K0 + 1; j < N; ++j)
+                w[j] = fma(-m, S.X[K0 * XP + j], w[j]);
+        }
+        Apply<K0 + 1, K1>::run(w, S);
+    }
+};
+template <int K1>
+struct Apply<K1, K1> {
+    __device__ __forceinline__ static void run(double (&)[N], const Smem&) {}
+};
+
+// Warp-split no-pivot LU of the 64 register rows.  S.flag must be 0 on entry.  Returns
+// breakdown (some |p| < floor); pmin/pmax over all pivots (every thread); my_rcp = 1/U_tt.
+__device__ __forceinline__ bool lu_rows(double (&w)[N], Smem& S, double floor, int t, double& my_rcp,
+                                        double& pmin, double& pmax) {
+    const int lane = t & 31, warp = t >> 5;
+    bool brk = false;
+    double pmn = 0.0, pmx = 0.0;
+    if (warp == 0)
+        Elim<0, 32>::run(w, S.X, lane, 0, floor, my_rcp, brk, pmn, pmx);
+    __syncthreads(); // the pivot-row buffers in X are free
+    if (warp == 0) { // publish rows 0..31 (U part read by warp 1) and 1/U_kk
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            S.X[t * XP + j] = w[j];
+        S.rcp[t] = my_rcp;
+        if (lane == 0) {
+            S.pm[0] = pmn;
+            S.pm[1] = pmx;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        Apply<0, 32>::run(w, S);
+        Elim<32, 64>::run(w, S.X + 34 * XP, lane, 32, floor, my_rcp, brk, pmn, pmx);
+        if (lane == 0) {
+            S.pm[2] = pmn;
+            S.pm[3] = pmx;
+        }
+    }
+    if (brk)
+        S.flag = 1;
+    __syncthreads();
+    pmin = min_fold(S.pm[0], S.pm[2]);
+    pmax = max_fold(S.pm[1], S.pm[3]);
+    return S.flag != 0;
+}
+
+// z = U^{-1} L^{-1} v for the register rows (v = this thread's rhs entry); z_t returned and
+// published in S.v0 (genp.cpp:106-124: forward unit-L, then backward U).
+__device__ __forceinline__ double solve_rows(const double (&w)[N], Smem& S, double v, double my_rcp, int t) {
+    const int lane = t & 31, warp = t >> 5;
+    if (warp == 0) { // forward, rows 0..31
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const double yj = __shfl_sync(0xffffffffu, v, j);
+            if (lane > j)
+                v = fma(-w[j], yj, v);
+        }
+        S.v0[t] = v;
+    }
+    __syncthreads();
+    if (warp == 1) { // forward, rows 32..63, then backward 63..32
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            v = fma(-w[j], S.v0[j], v);
+#pragma unroll
+        for (int j = 32; j < 64; ++j) {
+            const double yj = __shfl_sync(0xffffffffu, v, j - 32);
+            if (lane > j - 32)
+                v = fma(-w[j], yj, v);
+        }
+#pragma unroll
+        for (int j = 63; j >= 32; --j) {
+            const double xj = __shfl_sync(0xffffffffu, v * my_rcp, j - 32);
+            if (lane == j - 32)
+                v = xj;
+            else if (lane < j - 32)
+                v = fma(-w[j], xj, v);
+        }
+        S.v0[t] = v;
+    }
+    __syncthreads();
+    if (warp == 0) { // backward, rows 31..0
+#pragma unroll
+        for (int j = 32; j < 64; ++j)
+            v = fma(-w[j], S.v0[j], v);
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+            const double xj = __shfl_sync(0xffffffffu, v * my_rcp, j);
+            if (lane == j)
+                v = xj;
+            else if (lane < j)
+                v = fma(-w[j], xj, v);
+        }
+        S.v0[t] = v;
+    }
+    __syncthreads();
+    return v;
+}
+
+// (C z)_t, z in S.v0
+__device__ __forceinline__ double circ_vec(const Smem& S, uint64_t mask, int t) {
+    double y = 0.0;
+#pragma unroll 16
+    for (int j = 0; j < N; ++j)
+        y = fma(sgn(mask, t - j), S.v0[j], y);
+    return y;
+}
+
+// CTA-wide sum (64 threads), result in every thread
+__device__ __forceinline__ double cta_sum(Smem& S, double a, int t) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((t & 31) == 0)
+        S.red[t >> 5] = a;
+    __syncthreads();
+    const double s = S.red[0] + S.red[1];
+    __syncthreads();
+    return s;
+}
+
+// (A y)_t - b_t, A's row t from global (L2), y in S.v1
+__device__ __forceinline__ double row_residual(const double* __restrict__ Ag, const Smem& S, double bt, int t) {
+    const double2* row = reinterpret_cast<const double2*>(Ag + t * N);
+    double s = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < N / 2; ++j) {
+        const double2 a = row[j];
+        s = fma(a.x, S.v1[2 * j], s);
+        s = fma(a.y, S.v1[2 * j + 1], s);
+    }
+    return s - bt;
+}
+
+// exact singularity pre-screen: min_k |DFT(c)_k| < 1e-9 (k = 0..32 by conjugate symmetry)
+__device__ bool circ_singular(Smem& S, uint64_t mask, int t) {
+    if (t == 0)
+        S.flag = 0;
+    __syncthreads();
+    if (t <= 32) {
+        double re = 0.0, im = 0.0;
+#pragma unroll 8
+        for (int j = 0; j < N; ++j) {
+            const double2 w = S.tw[(j * t) & 63];
+            const double v = sgn(mask, j);
+            re = fma(v, w.x, re);
+            im = fma(-v, w.y, im);
+        }
+        if (sqrt(re * re + im * im) < 1e-9)
+            S.flag = 1;
+    }
+    __syncthreads();
+    const bool r = S.flag != 0;
+    __syncthreads();
+    return r;
+}
+
+// One CTA per system; the raw arm and the whole redraw protocol (8 attempts on stream
+// sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) run in-kernel.
+__global__ void __launch_bounds__(N) k_batched_circ64(const double* __restrict__ A, const double* __restrict__ B,
+                                                      const double* __restrict__ signs0, uint64_t seed,
+                                                      const uint64_t* __restrict__ sids, int refine,
+                                                      double* __restrict__ X, rl_precond_report* __restrict__ rep,
+                                                      int* __restrict__ status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    const int t = threadIdx.x, lane = t & 31;
+    const uint64_t sys = blockIdx.x;
+    const double* Ag = A + sys * N * N;
+    const double bt = B[sys * N + t];
+    {
+        const unsigned bal = __ballot_sync(0xffffffffu, signs0[sys * N + t] < 0.0);
+        if (lane == 0)
+            S.bal[t >> 5] = bal;
+        double s, c;
+        sincospi(static_cast<double>(t) / 32.0, &s, &c);
+        S.tw[t] = make_double2(c, s);
+    }
+    __syncthreads();
+    if (t == 0)
+        S.mask0 = (static_cast<uint64_t>(S.bal[1]) << 32) | S.bal[0];
+    const double bsq = cta_sum(S, bt * bt, t);
     const uint64_t sid = sids[sys];
-    double* xg = X + static_cast<size_t>(sys) * N;
+    double* xg = X + sys * N;
+    rl_precond_report r{};
+    r.attempt = -1;
     int st = RL_PIVOT_BREAKDOWN;
+    double w[N];
+    double my_rcp = 0.0;
+    // pass 0: raw arm (a = -1) + pre-screened protocol; pass 1 (rare): exact protocol
     for (int pass = 0; pass < 2; ++pass) {
         bool have_best = false, skipped = false, accepted = false;
         double best_res = 0.0;
-        for (int a = 0; a < 8; ++a) {
-            if (a > 0 || pass > 0) { // redraw: signs of stream (sid + 7919 a) ^ 0x5000...
-                if (tid == 0)
-                    S.mask = (a == 0) ? S.mask : sign_mask_stream(seed, (sid + 7919ULL * a) ^ 0x5000000000000000ULL);
+        for (int a = (pass == 0 ? -1 : 0); a < 8; ++a) {
+            uint64_t mask = 0;
+            if (a >= 0) {
+                __syncthreads(); // X is free
+                if (a == 0) {
+                    mask = S.mask0;
+                } else {
+                    if (t == 0)
+                        S.mask = sign_mask_stream(seed, (sid + 7919ULL * static_cast<uint64_t>(a)) ^
+                                                            0x5000000000000000ULL,
+                                                  reinterpret_cast<uint64_t*>(S.X));
+                    __syncthreads();
+                    mask = S.mask;
+                }
+                if (pass == 0 && circ_singular(S, mask, t)) {
+                    skipped = true;
+                    continue;
+                }
+            }
+            __syncthreads();
+            load_A(S, Ag, t);
+            if (t == 0)
+                S.flag = 0;
+            __syncthreads();
+            if (a < 0) {
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    w[j] = S.X[t * XP + j];
+            } else {
+                circ_product(S, mask, t, w);
+            }
+            __syncthreads();
+            double pmn, pmx;
+            const bool brk = lu_rows(w, S, a < 0 ? 0.0 : 1e-300, t, my_rcp, pmn, pmx);
+            if (a >= 0 && brk)
+                continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
+            double z = solve_rows(w, S, bt, my_rcp, t);
+            double y = (a < 0) ? z : circ_vec(S, mask, t);
+            __syncthreads();
+            S.v1[t] = y;
+            __syncthreads();
+            for (int s = 0; a >= 0 && s < refine; ++s) { // genp.cpp:263-274
+                const double rr = -row_residual(Ag, S, bt, t); // b - A y
+                z = solve_rows(w, S, rr, my_rcp, t);           // (barrier before its first write)
+                y += circ_vec(S, mask, t);
+                __syncthreads();
+                S.v1[t] = y;
                 __syncthreads();
             }
-            const uint64_t mask = S.mask;
-            if (pass == 0 && circ_singular(mask, tid, &S.flag)) {
-                skipped = true;
+            const double e = row_residual(Ag, S, bt, t);
+            const double res = sqrt(cta_sum(S, e * e, t)) / sqrt(bsq);
+            if (a < 0) { // contrast arm: non-finite solution -> +inf (genp.cpp:226-231)
+                const int fin = __syncthreads_and(isfinite(y));
+                r.raw_residual = fin ? res : INFINITY;
+                r.raw_pivot_min = pmn;
+                r.raw_pivot_max = pmx;
                 continue;
             }
-            double res, pmn, pmx;
-            if (attempt(As, Ws, S, mask, refine, tid, &res, &pmn, &pmx) != 0)
-                continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
             const bool acc = res <= 1e-7;
             if (acc || !have_best || res < best_res) {
-                if (tid < N)
-                    xg[tid] = S.yv[tid];
+                xg[t] = y;
                 r.residual = res;
                 r.pivot_min = pmn;
                 r.pivot_max = pmx;
@@ -433,17 +462,8 @@ __global__ void __launch_bounds__(THREADS) k_batched_circ64(
             st = 0;
         if (accepted || !skipped)
             break;
-        // pass 1: the exact protocol from attempt 0 (restore the attempt-0 mask)
-        if (warp == 0) {
-            const double* sg = signs0 + static_cast<size_t>(sys) * N;
-            unsigned lo = __ballot_sync(0xffffffffu, sg[lane] < 0.0);
-            unsigned hi = __ballot_sync(0xffffffffu, sg[lane + 32] < 0.0);
-            if (lane == 0)
-                S.mask = (static_cast<uint64_t>(hi) << 32) | lo;
-        }
-        __syncthreads();
     }
-    if (tid == 0) {
+    if (t == 0) {
         if (r.attempts_drawn == 0)
             r.attempts_drawn = 8;
         rep[sys] = r;
@@ -452,40 +472,25 @@ __global__ void __launch_bounds__(THREADS) k_batched_circ64(
     }
 }
 
-void init_twiddles() {
-    static bool done[16] = {};
-    int dev = ctx().device & 15;
-    if (done[dev])
-        return;
-    double2 tw[64];
-    for (int m = 0; m < 64; ++m) {
-        const double ang = 3.14159265358979323846 * static_cast<double>(m) / 32.0;
-        tw[m] = make_double2(std::cos(ang), std::sin(ang));
-    }
-    RL_CUDA(cudaMemcpyToSymbol(kTw, tw, sizeof(tw)));
-    done[dev] = true;
-}
-
 } // namespace
 
 // Returns RL_OK or RL_PIVOT_BREAKDOWN (some system broke down on every attempt).
 rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int refine, uint64_t seed,
                          const uint64_t* d_sids, double* dX, rl_precond_report* d_rep) {
     cudaStream_t st = stream();
-    constexpr size_t kDynSmem = 2 * N * P * sizeof(double);
+    constexpr size_t kSmem = sizeof(Smem);
     static bool attr[16] = {};
     if (!attr[ctx().device & 15]) {
         RL_CUDA(cudaFuncSetAttribute(k_batched_circ64, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kDynSmem)));
+                                     static_cast<int>(kSmem)));
         attr[ctx().device & 15] = true;
     }
-    init_twiddles();
     double* signs = ws<double>(WS_TMP1, batch * N + 1);
     int* d_status = reinterpret_cast<int*>(signs + batch * N);
     rng_sign_vectors_batched(seed, d_sids, 0, 0x5000000000000000ULL, batch, N, signs);
     RL_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), st));
-    k_batched_circ64<<<static_cast<unsigned>(batch), THREADS, kDynSmem, st>>>(dA, dB, signs, seed, d_sids,
-                                                                            refine, dX, d_rep, d_status);
+    k_batched_circ64<<<static_cast<unsigned>(batch), N, kSmem, st>>>(dA, dB, signs, seed, d_sids, refine, dX,
+                                                                      d_rep, d_status);
     RL_LAUNCHED();
     int h = 0;
     RL_CUDA(cudaMemcpyAsync(&h, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -132,18 +132,28 @@ __device__ __forceinline__ void emit_block(const uint64_t* w, int64_t o0, int64_
                                            const GenParams& p, int lane) {
     if (p.kind == static_cast<int>(Draw::Gaussian)) {
         // pairs (o, o+1) with o even: entries o (cos) and o+1 (sin)
-        for (int q = lane; q < kN / 2; q += 32) {
-            int64_t o = o0 + 2 * q;
+        // two independent Box-Muller pairs per iteration (q, q + 32): branch-free bodies so
+        // the two double-double chains interleave (ILP for the latency-bound FP64 pipe)
+        double* out = static_cast<double*>(p.out) - p.base;
+        auto store = [&](int q, double g0, double g1) {
+            const int64_t o = o0 + 2 * q;
             if (o < lo || o >= hi)
-                continue;
-            double g0, g1;
-            box_muller(temper(w[2 * q]), temper(w[2 * q + 1]), p.mu, p.sigma, &g0, &g1);
-            double* out = static_cast<double*>(p.out) - p.base;
-            if (static_cast<uint64_t>(o) + 1 < p.count) {
+                return;
+            if (static_cast<uint64_t>(o) + 1 < p.count)
                 *reinterpret_cast<double2*>(out + o) = make_double2(g0, g1);
-            } else {
+            else
                 out[o] = g0;
-            }
+        };
+        for (int q0 = lane; q0 < kN / 2; q0 += 64) {
+            const int q1 = q0 + 32;
+            const bool v1 = q1 < kN / 2;
+            const int qq = v1 ? q1 : q0;
+            double g00, g01, g10, g11;
+            box_muller(temper(w[2 * q0]), temper(w[2 * q0 + 1]), p.mu, p.sigma, &g00, &g01);
+            box_muller(temper(w[2 * qq]), temper(w[2 * qq + 1]), p.mu, p.sigma, &g10, &g11);
+            store(q0, g00, g01);
+            if (v1)
+                store(q1, g10, g11);
         }
         return;
     }
