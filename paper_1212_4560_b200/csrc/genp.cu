@@ -16,6 +16,9 @@
 // Without pivoting the panel is embarrassingly parallel: there is no tall
 // sequential panel factorisation on the critical path.
 #include "panel.cuh"
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -503,8 +506,20 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         ctx().stream = keep;
     };
     constexpr uint64_t W = 2 * NB;
+    // RL_LU_TRACE=1: per outer step, time of the panel path (s2) and of the step on s1 (dev)
+    static const bool trace = std::getenv("RL_LU_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace)
+            return;
+        cudaEvent_t e;
+        RL_CUDA(cudaEventCreate(&e));
+        RL_CUDA(cudaEventRecord(e, st));
+        tev.push_back(e);
+    };
     panel256(0, s1);
     for (uint64_t o = 0; o + W < n; o += W) {
+        mark(s1);
         const uint64_t rest = n - o - W;                 // trailing size after this outer step
         const uint64_t w2 = std::min<uint64_t>(W, rest); // width of the next outer panel
         const double* L21 = at(o + W, o);                // rest x 256
@@ -518,13 +533,31 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         cudaEvent_t strips = la.ev[0], done = la.ev[1];
         RL_CUDA(cudaEventRecord(strips, s1));
         RL_CUDA(cudaStreamWaitEvent(s2, strips, 0));
+        mark(s2);
         panel256(o + W, s2);
+        mark(s2);
         RL_CUDA(cudaEventRecord(done, s2));
         // (ii) ... while the main stream runs the remaining trailing update (K = 256)
         if (rest > w2)
             gemm(false, false, rest - w2, rest - w2, W, -1.0, at(o + W + w2, o), lda, at(o, o + W + w2), lda, 1.0,
                  at(o + W + w2, o + W + w2), lda);
+        mark(s1);
         RL_CUDA(cudaStreamWaitEvent(s1, done, 0));
+    }
+    mark(s1);
+    if (trace) { // per step: [s1 start, s2 start, s2 end, s1 trailing end], then the final mark
+        RL_CUDA(cudaEventSynchronize(tev.back()));
+        for (size_t i = 0; i + 4 < tev.size(); i += 4) {
+            float strip = 0, panel = 0, trail = 0, step = 0;
+            cudaEventElapsedTime(&strip, tev[i], tev[i + 1]);
+            cudaEventElapsedTime(&panel, tev[i + 1], tev[i + 2]);
+            cudaEventElapsedTime(&trail, tev[i + 1], tev[i + 3]);
+            cudaEventElapsedTime(&step, tev[i], tev[i + 4]);
+            std::fprintf(stderr, "lu step %3zu rest %6llu: strips %.3f panel %.3f trailing %.3f step %.3f ms\n",
+                         i / 4, static_cast<unsigned long long>(n - (i / 4 + 1) * W), strip, panel, trail, step);
+        }
+        for (auto e : tev)
+            cudaEventDestroy(e);
     }
 }
 

@@ -3,6 +3,9 @@ sys.path.insert(0, ".")
 import torch
 import paper_1212_4560_b200 as rl
 shapes = [(8192, 8192, 8192), (8064, 8064, 128), (4096, 4096, 128), (2048, 2048, 128), (8064, 128, 128), (128, 8064, 128)]
+if len(sys.argv) > 1 and sys.argv[1] == "small":
+    shapes = [(7936, 128, 128), (128, 7936, 128), (7936, 256, 256), (256, 7680, 256), (2048, 256, 256),
+              (256, 2048, 256), (1024, 1024, 256), (2048, 2048, 256), (4096, 4096, 256), (7680, 7680, 256)]
 big = torch.randn(2 * 8192 * 8192 + 1024, dtype=torch.float64, device="cuda")
 C = torch.randn(8192 * 8192, dtype=torch.float64, device="cuda")
 for (m, n, k) in shapes:
