@@ -239,98 +239,6 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_panel_trsm(double* a, uint64_
     }
 }
 
-// Diagonal-panel substitution of the multi-RHS solves (genp.cpp:106-124) on a bs x nrhs
-// slice of B: lower = unit-lower forward, upper = backward with x_i = s * (1/U_ii)
-// (within 1 ulp of the reference's division).  Blocks beyond bs are padded with the
-// identity; off-diagonal updates outside the 128-block are DMMA GEMMs (host loop).
-constexpr int SV_MAXRHS = 32;
-constexpr int SV_ROWS = 64;
-constexpr int SVP = SV_MAXRHS + 4;
-__global__ void __launch_bounds__(PK_THREADS, 1) k_block_solve(const double* __restrict__ lu, uint64_t lda,
-                                                               uint64_t n, uint64_t o, double* __restrict__ b,
-                                                               uint64_t ldb, int nrhs, int lower) {
-    extern __shared__ double T[]; // NB x PT, then Bs NB x SVP
-    double* Bs = T + NB * PT;
-    __shared__ double rcp[NB];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
-    const double* diag = lu + o * lda + o;
-    if (lower)
-        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, bs, bs, [](int i, int j) { return i > j; },
-                                             [](int, int) { return 0.0; });
-    else
-        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, bs, bs, [](int i, int j) { return j >= i; },
-                                             [](int i, int j) { return i == j ? 1.0 : 0.0; });
-    const int n8 = (nrhs + 7) & ~7;
-    panel::load_tile<NB, SV_MAXRHS, PK_THREADS>(Bs, SVP, b + o * ldb, ldb, bs, nrhs, [](int, int) { return true; },
-                                                [](int, int) { return 0.0; });
-    __syncthreads();
-    if (!lower)
-        for (int i = tid; i < NB; i += PK_THREADS)
-            rcp[i] = 1.0 / T[i * PT + i];
-    __syncthreads();
-    if (lower) {
-        for (int c0 = 0; c0 < NB; c0 += SB) {
-            for (int c = tid; c < nrhs; c += PK_THREADS) {
-                double y[SB];
-#pragma unroll
-                for (int i = 0; i < SB; ++i)
-                    y[i] = Bs[(c0 + i) * SVP + c];
-#pragma unroll
-                for (int i = 1; i < SB; ++i)
-#pragma unroll
-                    for (int l = 0; l < i; ++l)
-                        y[i] = fma(-T[(c0 + i) * PT + c0 + l], y[l], y[i]);
-#pragma unroll
-                for (int i = 1; i < SB; ++i)
-                    Bs[(c0 + i) * SVP + c] = y[i];
-            }
-            __syncthreads();
-            if (c0 + SB < NB)
-                panel::smem_update16(Bs + (c0 + SB) * SVP, SVP, T + (c0 + SB) * PT + c0, PT, Bs + c0 * SVP, SVP,
-                                     NB - c0 - SB, n8, warp, PK_WARPS, lane);
-            __syncthreads();
-        }
-    } else {
-        for (int c0 = NB - SB; c0 >= 0; c0 -= SB) {
-            for (int c = tid; c < nrhs; c += PK_THREADS) {
-                double y[SB];
-#pragma unroll
-                for (int i = 0; i < SB; ++i)
-                    y[i] = Bs[(c0 + i) * SVP + c];
-#pragma unroll
-                for (int i = SB - 1; i >= 0; --i) {
-                    const double xi = y[i] * rcp[c0 + i];
-                    y[i] = xi;
-#pragma unroll
-                    for (int l = 0; l < i; ++l)
-                        y[l] = fma(-T[(c0 + l) * PT + c0 + i], xi, y[l]);
-                }
-#pragma unroll
-                for (int i = 0; i < SB; ++i)
-                    Bs[(c0 + i) * SVP + c] = y[i];
-            }
-            __syncthreads();
-            if (c0 > 0)
-                panel::smem_update16(Bs, SVP, T + c0, PT, Bs + c0 * SVP, SVP, c0, n8, warp, PK_WARPS, lane);
-            __syncthreads();
-        }
-    }
-    panel::store_tile<NB, SV_MAXRHS, PK_THREADS>(b + o * ldb, ldb, Bs, SVP, bs, nrhs);
-}
-
-// diagonal 128-blocks of a packed LU -> contiguous [nblk][NB][NB] (ragged last block)
-__global__ void k_gather_diag(const double* __restrict__ lu, uint64_t lda, uint64_t n, double* __restrict__ out) {
-    const uint64_t o = static_cast<uint64_t>(blockIdx.x) * NB;
-    const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
-    double* dst = out + static_cast<uint64_t>(blockIdx.x) * NB * NB;
-    for (int e = threadIdx.x; e < bs * NB; e += blockDim.x) {
-        const int i = e / NB, j = e % NB;
-        if (j < bs)
-            dst[i * NB + j] = lu[(o + i) * lda + o + j];
-    }
-}
-
 __global__ void k_copy2d(uint64_t rows, uint64_t cols, const double* src, uint64_t lds, double* dst,
                          uint64_t ldd) {
     uint64_t total = rows * cols;
@@ -395,9 +303,202 @@ __global__ void k_colnorm_ratio(uint64_t n, uint64_t nrhs, const double* r, cons
     }
 }
 
+// Wavefront block substitution (genp.cpp:106-124, forward unit-L / backward U) for up to
+// WV_MAXRHS right-hand sides: one CTA per 128-row block, all launched at once.  A CTA takes
+// its block from an atomic ticket (so a CTA only ever waits on blocks owned by CTAs that
+// are already running: no deadlock whatever the residency), stages its diagonal triangle,
+// then for every earlier block j (in order, deterministic) prefetches the 128 x 128 block
+// L[b][j] into registers, waits for block j's published solution (acquire flag) and
+// accumulates L[b][j] x_j on DMMA; finally it substitutes its own 128 rows (one warp per
+// right-hand side, shuffle chain) and publishes x_b (release flag).  The critical path per
+// block is one 128 x 128 x nrhs product plus one 128-step substitution, instead of a block
+// solve launch plus a GEMM launch.
+constexpr int WV_THREADS = 512;
+constexpr int WV_MAXRHS = 32;
+constexpr int XJP = WV_MAXRHS + 4; // staged x_j pitch: B-fragment reads conflict-free
+__host__ __device__ constexpr size_t wave_smem_bytes() {
+    return (static_cast<size_t>(NB) * NB + static_cast<size_t>(WV_MAXRHS) * NB + NB + static_cast<size_t>(NB) * XJP) *
+           sizeof(double);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// RL_WAVE_TRACE=1 (dev): per-block %globaltimer stamps of the wavefront phases
+__device__ unsigned long long g_wave_ts[2][512][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+
+template <bool LOWER>
+__global__ void __launch_bounds__(WV_THREADS, 1) k_trsv_wave(const double* __restrict__ lu, uint64_t lda, uint64_t n,
+                                                             double* b, uint64_t ldb, int nrhs, int* sync,
+                                                             int trace) {
+    extern __shared__ __align__(16) double wsm[];
+    double* Dt = wsm;                       // Dt[k * NB + i] = D[i][k] (triangle, transposed)
+    double* xs = wsm + NB * NB;             // xs[c * NB + i]
+    double* rcp = xs + WV_MAXRHS * NB;      // 1 / U_ii (upper)
+    double* xj_s = rcp + NB;                // x_j staged: xj_s[k * XJP + c]
+    __shared__ int s_blk;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int nblk = static_cast<int>((n + NB - 1) / NB);
+    if (tid == 0) {
+        const int tk = atomicAdd(&sync[0], 1);
+        s_blk = LOWER ? tk : nblk - 1 - tk;
+    }
+    __syncthreads();
+    const int bi = s_blk;
+    const uint64_t o = static_cast<uint64_t>(bi) * NB;
+    const int bs = static_cast<int>(n - o < NB ? n - o : NB);
+    for (int e = tid; e < NB * NB; e += WV_THREADS) {
+        const int i = e >> 7, k = e & (NB - 1);
+        const double v = (i < bs && k < bs) ? lu[(o + i) * lda + o + k] : 0.0;
+        Dt[k * NB + i] = (LOWER ? (i > k) : (i < k)) ? v : 0.0;
+        if (!LOWER && i == k)
+            rcp[i] = (i < bs) ? 1.0 / v : 1.0;
+    }
+    // sum_j D[b][j] x_j over the finished blocks (DMMA m8n8k4: warp w owns rows 8w..8w+7)
+    const int r = 8 * warp + g;
+    const int nf = (nrhs + 7) >> 3;
+    double acc[4][4] = {}; // [f][chain * 2 + e]
+    const int nsteps = LOWER ? bi : nblk - 1 - bi;
+    unsigned long long ts[6] = {gtimer(), 0, 0, 0, 0, 0};
+    for (int s = 0; s < nsteps; ++s) {
+        const int j = LOWER ? s : nblk - 1 - s;
+        const uint64_t oj = static_cast<uint64_t>(j) * NB;
+        const int bj = static_cast<int>(n - oj < NB ? n - oj : NB);
+        double af[32];
+        const double* arow = lu + (o + (r < bs ? r : 0)) * lda + oj;
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) {
+            const int k = 4 * kk + t;
+            af[kk] = (r < bs && k < bj) ? arow[k] : 0.0;
+        }
+        if (tid == 0)
+            while (ld_acquire(&sync[1 + j]) == 0)
+                __nanosleep(32);
+        __syncthreads(); // also: every warp is done reading xj_s of the previous step
+        ts[1] = gtimer();
+        const double* xj = b + oj * ldb;
+        for (int e = tid; e < NB * WV_MAXRHS; e += WV_THREADS) {
+            const int k = e / WV_MAXRHS, c = e % WV_MAXRHS;
+            xj_s[k * XJP + c] = (k < bj && c < nrhs) ? __ldcg(xj + static_cast<uint64_t>(k) * ldb + c) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+            if (f < nf) {
+#pragma unroll
+                for (int kk = 0; kk < 32; ++kk) { // two independent accumulation chains
+                    const double bv = xj_s[(4 * kk + t) * XJP + 8 * f + g];
+                    double* ac = acc[f] + 2 * (kk & 1);
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                 : "+d"(ac[0]), "+d"(ac[1])
+                                 : "d"(af[kk]), "d"(bv));
+                }
+            }
+        }
+    }
+    ts[1] = ts[1] ? ts[1] : ts[0];
+    // In-block substitution on the DMMA accumulator layout: warp w keeps rows 8w..8w+7 of
+    // X = B_b - sum_j D[b][j] x_j as C fragments.  Per 8-row sub-block s (in sweep order) the
+    // owner warp s finishes its rows (8 x 8 triangle, one lane per right-hand side, through a
+    // double-buffered shared tile) and every warp still below (above) applies the solved
+    // 8 x nrhs block with two DMMA k-steps: one barrier per sub-block.
+    double X[4][2];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 8 * f + 2 * t + e;
+            X[f][e] = (f < nf && c < nrhs && r < bs) ? b[(o + r) * ldb + c] - (acc[f][e] + acc[f][2 + e]) : 0.0;
+        }
+    ts[2] = gtimer();
+#pragma unroll 1
+    for (int it = 0; it < NB / 8; ++it) {
+        const int sb = LOWER ? it : NB / 8 - 1 - it;
+        double* xt = xs + (it & 1) * (8 * WV_MAXRHS); // [i][c], 8 x 32
+        if (warp == sb) {
+            // coefficients of the 8 x 8 diagonal triangle (broadcast reads, independent of X)
+            double d[8][8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    d[i][k] = (LOWER ? (k < i) : (k > i)) ? Dt[(8 * sb + k) * NB + 8 * sb + i] : 0.0;
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+                if (f < nf)
+                    *reinterpret_cast<double2*>(xt + g * WV_MAXRHS + 8 * f + 2 * t) = make_double2(X[f][0], X[f][1]);
+            __syncwarp();
+            double v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                v[i] = xt[i * WV_MAXRHS + lane];
+            if (LOWER) {
+#pragma unroll
+                for (int i = 1; i < 8; ++i)
+#pragma unroll
+                    for (int k = 0; k < i; ++k)
+                        v[i] = fma(-d[i][k], v[k], v[i]);
+            } else {
+#pragma unroll
+                for (int i = 7; i >= 0; --i) {
+#pragma unroll
+                    for (int k = i + 1; k < 8; ++k)
+                        v[i] = fma(-d[i][k], v[k], v[i]);
+                    v[i] = v[i] * rcp[8 * sb + i];
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                xt[i * WV_MAXRHS + lane] = v[i];
+            if (lane < nrhs)
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (8 * sb + i < bs)
+                        b[(o + 8 * sb + i) * ldb + lane] = v[i];
+        }
+        __syncthreads();
+        if (LOWER ? (warp > sb) : (warp < sb)) {
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 4) {
+                const double a = -Dt[(8 * sb + kk + t) * NB + 8 * warp + g]; // -D[8w + g][8 sb + kk + t]
+#pragma unroll
+                for (int f = 0; f < 4; ++f)
+                    if (f < nf) {
+                        const double bv = xt[(kk + t) * WV_MAXRHS + 8 * f + g];
+                        asm volatile(
+                            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                            : "+d"(X[f][0]), "+d"(X[f][1])
+                            : "d"(a), "d"(bv));
+                    }
+            }
+        }
+    }
+    ts[3] = gtimer();
+    __syncthreads();
+    ts[4] = gtimer();
+    if (tid == 0) {
+        st_release(&sync[1 + bi], 1);
+        ts[5] = gtimer();
+        if (trace && bi < 512)
+            for (int q = 0; q < 6; ++q)
+                g_wave_ts[LOWER ? 0 : 1][bi][q] = ts[q];
+    }
+}
+
 size_t trsm_smem() { return (static_cast<size_t>(NB) * PT + static_cast<size_t>(NB) * (TR_TILE + 4)) * sizeof(double); }
 size_t diag_smem() { return static_cast<size_t>(NB) * PT * sizeof(double); }
-size_t solve_smem() { return static_cast<size_t>(NB) * (PT + SVP) * sizeof(double); }
 
 void prep_attrs() {
     static bool done[16] = {};
@@ -407,8 +508,10 @@ void prep_attrs() {
                                      static_cast<int>(trsm_smem())));
         RL_CUDA(cudaFuncSetAttribute(k_diag_lu, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(diag_smem())));
-        RL_CUDA(cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(solve_smem())));
+        RL_CUDA(cudaFuncSetAttribute(k_trsv_wave<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(wave_smem_bytes())));
+        RL_CUDA(cudaFuncSetAttribute(k_trsv_wave<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(wave_smem_bytes())));
 
         done[dev] = true;
     }
@@ -571,39 +674,41 @@ void genp_factor_dev(uint64_t n, double* a, uint64_t lda, double pivot_floor, do
 // Kept for the C-ABI signature (the solves need no precomputed block inverses).
 void genp_block_inverses(uint64_t, const double*, uint64_t, double*) {}
 
-// Forward (unit L) then backward (U) substitution, blocked: per 128-block a one-CTA
-// substitution on the diagonal panel + a DMMA GEMM update of the remaining rows;
-// b (n x nrhs, ldb) is overwritten by the solution (genp.cpp:106-124).
+// Forward (unit L) then backward (U) substitution (genp.cpp:106-124) as two wavefront
+// launches per slice of <= 32 right-hand sides; b (n x nrhs, ldb) is overwritten by the
+// solution.
 void genp_solve_blocked(uint64_t n, uint64_t nrhs, const double* lu, uint64_t lda, const double* aux,
                         double* b, uint64_t ldb) {
     (void)aux;
     prep_attrs();
     cudaStream_t st = stream();
-    const size_t sm = solve_smem();
-    // the 64 diagonal 128x128 blocks, gathered once into an L2-resident buffer (8 MiB at
-    // n = 8192) so each block solve reads its triangle from L2, not from the 512 MiB LU
     const uint64_t nblk = (n + NB - 1) / NB;
-    double* diag = ws<double>(WS_RF4, nblk * NB * NB);
-    k_gather_diag<<<static_cast<unsigned>(nblk), 256, 0, st>>>(lu, lda, n, diag);
-    RL_LAUNCHED();
-    for (uint64_t c0 = 0; c0 < nrhs; c0 += SV_MAXRHS) { // RHS in slices of <= 32 columns
-        const int nc = static_cast<int>(std::min<uint64_t>(SV_MAXRHS, nrhs - c0));
-        double* bc = b + c0;
-        for (uint64_t bi = 0; bi < nblk; ++bi) {
-            const uint64_t o = bi * NB, bs = std::min<uint64_t>(NB, n - o);
-            k_block_solve<<<1, PK_THREADS, sm, st>>>(diag + bi * NB * NB, NB, bs, 0, bc + o * ldb, ldb, nc, 1);
-            RL_LAUNCHED();
-            const uint64_t rest = n - o - bs;
-            if (rest)
-                gemm(false, false, rest, nc, bs, -1.0, lu + (o + bs) * lda + o, lda, bc + o * ldb, ldb, 1.0,
-                     bc + (o + bs) * ldb, ldb);
-        }
-        for (uint64_t bi = nblk; bi-- > 0;) {
-            const uint64_t o = bi * NB, bs = std::min<uint64_t>(NB, n - o);
-            k_block_solve<<<1, PK_THREADS, sm, st>>>(diag + bi * NB * NB, NB, bs, 0, bc + o * ldb, ldb, nc, 0);
-            RL_LAUNCHED();
-            if (o)
-                gemm(false, false, o, nc, bs, -1.0, lu + o, lda, bc + o * ldb, ldb, 1.0, bc, ldb);
+    int* sync = ws<int>(WS_WAVE, 2 * (nblk + 1));
+    static const bool trace = std::getenv("RL_WAVE_TRACE") != nullptr;
+    for (uint64_t c0 = 0; c0 < nrhs; c0 += WV_MAXRHS) {
+        const int nc = static_cast<int>(std::min<uint64_t>(WV_MAXRHS, nrhs - c0));
+        RL_CUDA(cudaMemsetAsync(sync, 0, 2 * (nblk + 1) * sizeof(int), st));
+        k_trsv_wave<true><<<static_cast<unsigned>(nblk), WV_THREADS, wave_smem_bytes(), st>>>(lu, lda, n, b + c0, ldb,
+                                                                                          nc, sync, trace);
+        RL_LAUNCHED();
+        k_trsv_wave<false><<<static_cast<unsigned>(nblk), WV_THREADS, wave_smem_bytes(), st>>>(
+            lu, lda, n, b + c0, ldb, nc, sync + nblk + 1, trace);
+        RL_LAUNCHED();
+    }
+    if (trace && nblk <= 512) {
+        static unsigned long long h[2][512][6];
+        RL_CUDA(cudaMemcpyFromSymbolAsync(h, g_wave_ts, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+        RL_CUDA(cudaStreamSynchronize(st));
+        for (int d = 0; d < 2; ++d) {
+            unsigned long long t0 = ~0ULL;
+            for (uint64_t i = 0; i < nblk; ++i)
+                t0 = std::min(t0, h[d][i][0]);
+            for (uint64_t i = 0; i < nblk; ++i) {
+                const auto* q = h[d][i];
+                std::fprintf(stderr, "wave %s blk %3llu: start %7.2f lastwait %7.2f dmma %6.2f rhs %6.2f solve %6.2f rel %6.2f us\n",
+                             d ? "U" : "L", static_cast<unsigned long long>(i), (q[0] - t0) * 1e-3, (q[1] - t0) * 1e-3,
+                             (q[2] - q[1]) * 1e-3, (q[3] - q[2]) * 1e-3, (q[4] - q[3]) * 1e-3, (q[5] - q[4]) * 1e-3);
+            }
         }
     }
 }
