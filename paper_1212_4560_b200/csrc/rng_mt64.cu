@@ -77,30 +77,38 @@ __device__ void warp_seed_window(uint64_t* w, uint64_t v, int lane) {
 }
 
 // In-place twist of a 312-word window held in shared memory by one warp.
-// Same recurrence as libstdc++'s mersenne_twister_engine::_M_gen_rand.
+// Same recurrence as libstdc++'s mersenne_twister_engine::_M_gen_rand: new[i] =
+// x[i+156] ^ tw(x[i], x[i+1]) for i < 156 (old values only), then for i >= 156 from the
+// new first half.  Each phase loads all its operands before any store (5 words per lane)
+// so the phase costs one shared-memory round trip.
 __device__ void warp_twist(uint64_t* w, int lane) {
-#pragma unroll 1
-    for (int base = 0; base < kN - kM; base += 32) {
-        int i = base + lane;
-        uint64_t v = 0;
-        if (i < kN - kM)
-            v = twist_word(w[i], w[i + 1], w[i + kM]);
-        __syncwarp();
-        if (i < kN - kM)
-            w[i] = v;
-        __syncwarp();
+    uint64_t v[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) { // branch-free loads (clamped index) so all 15 overlap
+        const int i = min(lane + 32 * q, kN - kM - 1);
+        v[q] = twist_word(w[i], w[i + 1], w[i + kM]);
     }
-#pragma unroll 1
-    for (int base = kN - kM; base < kN; base += 32) {
-        int i = base + lane;
-        uint64_t v = 0;
-        if (i < kN)
-            v = twist_word(w[i], w[(i + 1) % kN], w[i - (kN - kM)]);
-        __syncwarp();
-        if (i < kN)
-            w[i] = v;
-        __syncwarp();
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int i = lane + 32 * q;
+        if (i < kN - kM)
+            w[i] = v[q];
     }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int i = min(kN - kM + lane + 32 * q, kN - 1);
+        v[q] = twist_word(w[i], w[i + 1 < kN ? i + 1 : 0], w[i - kM]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int i = kN - kM + lane + 32 * q;
+        if (i < kN)
+            w[i] = v[q];
+    }
+    __syncwarp();
 }
 
 struct GenParams {
@@ -230,10 +238,10 @@ __global__ void k_window_sequence(const uint64_t* windows, uint64_t* seqs) {
 // Target b of block uses poly polys[(first_poly + b) % poly_mod] and base sequence
 // seqs[(b / seq_div)].
 constexpr int kJumpThreads = 320;
-__global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, int first_poly,
-                                                       int poly_mod, const uint64_t* seqs,
-                                                       int seq_div, int ntargets, int tgt_off,
-                                                       uint64_t* out) {
+__global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, uint64_t poly_mod,
+                                                       const uint64_t* seqs, bool seq_single,
+                                                       uint64_t c_first, int stride, uint64_t a_first,
+                                                       int ntargets, uint64_t* out) {
     extern __shared__ __align__(16) uint64_t sm[];
     uint64_t* x = sm;                                              // kSeqWords
     uint16_t* list = reinterpret_cast<uint16_t*>(sm + kSeqWords);  // up to 19937 offsets
@@ -242,8 +250,12 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, in
     const int tgt = blockIdx.x;
     if (tgt >= ntargets)
         return;
-    const uint64_t* poly = polys + static_cast<size_t>((first_poly + tgt) % poly_mod) * kN;
-    const uint64_t* seq = seqs + static_cast<size_t>((tgt + tgt_off) / seq_div) * kSeqWords;
+    // target chunk c = c_first + stride * tgt: poly c mod poly_mod applied to base sequence
+    // c / poly_mod (relative to a_first), result in out slot c - c_first
+    const uint64_t c = c_first + static_cast<uint64_t>(stride) * tgt;
+    const uint64_t* poly = polys + static_cast<size_t>(c % poly_mod) * kN;
+    const uint64_t* seq = seqs + (seq_single ? 0 : static_cast<size_t>(c / poly_mod - a_first) * kSeqWords);
+    out += static_cast<size_t>(c - c_first) * kN;
     const int t = threadIdx.x;
     for (int i = t; i < kSeqWords; i += kJumpThreads)
         x[i] = seq[i];
@@ -286,32 +298,140 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, in
         }
         for (; k < n; ++k)
             a0 ^= xj[list[k]];
-        out[static_cast<size_t>(tgt) * kN + t] = a0 ^ a1 ^ a2 ^ a3;
+        out[t] = a0 ^ a1 ^ a2 ^ a3;
     }
 }
 
-// One warp per chunk: window at stream position 8 + cJ -> outputs [cJ, cJ + J).
-constexpr int kGenWarps = 4;
-__global__ void __launch_bounds__(32 * kGenWarps) k_gen_chunks(const uint64_t* windows, uint64_t c_first,
-                                                               uint64_t nchunks, uint64_t nout,
-                                                               GenParams p) {
-    __shared__ uint64_t wbuf[kGenWarps][kN];
-    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint64_t ci = static_cast<uint64_t>(blockIdx.x) * kGenWarps + wid;
+// Chunk windows between jumped ones by twisting forward: warp k starts from the jumped
+// window of chunk kS and emits the windows of chunks kS + s (s = 1..S-1), which start
+// s J words later (J = 105 * 312 + 8, so a window straddles two twist blocks).  About
+// 105 twists per window instead of a 19937-term jump.
+__global__ void k_window_forward(uint64_t* cw, uint64_t nchunks, int stride) {
+    __shared__ uint64_t cur[kN], prev[kN];
+    const int lane = threadIdx.x;
+    const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * stride;
+    for (int i = lane; i < kN; i += 32)
+        cur[i] = cw[k0 * kN + i];
+    __syncwarp();
+    uint64_t m = 0; // cur holds block m (words [312 m, 312 m + 312) after the jumped window)
+    for (int sidx = 1; sidx < stride && k0 + sidx < nchunks; ++sidx) {
+        const uint64_t P = static_cast<uint64_t>(sidx) * kJ, mb = P / kN;
+        const int off = static_cast<int>(P % kN);
+        while (m < mb) {
+            warp_twist(cur, lane);
+            ++m;
+        }
+        uint64_t* dst = cw + (k0 + sidx) * kN;
+        if (off == 0) {
+            for (int i = lane; i < kN; i += 32)
+                dst[i] = cur[i];
+            continue;
+        }
+        for (int i = lane; i < kN; i += 32)
+            prev[i] = cur[i];
+        __syncwarp();
+        warp_twist(cur, lane);
+        ++m;
+        for (int i = lane; i < kN; i += 32)
+            dst[i] = (i < kN - off) ? prev[off + i] : cur[i - (kN - off)];
+        __syncwarp();
+    }
+}
+
+// Out-of-place twist dst = twist(src) by one warp (same recurrence as warp_twist).
+__device__ void warp_twist_oop(const uint64_t* src, uint64_t* dst, int lane) {
+    uint64_t v[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int i = min(lane + 32 * q, kN - kM - 1);
+        v[q] = twist_word(src[i], src[i + 1], src[i + kM]);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+        if (lane + 32 * q < kN - kM)
+            dst[lane + 32 * q] = v[q];
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int i = min(kN - kM + lane + 32 * q, kN - 1);
+        v[q] = twist_word(src[i], i + 1 < kN ? src[i + 1] : dst[0], dst[i - kM]);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+        if (kN - kM + lane + 32 * q < kN)
+            dst[kN - kM + lane + 32 * q] = v[q];
+}
+
+// One CTA of 160 threads per chunk: window at stream position 8 + cJ -> outputs
+// [cJ, cJ + J).  Per 312-word block warp 0 twists the next block into the other buffer
+// while every thread transforms its share of the current one (one Box-Muller pair per
+// thread for Gaussians), one barrier per block: five warps per chunk keep the FP64 pipe
+// fed where one warp per chunk left it latency-bound.
+constexpr int kGenThreads = 160;
+__global__ void __launch_bounds__(kGenThreads) k_gen_chunks(const uint64_t* windows, uint64_t c_first,
+                                                            uint64_t nchunks, uint64_t nout, GenParams p) {
+    __shared__ uint64_t wb[2][kN];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t ci = blockIdx.x;
     if (ci >= nchunks)
         return;
     const uint64_t c = c_first + ci;
-    uint64_t* w = wbuf[wid];
-    for (int i = lane; i < kN; i += 32)
-        w[i] = windows[ci * kN + i];
-    __syncwarp();
+    for (int i = tid; i < kN; i += kGenThreads)
+        wb[1][i] = windows[ci * kN + i];
+    __syncthreads();
+    if (warp == 0)
+        warp_twist_oop(wb[1], wb[0], lane);
+    __syncthreads();
     const int64_t clo = static_cast<int64_t>(c * kJ);
     const int64_t lo = max(clo, p.base);
     const int64_t hi = static_cast<int64_t>(min(nout, (c + 1) * kJ));
+    int cur = 0;
     for (int64_t o0 = clo; o0 < hi; o0 += kN) {
-        warp_twist(w, lane);
-        if (o0 + kN > lo)
-            emit_block(w, o0, lo, hi, p, lane);
+        const uint64_t* w = wb[cur];
+        if (warp == 0 && o0 + kN < hi)
+            warp_twist_oop(w, wb[cur ^ 1], lane);
+        if (o0 + kN > lo) {
+            if (p.kind == static_cast<int>(Draw::Gaussian)) {
+                const int q = tid; // pair (o, o + 1), o = o0 + 2q: entries o (cos) and o + 1 (sin)
+                if (q < kN / 2) {
+                    const int64_t o = o0 + 2 * q;
+                    if (o >= lo && o < hi) {
+                        double g0, g1;
+                        box_muller(temper(w[2 * q]), temper(w[2 * q + 1]), p.mu, p.sigma, &g0, &g1);
+                        double* out = static_cast<double*>(p.out) - p.base;
+                        if (static_cast<uint64_t>(o) + 1 < p.count)
+                            *reinterpret_cast<double2*>(out + o) = make_double2(g0, g1);
+                        else
+                            out[o] = g0;
+                    }
+                }
+            } else {
+                for (int i = tid; i < kN; i += kGenThreads) {
+                    const int64_t o = o0 + i;
+                    if (o < lo || o >= hi)
+                        continue;
+                    const uint64_t z = temper(w[i]);
+                    const int64_t oi = o - p.base;
+                    switch (p.kind) {
+                    case static_cast<int>(Draw::RawU64):
+                        static_cast<uint64_t*>(p.out)[oi] = z;
+                        break;
+                    case static_cast<int>(Draw::Uniform01):
+                        static_cast<double*>(p.out)[oi] = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+                        break;
+                    case static_cast<int>(Draw::UniformPm1):
+                        static_cast<double*>(p.out)[oi] =
+                            __dsub_rn(__dmul_rn(2.0, __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53)), 1.0);
+                        break;
+                    default: // Sign
+                        static_cast<double*>(p.out)[oi] = (z & 1ULL) ? 1.0 : -1.0;
+                        break;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        cur ^= 1;
     }
 }
 
@@ -394,6 +514,7 @@ const JumpTable& jump_table() {
 }
 
 constexpr size_t kJumpSmem = kSeqWords * 8 + 19968 * 2 + 16;
+constexpr int kFwdStride = 8; // chunks per level-2 jump (the rest twist forward)
 
 } // namespace
 
@@ -433,16 +554,21 @@ void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, ui
     uint64_t* cw = ws<uint64_t>(WS_RNG2, nchunks * kN);
     k_base_sequence<<<1, 32, 0, st>>>(eseed, base);
     RL_LAUNCHED();
-    k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(
-        jt.d_l1, static_cast<int>(a_first), jt.n_l1, base, 1 << 30, static_cast<int>(nl1), 0, l1w);
+    k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(jt.d_l1, 1ULL << 40, base, true, a_first, 1,
+                                                                        a_first, static_cast<int>(nl1), l1w);
     RL_LAUNCHED();
     k_window_sequence<<<static_cast<unsigned>(nl1), 32, 0, st>>>(l1w, l1s);
     RL_LAUNCHED();
-    k_jump<<<static_cast<unsigned>(nchunks), kJumpThreads, kJumpSmem, st>>>(
-        jt.d_l2, static_cast<int>(c_first % jt.n_l2), jt.n_l2, l1s, jt.n_l2, static_cast<int>(nchunks),
-        static_cast<int>(c_first % jt.n_l2), cw);
+    // level-2 jumps for every kFwdStride-th chunk, the others by twisting forward
+    const uint64_t njump = (nchunks + kFwdStride - 1) / kFwdStride;
+    k_jump<<<static_cast<unsigned>(njump), kJumpThreads, kJumpSmem, st>>>(
+        jt.d_l2, static_cast<uint64_t>(jt.n_l2), l1s, false, c_first, kFwdStride, a_first, static_cast<int>(njump), cw);
     RL_LAUNCHED();
-    k_gen_chunks<<<cdiv(nchunks, kGenWarps), 32 * kGenWarps, 0, st>>>(cw, c_first, nchunks, end, p);
+    if (nchunks > 1) {
+        k_window_forward<<<static_cast<unsigned>(njump), 32, 0, st>>>(cw, nchunks, kFwdStride);
+        RL_LAUNCHED();
+    }
+    k_gen_chunks<<<static_cast<unsigned>(nchunks), kGenThreads, 0, st>>>(cw, c_first, nchunks, end, p);
     RL_LAUNCHED();
 }
 
