@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(WV_THREADS, 1) k_trsv_wave(const double* __res
         if (!LOWER && i == k)
             rcp[i] = (i < bs) ? 1.0 / v : 1.0;
     }
+    __syncthreads(); // Dt / rcp complete (the first block of a sweep has no wait barrier below)
     // sum_j D[b][j] x_j over the finished blocks (DMMA m8n8k4: warp w owns rows 8w..8w+7)
     const int r = 8 * warp + g;
     const int nf = (nrhs + 7) >> 3;
