@@ -48,8 +48,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
                                                            double floor, double* pivots,
                                                            unsigned long long* breakdown) {
     extern __shared__ double W[]; // NB x PT
-    __shared__ double rcp[NB];
-    __shared__ double prow[SB];
+    __shared__ double rcp[NB], pabs[NB];
+    __shared__ double prow[2][SB + 2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
     double* blk = a + o * lda + o;
@@ -57,7 +57,9 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
                                          [](int i, int j) { return i == j ? 1.0 : 0.0; });
     __syncthreads();
     for (int c0 = 0; c0 < NB; c0 += SB) {
-        // (1) 16x16 diagonal sub-block, warp 0, lanes 0..15 own its rows
+        // (1) 16x16 diagonal sub-block, warp 0, lanes 0..15 own its rows.  Per step the
+        //     owner publishes its row tail and 1/p into a double-buffered shared row (one
+        //     __syncwarp per step); |pivots| go to shared memory and out after the loop.
         if (warp == 0) {
             double p[SB];
             const int r = c0 + (lane & (SB - 1));
@@ -66,32 +68,26 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
                 p[l] = W[r * PT + c0 + l];
 #pragma unroll
             for (int kk = 0; kk < SB; ++kk) {
+                double* pr = prow[kk & 1];
                 if (lane == kk) {
+                    const double pv = p[kk];
+                    const double iv = (pv == 0.0) ? 0.0 : 1.0 / pv;
 #pragma unroll
-                    for (int l = 0; l < SB; ++l)
-                        prow[l] = p[l];
+                    for (int l = kk; l < SB; ++l)
+                        pr[l] = p[l];
+                    pr[SB] = iv;
+                    rcp[c0 + kk] = iv;
+                    pabs[c0 + kk] = fabs(pv);
                 }
                 __syncwarp();
-                const double piv = prow[kk];
-                const double inv = (piv == 0.0) ? 0.0 : 1.0 / piv;
-                if (lane == 0) {
-                    const int k = c0 + kk;
-                    if (k < bs) {
-                        pivots[o + k] = fabs(piv);
-                        if (fabs(piv) < floor)
-                            atomicMin(breakdown, static_cast<unsigned long long>(o + k));
-                    }
-                    rcp[k] = inv;
-                }
                 if (lane < SB && lane > kk) {
-                    const double m = p[kk] * inv;
+                    const double m = p[kk] * pr[SB];
                     p[kk] = m;
                     if (m != 0.0)
 #pragma unroll
                         for (int l = kk + 1; l < SB; ++l)
-                            p[l] = fma(-m, prow[l], p[l]);
+                            p[l] = fma(-m, pr[l], p[l]);
                 }
-                __syncwarp();
             }
             if (lane < SB)
 #pragma unroll
@@ -145,6 +141,11 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
         __syncthreads();
     }
     panel::store_tile<NB, NB, PK_THREADS>(blk, lda, W, PT, bs, bs);
+    if (tid < bs) { // |pivots| and the first step below the floor (genp.cpp:24-26)
+        pivots[o + tid] = pabs[tid];
+        if (pabs[tid] < floor)
+            atomicMin(breakdown, static_cast<unsigned long long>(o + tid));
+    }
 }
 
 // Panel TRSMs of block step o (genp.cpp:77-92), in place, one launch:

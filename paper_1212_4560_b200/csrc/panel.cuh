@@ -29,8 +29,15 @@ __device__ __forceinline__ void smem_update16(double* C, int ldc, const double* 
                                               int ldb, int M, int N, int warp, int nwarps, int lane) {
     const int g = lane >> 2, t = lane & 3;
     const int fm = M >> 3, fn = N >> 3;
+    // fragment f = (mi, nj) row-major, walked with an incremental (mi, nj) (no divisions)
+    int mi = warp / fn, nj = warp - mi * fn;
     for (int f = warp; f < fm * fn; f += nwarps) {
-        const int m0 = (f / fn) << 3, n0 = (f % fn) << 3;
+        const int m0 = mi << 3, n0 = nj << 3;
+        nj += nwarps;
+        while (nj >= fn) {
+            nj -= fn;
+            ++mi;
+        }
         double acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int k0 = 0; k0 < SB; k0 += 4)
@@ -47,20 +54,21 @@ template <int R, int C, int THREADS, typename Keep, typename Fill>
 __device__ __forceinline__ void load_tile(double* s, int sp, const double* g, uint64_t ld, int vr, int vc,
                                           Keep keep, Fill fill) {
     constexpr int TOTAL = R * C;
-    static_assert(TOTAL % (THREADS * 8) == 0, "tile must split into 8-deep batches");
+    constexpr int D = (TOTAL % (THREADS * 16) == 0) ? 16 : 8; // loads in flight per thread
+    static_assert(TOTAL % (THREADS * D) == 0, "tile must split into 8-deep batches");
     const int tid = threadIdx.x;
 #pragma unroll 1
-    for (int base = 0; base < TOTAL; base += THREADS * 8) {
-        double v[8];
+    for (int base = 0; base < TOTAL; base += THREADS * D) {
+        double v[D];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < D; ++u) {
             const int e = base + u * THREADS + tid;
             const int i = e / C, j = e % C;
             const bool ok = i < vr && j < vc;
             v[u] = ok ? g[static_cast<uint64_t>(i) * ld + j] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < D; ++u) {
             const int e = base + u * THREADS + tid;
             const int i = e / C, j = e % C;
             const bool ok = i < vr && j < vc;
