@@ -33,7 +33,7 @@ __all__ = [
     "multiply", "circ_mul", "circulant_multiply_matrix", "genp_factor", "genp_solve", "randomized_genp",
     "randomized_genp_batched", "approx_basis", "qr_positive", "project_onto_basis", "numerical_rank",
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
-    "dev_randomized_genp_batched", "dev_range_finder", "probe_peaks", "launch_count", "LIB_PATH",
+    "dev_randomized_genp_batched", "dev_range_finder", "probe_peaks", "box_muller_fast_check", "launch_count", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -220,6 +220,7 @@ def lib() -> C.CDLL:
         "rl_numerical_rank": [u64, u64, _d, dbl, C.POINTER(u64), _d],
         "rl_dev_range_finder": [u64, u64, vp, u64, u64, u64, dbl, vp, vp, _d, C.POINTER(u64), C.POINTER(dbl)],
         "rl_probe_peaks": [C.POINTER(dbl), C.POINTER(dbl)],
+        "rl_box_muller_fast_check": [u64, vp, u64, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -515,6 +516,16 @@ def dev_range_finder(a, rho_plus: int, stream: RngStream, rank_tol: float, q, bm
     _chk(lib().rl_dev_range_finder(m, n, _ptr(a), rho_plus, stream.seed, stream.stream_id, rank_tol, _ptr(q),
                                    _ptr(bmat), sg, C.byref(r), C.byref(res) if want_residual else None))
     return sg, int(r.value), (res.value if want_residual else None)
+
+
+def box_muller_fast_check(npairs: int, raw=None, seed: int = 0) -> Tuple[int, int, int]:
+    """(fast-path pairs, of those bitwise different from the double-double path, deferred)."""
+    counts = np.zeros(3, dtype=np.uint64)
+    if raw is not None:
+        raw = np.ascontiguousarray(raw, dtype=np.uint64)
+        npairs = raw.size // 2
+    _chk(lib().rl_box_muller_fast_check(npairs, None if raw is None else raw.ctypes.data, seed, counts.ctypes.data))
+    return int(counts[0]), int(counts[1]), int(counts[2])
 
 
 def probe_peaks() -> Tuple[float, float]:

@@ -662,6 +662,15 @@ rl_status rl_box_muller(uint64_t npairs, const uint64_t* raw, double* out) {
     API_END
 }
 
+rl_status rl_box_muller_fast_check(uint64_t npairs, const uint64_t* raw, uint64_t seed, uint64_t* counts) {
+    API_BEGIN
+    const uint64_t* d = raw ? upload(WS_H0, raw, 2 * npairs) : nullptr;
+    unsigned long long* dc = ws<unsigned long long>(WS_H1, 3);
+    box_muller_fast_check_dev(d, npairs, seed, dc);
+    download(reinterpret_cast<unsigned long long*>(counts), dc, 3);
+    API_END
+}
+
 rl_status rl_dft(uint64_t n, const double* in, int inverse, double* out) {
     API_BEGIN
     if (n == 0 || (n & (n - 1)))

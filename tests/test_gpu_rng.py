@@ -84,3 +84,19 @@ def test_determinism_and_stream_independence(rl):
     b = rl.gaussian_matrix(300, 300, 0.0, 1.0, rl.RngStream(7, 3))
     c = rl.gaussian_matrix(300, 300, 0.0, 1.0, rl.RngStream(7, 4))
     assert np.array_equal(a, b) and not np.array_equal(a, c)
+
+
+def test_box_muller_fast_path_is_exact(rl):
+    """The generator's Ziv fast path must return exactly the double-double path's bits
+    whenever it accepts: random pairs, plus the edges (u1 -> 1 and 0, angles at k pi/2)."""
+    ok, bad, slow = rl.box_muller_fast_check(1 << 22, seed=12345)
+    assert bad == 0 and ok + slow == 1 << 22 and slow < (1 << 22) // 20
+    edge = []
+    for k in range(0, 1 << 12):
+        lo = k << 11                              # u1 = 1 - k 2^-53 -> log u1 ~ 0
+        hi = ((1 << 53) - 1 - k) << 11            # u1 = (k + 1) 2^-53
+        for q in range(5):                        # u2 near q/4 -> angle near q pi/2
+            u2 = ((q * (1 << 51) + k - 2048) % (1 << 53)) << 11
+            edge += [lo, u2, hi, u2]
+    ok, bad, slow = rl.box_muller_fast_check(0, raw=np.array(edge, dtype=np.uint64))
+    assert bad == 0
