@@ -7,6 +7,7 @@
 #include <limits>
 #include <vector>
 
+#include <cstdio>
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -67,6 +68,51 @@ T* upload(int slot, const T* h, uint64_t count) {
     if (count)
         RL_CUDA(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, stream()));
     return d;
+}
+
+
+// Upload a row-major n x n host matrix into dev in row panels on a copy stream, leaving
+// the transfer in flight (ctx().upload): the randomized GENP's first A * G product runs
+// one GEMM per panel as each arrives, so the 512 MiB copy of config 3 overlaps the DGEMM
+// instead of preceding it.  Small matrices upload in one piece.
+void upload_rows_async(double* dev, const double* host, uint64_t n) {
+    Ctx& c = ctx();
+    struct CopyStream {
+        cudaStream_t s = nullptr;
+        cudaEvent_t start = nullptr, done[8] = {};
+        int device = -1;
+    };
+    static thread_local CopyStream cs;
+    if (cs.device != c.device) {
+        RL_CUDA(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
+        RL_CUDA(cudaEventCreateWithFlags(&cs.start, cudaEventDisableTiming));
+        for (auto& e : cs.done)
+            RL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cs.device = c.device;
+    }
+    if (n < 2048) {
+        if (n)
+            RL_CUDA(cudaMemcpyAsync(dev, host, n * n * sizeof(double), cudaMemcpyHostToDevice, stream()));
+        return;
+    }
+    // previous users of the buffer (earlier calls on the main stream) finish first
+    RL_CUDA(cudaEventRecord(cs.start, stream()));
+    RL_CUDA(cudaStreamWaitEvent(cs.s, cs.start, 0));
+    const uint64_t ends[5] = {n / 16 & ~127ULL, n / 4 & ~127ULL, n / 2 & ~127ULL, 3 * n / 4 & ~127ULL, n};
+    PendingUpload up;
+    up.dev = dev;
+    uint64_t r0 = 0;
+    for (uint64_t r1 : ends) {
+        if (r1 <= r0)
+            continue;
+        RL_CUDA(cudaMemcpyAsync(dev + r0 * n, host + r0 * n, (r1 - r0) * n * sizeof(double), cudaMemcpyHostToDevice,
+                                cs.s));
+        RL_CUDA(cudaEventRecord(cs.done[up.npanels], cs.s));
+        up.done[up.npanels] = cs.done[up.npanels];
+        up.row_end[up.npanels++] = r1;
+        r0 = r1;
+    }
+    c.upload = up;
 }
 
 template <typename T>
@@ -433,10 +479,18 @@ rl_status rl_randomized_genp_ex(uint64_t n, uint64_t nrhs, const double* a, cons
                                 rl_precond_report* report, uint32_t flags) {
     API_BEGIN
     require_positive(n, nrhs, "randomized_genp");
-    double* da = upload(WS_H0, a, n * n);
     double* db = upload(WS_H1, b, n * nrhs);
+    double* da = ws<double>(WS_H0, n * n);
+    upload_rows_async(da, a, n);
     double* dx = ws<double>(WS_H2, n * nrhs);
-    rl_status s = randomized_genp_dev(n, nrhs, da, db, tag, mu, sigma, side, refine, seed, sid, dx, report, flags);
+    rl_status s;
+    try {
+        s = randomized_genp_dev(n, nrhs, da, db, tag, mu, sigma, side, refine, seed, sid, dx, report, flags);
+    } catch (...) {
+        wait_upload(da);
+        throw;
+    }
+    wait_upload(da);
     if (s != RL_OK)
         return s;
     download(x, dx, n * nrhs);

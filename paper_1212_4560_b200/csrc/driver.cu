@@ -49,6 +49,20 @@ namespace {
 
 constexpr int NB = 128;
 
+} // namespace
+
+void wait_upload(const double* dev) {
+    PendingUpload& up = ctx().upload;
+    if (up.dev != dev || up.npanels == 0)
+        return;
+    for (int p = 0; p < up.npanels; ++p) {
+        RL_CUDA(cudaStreamWaitEvent(stream(), up.done[p], 0));
+    }
+    up = PendingUpload{};
+}
+
+namespace {
+
 struct Mult {
     int tag = 0;
     uint64_t n = 0;
@@ -150,6 +164,20 @@ void draw(Mult& m, int tag, double mu, double sigma, uint64_t n, uint64_t seed, 
 // out = sys * M  (out != sys)
 void apply_right(const Mult& m, const double* sys, double* out) {
     const uint64_t n = m.n;
+    PendingUpload& up = ctx().upload;
+    if (up.dev == sys && up.npanels > 0 && m.dense && m.tag != RL_HOUSEHOLDER_PAIR && m.tag != RL_SPARSE_SIGN) {
+        // sys is still arriving from the host: one GEMM per row panel, each after its copy
+        uint64_t r0 = 0;
+        for (int p = 0; p < up.npanels; ++p) {
+            RL_CUDA(cudaStreamWaitEvent(stream(), up.done[p], 0));
+            const uint64_t r1 = up.row_end[p];
+            gemm(false, false, r1 - r0, n, n, 1.0, sys + r0 * n, n, m.dense, n, 0.0, out + r0 * n, n);
+            r0 = r1;
+        }
+        up = PendingUpload{};
+        return;
+    }
+    wait_upload(sys);
     switch (m.tag) {
     case RL_HOUSEHOLDER_PAIR:
         hh2_apply_right_dev(n, sys, n, m.u1, m.u2, m.s12, out, n);
@@ -165,6 +193,7 @@ void apply_right(const Mult& m, const double* sys, double* out) {
 // out = M * sys (out != sys)
 void apply_left(const Mult& m, const double* sys, uint64_t cols, double* out) {
     const uint64_t n = m.n;
+    wait_upload(sys);
     gemm(false, false, n, cols, n, 1.0, m.dense, n, sys, cols, 0.0, out, cols);
 }
 
@@ -262,6 +291,7 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
     rep.attempt = -1;
     if (!(flags & 1u)) {
         // raw-GENP contrast arm (genp.cpp:222-234)
+        wait_upload(A);
         copy2d_dev(n, n, A, n, sys, n);
         RL_CUDA(cudaMemsetAsync(brk, 0xff, 8, st));
         genp_factor_blocked(n, sys, n, 0.0, piv, brk, aux);
@@ -296,8 +326,11 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
             apply_right(right, src, tmp);
             std::swap(sys, tmp);
         }
-        if (!use_left && !use_right)
+        if (!use_left && !use_right) {
+            wait_upload(A);
             copy2d_dev(n, n, A, n, sys, n);
+        }
+        wait_upload(A); // (no-op once the first product consumed the upload)
         if (use_left)
             apply_vec(left, B, nrhs, Z);
         else

@@ -47,6 +47,15 @@ struct DevBuf {
     ~DevBuf();
 };
 
+// A host -> device upload of a row-major matrix still in flight, in row panels (the
+// host-pointer entry points overlap the upload of A with the first A * G product).
+struct PendingUpload {
+    const double* dev = nullptr; // device copy being filled
+    int npanels = 0;
+    uint64_t row_end[8] = {};    // panel p covers rows [row_end[p-1], row_end[p])
+    cudaEvent_t done[8] = {};    // recorded on the copy stream after panel p
+};
+
 struct Ctx {
     int device = -1;
     cudaStream_t own = nullptr;
@@ -54,7 +63,12 @@ struct Ctx {
     DevBuf ws[32];                 // named scratch slots (see WS_* below)
     uint64_t launches = 0;
     int sms = 148;
+    PendingUpload upload;          // set only inside a host-pointer call
 };
+
+// Make the current stream wait for every panel of a pending upload of `dev` (no-op when
+// none is pending); the upload is then complete as far as this stream is concerned.
+void wait_upload(const double* dev);
 
 enum WsSlot {
     WS_IN_A = 0, WS_IN_B, WS_OUT, WS_MULT, WS_SYS, WS_RHS, WS_TMP1, WS_TMP2, WS_RNG,
