@@ -240,8 +240,11 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const doub
         // epilogue overlaps the other's DMMA loop.  Measured (tools/gemm_sweep.py): 8192^3
         // 32.8 TF/s vs 31.3 for a 1-CTA 128x128 tile; rank-128 updates 23.3 vs 16.5 TF/s.
         launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (N > 32)
+    else if (N > 32 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= static_cast<uint64_t>(sms))
         launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    // small grids (the LU's diagonal-block and strip updates): a 128 x 64 tile would leave
+    // most SMs idle while each CTA runs a long DMMA chain; 64 x 32 tiles spread the same
+    // work over 4x the CTAs (tools/gemm_graph.py: 128^2 x 256 27 -> ~9 us)
     else
         launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }

@@ -44,57 +44,73 @@ constexpr int PK_WARPS = PK_THREADS / 32;
 //   right of it solves its 16 U entries against that unit L; (4) DMMA trailing update.
 // |pivots| and the first step with |p| < floor are recorded; 1/p := 0 when p == 0 gives
 // the reference's multiplier 0 (genp.cpp:27).
+__device__ unsigned long long g_diag_ts[64];
+__device__ unsigned long long g_trsm_ts[2][32];
+__device__ __forceinline__ unsigned long long gtimer0() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
 __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t lda, uint64_t n, uint64_t o,
                                                            double floor, double* pivots,
                                                            unsigned long long* breakdown) {
     extern __shared__ double W[]; // NB x PT
     __shared__ double rcp[NB], pabs[NB];
-    __shared__ double prow[2][SB + 2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
     double* blk = a + o * lda + o;
-    panel::load_tile<NB, NB, PK_THREADS>(W, PT, blk, lda, bs, bs, [](int, int) { return true; },
-                                         [](int i, int j) { return i == j ? 1.0 : 0.0; });
+    int tsi = 0;
+    if (tid == 0) g_diag_ts[tsi] = gtimer0();
+    ++tsi;
+    panel::load_tile_async<NB, NB, PK_THREADS>(W, PT, blk, lda, bs, bs, [](int, int) { return true; });
+    panel::cp_async_wait_all();
     __syncthreads();
-    for (int c0 = 0; c0 < NB; c0 += SB) {
-        // (1) 16x16 diagonal sub-block, warp 0, lanes 0..15 own its rows.  Per step the
-        //     owner publishes its row tail and 1/p into a double-buffered shared row (one
-        //     __syncwarp per step); |pivots| go to shared memory and out after the loop.
-        if (warp == 0) {
-            double p[SB];
-            const int r = c0 + (lane & (SB - 1));
+    for (int i = bs + tid; i < NB; i += PK_THREADS) // identity beyond a ragged last block
+        W[i * PT + i] = 1.0;
+    __syncthreads();
+    if (tid == 0) g_diag_ts[tsi] = gtimer0();
+    ++tsi;
+    // (1) 16x16 diagonal sub-block c0 by warp 0, lanes 0..15 own its rows, all in registers:
+    //     per step the pivot row is read from the owner lane by shuffles, every lane forms
+    //     1/p itself (correctly rounded reciprocal).
+    auto phase1 = [&](int c0) {
+        __syncwarp();
+        double p[SB];
+        const int r = c0 + (lane & (SB - 1));
 #pragma unroll
-            for (int l = 0; l < SB; ++l)
-                p[l] = W[r * PT + c0 + l];
+        for (int l = 0; l < SB; ++l)
+            p[l] = W[r * PT + c0 + l];
+        double invs[SB], pivs[SB];
+#pragma unroll
+        for (int kk = 0; kk < SB; ++kk) {
+            const double piv = __shfl_sync(0xffffffffu, p[kk], kk);
+            const double inv = (piv == 0.0) ? 0.0 : __drcp_rn(piv);
+            invs[kk] = inv;
+            pivs[kk] = piv;
+            const bool below = lane < SB && lane > kk;
+            const double m = below ? p[kk] * inv : 0.0;
+            p[kk] = below ? m : p[kk]; // selects, no branches: the shuffles stay converged
+#pragma unroll
+            for (int l = kk + 1; l < SB; ++l)
+                p[l] = fma(-m, __shfl_sync(0xffffffffu, p[l], kk), p[l]);
+        }
+        if (lane == 0)
 #pragma unroll
             for (int kk = 0; kk < SB; ++kk) {
-                double* pr = prow[kk & 1];
-                if (lane == kk) {
-                    const double pv = p[kk];
-                    const double iv = (pv == 0.0) ? 0.0 : 1.0 / pv;
-#pragma unroll
-                    for (int l = kk; l < SB; ++l)
-                        pr[l] = p[l];
-                    pr[SB] = iv;
-                    rcp[c0 + kk] = iv;
-                    pabs[c0 + kk] = fabs(pv);
-                }
-                __syncwarp();
-                if (lane < SB && lane > kk) {
-                    const double m = p[kk] * pr[SB];
-                    p[kk] = m;
-                    if (m != 0.0)
-#pragma unroll
-                        for (int l = kk + 1; l < SB; ++l)
-                            p[l] = fma(-m, pr[l], p[l]);
-                }
+                rcp[c0 + kk] = invs[kk];
+                pabs[c0 + kk] = fabs(pivs[kk]);
             }
-            if (lane < SB)
+        if (lane < SB)
 #pragma unroll
-                for (int l = 0; l < SB; ++l)
-                    W[r * PT + c0 + l] = p[l];
-        }
-        __syncthreads();
+            for (int l = 0; l < SB; ++l)
+                W[r * PT + c0 + l] = p[l];
+    };
+    if (warp == 0)
+        phase1(0);
+    __syncthreads();
+    if (tid == 0) g_diag_ts[tsi] = gtimer0();
+    ++tsi;
+    for (int c0 = 0; c0 < NB; c0 += SB) {
         const int rest = NB - c0 - SB;
         if (rest == 0)
             break;
@@ -135,12 +151,27 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
                 W[(c0 + i) * PT + c] = y[i];
         }
         __syncthreads();
-        // (4) trailing 128-c0-16 square: W22 -= L21 U12
-        panel::smem_update16(W + (c0 + SB) * PT + c0 + SB, PT, W + (c0 + SB) * PT + c0, PT, W + c0 * PT + c0 + SB,
-                             PT, rest, rest, warp, PK_WARPS, lane);
+        if (tid == 0) g_diag_ts[tsi] = gtimer0();
+        ++tsi;
+        // (4) trailing update W22 -= L21 U12 with lookahead: warp 0 updates the next 16 x 16
+        //     diagonal block and factors it (phase 1 of c0 + 16) while warps 1..7 update the rest
+        double* C22 = W + (c0 + SB) * PT + c0 + SB;
+        const double* L21 = W + (c0 + SB) * PT + c0;
+        const double* U12 = W + c0 * PT + c0 + SB;
+        if (warp == 0) {
+            panel::smem_update16(C22, PT, L21, PT, U12, PT, SB, SB, 0, 1, lane);
+            __syncwarp();
+            phase1(c0 + SB);
+        } else {
+            panel::smem_update16(C22, PT, L21, PT, U12, PT, rest, rest, warp - 1, PK_WARPS - 1, lane, true);
+        }
         __syncthreads();
+        if (tid == 0) g_diag_ts[tsi] = gtimer0();
+        ++tsi;
     }
     panel::store_tile<NB, NB, PK_THREADS>(blk, lda, W, PT, bs, bs);
+    if (tid == 0) g_diag_ts[tsi] = gtimer0();
+    if (tid == 0) g_diag_ts[63] = tsi + 1;
     if (tid < bs) { // |pivots| and the first step below the floor (genp.cpp:24-26)
         pivots[o + tid] = pabs[tid];
         if (pabs[tid] < floor)
@@ -153,8 +184,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
 //   CTAs [nrb, 2 nrb2): 64-column tiles of A12 <- L11^-1 A12 (L11 y = a, unit lower)
 // Each sub-panel: per-thread 16-step substitution, then a DMMA update of the remaining
 // columns (right) / rows (left) of the tile.
-constexpr int TR_TILE = 64;
-__global__ void __launch_bounds__(PK_THREADS, 1) k_panel_trsm(double* a, uint64_t lda, uint64_t o, uint64_t rest,
+constexpr int TR_TILE = 64;     // rows (right) / columns (left) per CTA
+constexpr int TR_THREADS = 256; // 8 warps
+constexpr int TR_WARPS = TR_THREADS / 32;
+__global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_t lda, uint64_t o, uint64_t rest,
                                                               int nrb) {
     extern __shared__ double smt[];
     double* T = smt;            // NB x PT triangle
@@ -163,26 +196,31 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_panel_trsm(double* a, uint64_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool right = static_cast<int>(blockIdx.x) < nrb;
     const double* diag = a + o * lda + o;
+    const bool tr = (blockIdx.x == 0 || static_cast<int>(blockIdx.x) == nrb) && tid == 0;
+    unsigned long long* tsb = g_trsm_ts[right ? 0 : 1];
+    int tsi = 0;
+    if (tr) tsb[tsi] = gtimer0();
+    ++tsi;
     if (right)
-        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return j >= i; },
-                                             [](int, int) { return 0.0; });
+        panel::load_tile_async<NB, NB, TR_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return j >= i; });
     else
-        panel::load_tile<NB, NB, PK_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return i > j; },
-                                             [](int, int) { return 0.0; });
+        panel::load_tile_async<NB, NB, TR_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return i > j; });
     if (right) {
         const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * TR_TILE;
         const int nr = static_cast<int>(rest - r0 < TR_TILE ? rest - r0 : TR_TILE);
         double* src = a + (o + NB + r0) * lda + o;
-        panel::load_tile<TR_TILE, NB, PK_THREADS>(X, PT, src, lda, nr, NB, [](int, int) { return true; },
-                                                  [](int, int) { return 0.0; });
+        panel::load_tile_async<TR_TILE, NB, TR_THREADS>(X, PT, src, lda, nr, NB, [](int, int) { return true; });
+        panel::cp_async_wait_all();
         __syncthreads();
-        for (int j = tid; j < NB; j += PK_THREADS) {
+        if (tr) tsb[tsi] = gtimer0();
+        ++tsi;
+        for (int j = tid; j < NB; j += TR_THREADS) {
             const double d = T[j * PT + j];
             rcp[j] = (d == 0.0) ? 0.0 : 1.0 / d;
         }
         __syncthreads();
         for (int c0 = 0; c0 < NB; c0 += SB) {
-            for (int r = tid; r < TR_TILE; r += PK_THREADS) {
+            for (int r = tid; r < TR_TILE; r += TR_THREADS) {
                 double x[SB];
 #pragma unroll
                 for (int l = 0; l < SB; ++l)
@@ -201,22 +239,27 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_panel_trsm(double* a, uint64_
                     X[r * PT + c0 + l] = x[l];
             }
             __syncthreads();
+            if (tr) tsb[tsi] = gtimer0();
+            ++tsi;
             if (c0 + SB < NB)
                 panel::smem_update16(X + c0 + SB, PT, X + c0, PT, T + c0 * PT + c0 + SB, PT, TR_TILE,
-                                     NB - c0 - SB, warp, PK_WARPS, lane);
+                                     NB - c0 - SB, warp, TR_WARPS, lane);
             __syncthreads();
+            if (tr) tsb[tsi] = gtimer0();
+            ++tsi;
         }
-        panel::store_tile<TR_TILE, NB, PK_THREADS>(src, lda, X, PT, nr, NB);
+        panel::store_tile<TR_TILE, NB, TR_THREADS>(src, lda, X, PT, nr, NB);
+        if (tr) { tsb[tsi] = gtimer0(); tsb[31] = tsi + 1; }
     } else {
         constexpr int XP = TR_TILE + 4;
         const uint64_t c0g = static_cast<uint64_t>(blockIdx.x - nrb) * TR_TILE;
         const int nc = static_cast<int>(rest - c0g < TR_TILE ? rest - c0g : TR_TILE);
         double* src = a + o * lda + o + NB + c0g;
-        panel::load_tile<NB, TR_TILE, PK_THREADS>(X, XP, src, lda, NB, nc, [](int, int) { return true; },
-                                                  [](int, int) { return 0.0; });
+        panel::load_tile_async<NB, TR_TILE, TR_THREADS>(X, XP, src, lda, NB, nc, [](int, int) { return true; });
+        panel::cp_async_wait_all();
         __syncthreads();
         for (int c0 = 0; c0 < NB; c0 += SB) {
-            for (int c = tid; c < TR_TILE; c += PK_THREADS) {
+            for (int c = tid; c < TR_TILE; c += TR_THREADS) {
                 double y[SB];
 #pragma unroll
                 for (int i = 0; i < SB; ++i)
@@ -233,10 +276,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_panel_trsm(double* a, uint64_
             __syncthreads();
             if (c0 + SB < NB)
                 panel::smem_update16(X + (c0 + SB) * XP, XP, T + (c0 + SB) * PT + c0, PT, X + c0 * XP, XP,
-                                     NB - c0 - SB, TR_TILE, warp, PK_WARPS, lane);
+                                     NB - c0 - SB, TR_TILE, warp, TR_WARPS, lane);
             __syncthreads();
         }
-        panel::store_tile<NB, TR_TILE, PK_THREADS>(src, lda, X, XP, NB, nc);
+        panel::store_tile<NB, TR_TILE, TR_THREADS>(src, lda, X, XP, NB, nc);
     }
 }
 
@@ -499,8 +542,15 @@ __global__ void __launch_bounds__(WV_THREADS, 1) k_trsv_wave(const double* __res
     }
 }
 
-size_t trsm_smem() { return (static_cast<size_t>(NB) * PT + static_cast<size_t>(NB) * (TR_TILE + 4)) * sizeof(double); }
-size_t diag_smem() { return static_cast<size_t>(NB) * PT * sizeof(double); }
+// The panel kernels are on the factorization's critical path and run beside the trailing
+// GEMMs of the other streams: they reserve (nearly) all of an SM's shared memory so no GEMM
+// CTA is co-scheduled on their SM and steals issue slots.
+constexpr size_t kPanelSmem = 220 * 1024;
+size_t trsm_smem() {
+    const size_t need = (static_cast<size_t>(NB) * PT + static_cast<size_t>(NB) * (TR_TILE + 4)) * sizeof(double);
+    return need > kPanelSmem ? need : kPanelSmem;
+}
+size_t diag_smem() { return kPanelSmem; }
 
 void prep_attrs() {
     static bool done[16] = {};
@@ -521,8 +571,8 @@ void prep_attrs() {
 
 // Per-thread helper stream (high priority) and events for the panel lookahead.
 struct Lookahead {
-    cudaStream_t s2 = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t s2 = nullptr, s3 = nullptr;
+    cudaEvent_t ev[6] = {};
     int device = -1;
 };
 
@@ -532,6 +582,7 @@ Lookahead& lookahead() {
         int lo = 0, hi = 0;
         RL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         RL_CUDA(cudaStreamCreateWithPriority(&la.s2, cudaStreamNonBlocking, hi));
+        RL_CUDA(cudaStreamCreateWithPriority(&la.s3, cudaStreamNonBlocking, hi));
         for (auto& e : la.ev)
             RL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         la.device = ctx().device;
@@ -564,51 +615,85 @@ void transpose_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, double
     RL_LAUNCHED();
 }
 
-// Blocked right-looking GENP in place (packed LU), outer block 256 built from two 128
-// steps, with one-panel lookahead:
-//   main stream : Schur update of outer step k split into the next outer panel's strips
-//                 (first) and the remaining trailing block (the big K = 256 DMMA GEMM)
-//   panel stream: the next outer panel (2 x [diagonal LU + both TRSMs] + the strip update
-//                 between them), started as soon as the strips of step k are done, so it
-//                 runs under the trailing GEMM of step k.
-// The regions written concurrently are disjoint.  The L and U produced are
-// those of block_ge with block 128 (genp.cpp:43-104) up to rounding.  aux is unused.
+void diag_trace_dump() {
+    unsigned long long h[64];
+    RL_CUDA(cudaDeviceSynchronize());
+    RL_CUDA(cudaMemcpyFromSymbol(h, g_diag_ts, sizeof(h)));
+    const int cnt = static_cast<int>(h[63]);
+    std::fprintf(stderr, "diag phases (us from start):");
+    for (int i = 1; i < cnt && i < 63; ++i)
+        std::fprintf(stderr, " %.2f", (h[i] - h[0]) * 1e-3);
+    std::fprintf(stderr, "\n");
+    unsigned long long t[2][32];
+    RL_CUDA(cudaMemcpyFromSymbol(t, g_trsm_ts, sizeof(t)));
+    std::fprintf(stderr, "trsm(right) phases (us from start):");
+    for (int i = 1; i < static_cast<int>(t[0][31]) && i < 31; ++i)
+        std::fprintf(stderr, " %.2f", (t[0][i] - t[0][0]) * 1e-3);
+    std::fprintf(stderr, "\n");
+}
+
+// Blocked right-looking GENP in place (packed LU), outer block W = 256 built from two 128
+// steps, with lookahead over three streams so that the critical chain per outer step is
+// only  diag LU -> TRSMs -> 128^3 update -> diag LU -> TRSMs  (+ one 128 x 128 x 256 GEMM):
+//   s1 (main)   after panel k: the next diagonal block (128^2 x 256) first [E_nd], then the
+//               next panel's column strip and row strip [E_strips], then the remaining
+//               trailing update (the big K = 256 DMMA GEMM) while panel k+1 runs;
+//   s2 (panel)  diag LU (waits E_nd only) -> TRSMs (wait E_strips) -> the second 128 block's
+//               own 128^3 update -> its diag LU -> its TRSMs (wait E_s3)  [E_panel];
+//   s3 (helper) the second 128 step's column / row strips (K = 128), beside s2.
+// s2 and s3 have high priority.  Concurrently written regions are disjoint.
+// The L and U produced are those of block_ge with block 128 (genp.cpp:43-104) up to
+// rounding.  aux is unused.
 void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor, double* d_pivots,
                          unsigned long long* d_breakdown, double* aux) {
     (void)aux;
     prep_attrs();
     cudaStream_t s1 = stream();
     Lookahead& la = lookahead();
-    cudaStream_t s2 = la.s2;
+    cudaStream_t s2 = la.s2, s3 = la.s3;
+    cudaEvent_t E_nd = la.ev[0], E_strips = la.ev[1], E_panel = la.ev[2], E_t1 = la.ev[3], E_s3 = la.ev[4];
     auto at = [&](uint64_t i, uint64_t j) { return a + i * lda + j; };
-    // one 128-wide step: diagonal LU + both TRSMs over everything below / right of it
-    auto panel128 = [&](uint64_t o, cudaStream_t st) {
+    const cudaStream_t keep = ctx().stream;
+    // C -= A B on stream st (m x nn x k, all blocks of a)
+    auto upd = [&](cudaStream_t st, uint64_t m, uint64_t nn, uint64_t k, const double* A, const double* B, double* C) {
+        if (m == 0 || nn == 0)
+            return;
+        ctx().stream = st;
+        gemm(false, false, m, nn, k, -1.0, A, lda, B, lda, 1.0, C, lda);
+        ctx().stream = keep;
+    };
+    auto diag = [&](uint64_t o, cudaStream_t st) {
         k_diag_lu<<<1, PK_THREADS, diag_smem(), st>>>(a, lda, n, o, pivot_floor, d_pivots, d_breakdown);
         RL_LAUNCHED();
+    };
+    auto trsm = [&](uint64_t o, cudaStream_t st) {
         const uint64_t rest = n - o - std::min<uint64_t>(NB, n - o);
         if (rest) {
             const int nrb = static_cast<int>((rest + TR_TILE - 1) / TR_TILE);
-            k_panel_trsm<<<2 * nrb, PK_THREADS, trsm_smem(), st>>>(a, lda, o, rest, nrb);
+            k_panel_trsm<<<2 * nrb, TR_THREADS, trsm_smem(), st>>>(a, lda, o, rest, nrb);
             RL_LAUNCHED();
         }
     };
-    // one outer panel of width W = 2 * NB at o (block LU with a 256 pivot block composed of two
-    // 128 steps): step 1, then only the second sub-panel's strips are updated (the trailing
-    // update is delayed), then step 2.  The trailing matrix is updated once with K = 256.
-    auto panel256 = [&](uint64_t o, cudaStream_t st) {
-        cudaStream_t keep = ctx().stream;
-        ctx().stream = st; // gemm() launches on ctx().stream
-        panel128(o, st);
+    // outer panel at o on s2: waits E_nd before its diag LU and E_strips before its TRSMs
+    auto panel256 = [&](uint64_t o) {
+        RL_CUDA(cudaStreamWaitEvent(s2, E_nd, 0));
+        diag(o, s2);
+        RL_CUDA(cudaStreamWaitEvent(s2, E_strips, 0));
+        trsm(o, s2);
         const uint64_t o2 = o + NB;
         if (o2 < n) {
-            const uint64_t rest = n - o2, w2 = std::min<uint64_t>(NB, rest);
-            gemm(false, false, rest, w2, NB, -1.0, at(o2, o), lda, at(o, o2), lda, 1.0, at(o2, o2), lda);
-            if (rest > w2)
-                gemm(false, false, w2, rest - w2, NB, -1.0, at(o2, o), lda, at(o, o2 + w2), lda, 1.0,
-                     at(o2, o2 + w2), lda);
-            panel128(o2, st);
+            const uint64_t rest2 = n - o2, w2 = std::min<uint64_t>(NB, rest2);
+            RL_CUDA(cudaEventRecord(E_t1, s2));
+            RL_CUDA(cudaStreamWaitEvent(s3, E_t1, 0));
+            upd(s2, w2, w2, NB, at(o2, o), at(o, o2), at(o2, o2));                             // own block
+            upd(s3, rest2 - w2, w2, NB, at(o2 + w2, o), at(o, o2), at(o2 + w2, o2));           // column strip
+            upd(s3, w2, rest2 - w2, NB, at(o2, o), at(o, o2 + w2), at(o2, o2 + w2));           // row strip
+            RL_CUDA(cudaEventRecord(E_s3, s3));
+            diag(o2, s2);
+            RL_CUDA(cudaStreamWaitEvent(s2, E_s3, 0));
+            trsm(o2, s2);
         }
-        ctx().stream = keep;
+        RL_CUDA(cudaEventRecord(E_panel, s2));
     };
     constexpr uint64_t W = 2 * NB;
     // RL_LU_TRACE=1: per outer step, time of the panel path (s2) and of the step on s1 (dev)
@@ -622,35 +707,37 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         RL_CUDA(cudaEventRecord(e, st));
         tev.push_back(e);
     };
-    panel256(0, s1);
+    // the first panel: nothing to wait for beyond the work already on s1
+    RL_CUDA(cudaEventRecord(E_nd, s1));
+    RL_CUDA(cudaEventRecord(E_strips, s1));
+    panel256(0);
     for (uint64_t o = 0; o + W < n; o += W) {
+        RL_CUDA(cudaStreamWaitEvent(s1, E_panel, 0));
         mark(s1);
-        const uint64_t rest = n - o - W;                 // trailing size after this outer step
-        const uint64_t w2 = std::min<uint64_t>(W, rest); // width of the next outer panel
-        const double* L21 = at(o + W, o);                // rest x 256
-        const double* U12 = at(o, o + W);                // 256 x rest
-        // (i) next outer panel's column strip and row strip (K = 256)
-        gemm(false, false, rest, w2, W, -1.0, L21, lda, U12, lda, 1.0, at(o + W, o + W), lda);
-        if (rest > w2)
-            gemm(false, false, w2, rest - w2, W, -1.0, L21, lda, at(o, o + W + w2), lda, 1.0,
-                 at(o + W, o + W + w2), lda);
-        // hand the next outer panel to the high-priority panel stream ...
-        cudaEvent_t strips = la.ev[0], done = la.ev[1];
-        RL_CUDA(cudaEventRecord(strips, s1));
-        RL_CUDA(cudaStreamWaitEvent(s2, strips, 0));
+        const uint64_t p = o + W, rest = n - p;             // next panel at p, trailing size
+        const uint64_t w2n = std::min<uint64_t>(W, rest);   // width of the next outer panel
+        const uint64_t nd = std::min<uint64_t>(NB, rest);   // its first diagonal block
+        const double* L21 = at(p, o);                       // rest x 256
+        const double* U12 = at(o, p);                       // 256 x rest
+        upd(s1, nd, nd, W, L21, U12, at(p, p));                                     // next diag block
+        RL_CUDA(cudaEventRecord(E_nd, s1));
+        upd(s1, nd, rest - nd, W, L21, at(o, p + nd), at(p, p + nd));               // its block row
+        upd(s1, rest - nd, w2n, W, at(p + nd, o), U12, at(p + nd, p));              // panel columns below
+        upd(s1, w2n - nd, rest - w2n, W, at(p + nd, o), at(o, p + w2n), at(p + nd, p + w2n)); // 2nd block row
+        RL_CUDA(cudaEventRecord(E_strips, s1));
         mark(s2);
-        panel256(o + W, s2);
+        panel256(p);
         mark(s2);
-        RL_CUDA(cudaEventRecord(done, s2));
-        // (ii) ... while the main stream runs the remaining trailing update (K = 256)
-        if (rest > w2)
-            gemm(false, false, rest - w2, rest - w2, W, -1.0, at(o + W + w2, o), lda, at(o, o + W + w2), lda, 1.0,
-                 at(o + W + w2, o + W + w2), lda);
+        // the remaining trailing update runs under the next panel
+        upd(s1, rest - w2n, rest - w2n, W, at(p + w2n, o), at(o, p + w2n), at(p + w2n, p + w2n));
         mark(s1);
-        RL_CUDA(cudaStreamWaitEvent(s1, done, 0));
     }
+    RL_CUDA(cudaStreamWaitEvent(s1, E_panel, 0));
     mark(s1);
-    if (trace) { // per step: [s1 start, s2 start, s2 end, s1 trailing end], then the final mark
+    static const bool dtrace = std::getenv("RL_DIAG_TRACE") != nullptr;
+    if (dtrace)
+        diag_trace_dump();
+    if (trace) { // per step: [s1 start, s2 start, s2 end, s1 trailing end], then the next s1 start
         RL_CUDA(cudaEventSynchronize(tev.back()));
         for (size_t i = 0; i + 4 < tev.size(); i += 4) {
             float strip = 0, panel = 0, trail = 0, step = 0;
@@ -671,6 +758,7 @@ void genp_factor_dev(uint64_t n, double* a, uint64_t lda, double pivot_floor, do
     RL_CUDA(cudaMemsetAsync(d_breakdown, 0xff, sizeof(int64_t), stream())); // -1 == none
     genp_factor_blocked(n, a, lda, pivot_floor, d_pivots,
                         reinterpret_cast<unsigned long long*>(d_breakdown), nullptr);
+
 }
 
 // Kept for the C-ABI signature (the solves need no precomputed block inverses).

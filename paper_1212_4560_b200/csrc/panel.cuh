@@ -24,9 +24,11 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 // C[0:M, 0:N] -= A[0:M, 0:16] * B[0:16, 0:N] on shared-memory tiles (row-major, pitches
-// lda/ldb/ldc).  M, N multiples of 8.  Warps take 8x8 output fragments round-robin.
+// lda/ldb/ldc).  M, N multiples of 8.  Warps take 8x8 output fragments round-robin;
+// skip_corner leaves the top-left 16 x 16 block out.
 __device__ __forceinline__ void smem_update16(double* C, int ldc, const double* A, int lda, const double* B,
-                                              int ldb, int M, int N, int warp, int nwarps, int lane) {
+                                              int ldb, int M, int N, int warp, int nwarps, int lane,
+                                              bool skip_corner = false) {
     const int g = lane >> 2, t = lane & 3;
     const int fm = M >> 3, fn = N >> 3;
     // fragment f = (mi, nj) row-major, walked with an incremental (mi, nj) (no divisions)
@@ -38,6 +40,8 @@ __device__ __forceinline__ void smem_update16(double* C, int ldc, const double* 
             nj -= fn;
             ++mi;
         }
+        if (skip_corner && m0 < 16 && n0 < 16) // the 16 x 16 corner is updated by its own warp
+            continue;
         double acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int k0 = 0; k0 < SB; k0 += 4)
@@ -76,6 +80,25 @@ __device__ __forceinline__ void load_tile(double* s, int sp, const double* g, ui
         }
     }
 }
+
+// Global -> shared copy of an R x C tile with cp.async (8-byte copies, all in flight at
+// once, no register staging): elements outside vr x vc or with keep(i, j) false are
+// zero-filled without reading global memory.  Caller: cp_async_wait_all() + __syncthreads().
+template <int R, int C, int THREADS, typename Keep>
+__device__ __forceinline__ void load_tile_async(double* s, int sp, const double* g, uint64_t ld, int vr, int vc,
+                                                Keep keep) {
+    const int tid = threadIdx.x;
+#pragma unroll 4
+    for (int e = tid; e < R * C; e += THREADS) {
+        const int i = e / C, j = e % C;
+        const bool ok = i < vr && j < vc && keep(i, j);
+        const double* src = ok ? g + static_cast<uint64_t>(i) * ld + j : g;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(s + i * sp + j));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // Shared -> global store of the valid vr x vc part of an R x C tile (8-deep batches).
 template <int R, int C, int THREADS>
