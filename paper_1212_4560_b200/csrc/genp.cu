@@ -26,6 +26,7 @@ namespace rl {
 namespace {
 
 constexpr int NB = 128;        // block size (config 3's "Block size 128")
+constexpr int kOuterSteps = 4; // 128-steps per outer block (trailing updates with K = 512)
 
 // ------------------------------------------------------------ panel kernels ----
 // All three use the two-level scheme of panel.cuh: 16-wide sub-panels, per-thread
@@ -654,6 +655,7 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
     cudaEvent_t E_nd = la.ev[0], E_strips = la.ev[1], E_panel = la.ev[2], E_t1 = la.ev[3], E_s3 = la.ev[4];
     auto at = [&](uint64_t i, uint64_t j) { return a + i * lda + j; };
     const cudaStream_t keep = ctx().stream;
+    const uint64_t W = static_cast<uint64_t>(kOuterSteps) * NB; // outer block
     // C -= A B on stream st (m x nn x k, all blocks of a)
     auto upd = [&](cudaStream_t st, uint64_t m, uint64_t nn, uint64_t k, const double* A, const double* B, double* C) {
         if (m == 0 || nn == 0)
@@ -674,28 +676,33 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
             RL_LAUNCHED();
         }
     };
-    // outer panel at o on s2: waits E_nd before its diag LU and E_strips before its TRSMs
-    auto panel256 = [&](uint64_t o) {
+    // outer panel [o, o + W) on s2 as W / 128 steps: waits E_nd before its first diag LU and
+    // E_strips before its first TRSMs.  After step i (K = 128 from its L and U): the next
+    // step's own 128 x 128 block on s2 (its LU starts next), and on s3 the rest of the panel's
+    // columns (rows below) and the rest of the panel's rows (columns right, up to n), which
+    // the next step's TRSMs wait for.  Rows and columns beyond the panel get their update
+    // later with K = W (the trailing update of the outer step).
+    auto panelW = [&](uint64_t o) {
+        const uint64_t oe = std::min<uint64_t>(o + W, n);
         RL_CUDA(cudaStreamWaitEvent(s2, E_nd, 0));
         diag(o, s2);
         RL_CUDA(cudaStreamWaitEvent(s2, E_strips, 0));
         trsm(o, s2);
-        const uint64_t o2 = o + NB;
-        if (o2 < n) {
-            const uint64_t rest2 = n - o2, w2 = std::min<uint64_t>(NB, rest2);
+        for (uint64_t oi = o; oi + NB < oe; oi += NB) {
+            const uint64_t on = oi + NB, wn = std::min<uint64_t>(NB, oe - on);
             RL_CUDA(cudaEventRecord(E_t1, s2));
             RL_CUDA(cudaStreamWaitEvent(s3, E_t1, 0));
-            upd(s2, w2, w2, NB, at(o2, o), at(o, o2), at(o2, o2));                             // own block
-            upd(s3, rest2 - w2, w2, NB, at(o2 + w2, o), at(o, o2), at(o2 + w2, o2));           // column strip
-            upd(s3, w2, rest2 - w2, NB, at(o2, o), at(o, o2 + w2), at(o2, o2 + w2));           // row strip
+            upd(s2, wn, wn, NB, at(on, oi), at(oi, on), at(on, on));                           // own block
+            upd(s3, n - on - wn, oe - on, NB, at(on + wn, oi), at(oi, on), at(on + wn, on));   // panel cols below
+            upd(s3, wn, oe - on - wn, NB, at(on, oi), at(oi, on + wn), at(on, on + wn));       // rest of its rows in panel
+            upd(s3, oe - on, n - oe, NB, at(on, oi), at(oi, oe), at(on, oe));                  // panel rows, right of panel
             RL_CUDA(cudaEventRecord(E_s3, s3));
-            diag(o2, s2);
+            diag(on, s2);
             RL_CUDA(cudaStreamWaitEvent(s2, E_s3, 0));
-            trsm(o2, s2);
+            trsm(on, s2);
         }
         RL_CUDA(cudaEventRecord(E_panel, s2));
     };
-    constexpr uint64_t W = 2 * NB;
     // RL_LU_TRACE=1: per outer step, time of the panel path (s2) and of the step on s1 (dev)
     static const bool trace = std::getenv("RL_LU_TRACE") != nullptr;
     std::vector<cudaEvent_t> tev;
@@ -710,7 +717,7 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
     // the first panel: nothing to wait for beyond the work already on s1
     RL_CUDA(cudaEventRecord(E_nd, s1));
     RL_CUDA(cudaEventRecord(E_strips, s1));
-    panel256(0);
+    panelW(0);
     for (uint64_t o = 0; o + W < n; o += W) {
         RL_CUDA(cudaStreamWaitEvent(s1, E_panel, 0));
         mark(s1);
@@ -726,7 +733,7 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         upd(s1, w2n - nd, rest - w2n, W, at(p + nd, o), at(o, p + w2n), at(p + nd, p + w2n)); // 2nd block row
         RL_CUDA(cudaEventRecord(E_strips, s1));
         mark(s2);
-        panel256(p);
+        panelW(p);
         mark(s2);
         // the remaining trailing update runs under the next panel
         upd(s1, rest - w2n, rest - w2n, W, at(p + w2n, o), at(o, p + w2n), at(p + w2n, p + w2n));
