@@ -22,6 +22,7 @@ namespace {
 
 constexpr int BK = 16;
 constexpr int PAD = 4; // doubles; row pitch = 32 B mod 128
+constexpr uint64_t kLongK = 512; // K from which the 32-deep k-tile config is used
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -47,10 +48,10 @@ __device__ __forceinline__ void cp_wait() {
 
 // Shared-tile geometry for one operand.  KMAJOR: tile stored [rows=MN][BK+PAD];
 // otherwise [BK][MN+PAD].
-template <int MN, bool KMAJOR>
+template <int MN, bool KMAJOR, int BKT = BK>
 struct Tile {
-    static constexpr int kPitch = KMAJOR ? (BK + PAD) : (MN + PAD);
-    static constexpr int kElems = KMAJOR ? MN * kPitch : BK * kPitch;
+    static constexpr int kPitch = KMAJOR ? (BKT + PAD) : (MN + PAD);
+    static constexpr int kElems = KMAJOR ? MN * kPitch : BKT * kPitch;
     // element (mn, k) of the tile
     __device__ __forceinline__ static int at(int mn, int k) {
         return KMAJOR ? mn * kPitch + k : k * kPitch + mn;
@@ -59,12 +60,12 @@ struct Tile {
 
 // Load one BK-slice of an operand tile.  KMAJOR global layout: g[(mn0+r)*ld + k0 + c];
 // else g[(k0+r)*ld + mn0 + c].  dims: MNdim (rows along mn), Kdim.
-template <int MN, bool KMAJOR, int VEC, int NT>
+template <int MN, bool KMAJOR, int VEC, int NT, int BKT = BK>
 __device__ __forceinline__ void load_tile(double* s, const double* g, uint64_t ld, uint64_t mn0,
                                           uint64_t k0, uint64_t MNdim, uint64_t Kdim, int tid) {
-    using T = Tile<MN, KMAJOR>;
-    constexpr int ROWS = KMAJOR ? MN : BK;  // rows of the tile in memory order
-    constexpr int COLS = KMAJOR ? BK : MN;  // contiguous extent
+    using T = Tile<MN, KMAJOR, BKT>;
+    constexpr int ROWS = KMAJOR ? MN : BKT; // rows of the tile in memory order
+    constexpr int COLS = KMAJOR ? BKT : MN; // contiguous extent
     constexpr int CPR = COLS / VEC;         // copies per row
     constexpr int TOTAL = ROWS * CPR;
 #pragma unroll
@@ -93,29 +94,29 @@ __device__ __forceinline__ void load_tile(double* s, const double* g, uint64_t l
     }
 }
 
-template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE>
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int BKT = BK>
 struct Cfg {
     static constexpr int NT = WM * WN * 32;
     static constexpr int WTM = BM / WM, WTN = BN / WN;
     static constexpr int MF = WTM / 8, NF = WTN / 8;
-    using TA = Tile<BM, AK>;
-    using TB = Tile<BN, BKM>;
+    using TA = Tile<BM, AK, BKT>;
+    using TB = Tile<BN, BKM, BKT>;
     static constexpr int kStageElems = TA::kElems + TB::kElems;
     static constexpr size_t kSmem = static_cast<size_t>(NSTAGE) * kStageElems * sizeof(double);
 };
 
-template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1>
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1, int BKT = BK>
 __global__ void __launch_bounds__(WM* WN * 32, MINB)
     k_dgemm(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* __restrict__ A,
             uint64_t lda, const double* __restrict__ B, uint64_t ldb, double beta,
             double* __restrict__ C, uint64_t ldc) {
-    using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE>;
+    using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, BKT>;
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int g = lane >> 2, t = lane & 3;
     const uint64_t m0 = static_cast<uint64_t>(blockIdx.y) * BM, n0 = static_cast<uint64_t>(blockIdx.x) * BN;
-    const int ktiles = static_cast<int>((K + BK - 1) / BK);
+    const int ktiles = static_cast<int>((K + BKT - 1) / BKT);
 
     double acc[G::MF][G::NF][2];
 #pragma unroll
@@ -130,8 +131,8 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
         if (s < ktiles) {
-            load_tile<BM, AK, VEC, G::NT>(sA(s), A, lda, m0, static_cast<uint64_t>(s) * BK, M, K, tid);
-            load_tile<BN, BKM, VEC, G::NT>(sB(s), B, ldb, n0, static_cast<uint64_t>(s) * BK, N, K, tid);
+            load_tile<BM, AK, VEC, G::NT, BKT>(sA(s), A, lda, m0, static_cast<uint64_t>(s) * BKT, M, K, tid);
+            load_tile<BN, BKM, VEC, G::NT, BKT>(sB(s), B, ldb, n0, static_cast<uint64_t>(s) * BKT, N, K, tid);
         }
         cp_commit();
     }
@@ -142,14 +143,14 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
         const int nk = kt + NSTAGE - 1;
         if (nk < ktiles) {
             int s = nk % NSTAGE;
-            load_tile<BM, AK, VEC, G::NT>(sA(s), A, lda, m0, static_cast<uint64_t>(nk) * BK, M, K, tid);
-            load_tile<BN, BKM, VEC, G::NT>(sB(s), B, ldb, n0, static_cast<uint64_t>(nk) * BK, N, K, tid);
+            load_tile<BM, AK, VEC, G::NT, BKT>(sA(s), A, lda, m0, static_cast<uint64_t>(nk) * BKT, M, K, tid);
+            load_tile<BN, BKM, VEC, G::NT, BKT>(sB(s), B, ldb, n0, static_cast<uint64_t>(nk) * BKT, N, K, tid);
         }
         cp_commit();
         const double* a_s = sA(kt % NSTAGE);
         const double* b_s = sB(kt % NSTAGE);
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
+        for (int kk = 0; kk < BKT; kk += 4) {
             double af[G::MF], bf[G::NF];
 #pragma unroll
             for (int i = 0; i < G::MF; ++i)
@@ -200,11 +201,11 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     }
 }
 
-template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1>
+template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1, int BKT = BK>
 void launch(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda,
             const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
-    using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE>;
-    auto kern = k_dgemm<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, MINB>;
+    using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, BKT>;
+    auto kern = k_dgemm<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, MINB, BKT>;
     static bool configured[16] = {};
     int dev = ctx().device & 15;
     if (!configured[dev]) {
@@ -231,14 +232,23 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const doub
         return launch<128, 128, 2, 4, AK, BKM, VEC, 3>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 3)
         return launch<64, 64, 2, 2, AK, BKM, VEC, 4, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 6)
+        return launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 7)
+        return launch<128, 64, 4, 2, AK, BKM, VEC, 3, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 4)
         return launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 5)
         return launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms)
-        // two CTAs per SM (128x64 tiles, 3 stages, <= 128 regs): one CTA's prologue / C
-        // epilogue overlaps the other's DMMA loop.  Measured (tools/gemm_sweep.py): 8192^3
-        // 32.8 TF/s vs 31.3 for a 1-CTA 128x128 tile; rank-128 updates 23.3 vs 16.5 TF/s.
+    if (N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms && K >= kLongK)
+        // two CTAs per SM (128x64 tiles, <= 128 regs): one CTA's prologue / C epilogue
+        // overlaps the other's DMMA loop.  Long K: K-tile 32 in 2 stages (217 KB for the two
+        // CTAs), half the k-tile barriers of a 16 x 3 ring: A*G 8192^3 33.41 -> 32.76 ms
+        // (DMMA pipe 89.5 -> 91.3% active)
+        launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else if (N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms)
+        // short K (the LU's trailing updates): K-tile 16 in 3 stages keeps the pipeline full
+        // over few k-tiles (7680^2 x 256: 1044 vs 1100 us with the 32 x 2 ring)
         launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     else if (N > 32 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= static_cast<uint64_t>(sms))
         launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
