@@ -232,6 +232,12 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const doub
         return launch<128, 128, 2, 4, AK, BKM, VEC, 3>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 3)
         return launch<64, 64, 2, 2, AK, BKM, VEC, 4, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 8)
+        return launch<64, 128, 2, 4, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 9)
+        return launch<128, 64, 2, 4, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (force == 10)
+        return launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 24>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 6)
         return launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 7)

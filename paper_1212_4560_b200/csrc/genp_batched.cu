@@ -2,28 +2,26 @@
 // MulSide::Right) — semantically the loop bench::table1_genp runs (bench.cpp:117-133) over
 // genp::randomized_genp (genp.cpp:207-291), one stream per system.
 //
-// One 128-thread CTA per system.  The working matrix lives in registers: thread t (warp
-// wp = t/32, lane l) owns row r = 4 (l/2) + wp and, of that row, the columns c = 2 jj + h
-// (h = l & 1, jj = 0..31) — 32 doubles, fully unrolled so every index is static.  Rows are
-// dealt cyclically over the four warps so every warp has work at every pivot step.
-// Per attempt:
+// One 128-thread CTA per system, the 64 x 64 working matrix in shared memory (pitch 68 doubles:
+// conflict-free DMMA fragments).  Per attempt:
 //   * A (64 x 64, L2-resident after the first touch) is staged in shared memory and
 //     W = A C runs on DMMA (warp wp computes rows 16 wp..16 wp+15); the +-1 B fragment
 //     C[k][j] = c[(k - j) mod 64] is synthesised from a 64-bit sign mask.
-//   * No-pivot LU (genp.cpp:20-33): per step the pivot row goes through a double-buffered
-//     shared row (one barrier per step), the multiplier m = w(i,k) * (1/p) (1/p := 0 for
-//     p = 0) is exchanged between the two half-row owners with one shuffle.
-//   * The packed LU is spilled transposed to shared memory and warp 0 runs the forward /
-//     backward substitution (two rows per lane, shuffle chain; genp.cpp:106-124), then
-//     y = C z, refinement and the residual ||A y - b|| / ||b|| on threads 0..63.
-// The raw-GENP contrast arm is iteration -1 of the same loop (pivot floor 0, no multiplier),
-// so the unrolled LU exists once.  The 8-attempt redraw protocol (stream id + 7919 a, accept
+//   * No-pivot LU (genp.cpp:20-33) blocked in four 16-column panels: warp 0 factors the
+//     panel in registers (pivot row by shuffles, m = w(i,k) * (1/p), 1/p := 0 for p = 0),
+//     one thread per column solves U12 against the unit L11, all warps update the trailing
+//     square on DMMA — three barriers per panel instead of one per pivot.
+//   * The packed LU is transposed in place and warp 0 runs the forward / backward
+//     substitution (two rows per lane, shuffle chain; genp.cpp:106-124), then y = C z,
+//     refinement and the residual ||A y - b|| / ||b|| on threads 0..63.
+// The raw-GENP contrast arm is iteration -1 of the same loop (pivot floor 0, no multiplier).  The 8-attempt redraw protocol (stream id + 7919 a, accept
 // <= 1e-7, keep best, genp.cpp:236-290) runs in-kernel.  Exactly singular circulants (a
 // vanishing 64-point DFT coefficient) are pre-screened and skipped; a
 // system that exhausts its attempts is re-run with the exact protocol (pass 1) so the
 // returned best attempt is the reference's.
 #include <cmath>
 
+#include "panel.cuh"
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -33,11 +31,10 @@ namespace {
 constexpr int N = 64;
 constexpr int THREADS = 128;
 constexpr int XP = N + 4; // shared pitch: 544 B = 32 mod 128 -> conflict-free DMMA fragments
-constexpr int RBH = 36;   // half-row stride inside a pivot-row buffer (16 B aligned)
 
 struct Smem {
     double X[N * XP];      // A / W staging, transposed packed LU, LCG scratch
-    double rb[2][2 * RBH]; // pivot row, double-buffered: [h * RBH + jj] = row[2 jj + h]; 1/p at [RBH - 1]
+    double pm[2];          // running |pivot| min / max of the LU
     double v0[N], v1[N];
     double2 tw[N];         // DFT twiddles (cos, sin)(2 pi m / 64)
     double red[4];
@@ -133,58 +130,106 @@ __device__ __forceinline__ void circ_product(Smem& S, uint64_t mask, int t) {
                 make_double2(acc[i][jb][0], acc[i][jb][1]);
 }
 
-// One pivot step K (static).  Thread owns row r, half h; w[jj] = W(r, 2 jj + h).
-template <int K>
-__device__ __forceinline__ void lu_step(double (&w)[32], Smem& S, int r, int h, int lane, double floor, bool& brk,
-                                        double& pmn, double& pmx) {
-    constexpr int KJ = K >> 1, KH = K & 1;
-    double* rb = S.rb[K & 1];
-    if (r == K) { // publish the pivot row (entries with column >= K suffice)
-        double* dst = rb + h * RBH;
+// Blocked no-pivot LU of the 64 x 64 working matrix in S.X (row-major, genp.cpp:20-33 per
+// column step): four 16-column panels.  (a) warp 0 factors the panel rows c0..63 x 16 in
+// registers (two rows per lane, pivot row by shuffles, 1/p := 0 for p = 0), (b) every column
+// right of the panel solves its 16 U entries against the unit L11 (one thread per column),
+// (c) the trailing square is updated on DMMA (K = 16) by all warps.  Three barriers per panel
+// instead of one per pivot.  Returns breakdown (some |p| < floor); pmin/pmax of |pivots|
+// (in pivot order) for every thread; S.rcp = 1/U_kk.
+__device__ __forceinline__ bool lu_blocked(Smem& S, double floor, int t, double& pmin, double& pmax) {
+    const int lane = t & 31, warp = t >> 5;
+#pragma unroll 1
+    for (int c0 = 0; c0 < N; c0 += 16) {
+        if (warp == 0) {
+            const int r0 = c0 + lane, r1 = c0 + 32 + lane;
+            const bool v0 = r0 < N, v1 = r1 < N;
+            double a0[16], a1[16], invs[16];
 #pragma unroll
-        for (int jj = (KJ & ~1); jj < 32; jj += 2)
-            *reinterpret_cast<double2*>(dst + jj) = make_double2(w[jj], w[jj + 1]);
-        if (h == KH) {
-            const double p = w[KJ];
-            const double rc = (p == 0.0) ? 0.0 : 1.0 / p;
-            rb[RBH - 1] = rc;
-            S.rcp[K] = rc;
+            for (int j = 0; j < 16; ++j) {
+                a0[j] = v0 ? S.X[r0 * XP + c0 + j] : 0.0;
+                a1[j] = v1 ? S.X[r1 * XP + c0 + j] : 0.0;
+            }
+            double mn = S.pm[0], mx = S.pm[1];
+            bool brk = S.flag != 0;
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+                const double piv = __shfl_sync(0xffffffffu, a0[kk], kk);
+                const double inv = (piv == 0.0) ? 0.0 : __drcp_rn(piv);
+                invs[kk] = inv;
+                const double ap = fabs(piv);
+                mn = (c0 + kk == 0) ? ap : min_fold(mn, ap);
+                mx = (c0 + kk == 0) ? ap : max_fold(mx, ap);
+                brk |= ap < floor;
+                const bool b0 = v0 && lane > kk;
+                const double m0 = b0 ? a0[kk] * inv : 0.0;
+                const double m1 = v1 ? a1[kk] * inv : 0.0;
+                a0[kk] = b0 ? m0 : a0[kk];
+                a1[kk] = v1 ? m1 : a1[kk];
+#pragma unroll
+                for (int l = kk + 1; l < 16; ++l) {
+                    const double u = __shfl_sync(0xffffffffu, a0[l], kk);
+                    a0[l] = fma(-m0, u, a0[l]);
+                    a1[l] = fma(-m1, u, a1[l]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                if (v0)
+                    S.X[r0 * XP + c0 + j] = a0[j];
+                if (v1)
+                    S.X[r1 * XP + c0 + j] = a1[j];
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk)
+                    S.rcp[c0 + kk] = invs[kk];
+                S.pm[0] = mn;
+                S.pm[1] = mx;
+                if (brk)
+                    S.flag = 1;
+            }
         }
-    }
-    __syncthreads();
-    const double p = rb[KH * RBH + KJ], rc = rb[RBH - 1];
-    const double ap = fabs(p);
-    pmn = (K == 0) ? ap : min_fold(pmn, ap);
-    pmx = (K == 0) ? ap : max_fold(pmx, ap);
-    brk |= ap < floor;
-    const double m = __shfl_sync(0xffffffffu, w[KJ] * rc, (lane & ~1) | KH);
-    if (r > K) {
-        if (h == KH)
-            w[KJ] = m;
-        if (m != 0.0) {
-            const double* src = rb + h * RBH;
-            if (2 * KJ == K && h == 1) // column K + 1 when K is even
-                w[KJ] = fma(-m, src[KJ], w[KJ]);
+        __syncthreads();
+        const int nc = N - c0 - 16;
+        if (nc == 0)
+            break;
+        if (t < nc) { // U12: column c0 + 16 + t against the unit L11 (broadcast reads)
+            const int c = c0 + 16 + t;
+            double y[16];
 #pragma unroll
-            for (int jj = KJ + 1; jj < 32; ++jj)
-                w[jj] = fma(-m, src[jj], w[jj]);
+            for (int i = 0; i < 16; ++i)
+                y[i] = S.X[(c0 + i) * XP + c];
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+#pragma unroll
+                for (int k = 0; k < i; ++k)
+                    y[i] = fma(-S.X[(c0 + i) * XP + c0 + k], y[k], y[i]);
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+                S.X[(c0 + i) * XP + c] = y[i];
+        }
+        __syncthreads();
+        panel::smem_update16(S.X + (c0 + 16) * XP + c0 + 16, XP, S.X + (c0 + 16) * XP + c0, XP,
+                             S.X + c0 * XP + c0 + 16, XP, nc, nc, warp, THREADS / 32, lane);
+        __syncthreads();
+    }
+    pmin = S.pm[0];
+    pmax = S.pm[1];
+    return S.flag != 0;
+}
+
+// X <- X^T in place (the solves read columns of L and U)
+__device__ __forceinline__ void transpose_X(Smem& S, int t) {
+    for (int e = t; e < N * N; e += THREADS) {
+        const int i = e >> 6, j = e & 63;
+        if (i < j) {
+            const double v = S.X[i * XP + j];
+            S.X[i * XP + j] = S.X[j * XP + i];
+            S.X[j * XP + i] = v;
         }
     }
 }
-
-template <int K0, int K1>
-struct LU {
-    __device__ __forceinline__ static void run(double (&w)[32], Smem& S, int r, int h, int lane, double floor,
-                                               bool& brk, double& pmn, double& pmx) {
-        lu_step<K0>(w, S, r, h, lane, floor, brk, pmn, pmx);
-        LU<K0 + 1, K1>::run(w, S, r, h, lane, floor, brk, pmn, pmx);
-    }
-};
-template <int K1>
-struct LU<K1, K1> {
-    __device__ __forceinline__ static void run(double (&)[32], Smem&, int, int, int, double, bool&, double&,
-                                               double&) {}
-};
 
 // warp 0: S.v0 <- U^{-1} L^{-1} S.v0 with the packed LU transposed in X (X[c * XP + r]).
 __device__ __forceinline__ void solve_warp0(Smem& S, int lane) {
@@ -271,14 +316,13 @@ __device__ bool circ_singular(Smem& S, uint64_t mask, int t) {
 
 // One CTA per system; the raw arm and the whole redraw protocol (8 attempts on stream
 // sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) run in-kernel.
-__global__ void __launch_bounds__(THREADS, 5) k_batched_circ64(
+__global__ void __launch_bounds__(THREADS, 4) k_batched_circ64(
     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs0, uint64_t seed,
     const uint64_t* __restrict__ sids, int refine, double* __restrict__ X, rl_precond_report* __restrict__ rep,
     int* __restrict__ status) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int r = 4 * (lane >> 1) + warp, h = lane & 1; // LU ownership
     const bool vt = t < N;                              // vector-row owner (row t)
     const uint64_t sys = blockIdx.x;
     const double* Ag = A + sys * N * N;
@@ -300,7 +344,6 @@ __global__ void __launch_bounds__(THREADS, 5) k_batched_circ64(
     rl_precond_report rp{};
     rp.attempt = -1;
     int st = RL_PIVOT_BREAKDOWN;
-    double w[32];
     // pass 0: raw arm (a = -1) + pre-screened protocol; pass 1 (rare): exact protocol
     for (int pass = 0; pass < 2; ++pass) {
         bool have_best = false, skipped = false, accepted = false;
@@ -331,17 +374,16 @@ __global__ void __launch_bounds__(THREADS, 5) k_batched_circ64(
                 circ_product(S, mask, t);
                 __syncthreads();
             }
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-                w[jj] = S.X[r * XP + 2 * jj + h];
-            bool brk = false;
+            if (t == 0) {
+                S.flag = 0;
+                S.pm[0] = S.pm[1] = 0.0;
+            }
+            __syncthreads();
             double pmn = 0.0, pmx = 0.0;
-            LU<0, N>::run(w, S, r, h, lane, a < 0 ? 0.0 : 1e-300, brk, pmn, pmx);
-            if (__syncthreads_or(brk) && a >= 0)
+            const bool brk = lu_blocked(S, a < 0 ? 0.0 : 1e-300, t, pmn, pmx);
+            if (brk && a >= 0)
                 continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-                S.X[(2 * jj + h) * XP + r] = w[jj];
+            transpose_X(S, t);
             if (vt)
                 S.v0[t] = bt;
             __syncthreads();
