@@ -46,7 +46,7 @@ constexpr int PK_WARPS = PK_THREADS / 32;
 // |pivots| and the first step with |p| < floor are recorded; 1/p := 0 when p == 0 gives
 // the reference's multiplier 0 (genp.cpp:27).
 __device__ unsigned long long g_diag_ts[64];
-__device__ unsigned long long g_trsm_ts[2][32];
+__device__ unsigned long long g_trsm_ts[2][40];
 __device__ __forceinline__ unsigned long long gtimer0() {
     unsigned long long v;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
@@ -185,16 +185,29 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
 //   CTAs [nrb, 2 nrb2): 64-column tiles of A12 <- L11^-1 A12 (L11 y = a, unit lower)
 // Each sub-panel: per-thread 16-step substitution, then a DMMA update of the remaining
 // columns (right) / rows (left) of the tile.
+// Panel TRSMs of block step o (genp.cpp:77-92), in place, one launch.  Both sides are
+// solved as X <- X T^{-1} with X a 64 x 128 tile and T upper triangular (staged in shared
+// memory):
+//   CTAs [0, nrb):      X = 64 rows of A21, T = U11            (L21 = A21 U11^-1)
+//   CTAs [nrb, 2 nrb):  X = (64 columns of A12)^T, T = L11^T   (U12 = L11^-1 A12, unit T)
+// X lives in DMMA accumulator registers for the whole solve: warp w holds rows 8w..8w+7, lane
+// (g, q) the columns 8f + 2q, +1 of every 8-column fragment f.  Per 16-column sub-panel: the
+// rows' 16-step substitution runs inside each quad (x_j formed by the lane holding column j,
+// shared by one shuffle, x_j = (w_j - sum_l x_l T_lj) * (1/T_jj) in the reference's order),
+// then the rest of the tile gets X[:, right] -= X[:, sub] T[sub, right] on DMMA with the A
+// fragments gathered from the quad by shuffles and T from shared memory — no shared-memory
+// read-modify-write of X.
 constexpr int TR_TILE = 64;     // rows (right) / columns (left) per CTA
-constexpr int TR_THREADS = 256; // 8 warps
-constexpr int TR_WARPS = TR_THREADS / 32;
+constexpr int TR_THREADS = 256; // 8 warps x 8 rows
+constexpr int TP = NB + 4;      // staged T / X pitch (doubles): conflict-free fragment reads
+
 __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_t lda, uint64_t o, uint64_t rest,
                                                               int nrb) {
     extern __shared__ double smt[];
-    double* T = smt;            // NB x PT triangle
-    double* X = smt + NB * PT;  // right: 64 x PT ; left: NB x (64 + 4)
+    double* T = smt;           // NB x TP: upper triangular factor (T[j][c], c >= j)
+    double* Xs = smt + NB * TP; // staging of the X tile (right: 64 x TP; left: NB x (64 + 4), A12 rows)
     __shared__ double rcp[NB];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
     const bool right = static_cast<int>(blockIdx.x) < nrb;
     const double* diag = a + o * lda + o;
     const bool tr = (blockIdx.x == 0 || static_cast<int>(blockIdx.x) == nrb) && tid == 0;
@@ -202,85 +215,118 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
     int tsi = 0;
     if (tr) tsb[tsi] = gtimer0();
     ++tsi;
-    if (right)
-        panel::load_tile_async<NB, NB, TR_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return j >= i; });
-    else
-        panel::load_tile_async<NB, NB, TR_THREADS>(T, PT, diag, lda, NB, NB, [](int i, int j) { return i > j; });
+    uint64_t x0;
+    int nx;
+    double* base;
     if (right) {
-        const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * TR_TILE;
-        const int nr = static_cast<int>(rest - r0 < TR_TILE ? rest - r0 : TR_TILE);
-        double* src = a + (o + NB + r0) * lda + o;
-        panel::load_tile_async<TR_TILE, NB, TR_THREADS>(X, PT, src, lda, nr, NB, [](int, int) { return true; });
-        panel::cp_async_wait_all();
-        __syncthreads();
+        x0 = static_cast<uint64_t>(blockIdx.x) * TR_TILE;
+        nx = static_cast<int>(rest - x0 < TR_TILE ? rest - x0 : TR_TILE);
+        base = a + (o + NB + x0) * lda + o; // rows x0.. of A21, 128 columns
+        panel::load_tile_async<NB, NB, TR_THREADS>(T, TP, diag, lda, NB, NB, [](int i, int j) { return j >= i; });
+        panel::load_tile_async<TR_TILE, NB, TR_THREADS>(Xs, TP, base, lda, nx, NB, [](int, int) { return true; });
+    } else {
+        x0 = static_cast<uint64_t>(blockIdx.x - nrb) * TR_TILE;
+        nx = static_cast<int>(rest - x0 < TR_TILE ? rest - x0 : TR_TILE);
+        base = a + o * lda + o + NB + x0; // 128 rows of A12, columns x0..
+        panel::load_tile_async<NB, TR_TILE, TR_THREADS>(Xs, TR_TILE + 4, base, lda, NB, nx,
+                                                        [](int, int) { return true; });
+        // T = L11^T (strictly upper): coalesced reads along L11's rows, transposed stores
+        for (int e = tid; e < NB * NB; e += TR_THREADS) {
+            const int c = e >> 7, j = e & (NB - 1); // L11[c][j] -> T[j][c]
+            T[j * TP + c] = (c > j) ? __ldg(diag + static_cast<uint64_t>(c) * lda + j) : 0.0;
+        }
+    }
+    panel::cp_async_wait_all();
+    __syncthreads();
+    if (tr) tsb[tsi] = gtimer0();
+    ++tsi;
+    if (right && tid < NB) {
+        const double d = T[tid * TP + tid];
+        rcp[tid] = (d == 0.0) ? 0.0 : 1.0 / d;
+    }
+    // X rows 8 warp + g: x[f][e] = X[row][8 f + 2 q + e]
+    const int row = 8 * warp + g;
+    double x[NB / 8][2];
+#pragma unroll
+    for (int f = 0; f < NB / 8; ++f)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 8 * f + 2 * q + e;
+            x[f][e] = right ? Xs[row * TP + c] : Xs[c * (TR_TILE + 4) + row];
+        }
+    __syncthreads();
+    if (tr) tsb[tsi] = gtimer0();
+    ++tsi;
+#pragma unroll
+    for (int c0 = 0; c0 < NB; c0 += 16) {
+        const int f0 = c0 / 8;
+        // (1) substitution over columns c0..c0+15 inside the quad: this lane holds columns
+        //     c0 + 8 h + 2 q + e (h, e in {0, 1}) of the sub-panel
+        double rc16[16], tv[16][4];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) { // everything off the chain is loaded up front
+            rc16[jj] = right ? rcp[c0 + jj] : 1.0;
+#pragma unroll
+            for (int hs = 0; hs < 4; ++hs)
+                tv[jj][hs] = T[(c0 + jj) * TP + c0 + 8 * (hs >> 1) + 2 * q + (hs & 1)];
+        }
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            const int j = c0 + jj, fj = j >> 3, qj = (j & 7) >> 1, ej = j & 1;
+            const double xj = __shfl_sync(0xffffffffu, x[fj][ej] * rc16[jj], (lane & ~3) | qj);
+#pragma unroll
+            for (int hs = 0; hs < 4; ++hs) {
+                const int h = hs >> 1, e = hs & 1;
+                const int c = c0 + 8 * h + 2 * q + e;
+                double& v = x[f0 + h][e];
+                const double upd = fma(-xj, tv[jj][hs], v);
+                v = (c == j) ? xj : ((c > j) ? upd : v);
+            }
+        }
         if (tr) tsb[tsi] = gtimer0();
         ++tsi;
-        for (int j = tid; j < NB; j += TR_THREADS) {
-            const double d = T[j * PT + j];
-            rcp[j] = (d == 0.0) ? 0.0 : 1.0 / d;
-        }
-        __syncthreads();
-        for (int c0 = 0; c0 < NB; c0 += SB) {
-            for (int r = tid; r < TR_TILE; r += TR_THREADS) {
-                double x[SB];
+        if (c0 + 16 < NB) {
+            // (2) X[:, c0+16:] -= X[:, c0:c0+16] T[c0:c0+16, c0+16:]  (DMMA, K = 16)
+            double af[4];
 #pragma unroll
-                for (int l = 0; l < SB; ++l)
-                    x[l] = X[r * PT + c0 + l];
-#pragma unroll
-                for (int j = 0; j < SB; ++j) {
-                    const double xj = x[j] * rcp[c0 + j];
-                    x[j] = xj;
-                    if (xj != 0.0)
-#pragma unroll
-                        for (int l = j + 1; l < SB; ++l)
-                            x[l] = fma(-xj, T[(c0 + j) * PT + c0 + l], x[l]);
-                }
-#pragma unroll
-                for (int l = 0; l < SB; ++l)
-                    X[r * PT + c0 + l] = x[l];
+            for (int ks = 0; ks < 4; ++ks) { // A fragment: row g, column c0 + 4 ks + q
+                const int c = 4 * ks + q;     // column within the sub-panel (0..15)
+                const int src = (lane & ~3) | ((c & 7) >> 1);
+                const double v0 = __shfl_sync(0xffffffffu, x[f0 + (c >> 3)][0], src);
+                const double v1 = __shfl_sync(0xffffffffu, x[f0 + (c >> 3)][1], src);
+                af[ks] = (c & 1) ? v1 : v0;
             }
-            __syncthreads();
-            if (tr) tsb[tsi] = gtimer0();
-            ++tsi;
-            if (c0 + SB < NB)
-                panel::smem_update16(X + c0 + SB, PT, X + c0, PT, T + c0 * PT + c0 + SB, PT, TR_TILE,
-                                     NB - c0 - SB, warp, TR_WARPS, lane);
-            __syncthreads();
-            if (tr) tsb[tsi] = gtimer0();
-            ++tsi;
-        }
-        panel::store_tile<TR_TILE, NB, TR_THREADS>(src, lda, X, PT, nr, NB);
-        if (tr) { tsb[tsi] = gtimer0(); tsb[31] = tsi + 1; }
-    } else {
-        constexpr int XP = TR_TILE + 4;
-        const uint64_t c0g = static_cast<uint64_t>(blockIdx.x - nrb) * TR_TILE;
-        const int nc = static_cast<int>(rest - c0g < TR_TILE ? rest - c0g : TR_TILE);
-        double* src = a + o * lda + o + NB + c0g;
-        panel::load_tile_async<NB, TR_TILE, TR_THREADS>(X, XP, src, lda, NB, nc, [](int, int) { return true; });
-        panel::cp_async_wait_all();
-        __syncthreads();
-        for (int c0 = 0; c0 < NB; c0 += SB) {
-            for (int c = tid; c < TR_TILE; c += TR_THREADS) {
-                double y[SB];
 #pragma unroll
-                for (int i = 0; i < SB; ++i)
-                    y[i] = X[(c0 + i) * XP + c];
+            for (int f = f0 + 2; f < NB / 8; ++f) {
+                double acc[2] = {0.0, 0.0};
 #pragma unroll
-                for (int i = 1; i < SB; ++i)
-#pragma unroll
-                    for (int l = 0; l < i; ++l)
-                        y[i] = fma(-T[(c0 + i) * PT + c0 + l], y[l], y[i]);
-#pragma unroll
-                for (int i = 1; i < SB; ++i)
-                    X[(c0 + i) * XP + c] = y[i];
+                for (int ks = 0; ks < 4; ++ks)
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                 : "+d"(acc[0]), "+d"(acc[1])
+                                 : "d"(af[ks]), "d"(T[(c0 + 4 * ks + q) * TP + 8 * f + g]));
+                x[f][0] -= acc[0];
+                x[f][1] -= acc[1];
             }
-            __syncthreads();
-            if (c0 + SB < NB)
-                panel::smem_update16(X + (c0 + SB) * XP, XP, T + (c0 + SB) * PT + c0, PT, X + c0 * XP, XP,
-                                     NB - c0 - SB, TR_TILE, warp, TR_WARPS, lane);
-            __syncthreads();
         }
-        panel::store_tile<NB, TR_TILE, TR_THREADS>(src, lda, X, XP, NB, nc);
+    }
+    if (tr) tsb[tsi] = gtimer0();
+    ++tsi;
+    // store
+    if (row < nx) {
+        if (right) {
+#pragma unroll
+            for (int f = 0; f < NB / 8; ++f) {
+                double* d = base + static_cast<uint64_t>(row) * lda + 8 * f + 2 * q;
+                d[0] = x[f][0];
+                d[1] = x[f][1];
+            }
+        } else {
+#pragma unroll
+            for (int f = 0; f < NB / 8; ++f)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    base[static_cast<uint64_t>(8 * f + 2 * q + e) * lda + row] = x[f][e];
+        }
     }
 }
 
@@ -548,7 +594,8 @@ __global__ void __launch_bounds__(WV_THREADS, 1) k_trsv_wave(const double* __res
 // CTA is co-scheduled on their SM and steals issue slots.
 constexpr size_t kPanelSmem = 220 * 1024;
 size_t trsm_smem() {
-    const size_t need = (static_cast<size_t>(NB) * PT + static_cast<size_t>(NB) * (TR_TILE + 4)) * sizeof(double);
+    // T (NB x TP) + staging of the X tile (right 64 x TP, left NB x (64 + 4))
+    const size_t need = (static_cast<size_t>(NB) * TP + static_cast<size_t>(NB) * (TR_TILE + 4)) * sizeof(double);
     return need > kPanelSmem ? need : kPanelSmem;
 }
 size_t diag_smem() { return kPanelSmem; }
@@ -621,16 +668,19 @@ void diag_trace_dump() {
     RL_CUDA(cudaDeviceSynchronize());
     RL_CUDA(cudaMemcpyFromSymbol(h, g_diag_ts, sizeof(h)));
     const int cnt = static_cast<int>(h[63]);
+    unsigned long long t[2][40];
+    RL_CUDA(cudaMemcpyFromSymbol(t, g_trsm_ts, sizeof(t)));
+    for (int side = 0; side < 2; ++side) {
+        std::fprintf(stderr, "trsm %s phases:", side ? "left" : "right");
+        for (int i = 1; i < 20; ++i)
+            std::fprintf(stderr, " %.2f", (t[side][i] - t[side][0]) * 1e-3);
+        std::fprintf(stderr, "\n");
+    }
     std::fprintf(stderr, "diag phases (us from start):");
     for (int i = 1; i < cnt && i < 63; ++i)
         std::fprintf(stderr, " %.2f", (h[i] - h[0]) * 1e-3);
     std::fprintf(stderr, "\n");
-    unsigned long long t[2][32];
-    RL_CUDA(cudaMemcpyFromSymbol(t, g_trsm_ts, sizeof(t)));
-    std::fprintf(stderr, "trsm(right) phases (us from start):");
-    for (int i = 1; i < static_cast<int>(t[0][31]) && i < 31; ++i)
-        std::fprintf(stderr, " %.2f", (t[0][i] - t[0][0]) * 1e-3);
-    std::fprintf(stderr, "\n");
+
 }
 
 // Blocked right-looking GENP in place (packed LU), outer block W = 256 built from two 128
