@@ -228,24 +228,12 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const doub
         return launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 1)
         return launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (force == 2)
-        return launch<128, 128, 2, 4, AK, BKM, VEC, 3>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 3)
         return launch<64, 64, 2, 2, AK, BKM, VEC, 4, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (force == 8)
-        return launch<64, 128, 2, 4, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (force == 9)
-        return launch<128, 64, 2, 4, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (force == 10)
-        return launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 24>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 6)
         return launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (force == 7)
-        return launch<128, 64, 4, 2, AK, BKM, VEC, 3, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (force == 4)
         return launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (force == 5)
-        return launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms && K >= kLongK)
         // two CTAs per SM (128x64 tiles, <= 128 regs): one CTA's prologue / C epilogue
         // overlaps the other's DMMA loop.  Long K: K-tile 32 in 2 stages (217 KB for the two

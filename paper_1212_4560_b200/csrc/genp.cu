@@ -45,6 +45,30 @@ constexpr int PK_WARPS = PK_THREADS / 32;
 //   right of it solves its 16 U entries against that unit L; (4) DMMA trailing update.
 // |pivots| and the first step with |p| < floor are recorded; 1/p := 0 when p == 0 gives
 // the reference's multiplier 0 (genp.cpp:27).
+// Panel-kernel phase timestamps (dev aid): build with -DRL_PANEL_TRACE and run with
+// RL_DIAG_TRACE=1 to print the last diagonal-LU / TRSM launch's phase times.
+#ifdef RL_PANEL_TRACE
+#define RL_TS_DIAG()                                                                     \
+    do {                                                                                 \
+        if (tid == 0)                                                                    \
+            g_diag_ts[tsi] = gtimer0();                                                  \
+        ++tsi;                                                                           \
+    } while (0)
+#define RL_TS_TRSM()                                                                     \
+    do {                                                                                 \
+        if (tr)                                                                          \
+            tsb[tsi] = gtimer0();                                                        \
+        ++tsi;                                                                           \
+    } while (0)
+#else
+#define RL_TS_DIAG() \
+    do {             \
+    } while (0)
+#define RL_TS_TRSM() \
+    do {             \
+    } while (0)
+#endif
+#ifdef RL_PANEL_TRACE
 __device__ unsigned long long g_diag_ts[64];
 __device__ unsigned long long g_trsm_ts[2][40];
 __device__ __forceinline__ unsigned long long gtimer0() {
@@ -52,6 +76,7 @@ __device__ __forceinline__ unsigned long long gtimer0() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
     return v;
 }
+#endif
 __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t lda, uint64_t n, uint64_t o,
                                                            double floor, double* pivots,
                                                            unsigned long long* breakdown) {
@@ -60,17 +85,17 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
     double* blk = a + o * lda + o;
+#ifdef RL_PANEL_TRACE
     int tsi = 0;
-    if (tid == 0) g_diag_ts[tsi] = gtimer0();
-    ++tsi;
+#endif
+    RL_TS_DIAG();
     panel::load_tile_async<NB, NB, PK_THREADS>(W, PT, blk, lda, bs, bs, [](int, int) { return true; });
     panel::cp_async_wait_all();
     __syncthreads();
     for (int i = bs + tid; i < NB; i += PK_THREADS) // identity beyond a ragged last block
         W[i * PT + i] = 1.0;
     __syncthreads();
-    if (tid == 0) g_diag_ts[tsi] = gtimer0();
-    ++tsi;
+    RL_TS_DIAG();
     // (1) 16x16 diagonal sub-block c0 by warp 0, lanes 0..15 own its rows, all in registers:
     //     per step the pivot row is read from the owner lane by shuffles, every lane forms
     //     1/p itself (correctly rounded reciprocal).
@@ -109,8 +134,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
     if (warp == 0)
         phase1(0);
     __syncthreads();
-    if (tid == 0) g_diag_ts[tsi] = gtimer0();
-    ++tsi;
+    RL_TS_DIAG();
     for (int c0 = 0; c0 < NB; c0 += SB) {
         const int rest = NB - c0 - SB;
         if (rest == 0)
@@ -152,8 +176,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
                 W[(c0 + i) * PT + c] = y[i];
         }
         __syncthreads();
-        if (tid == 0) g_diag_ts[tsi] = gtimer0();
-        ++tsi;
+        RL_TS_DIAG();
         // (4) trailing update W22 -= L21 U12 with lookahead: warp 0 updates the next 16 x 16
         //     diagonal block and factors it (phase 1 of c0 + 16) while warps 1..7 update the rest
         double* C22 = W + (c0 + SB) * PT + c0 + SB;
@@ -167,12 +190,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
             panel::smem_update16(C22, PT, L21, PT, U12, PT, rest, rest, warp - 1, PK_WARPS - 1, lane, true);
         }
         __syncthreads();
-        if (tid == 0) g_diag_ts[tsi] = gtimer0();
-        ++tsi;
+        RL_TS_DIAG();
     }
     panel::store_tile<NB, NB, PK_THREADS>(blk, lda, W, PT, bs, bs);
-    if (tid == 0) g_diag_ts[tsi] = gtimer0();
-    if (tid == 0) g_diag_ts[63] = tsi + 1;
+    RL_TS_DIAG();
+#ifdef RL_PANEL_TRACE
+    if (tid == 0)
+        g_diag_ts[63] = tsi;
+#endif
     if (tid < bs) { // |pivots| and the first step below the floor (genp.cpp:24-26)
         pivots[o + tid] = pabs[tid];
         if (pabs[tid] < floor)
@@ -210,11 +235,12 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
     const bool right = static_cast<int>(blockIdx.x) < nrb;
     const double* diag = a + o * lda + o;
+#ifdef RL_PANEL_TRACE
     const bool tr = (blockIdx.x == 0 || static_cast<int>(blockIdx.x) == nrb) && tid == 0;
     unsigned long long* tsb = g_trsm_ts[right ? 0 : 1];
     int tsi = 0;
-    if (tr) tsb[tsi] = gtimer0();
-    ++tsi;
+#endif
+    RL_TS_TRSM();
     uint64_t x0;
     int nx;
     double* base;
@@ -238,8 +264,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
     }
     panel::cp_async_wait_all();
     __syncthreads();
-    if (tr) tsb[tsi] = gtimer0();
-    ++tsi;
+    RL_TS_TRSM();
     if (right && tid < NB) {
         const double d = T[tid * TP + tid];
         rcp[tid] = (d == 0.0) ? 0.0 : 1.0 / d;
@@ -255,8 +280,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
             x[f][e] = right ? Xs[row * TP + c] : Xs[c * (TR_TILE + 4) + row];
         }
     __syncthreads();
-    if (tr) tsb[tsi] = gtimer0();
-    ++tsi;
+    RL_TS_TRSM();
 #pragma unroll
     for (int c0 = 0; c0 < NB; c0 += 16) {
         const int f0 = c0 / 8;
@@ -283,8 +307,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
                 v = (c == j) ? xj : ((c > j) ? upd : v);
             }
         }
-        if (tr) tsb[tsi] = gtimer0();
-        ++tsi;
+        RL_TS_TRSM();
         if (c0 + 16 < NB) {
             // (2) X[:, c0+16:] -= X[:, c0:c0+16] T[c0:c0+16, c0+16:]  (DMMA, K = 16)
             double af[4];
@@ -309,8 +332,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
             }
         }
     }
-    if (tr) tsb[tsi] = gtimer0();
-    ++tsi;
+    RL_TS_TRSM();
     // store
     if (row < nx) {
         if (right) {
@@ -664,6 +686,9 @@ void transpose_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, double
 }
 
 void diag_trace_dump() {
+#ifndef RL_PANEL_TRACE
+    std::fprintf(stderr, "RL_DIAG_TRACE: build with -DRL_PANEL_TRACE for panel phase times\n");
+#else
     unsigned long long h[64];
     RL_CUDA(cudaDeviceSynchronize());
     RL_CUDA(cudaMemcpyFromSymbol(h, g_diag_ts, sizeof(h)));
@@ -681,6 +706,7 @@ void diag_trace_dump() {
         std::fprintf(stderr, " %.2f", (h[i] - h[0]) * 1e-3);
     std::fprintf(stderr, "\n");
 
+#endif
 }
 
 // Blocked right-looking GENP in place (packed LU), outer block W = 256 built from two 128

@@ -8,7 +8,7 @@ import torch  # noqa: E402
 
 import paper_1212_4560_b200 as rl  # noqa: E402
 
-shapes = [(7936, 128, 128), (128, 7936, 128), (7936, 256, 256), (256, 7680, 256), (2048, 256, 256),
+shapes = [(7168, 7168, 512), (5120, 5120, 512), (3072, 3072, 512), (2048, 2048, 512), (7936, 128, 128), (128, 7936, 128), (7936, 256, 256), (256, 7680, 256), (2048, 256, 256),
           (256, 2048, 256), (1024, 1024, 256), (2048, 2048, 256), (4096, 4096, 256), (7680, 7680, 256),
           (512, 512, 256), (768, 768, 256), (128, 128, 256), (128, 128, 128), (128, 1024, 256), (1024, 256, 256),
           (896, 128, 128), (128, 896, 128)]
