@@ -307,15 +307,43 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
     std::vector<char> col_accepted(nrhs, 0), col_have(nrhs, 0);
     std::vector<double> col_best(nrhs, 0.0), col_pmin(nrhs, 0.0), col_pmax(nrhs, 0.0);
     std::vector<int> col_attempt(nrhs, -1);
+    // Speculative next multiplier: for a dense right-only multiplier, attempt a+1's G is
+    // generated on a side stream while attempt a solves (the wavefront solve leaves most SMs
+    // idle); it is used if attempt a+1 happens, else discarded.  Attempts alternate between
+    // two multiplier slots so the speculation never overwrites the live one.
+    const bool speculate = use_right && !use_left && (tag == RL_GAUSSIAN || tag == RL_UNIFORM_PM1);
+    struct Spec {
+        cudaStream_t s = nullptr;
+        cudaEvent_t start = nullptr, done = nullptr;
+        int device = -1;
+    };
+    static thread_local Spec sp;
+    if (speculate && sp.device != ctx().device) {
+        RL_CUDA(cudaStreamCreateWithFlags(&sp.s, cudaStreamNonBlocking));
+        RL_CUDA(cudaEventCreateWithFlags(&sp.start, cudaEventDisableTiming));
+        RL_CUDA(cudaEventCreateWithFlags(&sp.done, cudaEventDisableTiming));
+        sp.device = ctx().device;
+    }
+    int spec_attempt = -1; // attempt whose right multiplier the side stream has generated
+    const int mult_slot[2] = {WS_MULT, WS_MULT2};
     for (int attempt = 0; attempt < 8; ++attempt) {
         const uint64_t ds = sid + 7919ULL * static_cast<uint64_t>(attempt);
         rep.attempts_drawn = attempt + 1;
         Mult left, right;
         if (use_left)
             draw(left, tag, mu, sigma, n, seed, ds, WS_MULT, WS_LVEC, true);
-        if (use_right)
-            draw(right, tag, mu, sigma, n, seed, ds ^ 0x5000000000000000ULL, use_left ? WS_RF1 : WS_MULT,
-                 WS_RF2, true);
+        if (use_right) {
+            if (spec_attempt == attempt) {
+                right.tag = tag;
+                right.n = n;
+                right.dense = ws<double>(mult_slot[attempt & 1], n * n);
+                RL_CUDA(cudaStreamWaitEvent(st, sp.done, 0));
+                spec_attempt = -1;
+            } else {
+                draw(right, tag, mu, sigma, n, seed, ds ^ 0x5000000000000000ULL,
+                     use_left ? WS_RF1 : (speculate ? mult_slot[attempt & 1] : WS_MULT), WS_RF2, true);
+            }
+        }
         const double* src = A;
         if (use_left) {
             apply_left(left, src, n, tmp);
@@ -346,6 +374,18 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
                 set_error("genp_factor: pivot below floor at step " + std::to_string(hb));
             }
             continue;
+        }
+        if (speculate && attempt + 1 < 8) { // next attempt's G beside this attempt's solves
+            const uint64_t dn = (sid + 7919ULL * static_cast<uint64_t>(attempt + 1)) ^ 0x5000000000000000ULL;
+            double* next = ws<double>(mult_slot[(attempt + 1) & 1], n * n);
+            RL_CUDA(cudaEventRecord(sp.start, st));
+            RL_CUDA(cudaStreamWaitEvent(sp.s, sp.start, 0));
+            ctx().stream = sp.s;
+            rng_generate(seed, dn, tag == RL_GAUSSIAN ? Draw::Gaussian : Draw::UniformPm1, n * n,
+                         tag == RL_GAUSSIAN ? mu : 0.0, tag == RL_GAUSSIAN ? sigma : 1.0, next);
+            ctx().stream = st;
+            RL_CUDA(cudaEventRecord(sp.done, sp.s));
+            spec_attempt = attempt + 1;
         }
         genp_solve_blocked(n, nrhs, sys, n, aux, Z, nrhs);
         if (use_right)
@@ -396,6 +436,8 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
         if (all_done)
             break;
     }
+    if (spec_attempt >= 0) // an unused speculative draw still owns its slot and the RNG workspace
+        RL_CUDA(cudaStreamWaitEvent(st, sp.done, 0));
     if (have_best) {
         // report: worst column; its attempt and pivots (nrhs = 1: exactly the reference's report)
         uint64_t w = 0;
