@@ -654,45 +654,115 @@ void rng_sign_vectors_batched(uint64_t seed, const uint64_t* d_sids, uint64_t ad
 
 // ------------------------------------------------------ sparse +-1 (NEW) --
 namespace {
-// Serial consumption of a raw pool: per column nnz distinct rows by
-// uniform_int(0, n-1) (random_gen.cpp:59-70 rejection) then nnz signs.
-__global__ void k_sparse_consume(const uint64_t* pool, uint64_t pool_len, uint64_t n, int nnz,
-                                 int32_t* rows, double* signs, int* status) {
-    if (threadIdx.x != 0 || blockIdx.x != 0)
-        return;
-    const uint64_t span = n;
-    const uint64_t limit = (~0ULL) / span * span;
-    uint64_t k = 0;
-    for (uint64_t j = 0; j < n; ++j) {
-        int32_t* rj = rows + j * nnz;
-        for (int t = 0; t < nnz; ++t) {
-            for (;;) {
-                if (k >= pool_len) {
-                    *status = 1;
-                    return;
-                }
-                uint64_t v = pool[k++];
-                if (v >= limit)
-                    continue;
-                int32_t r = static_cast<int32_t>(v % span);
-                bool dup = false;
-                for (int s = 0; s < t; ++s)
-                    dup |= (rj[s] == r);
-                if (!dup) {
-                    rj[t] = r;
-                    break;
-                }
-            }
-        }
-        for (int t = 0; t < nnz; ++t) {
+// Consumption of a raw pool (random_gen.cpp:59-70 uniform_int rejection, then signs): per
+// column nnz distinct rows by uniform_int(0, n-1) then nnz signs, columns in order on ONE
+// stream.  A column normally takes 2 nnz draws; a rejected or duplicate row costs one more,
+// which shifts every later column.  One CTA resolves the offsets by fixed-point iteration:
+// every column is consumed in parallel from its current offset guess, the guesses are
+// replaced by the exclusive prefix sum of the draw counts, and this repeats until no count
+// changes (the first column whose count changed is exact after each round, and extra draws
+// are rare: a few rounds).  The result equals the serial consumption bit for bit.
+constexpr int kSpThreads = 1024;
+__device__ __forceinline__ int sparse_column(const uint64_t* pool, uint64_t pool_len, uint64_t s, uint64_t span,
+                                             uint64_t limit, int nnz, int32_t* rj, double* sj, bool write,
+                                             bool& exhausted) {
+    uint64_t k = s;
+    int32_t rows[8];
+    for (int t = 0; t < nnz; ++t) {
+        for (;;) {
             if (k >= pool_len) {
-                *status = 1;
-                return;
+                exhausted = true;
+                return static_cast<int>(k - s);
             }
-            signs[j * nnz + t] = (pool[k++] & 1ULL) ? 1.0 : -1.0;
+            const uint64_t v = pool[k++];
+            if (v >= limit)
+                continue;
+            const int32_t r = static_cast<int32_t>(v % span);
+            bool dup = false;
+            for (int u = 0; u < t; ++u)
+                dup |= (rows[u] == r);
+            if (!dup) {
+                rows[t] = r;
+                break;
+            }
         }
     }
-    *status = 0;
+    for (int t = 0; t < nnz; ++t) {
+        if (k >= pool_len) {
+            exhausted = true;
+            return static_cast<int>(k - s);
+        }
+        const double sg = (pool[k++] & 1ULL) ? 1.0 : -1.0;
+        if (write) {
+            rj[t] = rows[t];
+            sj[t] = sg;
+        }
+    }
+    return static_cast<int>(k - s);
+}
+
+__global__ void __launch_bounds__(kSpThreads) k_sparse_consume(const uint64_t* pool, uint64_t pool_len, uint64_t n,
+                                                               int nnz, int32_t* rows, double* signs,
+                                                               uint64_t* offs, int* status) {
+    __shared__ unsigned long long part[kSpThreads];
+    __shared__ int changed, exhausted_any;
+    const int tid = threadIdx.x;
+    const uint64_t span = n, limit = (~0ULL) / span * span;
+    const uint64_t per = (n + kSpThreads - 1) / kSpThreads; // columns per thread (contiguous)
+    const uint64_t j0 = tid * per, j1 = j0 + per < n ? j0 + per : n;
+    for (uint64_t j = j0; j < j1; ++j)
+        offs[j] = static_cast<uint64_t>(2 * nnz) * j;
+    __syncthreads();
+    for (int round = 0; round < 64; ++round) {
+        if (tid == 0) {
+            changed = 0;
+            exhausted_any = 0;
+        }
+        __syncthreads();
+        // draw counts from the current offsets, prefix sums within the thread's columns
+        unsigned long long local = 0;
+        bool ex = false;
+        for (uint64_t j = j0; j < j1; ++j)
+            local += sparse_column(pool, pool_len, offs[j], span, limit, nnz, nullptr, nullptr, false, ex);
+        part[tid] = local;
+        if (ex)
+            exhausted_any = 1;
+        __syncthreads();
+        // exclusive scan of the per-thread totals (Hillis-Steele over 1024 entries)
+        for (int d = 1; d < kSpThreads; d <<= 1) {
+            const unsigned long long v = tid >= d ? part[tid - d] : 0ULL;
+            __syncthreads();
+            part[tid] += v;
+            __syncthreads();
+        }
+        uint64_t s = tid ? part[tid - 1] : 0ULL;
+        for (uint64_t j = j0; j < j1; ++j) {
+            if (offs[j] != s) {
+                offs[j] = s;
+                changed = 1;
+            }
+            bool ex2 = false;
+            s += sparse_column(pool, pool_len, s, span, limit, nnz, nullptr, nullptr, false, ex2);
+        }
+        __syncthreads();
+        if (!changed)
+            break;
+        __syncthreads();
+    }
+    bool ex = false;
+    if (!changed) {
+        for (uint64_t j = j0; j < j1; ++j)
+            sparse_column(pool, pool_len, offs[j], span, limit, nnz, rows + j * nnz, signs + j * nnz, true, ex);
+    } else if (tid == 0) { // no fixed point within the round cap: the serial consumption
+        uint64_t k = 0;
+        for (uint64_t j = 0; j < n && !ex; ++j)
+            k += sparse_column(pool, pool_len, k, span, limit, nnz, rows + j * nnz, signs + j * nnz, true, ex);
+    }
+    if (ex)
+        exhausted_any = 1;
+    __syncthreads();
+    if (tid == 0)
+        *status = exhausted_any ? 1 : 0;
 }
 } // namespace
 
@@ -702,10 +772,11 @@ void rng_sparse_sign(uint64_t seed, uint64_t sid, uint64_t n, int nnz, int32_t* 
     uint64_t slack = 1024 + n / 8;
     for (int tries = 0; tries < 4; ++tries, slack *= 8) {
         uint64_t len = 2ULL * nnz * n + slack;
-        uint64_t* pool = ws<uint64_t>(WS_TMP2, len + 1);
-        int* d_status = reinterpret_cast<int*>(pool + len);
+        uint64_t* pool = ws<uint64_t>(WS_TMP2, len + n + 1);
+        uint64_t* offs = pool + len;
+        int* d_status = reinterpret_cast<int*>(offs + n);
         rng_generate(seed, sid, Draw::RawU64, len, 0.0, 1.0, pool);
-        k_sparse_consume<<<1, 32, 0, stream()>>>(pool, len, n, nnz, d_rows, d_signs, d_status);
+        k_sparse_consume<<<1, kSpThreads, 0, stream()>>>(pool, len, n, nnz, d_rows, d_signs, offs, d_status);
         RL_LAUNCHED();
         int h = 0;
         RL_CUDA(cudaMemcpyAsync(&h, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream()));
