@@ -662,7 +662,7 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
     double* dh = ws<double>(WS_RF1, n * rho);
     rng_generate(seed, sid, Draw::Gaussian, n * rho, 0.0, 1.0, dh);
     double* dy = ws<double>(WS_RF2, m * rho);
-    gemm(false, false, m, rho, n, 1.0, d_a, n, dh, rho, 0.0, dy, rho);
+    gemm_splitk(false, false, m, rho, n, 1.0, d_a, n, dh, rho, 0.0, dy, rho, splits_for(m, rho, n));
     // [Q, R] = qr_positive(Y)
     double* dr = ws<double>(WS_RF3, rho * rho);
     if (!cholqr3(m, static_cast<int>(rho), dy, d_q, dr))

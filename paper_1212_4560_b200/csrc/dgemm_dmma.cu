@@ -24,6 +24,12 @@ constexpr int BK = 16;
 constexpr int PAD = 4; // doubles; row pitch = 32 B mod 128
 constexpr uint64_t kLongK = 512; // K from which the 32-deep k-tile config is used
 
+struct Split {
+    int splits = 1;       // gridDim.z
+    uint64_t kchunk = 0;  // K per slice (multiple of 16)
+    uint64_t cstride = 0; // elements between the slices' C panels
+};
+
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d[0]), "+d"(d[1])
@@ -109,9 +115,17 @@ template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE
 __global__ void __launch_bounds__(WM* WN * 32, MINB)
     k_dgemm(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* __restrict__ A,
             uint64_t lda, const double* __restrict__ B, uint64_t ldb, double beta,
-            double* __restrict__ C, uint64_t ldc) {
+            double* __restrict__ C, uint64_t ldc, uint64_t kchunk, uint64_t cstride) {
     using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, BKT>;
     extern __shared__ __align__(16) double smem[];
+    if (gridDim.z > 1) {
+        // split-K: slice z covers k in [z kchunk, (z+1) kchunk) and writes its own C panel
+        const uint64_t kz0 = blockIdx.z * kchunk;
+        A += AK ? kz0 : kz0 * lda;
+        B += BKM ? kz0 : kz0 * ldb;
+        K = kz0 < K ? (K - kz0 < kchunk ? K - kz0 : kchunk) : 0;
+        C += blockIdx.z * cstride;
+    }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int g = lane >> 2, t = lane & 3;
@@ -203,7 +217,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
 
 template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1, int BKT = BK>
 void launch(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda,
-            const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
+            const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, const Split& sp) {
     using G = Cfg<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, BKT>;
     auto kern = k_dgemm<BM, BN, WM, WN, AK, BKM, VEC, NSTAGE, MINB, BKT>;
     static bool configured[16] = {};
@@ -213,44 +227,87 @@ void launch(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, u
                                      static_cast<int>(G::kSmem)));
         configured[dev] = true;
     }
-    dim3 grid(cdiv(N, BN), cdiv(M, BM));
-    kern<<<grid, G::NT, G::kSmem, stream()>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    dim3 grid(cdiv(N, BN), cdiv(M, BM), sp.splits);
+    kern<<<grid, G::NT, G::kSmem, stream()>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sp.kchunk,
+                                              sp.cstride);
     RL_LAUNCHED();
 }
 
 template <bool AK, bool BKM, int VEC>
-void dispatch_shape(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda,
-                    const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
+void dispatch_shape(uint64_t M, uint64_t N, uint64_t Kfull, double alpha, const double* A, uint64_t lda,
+                    const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, const Split& sp) {
     const int sms = ctx().sms;
+    // shape decisions see one split-K slice: K per CTA and CTAs over all slices
+    const uint64_t K = sp.splits > 1 ? sp.kchunk : Kfull;
+    const uint64_t z = static_cast<uint64_t>(sp.splits);
     uint64_t big_tiles = static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 128);
     static const int force = getenv("RL_GEMM_FORCE") ? atoi(getenv("RL_GEMM_FORCE")) : -1; // dev sweeps
     if (force == 0)
-        return launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+        return launch<128, 128, 2, 4, AK, BKM, VEC, 4>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     if (force == 1)
-        return launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+        return launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     if (force == 3)
-        return launch<64, 64, 2, 2, AK, BKM, VEC, 4, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+        return launch<64, 64, 2, 2, AK, BKM, VEC, 4, 4>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     if (force == 6)
-        return launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+        return launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     if (force == 4)
-        return launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms && K >= kLongK)
+        return launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    // rho+ = 64 + 8 (the range finder's sketch width): 72-wide tiles instead of a 64-wide
+    // tile plus a mostly empty second one (Y = A H, Q = Y R^-1: N = 72; Q^T A: M = 72; the
+    // Gram Y^T Y: both)
+    if (M > 64 && M <= 72 && N > 64 && N <= 72)
+        return launch<72, 72, 3, 3, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    if (N > 64 && N <= 72)
+        return launch<128, 72, 4, 3, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    if (M > 64 && M <= 72)
+        return launch<72, 128, 3, 4, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    if (N > 64 && z * cdiv(M, 128) * cdiv(N, 64) >= 2ULL * sms && K >= kLongK)
         // two CTAs per SM (128x64 tiles, <= 128 regs): one CTA's prologue / C epilogue
         // overlaps the other's DMMA loop.  Long K: K-tile 32 in 2 stages (217 KB for the two
         // CTAs), half the k-tile barriers of a 16 x 3 ring: A*G 8192^3 33.41 -> 32.76 ms
         // (DMMA pipe 89.5 -> 91.3% active)
-        launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (N > 64 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= 2ULL * sms)
+        launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    else if (N > 64 && z * cdiv(M, 128) * cdiv(N, 64) >= 2ULL * sms)
         // short K (the LU's trailing updates): K-tile 16 in 3 stages keeps the pipeline full
         // over few k-tiles (7680^2 x 256: 1044 vs 1100 us with the 32 x 2 ring)
-        launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (N > 32 && static_cast<uint64_t>(cdiv(M, 128)) * cdiv(N, 64) >= static_cast<uint64_t>(sms))
-        launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+        launch<128, 64, 4, 2, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    else if (N > 32 && z * cdiv(M, 128) * cdiv(N, 64) >= static_cast<uint64_t>(sms))
+        launch<128, 64, 4, 2, AK, BKM, VEC, 4>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     // small grids (the LU's diagonal-block and strip updates): a 128 x 64 tile would leave
     // most SMs idle while each CTA runs a long DMMA chain; 64 x 32 tiles spread the same
     // work over 4x the CTAs (tools/gemm_graph.py: 128^2 x 256 27 -> ~9 us)
     else
-        launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+        launch<64, 32, 4, 2, AK, BKM, VEC, 4>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+}
+
+} // namespace
+
+namespace {
+
+void gemm_any(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double alpha, const double* a,
+              uint64_t lda, const double* b, uint64_t ldb, double beta, double* c, uint64_t ldc,
+              const Split& sp) {
+    // operand contiguous extents must be even and 16-byte aligned for 16-byte copies
+    bool aligned = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                     reinterpret_cast<uintptr_t>(c)) & 15) == 0 &&
+                   lda % 2 == 0 && ldb % 2 == 0 && ldc % 2 == 0 && (ta ? m : k) % 2 == 0 &&
+                   (tb ? k : n) % 2 == 0;
+    // AK = A is K-major (row-major m x k, not transposed); BKM = B is K-major (tb)
+#define RL_GEMM_CASE(AK_, BK_)                                                          \
+    if (aligned)                                                                        \
+        dispatch_shape<AK_, BK_, 2>(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, sp);     \
+    else                                                                                \
+        dispatch_shape<AK_, BK_, 1>(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, sp);
+    if (!ta && !tb) {
+        RL_GEMM_CASE(true, false)
+    } else if (!ta && tb) {
+        RL_GEMM_CASE(true, true)
+    } else if (ta && !tb) {
+        RL_GEMM_CASE(false, false)
+    } else {
+        RL_GEMM_CASE(false, true)
+    }
+#undef RL_GEMM_CASE
 }
 
 } // namespace
@@ -264,27 +321,31 @@ void gemm(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double alpha, co
         gemm(false, false, m, n, 1, 0.0, c, ldc, c, ldc, beta, c, ldc);
         return;
     }
-    // operand contiguous extents must be even and 16-byte aligned for 16-byte copies
-    bool aligned = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
-                     reinterpret_cast<uintptr_t>(c)) & 15) == 0 &&
-                   lda % 2 == 0 && ldb % 2 == 0 && ldc % 2 == 0 && (ta ? m : k) % 2 == 0 &&
-                   (tb ? k : n) % 2 == 0;
-    // AK = A is K-major (row-major m x k, not transposed); BKM = B is K-major (tb)
-#define RL_GEMM_CASE(AK_, BK_)                                                          \
-    if (aligned)                                                                        \
-        dispatch_shape<AK_, BK_, 2>(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);     \
-    else                                                                                \
-        dispatch_shape<AK_, BK_, 1>(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
-    if (!ta && !tb) {
-        RL_GEMM_CASE(true, false)
-    } else if (!ta && tb) {
-        RL_GEMM_CASE(true, true)
-    } else if (ta && !tb) {
-        RL_GEMM_CASE(false, false)
-    } else {
-        RL_GEMM_CASE(false, true)
-    }
-#undef RL_GEMM_CASE
+    gemm_any(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, Split{});
+}
+
+// CTA tiles dispatch_shape uses for an M x N output (split planning).
+uint64_t gemm_tiles(uint64_t M, uint64_t N) {
+    if (M > 64 && M <= 72 && N > 64 && N <= 72)
+        return 1;
+    if (N > 64 && N <= 72)
+        return cdiv(M, 128);
+    if (M > 64 && M <= 72)
+        return cdiv(N, 128);
+    return static_cast<uint64_t>(cdiv(M, 64)) * cdiv(N, 32);
+}
+
+// One launch, `splits` K-slices of `kchunk` (multiple of 16): slice z writes
+// op(A)[:, slice] op(B)[slice, :] to parts + z m n (ld n).
+void gemm_splitk_parts(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, const double* a, uint64_t lda,
+                       const double* b, uint64_t ldb, double* parts, int splits, uint64_t kchunk) {
+    if (m == 0 || n == 0)
+        return;
+    Split sp;
+    sp.splits = splits;
+    sp.kchunk = kchunk;
+    sp.cstride = m * n;
+    gemm_any(ta, tb, m, n, k, 1.0, a, lda, b, ldb, 0.0, parts, n, sp);
 }
 
 } // namespace rl

@@ -16,6 +16,8 @@
 // one-sided Jacobi SVD of that 72x72 R in one CTA.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "rl_internal.cuh"
@@ -23,6 +25,9 @@
 namespace rl {
 
 void copy2d_dev(uint64_t rows, uint64_t cols, const double* src, uint64_t lds, double* dst, uint64_t ldd);
+void gemm_splitk_parts(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, const double* a, uint64_t lda,
+                       const double* b, uint64_t ldb, double* parts, int splits, uint64_t kchunk);
+uint64_t gemm_tiles(uint64_t m, uint64_t n);
 
 namespace {
 
@@ -44,178 +49,593 @@ __global__ void k_splitk_reduce(uint64_t m, uint64_t n, int splits, const double
     }
 }
 
-// In-place Cholesky G = R^T R (k x k, ld k) -> R upper (zeros below) and Rinv (upper).
-// shift is added to the diagonal first.  *ok = 0 on a non-positive pivot.
-__global__ void __launch_bounds__(1024) k_chol_inv(int k, double* g, double shift, double* rinv, int* ok) {
-    extern __shared__ double w[]; // KMAX x (KMAX+1)
-    __shared__ double colv[KMAX];
-    __shared__ int good;
-    constexpr int P = KMAX + 1;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < k * k; e += blockDim.x) {
-        int i = e / k, j = e % k;
-        w[i * P + j] = g[e] + (i == j ? shift : 0.0);
-    }
-    if (tid == 0)
-        good = 1;
-    __syncthreads();
-    // right-looking Cholesky on the upper triangle: R[j][j] = sqrt(w_jj); R[j][l] = w_jl / R_jj;
-    // w_il -= R_ji R_jl (i, l > j)
-    for (int j = 0; j < k; ++j) {
-        double d = w[j * P + j];
-        if (!(d > 0.0)) {
-            if (tid == 0)
-                good = 0;
-            break;
-        }
-        double r = sqrt(d);
-        __syncthreads();
-        for (int l = j + tid; l < k; l += blockDim.x)
-            w[j * P + l] = (l == j) ? r : w[j * P + l] / r;
-        __syncthreads();
-        const int rem = k - j - 1;
-        for (int e = tid; e < rem * rem; e += blockDim.x) {
-            int i = j + 1 + e / rem, l = j + 1 + e % rem;
-            if (l >= i)
-                w[i * P + l] -= w[j * P + i] * w[j * P + l];
-        }
-        __syncthreads();
-    }
-    __syncthreads();
-    if (!good) {
-        if (tid == 0)
-            *ok = 0;
-        return;
-    }
-    // write R, then invert in place (Gauss-Jordan on the upper triangle, as genp.cu)
-    for (int e = tid; e < k * k; e += blockDim.x) {
-        int i = e / k, j = e % k;
-        g[e] = (j >= i) ? w[i * P + j] : 0.0;
-    }
-    for (int kk = k - 1; kk >= 0; --kk) {
-        __syncthreads();
-        const double d = w[kk * P + kk];
-        const double r = 1.0 / d;
-        for (int i = tid; i < kk; i += blockDim.x)
-            colv[i] = w[i * P + kk];
-        __syncthreads();
-        for (int j = kk + tid; j < k; j += blockDim.x)
-            w[kk * P + j] = (j == kk) ? r : w[kk * P + j] * r;
-        __syncthreads();
-        const int cols = k - kk;
-        for (int e = tid; e < kk * cols; e += blockDim.x) {
-            int i = e / cols, j = kk + e % cols;
-            double u = colv[i];
-            w[i * P + j] = (j == kk) ? -u * w[kk * P + kk] : w[i * P + j] - u * w[kk * P + j];
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < k * k; e += blockDim.x) {
-        int i = e / k, j = e % k;
-        rinv[e] = (j >= i) ? w[i * P + j] : 0.0;
-    }
-    if (tid == 0)
-        *ok = 1;
+// Reciprocal and reciprocal square root from the SFU seed plus two Newton steps (a few ulp;
+// no IEEE slow path): the Jacobi rotation only needs c^2 + s^2 = 1 to rounding level.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    return y * fma(-h * y, y, 1.5);
 }
 
-// Singular values of a k x k matrix (ld k) by one-sided Jacobi with round-robin
-// pairing; one warp per column pair.  sigma sorted non-increasing.
-__global__ void __launch_bounds__(1024) k_jacobi_sv(int k, const double* a, double* sigma) {
-    extern __shared__ double w[]; // KMAX x KMAX column-major: column j at w + j*k
-    __shared__ int perm[KMAX + 1];
-    __shared__ double off_max;
-    __shared__ double nrm[KMAX];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    const int kk = (k + 1) & ~1; // even number of slots (a dummy column when k is odd)
-    for (int e = tid; e < k * k; e += blockDim.x) {
-        int i = e / k, j = e % k;
-        w[j * k + i] = a[e];
+// Cholesky G + shift I = R^T R and X = R^-1 for k <= 128 in one 512-thread CTA, in shared
+// memory (k padded to KP = 8 ceil(k/8) with an identity corner), 8-column blocks J, three
+// barriers per block:
+//   A  warp 0 factors the 8 x 8 diagonal block in registers (lane c holds column c, pivot
+//      rows by shuffle) and inverts it (X_JJ);
+//   B  one thread per trailing column solves the block's panel row R_J,rest; the others form
+//      T = R_0:J,J X_JJ;
+//   C  rank-8 update of the trailing upper triangle; X_0:J,J = -X_0:J,0:J T.
+// X_ij (i < j) lives in the free lower triangle at W[j][i], its diagonal in rdiag.
+//   shift = shift_coef * sum(shift_part[0..nshift))    (pass 0 of CholeskyQR3; else 0)
+// g <- R (upper, zeros below), rinv <- R^-1.  *bad is sticky: a kernel whose earlier pass
+// failed returns at once; a non-positive pivot sets it.
+constexpr int CH_T = 512;
+__global__ void __launch_bounds__(CH_T) k_chol_inv(int k, double* g, const double* shift_part, int nshift,
+                                                   double shift_coef, double* rinv, int* bad) {
+    extern __shared__ double W[]; // KP x (KP + 1)
+    __shared__ double rdiag[KMAX];
+    __shared__ double T[8][KMAX + 1]; // T[c][l] = (R_0:J,J X_JJ)[l][c]; padded: 8 c's hit 8 banks
+    __shared__ double s_shift;
+    __shared__ int s_bad;
+    if (*bad)
+        return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int KP = (k + 7) & ~7, P = KP + 1;
+    if (warp == 0) {
+        double p = 0.0;
+        if (shift_part)
+            for (int i = lane; i < nshift; i += 32)
+                p += shift_part[i];
+        for (int o = 16; o > 0; o >>= 1)
+            p += __shfl_xor_sync(0xffffffffu, p, o);
+        if (lane == 0) {
+            s_shift = shift_coef * p;
+            s_bad = 0;
+        }
     }
-    for (int i = tid; i < kk; i += blockDim.x)
-        perm[i] = i;
     __syncthreads();
-    for (int sweep = 0; sweep < 60; ++sweep) {
-        if (tid == 0)
-            off_max = 0.0;
+    const double shift = s_shift;
+    for (int e = tid; e < KP * KP; e += CH_T) {
+        const int i = e / KP, l = e - i * KP;
+        double v;
+        if (i < k && l < k)
+            v = g[i * k + l] + (i == l ? shift : 0.0);
+        else
+            v = (i == l) ? 1.0 : 0.0;
+        W[i * P + l] = v;
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < KP; c0 += 8) {
+        // ---- A: R_JJ and X_JJ
+        if (warp == 0) {
+            const int c = lane & 7;
+            double col[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                col[r] = W[(c0 + r) * P + c0 + c];
+            bool ok = true;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const double d = __shfl_sync(0xffffffffu, col[t], t);
+                ok = ok && (d > 0.0);
+                const double inv = rsqrt_nr(d); // 1 / R_tt
+                const double rtc = (c == t) ? d * inv : col[t] * inv; // R_{t,c} (c >= t)
+                col[t] = rtc;
+                if (c == t)
+                    rdiag[c0 + t] = inv;
+#pragma unroll
+                for (int r = t + 1; r < 8; ++r) {
+                    const double rtr = __shfl_sync(0xffffffffu, rtc, r); // R_{t,r}
+                    col[r] = fma(-rtr, rtc, col[r]);
+                }
+            }
+            if (lane < 8) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (r <= c)
+                        W[(c0 + r) * P + c0 + c] = col[r];
+            }
+            __syncwarp();
+            if (lane < 8) { // X_JJ column c: back substitution, X_rc at W[c0+c][c0+r] (r < c)
+                double x[8];
+#pragma unroll
+                for (int r = 7; r >= 0; --r) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int l = r + 1; l < 8; ++l)
+                        if (l <= c)
+                            v = fma(W[(c0 + r) * P + c0 + l], x[l], v);
+                    x[r] = (r == c) ? rdiag[c0 + c] : (r < c ? -v * rdiag[c0 + r] : 0.0);
+                    if (r < c)
+                        W[(c0 + c) * P + c0 + r] = x[r];
+                }
+            }
+            if (lane == 0 && !ok)
+                s_bad = 1;
+        }
         __syncthreads();
+        if (s_bad) { // uniform
+            if (tid == 0)
+                *bad = 1;
+            return;
+        }
+        // ---- B: panel row of R; T = R_0:J,J X_JJ
+        const int rest = KP - c0 - 8;
+        if (tid < rest) { // R_{c0+t, l} = (W_{c0+t, l} - sum_{s<t} R_{c0+s, c0+t} R_{c0+s, l}) / R_tt
+            const int l = c0 + 8 + tid;
+            double x[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                double v = W[(c0 + t) * P + l];
+#pragma unroll
+                for (int s2 = 0; s2 < t; ++s2)
+                    v = fma(-W[(c0 + s2) * P + c0 + t], x[s2], v);
+                x[t] = v * rdiag[c0 + t];
+                W[(c0 + t) * P + l] = x[t];
+            }
+        }
+        for (int e = tid - rest; e >= 0 && e < 8 * c0; e += CH_T - rest) { // threads >= rest
+            const int l = e >> 3, c = e & 7; // T[l][c] = sum_{m <= c} R_{l, c0+m} X_JJ[m][c]
+            double v = 0.0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (m <= c) {
+                    const double xm = (m == c) ? rdiag[c0 + c] : W[(c0 + c) * P + c0 + m];
+                    v = fma(W[l * P + c0 + m], xm, v);
+                }
+            T[c][l] = v;
+        }
+        __syncthreads();
+        // ---- C: trailing update; X_0:J,J
+        if (rest > 0) {
+            const int ty = tid >> 5, tx = tid & 31;
+            for (int i = c0 + 8 + ty; i < KP; i += 16) {
+                double pi[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    pi[t] = W[(c0 + t) * P + i];
+                for (int l = c0 + 8 + tx; l < KP; l += 32) {
+                    if (l < i)
+                        continue;
+                    double v = W[i * P + l];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        v = fma(-pi[t], W[(c0 + t) * P + l], v);
+                    W[i * P + l] = v;
+                }
+            }
+        }
+        for (int e = tid; e < 8 * c0; e += CH_T) { // X_{i, c0+c} = -sum_{l=i}^{c0-1} X_il T[l][c]
+            const int i = e >> 3, c = e & 7;
+            double v0 = rdiag[i] * T[c][i], v1 = 0.0, v2 = 0.0, v3 = 0.0;
+            int l = i + 1;
+            for (; l + 3 < c0; l += 4) { // four chains: the loads pipeline
+                v0 = fma(W[l * P + i], T[c][l], v0);
+                v1 = fma(W[(l + 1) * P + i], T[c][l + 1], v1);
+                v2 = fma(W[(l + 2) * P + i], T[c][l + 2], v2);
+                v3 = fma(W[(l + 3) * P + i], T[c][l + 3], v3);
+            }
+            for (; l < c0; ++l)
+                v0 = fma(W[l * P + i], T[c][l], v0);
+            W[(c0 + c) * P + i] = -((v0 + v1) + (v2 + v3));
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < k * k; e += CH_T) {
+        const int i = e / k, l = e - i * k;
+        g[e] = (l >= i) ? W[i * P + l] : 0.0;
+        rinv[e] = (l > i) ? W[l * P + i] : (l == i ? rdiag[i] : 0.0);
+    }
+}
+
+// Singular values of a k x k matrix (row-major, ld k, k <= 128) by one-sided Jacobi on the
+// columns of its transpose (= its rows: for the triangular factors this is fed, fewer sweeps
+// than on its columns).  Four lanes per column pair, eight pairs per warp, all k/2 pairs of a
+// round at once (round-robin "circle" pairing computed from the round index: slot kk-1
+// fixed, the others rotate), one barrier per round.  The kernel is issue-bound on its one
+// SM, so a pair's dot products, reductions and rotation are shared by as few warps as
+// possible.  A sweep rotates every pair whose cosine |a_p.a_q| / (|a_p||a_q|) exceeds 1e-15;
+// the iteration stops after a sweep with no rotation.  sigma (non-increasing) = final
+// column norms; sigma[KMAX] = sweeps used.  NE >= ceil(k / 4) elements per lane.
+constexpr int JS_T = 256;
+template <int NE>
+__global__ void __launch_bounds__(JS_T) k_jacobi_sv(int k, const double* a, double* sigma) {
+    extern __shared__ double w[]; // column j (= row j of a) at w + j * k
+    __shared__ double nrm[KMAX];
+    __shared__ int rotated[3];
+    const int tid = threadIdx.x, pg = tid >> 2, pl = tid & 3, warp = tid >> 5;
+    const int kk = (k + 1) & ~1; // even slot count (one dummy column when k is odd)
+    const int npairs = kk / 2;
+    for (int e = tid; e < k * k; e += JS_T)
+        w[e] = a[e];
+    if (tid < 3)
+        rotated[tid] = 0;
+    __syncthreads();
+    const double tol = 1e-15;
+    const bool warp_live = warp * 8 < npairs; // warp-uniform
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+        if (tid == 0)
+            rotated[(sweep + 1) % 3] = 0;
         for (int round = 0; round < kk - 1; ++round) {
-            for (int pr = warp; pr < kk / 2; pr += nw) {
-                int p = perm[pr], q = perm[kk - 1 - pr];
-                if (p >= k || q >= k)
-                    continue;
+            if (warp_live) {
+                int p = kk - 1, q = round; // pair 0
+                if (pg > 0) {
+                    p = round + pg;
+                    if (p >= kk - 1)
+                        p -= kk - 1;
+                    q = round - pg;
+                    if (q < 0)
+                        q += kk - 1;
+                }
+                const bool live = pg < npairs && p < k && q < k;
                 if (p > q) {
                     int t = p;
                     p = q;
                     q = t;
                 }
-                double* wp = w + p * k;
-                double* wq = w + q * k;
+                double* wp = w + (live ? p : 0) * k;
+                double* wq = w + (live ? q : 0) * k;
+                double xs[NE], ys[NE];
                 double al = 0.0, be = 0.0, ga = 0.0;
-                for (int i = lane; i < k; i += 32) {
-                    al = fma(wp[i], wp[i], al);
-                    be = fma(wq[i], wq[i], be);
-                    ga = fma(wp[i], wq[i], ga);
+#pragma unroll
+                for (int r = 0; r < NE; ++r) {
+                    const int i = pl + 4 * r;
+                    const bool in = live && i < k;
+                    xs[r] = in ? wp[i] : 0.0;
+                    ys[r] = in ? wq[i] : 0.0;
+                    al = fma(xs[r], xs[r], al);
+                    be = fma(ys[r], ys[r], be);
+                    ga = fma(xs[r], ys[r], ga);
                 }
-                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                for (int o = 2; o > 0; o >>= 1) {
                     al += __shfl_xor_sync(0xffffffffu, al, o);
                     be += __shfl_xor_sync(0xffffffffu, be, o);
                     ga += __shfl_xor_sync(0xffffffffu, ga, o);
                 }
-                if (ga == 0.0)
-                    continue;
-                double rel = fabs(ga) / sqrt(al * be);
-                if (!(rel > 1e-15))
-                    continue;
-                if (lane == 0) {
-                    // monotone max via atomicMax on the bit pattern (non-negative doubles)
-                    atomicMax(reinterpret_cast<unsigned long long*>(&off_max),
-                              static_cast<unsigned long long>(__double_as_longlong(rel)));
+                if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+                    if (pl == 0)
+                        rotated[sweep % 3] = 1;
+                    const double zeta = (be - al) * 0.5 * rcp_nr(ga);
+                    const double v = fma(zeta, zeta, 1.0);
+                    const double t = copysign(rcp_nr(fabs(zeta) + v * rsqrt_nr(v)), zeta);
+                    const double c = rsqrt_nr(fma(t, t, 1.0)), s = c * t;
+#pragma unroll
+                    for (int r = 0; r < NE; ++r) {
+                        const int i = pl + 4 * r;
+                        if (i < k) {
+                            wp[i] = c * xs[r] - s * ys[r];
+                            wq[i] = s * xs[r] + c * ys[r];
+                        }
+                    }
                 }
-                double zeta = (be - al) / (2.0 * ga);
-                double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-                for (int i = lane; i < k; i += 32) {
-                    double x = wp[i], y = wq[i];
-                    wp[i] = c * x - s * y;
-                    wq[i] = s * x + c * y;
-                }
-            }
-            __syncthreads();
-            // rotate the round-robin schedule (slot 0 fixed)
-            if (tid == 0) {
-                int last = perm[kk - 1];
-                for (int i = kk - 1; i > 1; --i)
-                    perm[i] = perm[i - 1];
-                perm[1] = last;
             }
             __syncthreads();
         }
-        if (off_max <= 1e-15)
+        if (!rotated[sweep % 3])
             break;
-        __syncthreads();
     }
-    for (int j = warp; j < k; j += nw) {
+    for (int j0 = 0; j0 < k; j0 += JS_T / 4) { // trip count uniform: the shuffles span the warp
+        const int j = j0 + pg;
         double s = 0.0;
-        for (int i = lane; i < k; i += 32)
-            s = fma(w[j * k + i], w[j * k + i], s);
-        for (int o = 16; o > 0; o >>= 1)
+        if (j < k)
+            for (int i = pl; i < k; i += 4)
+                s = fma(w[j * k + i], w[j * k + i], s);
+        for (int o = 2; o > 0; o >>= 1)
             s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0)
+        if (pl == 0 && j < k)
             nrm[j] = sqrt(s);
     }
     __syncthreads();
-    if (tid == 0) { // selection sort, descending
+    if (tid < k) { // rank sort, descending, ties by index
+        const double v = nrm[tid];
+        int rank = 0;
         for (int i = 0; i < k; ++i) {
-            int best = i;
-            for (int j = i + 1; j < k; ++j)
-                if (nrm[j] > nrm[best])
-                    best = j;
-            double t = nrm[i];
-            nrm[i] = nrm[best];
-            nrm[best] = t;
-            sigma[i] = nrm[i];
+            const double u = nrm[i];
+            rank += (u > v) || (u == v && i < tid);
+        }
+        sigma[rank] = v;
+    }
+    if (tid == 0)
+        sigma[KMAX] = sweep + 1;
+}
+
+// Singular values of a k x k matrix (row-major, ld k, 16 <= k <= 128): Householder
+// bidiagonalization then multisection on the Golub-Kahan form, one 512-thread CTA.  This is
+// the reference's own split (dense_core.cpp:28-43: BDCSVD from min(rows, cols) >= 16, which
+// is backward stable, i.e. absolutely accurate to ~u sigma_1; Jacobi below that).
+//   Bidiagonalization, two barriers per column j.  Every warp forms the left reflector of
+//   column j itself from the squares the previous phase left in sq[] (no broadcast barrier),
+//   then four threads per column c > j apply it to column c and record row j's new squares in
+//   sq2[]; every warp forms the right reflector of row j from sq2[], four threads per row r > j
+//   apply it and record column j+1's squares in sq[].
+//   sigma: the 2k x 2k tridiagonal TGK(d, e) (zero diagonal, off-diagonals d0 e0 d1 ...
+//   d_{k-1}) has eigenvalues +-sigma_i, so #{sigma_i < x} = #{negative pivots of TGK - x I}
+//   - k.  The pivots are ratios of leading (top) and trailing (bottom) minors; the minors'
+//   three-term recurrences need one FMA per step on the dependency chain (the pivot form
+//   needs a division), rescaled by powers of two every 8 steps, and the two chains meet at
+//   row k (twisted factorization).  d, e are pre-scaled by a power of two to sigma_max ~ 1.
+//   Each round every unconverged interval gets G = 3 probe points (one thread each);
+//   intervals shrink 4x per round to width 2^-52 sigma_max.
+constexpr int BD_T = 512;
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// sum of v[lo .. hi) (hi - lo <= 128), the same value in every lane of every warp
+__device__ __forceinline__ double range_sum(const double* v, int lo, int hi, int lane) {
+    double t = 0.0;
+    for (int i = lo + lane; i < hi; i += 32)
+        t += v[i];
+    return warp_sum(t);
+}
+// power-of-two rescale of the pair (a, b) so that max(|a|, |b|) lies in [1, 2)
+__device__ __forceinline__ void rescale2(double& a, double& b) {
+    const int ea = (__double2hiint(a) >> 20) & 0x7ff, eb = (__double2hiint(b) >> 20) & 0x7ff;
+    const int e = max(ea, eb);
+    if (e > 0 && e < 2047) {
+        const double sc = __hiloint2double((2046 - e) << 20, 0); // 2^(1023 - e)
+        a *= sc;
+        b *= sc;
+    }
+}
+// #{sigma_i < x} for the bidiagonal with squared off-diagonals bb[0 .. 2k-2] of TGK.
+//   top: P_0 = 1, P_1 = -x, P_{i+1} = -x P_i - bb[i-1] P_{i-1}; pivot D+_i = P_{i+1} / P_i
+//   bottom: Q_0 = 1, Q_1 = -x, Q_{i+1} = -x Q_i - bb[2k-1-i] Q_{i-1}; D-_{2k-1-i} = Q_{i+1} / Q_i
+// A pivot is negative iff consecutive minors differ in sign bit (integer XOR of the high
+// words: the count runs on the integer pipe, the FP64 pipe only carries the recurrence).
+__device__ __forceinline__ int sbit(double v) { return static_cast<int>(static_cast<unsigned>(__double2hiint(v)) >> 31); }
+__device__ __forceinline__ int tgk_count_below(const double* bb, int k, double x) {
+    double p0 = 1.0, p1 = -x, q0 = 1.0, q1 = -x;
+    int neg = 2 * sbit(-x); // D+_0 = P_1 / P_0 and D-_{2k-1} = Q_1 / Q_0
+    const double* bt = bb;             // bb[i - 1] for step i
+    const double* bq = bb + 2 * k - 2; // bb[2k - 1 - i] for step i
+    int i = 1;
+    // steps 1 .. k-2 count both chains; the bottom chain's step k-1 is D-_k (the twist)
+    for (; i + 8 <= k - 1; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double p2 = fma(-x, p1, -bt[u] * p0);
+            const double q2 = fma(-x, q1, -bq[-u] * q0);
+            neg += (sbit(p2) ^ sbit(p1)) + (sbit(q2) ^ sbit(q1));
+            p0 = p1;
+            p1 = p2;
+            q0 = q1;
+            q1 = q2;
+        }
+        bt += 8;
+        bq -= 8;
+        rescale2(p0, p1);
+        rescale2(q0, q1);
+    }
+    for (; i < k - 1; ++i) {
+        const double p2 = fma(-x, p1, -bt[0] * p0);
+        const double q2 = fma(-x, q1, -bq[0] * q0);
+        neg += (sbit(p2) ^ sbit(p1)) + (sbit(q2) ^ sbit(q1));
+        p0 = p1;
+        p1 = p2;
+        q0 = q1;
+        q1 = q2;
+        ++bt;
+        --bq;
+    }
+    { // step k-1: top pivot D+_{k-1} counted, bottom minor Q_k feeds the twist
+        const double p2 = fma(-x, p1, -bt[0] * p0);
+        const double q2 = fma(-x, q1, -bq[0] * q0);
+        neg += sbit(p2) ^ sbit(p1);
+        p0 = p1;
+        p1 = p2;
+        q0 = q1;
+        q1 = q2;
+        ++bt;
+    }
+    // p1 = P_k, p0 = P_{k-1}, q1 = Q_k, q0 = Q_{k-1}; D+_k = P_{k+1} / P_k, D-_k = Q_k / Q_{k-1}
+    const double pk1 = fma(-x, p1, -bt[0] * p0);
+    const double dp = (p1 == 0.0) ? 1e300 : pk1 * rcp_nr(p1);
+    const double dm = (q0 == 0.0) ? 1e300 : q1 * rcp_nr(q0);
+    return neg + ((dp + dm + x) < 0.0) - k;
+}
+__global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, double* sigma) {
+    extern __shared__ double A[]; // k x (k + 1)
+    __shared__ double sq[KMAX], sq2[KMAX], d[KMAX], e[KMAX], bb[2 * KMAX], lo[KMAX], up[KMAX];
+    __shared__ int cnt[BD_T];
+    __shared__ double s_hi;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int P = k + 1;
+    const long long t_start = clock64();
+    for (int x = tid; x < k * k; x += BD_T) {
+        const int i = x / k, l = x - i * k;
+        A[i * P + l] = a[x];
+        if (l == 0)
+            sq[i] = a[x] * a[x];
+    }
+    __syncthreads();
+    for (int j = 0; j < k; ++j) {
+        { // left reflector of column j (rows j .. k-1), formed by every warp; applied to c > j
+            const double ts = range_sum(sq, j + 1, k, lane);
+            const double x0 = A[j * P + j], ss = fma(x0, x0, ts);
+            double alpha = 0.0, tau = 0.0, v0 = x0;
+            if (ss > 0.0) {
+                alpha = -copysign(sqrt(ss), x0);
+                v0 = x0 - alpha;
+                const double den = fma(v0, v0, ts);
+                tau = den > 0.0 ? 2.0 / den : 0.0;
+            }
+            if (tid == 0)
+                d[j] = alpha;
+            const int c = j + 1 + (tid >> 2), sub = tid & 3;
+            const bool on = c < k && tau != 0.0;
+            double s0 = 0.0, s1 = 0.0;
+            if (on) {
+                int i = j + sub;
+                for (; i + 4 < k; i += 8) {
+                    s0 = fma(i == j ? v0 : A[i * P + j], A[i * P + c], s0);
+                    s1 = fma(A[(i + 4) * P + j], A[(i + 4) * P + c], s1);
+                }
+                if (i < k)
+                    s0 = fma(i == j ? v0 : A[i * P + j], A[i * P + c], s0);
+            }
+            s0 += s1;
+            s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+            s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+            if (on) {
+                const double w = tau * s0;
+                int i = j + sub;
+                for (; i + 4 < k; i += 8) { // loads ahead of stores: two independent updates
+                    const double a0 = A[i * P + c], a1 = A[(i + 4) * P + c];
+                    const double v0i = i == j ? v0 : A[i * P + j], v1 = A[(i + 4) * P + j];
+                    A[i * P + c] = fma(-w, v0i, a0);
+                    A[(i + 4) * P + c] = fma(-w, v1, a1);
+                }
+                if (i < k)
+                    A[i * P + c] = fma(-w, i == j ? v0 : A[i * P + j], A[i * P + c]);
+            }
+            if (c < k && sub == 0) {
+                const double y = A[j * P + c]; // row j's new entry (this thread's i = j update)
+                sq2[c] = y * y;
+            }
+        }
+        __syncthreads();
+        if (j == k - 1)
+            break;
+        { // right reflector of row j (columns j+1 .. k-1), formed by every warp; applied to r > j
+            const double ts = range_sum(sq2, j + 2, k, lane);
+            const double y0 = A[j * P + j + 1], ss = fma(y0, y0, ts);
+            double beta = 0.0, tau = 0.0, u0 = y0;
+            if (ss > 0.0) {
+                beta = -copysign(sqrt(ss), y0);
+                u0 = y0 - beta;
+                const double den = fma(u0, u0, ts);
+                tau = den > 0.0 ? 2.0 / den : 0.0;
+            }
+            if (tid == 0)
+                e[j] = beta;
+            const double* urow = A + j * P;
+            const int r = j + 1 + (tid >> 2), sub = tid & 3;
+            const bool on = r < k && tau != 0.0;
+            double* row = A + (r < k ? r : 0) * P;
+            double s0 = 0.0, s1 = 0.0;
+            if (on) {
+                int c = j + 1 + sub;
+                for (; c + 4 < k; c += 8) {
+                    s0 = fma(row[c], c == j + 1 ? u0 : urow[c], s0);
+                    s1 = fma(row[c + 4], urow[c + 4], s1);
+                }
+                if (c < k)
+                    s0 = fma(row[c], c == j + 1 ? u0 : urow[c], s0);
+            }
+            s0 += s1;
+            s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+            s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+            if (on) {
+                const double w = tau * s0;
+                int c = j + 1 + sub;
+                for (; c + 4 < k; c += 8) {
+                    const double a0 = row[c], a1 = row[c + 4];
+                    const double u0c = c == j + 1 ? u0 : urow[c], u1 = urow[c + 4];
+                    row[c] = fma(-w, u0c, a0);
+                    row[c + 4] = fma(-w, u1, a1);
+                }
+                if (c < k)
+                    row[c] = fma(-w, c == j + 1 ? u0 : urow[c], row[c]);
+            }
+            if (r < k && sub == 0) {
+                const double y = row[j + 1]; // column j+1's new entry (this thread's c = j+1 update)
+                sq[r] = y * y;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- multisection on TGK(d, e), scaled by a power of two so that sigma_max ~ 1
+    const long long t_bidiag = clock64();
+    if (warp == 0) {
+        double md = 0.0, me = 0.0;
+        for (int i = lane; i < k; i += 32) {
+            md = fmax(md, fabs(d[i]));
+            if (i < k - 1)
+                me = fmax(me, fabs(e[i]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+            me = fmax(me, __shfl_xor_sync(0xffffffffu, me, o));
+        }
+        double hb = md + me, sc = 1.0;
+        if (hb > 0.0) {
+            const int eh = (__double2hiint(hb) >> 20) & 0x7ff; // hb in [2^(eh-1023), 2^(eh-1022))
+            sc = __hiloint2double((2045 - eh) << 20, 0);       // 2^(1022 - eh): hb sc in [0.5, 1)
+            if (eh == 0 || eh >= 2046)
+                sc = 1.0;
+        }
+        for (int i = lane; i < k; i += 32) {
+            const double di = d[i] * sc;
+            bb[2 * i] = di * di;
+            if (i < k - 1) {
+                const double ei = e[i] * sc;
+                bb[2 * i + 1] = ei * ei;
+            }
+        }
+        if (lane == 0) {
+            s_hi = hb * sc * (1.0 + 4.4e-16);
+            sq[0] = sc; // kept for the unscaling
         }
     }
+    __syncthreads();
+    const double hi = s_hi, unscale = 1.0 / sq[0], tol = 2.3e-16 * hi;
+    if (tid < k) {
+        lo[tid] = 0.0;
+        up[tid] = hi;
+    }
+    __syncthreads();
+    // probes per interval: 3 (2 bits a round) keeps the count evaluations off the issue limit
+    const int G = min(3, BD_T / k);
+    for (int round = 0; round < 200; ++round) {
+        const int m = tid / G, g = tid - m * G;
+        int c = -1;
+        if (m < k) {
+            const double l0 = lo[m], w = up[m] - l0;
+            if (w > tol)
+                c = tgk_count_below(bb, k, l0 + (g + 1) * (w / (G + 1)));
+        }
+        cnt[tid] = c;
+        __syncthreads();
+        bool open = false;
+        if (tid < k) { // ascending sigma_m lies in [lo, up): #{sigma < x} <= m  <=>  x <= sigma_m
+            const double l0 = lo[tid], w = up[tid] - l0;
+            if (w > tol) {
+                double nl = l0, nu = up[tid];
+                for (int g2 = 0; g2 < G; ++g2) {
+                    const double x = l0 + (g2 + 1) * (w / (G + 1));
+                    if (cnt[tid * G + g2] <= tid)
+                        nl = fmax(nl, x);
+                    else
+                        nu = fmin(nu, x);
+                }
+                lo[tid] = nl;
+                up[tid] = nu;
+                open = nu - nl > tol;
+            }
+        }
+        if (!__syncthreads_or(open))
+            break;
+    }
+    if (tid < k)
+        sigma[k - 1 - tid] = hi > 0.0 ? 0.5 * (lo[tid] + up[tid]) * unscale : 0.0;
+    if (tid == 0) // phase cycles (bidiagonalization, multisection) packed for RL_JACOBI_TRACE
+        sigma[KMAX] = static_cast<double>(t_bidiag - t_start) * 1e6 + static_cast<double>(clock64() - t_bidiag);
 }
 
 __global__ void k_sumsq_partial(uint64_t count, const double* x, double* partial) {
@@ -246,98 +666,148 @@ std::vector<double> to_host(const double* d, uint64_t count) {
 
 } // namespace
 
-// C = alpha op(A) op(B) + beta C with K split into `splits` slices (fixed-order sum).
+// C = alpha op(A) op(B) + beta C with K split into `splits` slices: one split-K GEMM launch
+// (slice partials) and one fixed-order reduction, so the result is run-to-run identical.
 void gemm_splitk(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double alpha, const double* a,
                  uint64_t lda, const double* b, uint64_t ldb, double beta, double* c, uint64_t ldc,
                  int splits) {
-    if (splits <= 1 || k < static_cast<uint64_t>(splits) * 64) {
+    if (splits <= 1 || k < static_cast<uint64_t>(splits) * 16) {
         gemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
         return;
     }
-    uint64_t chunk = ((k + splits - 1) / splits + 15) / 16 * 16;
-    double* parts = ws<double>(WS_RF6, static_cast<uint64_t>(splits) * m * n);
-    int used = 0;
-    for (int s = 0; s < splits; ++s) {
-        uint64_t k0 = s * chunk;
-        if (k0 >= k)
-            break;
-        uint64_t kl = std::min<uint64_t>(chunk, k - k0);
-        const double* as = ta ? a + k0 * lda : a + k0;
-        const double* bs = tb ? b + k0 : b + k0 * ldb;
-        gemm(ta, tb, m, n, kl, 1.0, as, lda, bs, ldb, 0.0, parts + used * m * n, n);
-        ++used;
-    }
+    const uint64_t chunk = ((k + splits - 1) / splits + 15) / 16 * 16;
+    const int used = static_cast<int>(cdiv(k, chunk));
+    double* parts = ws<double>(WS_RF6, static_cast<uint64_t>(used) * m * n);
+    gemm_splitk_parts(ta, tb, m, n, k, a, lda, b, ldb, parts, used, chunk);
     k_splitk_reduce<<<cdiv(m * n, 256), 256, 0, stream()>>>(m, n, used, parts, alpha, beta, c, ldc);
     RL_LAUNCHED();
 }
 
+// K slices for an m x n output over K = k, from a small cost model: DMMA time at the
+// fraction of two-CTA-per-SM waves the grid fills, ~2 us per wave of fixed CTA cost, and the
+// partials' HBM round trip plus the reduction launch when split.
 int splits_for(uint64_t m, uint64_t n, uint64_t k) {
-    uint64_t tiles = static_cast<uint64_t>(cdiv(m, 64)) * cdiv(n, 64);
-    int s = 1;
-    while (tiles * s < 2ULL * ctx().sms && k / (s * 2) >= 512 && s < 32)
-        s *= 2;
-    return s;
+    static const int force = getenv("RL_SPLITK_FORCE") ? atoi(getenv("RL_SPLITK_FORCE")) : 0; // dev sweeps
+    if (force > 0 && static_cast<uint64_t>(force) * 16 <= k)
+        return force;
+    const double tiles = static_cast<double>(gemm_tiles(m, n));
+    const double slots = 2.0 * ctx().sms;
+    const double flops = 2.0 * static_cast<double>(m) * n * k;
+    int best = 1;
+    double best_t = 1e30;
+    for (int s = 1; s <= 256 && k / s >= 16; ++s) {
+        const double ctas = tiles * s, waves = std::ceil(ctas / slots);
+        const double eff = (ctas / slots) / waves;
+        double t = flops / (33e12 * eff) + waves * 2e-6;
+        if (s > 1)
+            t += 2.0 * s * static_cast<double>(m) * n * 8.0 / 5.5e12 + 2e-6;
+        if (t < best_t * 0.98) {
+            best = s;
+            best_t = t;
+        }
+    }
+    return best;
 }
+
+namespace {
+using JacobiKernel = void (*)(int, const double*, double*);
+template <int NE>
+JacobiKernel jacobi_kernel() {
+    static bool attr[16] = {};
+    if (!attr[ctx().device & 15]) {
+        RL_CUDA(cudaFuncSetAttribute(k_jacobi_sv<NE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     KMAX * KMAX * 8));
+        attr[ctx().device & 15] = true;
+    }
+    return k_jacobi_sv<NE>;
+}
+JacobiKernel jacobi_for(int k) {
+    switch ((k + 7) / 8) { // NE = ceil(k / 4) rounded up to even
+    case 1: return jacobi_kernel<2>();
+    case 2: return jacobi_kernel<4>();
+    case 3: return jacobi_kernel<6>();
+    case 4: return jacobi_kernel<8>();
+    case 5: return jacobi_kernel<10>();
+    case 6: return jacobi_kernel<12>();
+    case 7: return jacobi_kernel<14>();
+    case 8: return jacobi_kernel<16>();
+    case 9: return jacobi_kernel<18>();
+    case 10: return jacobi_kernel<20>();
+    case 11: return jacobi_kernel<22>();
+    case 12: return jacobi_kernel<24>();
+    case 13: return jacobi_kernel<26>();
+    case 14: return jacobi_kernel<28>();
+    case 15: return jacobi_kernel<30>();
+    default: return jacobi_kernel<32>();
+    }
+}
+void chol_attrs() {
+    static bool attr[16] = {};
+    if (!attr[ctx().device & 15]) {
+        RL_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     KMAX * (KMAX + 1) * 8));
+        attr[ctx().device & 15] = true;
+    }
+}
+} // namespace
 
 // Singular values of a k x k device matrix -> host vector.
 std::vector<double> small_singular_values(int k, const double* d_a) {
     if (k > KMAX)
         fail(RL_TOO_LARGE, "small SVD: k > 128");
-    double* sg = ws<double>(WS_RF5, KMAX);
-    static bool attr[16] = {};
-    if (!attr[ctx().device & 15]) {
-        RL_CUDA(cudaFuncSetAttribute(k_jacobi_sv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     KMAX * KMAX * 8));
-        RL_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     KMAX * (KMAX + 1) * 8));
-        attr[ctx().device & 15] = true;
-    }
-    k_jacobi_sv<<<1, 1024, KMAX * KMAX * 8, stream()>>>(k, d_a, sg);
-    RL_LAUNCHED();
-    return to_host(sg, k);
-}
-
-// Shifted CholeskyQR3 of Y (m x k, row-major, ld k): q (m x k) and r (k x k) with
-// diag(r) > 0.  Returns false if a Cholesky step broke down.
-bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r) {
-    if (k > KMAX)
-        fail(RL_TOO_LARGE, "qr_positive: more than 128 columns");
-    {
+    double* sg = ws<double>(WS_RF5, KMAX + 1);
+    if (k >= 16) { // the reference's BDCSVD range (dense_core.cpp:28)
         static bool attr[16] = {};
         if (!attr[ctx().device & 15]) {
-            RL_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            RL_CUDA(cudaFuncSetAttribute(k_bidiag_sv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          KMAX * (KMAX + 1) * 8));
             attr[ctx().device & 15] = true;
         }
+        k_bidiag_sv<<<1, BD_T, static_cast<size_t>(k) * (k + 1) * 8, stream()>>>(k, d_a, sg);
+    } else {
+        JacobiKernel kern = jacobi_for(k);
+        kern<<<1, JS_T, static_cast<size_t>(k) * k * 8, stream()>>>(k, d_a, sg);
     }
+    RL_LAUNCHED();
+    std::vector<double> h = to_host(sg, KMAX + 1);
+    static const bool trace = getenv("RL_JACOBI_TRACE") != nullptr;
+    if (trace)
+        fprintf(stderr, "[rl] small svd k=%d: %s %.0f\n", k, k >= 16 ? "cycles(bidiag*1e6+multisection)" : "sweeps",
+                h[KMAX]);
+    h.resize(k);
+    return h;
+}
+
+// Shifted CholeskyQR3 of Y (m x k, row-major, ld k): q (m x k) and r (k x k) with
+// diag(r) > 0.  Returns false if a Cholesky step broke down.  The three passes run without a
+// host round trip (the shift is summed on the device, a failure flag is sticky); one
+// synchronisation at the end reads the flag.
+bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r) {
+    if (k > KMAX)
+        fail(RL_TOO_LARGE, "qr_positive: more than 128 columns");
     double* g = ws<double>(WS_RF4, 3 * KMAX * KMAX + 64);
     double* rinv = g + KMAX * KMAX;
     double* racc = rinv + KMAX * KMAX;
-    int* d_ok = reinterpret_cast<int*>(racc + KMAX * KMAX);
-    double* tmpq = ws<double>(WS_RF5, m * k + KMAX);
+    int* d_bad = reinterpret_cast<int*>(racc + KMAX * KMAX);
+    double* tmpq = ws<double>(WS_RF5, m * k + KMAX + 1);
     const int sp = splits_for(k, k, m);
+    chol_attrs();
+    const int kp = (k + 7) & ~7;
+    const size_t chol_smem = static_cast<size_t>(kp) * (kp + 1) * 8;
     // ||Y||_F^2 for the shift (Fukaya et al.: s = 11 (m k + k(k+1)) u ||Y||_2^2, F-norm bound)
-    double* part = ws<double>(WS_RESID, 256);
-    k_sumsq_partial<<<256, 256, 0, stream()>>>(m * k, y, part);
+    constexpr int kParts = 256;
+    double* part = ws<double>(WS_RESID, kParts);
+    k_sumsq_partial<<<kParts, 256, 0, stream()>>>(m * k, y, part);
     RL_LAUNCHED();
-    std::vector<double> hp = to_host(part, 256);
-    double fro2 = 0.0;
-    for (double v : hp)
-        fro2 += v;
+    RL_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), stream()));
     const double u = 1.1102230246251565e-16;
-    const double shift = 11.0 * (static_cast<double>(m) * k + static_cast<double>(k) * (k + 1)) * u * fro2;
+    const double coef = 11.0 * (static_cast<double>(m) * k + static_cast<double>(k) * (k + 1)) * u;
     const double* src = y;
     for (int pass = 0; pass < 3; ++pass) {
         // G = src^T src
         gemm_splitk(true, false, k, k, m, 1.0, src, k, src, k, 0.0, g, k, sp);
-        RL_CUDA(cudaMemsetAsync(d_ok, 0, sizeof(int), stream()));
-        k_chol_inv<<<1, 1024, KMAX * (KMAX + 1) * 8, stream()>>>(k, g, pass == 0 ? shift : 0.0, rinv, d_ok);
+        k_chol_inv<<<1, CH_T, chol_smem, stream()>>>(k, g, pass == 0 ? part : nullptr, kParts, coef, rinv, d_bad);
         RL_LAUNCHED();
-        int ok = 0;
-        RL_CUDA(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-        RL_CUDA(cudaStreamSynchronize(stream()));
-        if (!ok)
-            return false;
         // Q_pass = src R^-1
         double* dst = (pass == 1) ? tmpq : q;
         gemm(false, false, m, k, k, 1.0, src, k, rinv, k, 0.0, dst, k);
@@ -351,7 +821,10 @@ bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r) {
         src = dst;
     }
     copy2d_dev(k, k, racc, k, r, k);
-    return true;
+    int bad = 0;
+    RL_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+    return bad == 0;
 }
 
 // ||X||_F^2 (deterministic two-level reduction)

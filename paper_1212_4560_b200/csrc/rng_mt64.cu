@@ -479,6 +479,18 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_chunks(const uint64_t* wind
     }
 }
 
+// Gaussian pairs from tempered words: pair q = entries base + 2q (cos), base + 2q + 1 (sin).
+__global__ void k_gaussian_pairs(const uint64_t* raw, uint64_t npairs, GenParams p) {
+    const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (q >= npairs)
+        return;
+    const ulonglong2 w = reinterpret_cast<const ulonglong2*>(raw)[q];
+    double g0, g1;
+    if (!box_muller_fast(w.x, w.y, p.mu, p.sigma, &g0, &g1))
+        box_muller(w.x, w.y, p.mu, p.sigma, &g0, &g1);
+    store_pair(p, p.base + static_cast<int64_t>(2 * q), g0, g1);
+}
+
 // Per-thread streams, n <= 148 sign draws each (only the first twist's phase 1 is
 // needed: new[i] = x[i+156] ^ tw(x[i], x[i+1]) for i < 8 + n <= 156).
 __global__ void k_sign_batched(uint64_t seed, const uint64_t* sids, uint64_t add, uint64_t xor_mask,
@@ -603,14 +615,30 @@ void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, ui
     RL_LAUNCHED();
     k_window_sequence<<<static_cast<unsigned>(nl1), 32, 0, st>>>(l1w, l1s);
     RL_LAUNCHED();
-    // level-2 jumps for every kFwdStride-th chunk, the others by twisting forward
-    const uint64_t njump = (nchunks + kFwdStride - 1) / kFwdStride;
+    // level-2 jumps for every stride-th chunk, the others by twisting forward.  A draw of at
+    // most one wave of chunks jumps to every chunk (the jumps run side by side; forward
+    // twisting would add a serial 7-chunk walk).
+    const uint64_t sms = static_cast<uint64_t>(ctx().sms);
+    const int stride = nchunks <= sms ? 1 : kFwdStride;
+    const uint64_t njump = (nchunks + stride - 1) / stride;
     k_jump<<<static_cast<unsigned>(njump), kJumpThreads, kJumpSmem, st>>>(
-        jt.d_l2, static_cast<uint64_t>(jt.n_l2), l1s, false, c_first, kFwdStride, a_first, static_cast<int>(njump), cw);
+        jt.d_l2, static_cast<uint64_t>(jt.n_l2), l1s, false, c_first, stride, a_first, static_cast<int>(njump), cw);
     RL_LAUNCHED();
-    if (nchunks > 1) {
-        k_window_forward<<<static_cast<unsigned>(njump), 32, 0, st>>>(cw, nchunks, kFwdStride);
+    if (stride > 1 && nchunks > 1) {
+        k_window_forward<<<static_cast<unsigned>(njump), 32, 0, st>>>(cw, nchunks, stride);
         RL_LAUNCHED();
+    }
+    if (kind == Draw::Gaussian && nchunks * 2 <= sms) {
+        // few chunks: one CTA per chunk would run the Box-Muller chain latency-bound on a
+        // handful of SMs; emit the tempered words, then transform all pairs grid-wide
+        uint64_t* raw = ws<uint64_t>(WS_RNG3, nend - offset);
+        GenParams pr{static_cast<int>(Draw::RawU64), 0.0, 0.0, nend, raw, static_cast<int64_t>(offset)};
+        k_gen_chunks<<<static_cast<unsigned>(nchunks), kGenThreads, 0, st>>>(cw, c_first, nchunks, nend, pr);
+        RL_LAUNCHED();
+        const uint64_t npairs = (nend - offset) / 2;
+        k_gaussian_pairs<<<cdiv(npairs, 128), 128, 0, st>>>(raw, npairs, p);
+        RL_LAUNCHED();
+        return;
     }
     k_gen_chunks<<<static_cast<unsigned>(nchunks), kGenThreads, 0, st>>>(cw, c_first, nchunks, end, p);
     RL_LAUNCHED();

@@ -77,6 +77,7 @@ static Matrix diag_dominant(std::size_t n, rnd::RngStream s) {
 }
 
 int main() {
+    std::fprintf(stderr, "[dropin] random_gen\n");
     // ---- random_gen (test_random_gen.cpp) ----
     {
         rnd::Rng a({7, 3}), b({7, 3}), c({7, 4});
@@ -125,6 +126,7 @@ int main() {
         Matrix h = rnd::householder_sign(12, {5, 5});
         CHECK(rel_diff(naive(h, h), h) < 1e-12); // idempotent (test_random_gen.cpp:99-109)
     }
+    std::fprintf(stderr, "[dropin] structured\n");
     // ---- structured (test_structured.cpp) ----
     {
         auto c = structured::StructuredSpec::circulant({1.0, 2.0, 3.0});
@@ -148,6 +150,7 @@ int main() {
         auto ty = structured::toeplitz_mul(t, std::vector<double>{1.0, 1.0});
         CHECK(std::fabs(ty[0] - 6.0) < 1e-14 && std::fabs(ty[1] - 5.0) < 1e-14);
     }
+    std::fprintf(stderr, "[dropin] genp\n");
     // ---- genp (test_genp.cpp) ----
     {
         auto f = genp::genp_factor(Matrix::identity(4));
@@ -230,6 +233,7 @@ int main() {
         }
         CHECK(agree);
     }
+    std::fprintf(stderr, "[dropin] dense core / lowrank\n");
     // ---- dense core / lowrank (test_dense_core.cpp, test_lowrank.cpp) ----
     {
         auto f = dense::qr_positive(Matrix::from_rows({{2.0, 0.0}, {0.0, 3.0}}));
