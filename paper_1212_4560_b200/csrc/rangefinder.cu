@@ -369,6 +369,9 @@ __global__ void __launch_bounds__(JS_T) k_jacobi_sv(int k, const double* a, doub
 //   Each round every unconverged interval gets G = 3 probe points (one thread each);
 //   intervals shrink 4x per round to width 2^-52 sigma_max.
 constexpr int BD_T = 512;
+// Row pitch = 4 (mod 16) doubles: a half-warp touching 4 rows x 4 consecutive columns hits
+// 16 distinct 8-byte bank pairs (the updates are shared-memory-bandwidth bound).
+__host__ __device__ constexpr int bd_pitch(int k) { return k + ((4 - k) & 15); }
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -449,12 +452,12 @@ __device__ __forceinline__ int tgk_count_below(const double* bb, int k, double x
     return neg + ((dp + dm + x) < 0.0) - k;
 }
 __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, double* sigma) {
-    extern __shared__ double A[]; // k x (k + 1)
+    extern __shared__ double A[]; // k x bd_pitch(k)
     __shared__ double sq[KMAX], sq2[KMAX], d[KMAX], e[KMAX], bb[2 * KMAX], lo[KMAX], up[KMAX];
     __shared__ int cnt[BD_T];
     __shared__ double s_hi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int P = k + 1;
+    const int P = bd_pitch(k);
     const long long t_start = clock64();
     for (int x = tid; x < k * k; x += BD_T) {
         const int i = x / k, l = x - i * k;
@@ -464,7 +467,8 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
     }
     __syncthreads();
     for (int j = 0; j < k; ++j) {
-        { // left reflector of column j (rows j .. k-1), formed by every warp; applied to c > j
+        if (j + 1 + warp * 8 < k) { // left reflector of column j (rows j .. k-1), formed by every
+                                     // warp with a column c > j to update
             const double ts = range_sum(sq, j + 1, k, lane);
             const double x0 = A[j * P + j], ss = fma(x0, x0, ts);
             double alpha = 0.0, tau = 0.0, v0 = x0;
@@ -478,40 +482,51 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
                 d[j] = alpha;
             const int c = j + 1 + (tid >> 2), sub = tid & 3;
             const bool on = c < k && tau != 0.0;
-            double s0 = 0.0, s1 = 0.0;
+            // rows: sub 0 takes row j (v_j = v0) then j+4, j+8, ...; sub s takes j+s, j+s+4, ...
+            const int i0 = j + sub + (sub == 0 ? 4 : 0);
+            double s0 = 0.0, s1 = 0.0, ajc = 0.0;
             if (on) {
-                int i = j + sub;
+                ajc = A[j * P + c];
+                if (sub == 0)
+                    s0 = v0 * ajc;
+                int i = i0;
                 for (; i + 4 < k; i += 8) {
-                    s0 = fma(i == j ? v0 : A[i * P + j], A[i * P + c], s0);
+                    s0 = fma(A[i * P + j], A[i * P + c], s0);
                     s1 = fma(A[(i + 4) * P + j], A[(i + 4) * P + c], s1);
                 }
                 if (i < k)
-                    s0 = fma(i == j ? v0 : A[i * P + j], A[i * P + c], s0);
+                    s0 = fma(A[i * P + j], A[i * P + c], s0);
             }
             s0 += s1;
             s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
             s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
             if (on) {
                 const double w = tau * s0;
-                int i = j + sub;
+                if (sub == 0)
+                    A[j * P + c] = fma(-w, v0, ajc);
+                int i = i0;
                 for (; i + 4 < k; i += 8) { // loads ahead of stores: two independent updates
                     const double a0 = A[i * P + c], a1 = A[(i + 4) * P + c];
-                    const double v0i = i == j ? v0 : A[i * P + j], v1 = A[(i + 4) * P + j];
+                    const double v0i = A[i * P + j], v1 = A[(i + 4) * P + j];
                     A[i * P + c] = fma(-w, v0i, a0);
                     A[(i + 4) * P + c] = fma(-w, v1, a1);
                 }
                 if (i < k)
-                    A[i * P + c] = fma(-w, i == j ? v0 : A[i * P + j], A[i * P + c]);
+                    A[i * P + c] = fma(-w, A[i * P + j], A[i * P + c]);
             }
             if (c < k && sub == 0) {
                 const double y = A[j * P + c]; // row j's new entry (this thread's i = j update)
                 sq2[c] = y * y;
             }
+        } else if (j == k - 1 && tid == 0) { // last column: a 1 x 1 reflector
+            const double x0 = A[j * P + j];
+            d[j] = x0 != 0.0 ? -x0 : 0.0;
         }
         __syncthreads();
         if (j == k - 1)
             break;
-        { // right reflector of row j (columns j+1 .. k-1), formed by every warp; applied to r > j
+        if (j + 1 + warp * 8 < k) { // right reflector of row j (columns j+1 .. k-1), formed by
+                                     // every warp with a row r > j to update
             const double ts = range_sum(sq2, j + 2, k, lane);
             const double y0 = A[j * P + j + 1], ss = fma(y0, y0, ts);
             double beta = 0.0, tau = 0.0, u0 = y0;
@@ -527,30 +542,37 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
             const int r = j + 1 + (tid >> 2), sub = tid & 3;
             const bool on = r < k && tau != 0.0;
             double* row = A + (r < k ? r : 0) * P;
-            double s0 = 0.0, s1 = 0.0;
+            // columns: sub 0 takes column j+1 (u = u0) then j+5, ...; sub s takes j+1+s, ...
+            const int c0 = j + 1 + sub + (sub == 0 ? 4 : 0);
+            double s0 = 0.0, s1 = 0.0, arj = 0.0;
             if (on) {
-                int c = j + 1 + sub;
+                arj = row[j + 1];
+                if (sub == 0)
+                    s0 = arj * u0;
+                int c = c0;
                 for (; c + 4 < k; c += 8) {
-                    s0 = fma(row[c], c == j + 1 ? u0 : urow[c], s0);
+                    s0 = fma(row[c], urow[c], s0);
                     s1 = fma(row[c + 4], urow[c + 4], s1);
                 }
                 if (c < k)
-                    s0 = fma(row[c], c == j + 1 ? u0 : urow[c], s0);
+                    s0 = fma(row[c], urow[c], s0);
             }
             s0 += s1;
             s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
             s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
             if (on) {
                 const double w = tau * s0;
-                int c = j + 1 + sub;
+                if (sub == 0)
+                    row[j + 1] = fma(-w, u0, arj);
+                int c = c0;
                 for (; c + 4 < k; c += 8) {
                     const double a0 = row[c], a1 = row[c + 4];
-                    const double u0c = c == j + 1 ? u0 : urow[c], u1 = urow[c + 4];
+                    const double u0c = urow[c], u1 = urow[c + 4];
                     row[c] = fma(-w, u0c, a0);
                     row[c + 4] = fma(-w, u1, a1);
                 }
                 if (c < k)
-                    row[c] = fma(-w, c == j + 1 ? u0 : urow[c], row[c]);
+                    row[c] = fma(-w, urow[c], row[c]);
             }
             if (r < k && sub == 0) {
                 const double y = row[j + 1]; // column j+1's new entry (this thread's c = j+1 update)
@@ -760,10 +782,10 @@ std::vector<double> small_singular_values(int k, const double* d_a) {
         static bool attr[16] = {};
         if (!attr[ctx().device & 15]) {
             RL_CUDA(cudaFuncSetAttribute(k_bidiag_sv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         KMAX * (KMAX + 1) * 8));
+                                         KMAX * bd_pitch(KMAX) * 8));
             attr[ctx().device & 15] = true;
         }
-        k_bidiag_sv<<<1, BD_T, static_cast<size_t>(k) * (k + 1) * 8, stream()>>>(k, d_a, sg);
+        k_bidiag_sv<<<1, BD_T, static_cast<size_t>(k) * bd_pitch(k) * 8, stream()>>>(k, d_a, sg);
     } else {
         JacobiKernel kern = jacobi_for(k);
         kern<<<1, JS_T, static_cast<size_t>(k) * k * 8, stream()>>>(k, d_a, sg);

@@ -219,52 +219,58 @@ __global__ void k_gen_small(uint64_t eseed, uint64_t nout, GenParams p) {
     }
 }
 
-// Word sequence x_0 .. x_{kSeqWords-1} of a seeded engine (the base for level-1 jumps).
-__global__ void k_base_sequence(uint64_t eseed, uint64_t* seq) {
-    __shared__ uint64_t w[kN];
-    int lane = threadIdx.x;
-    warp_seed_window(w, eseed, lane);
+// Word sequences x_0 .. x_{kSeqWords-1} that feed the jumps: from a seeded engine
+// (k_base_sequence, the base for level-1 jumps) or continuing each jumped window
+// (k_window_sequence).  One 320-thread CTA per sequence, every thread twisting
+// (cta_twist_oop): 65 twist blocks in a row, where one warp per sequence was latency-bound.
+constexpr int kSeqThreads = 320;
+__device__ __forceinline__ void cta_twist_oop(const uint64_t* src, uint64_t* dst, int t);
+__device__ __forceinline__ void cta_sequence(uint64_t (*wb)[kN], uint64_t* seq, int t) {
+    int cur = 0;
     for (int base = 0; base < kSeqWords; base += kN) {
-        for (int i = lane; i < kN; i += 32)
-            if (base + i < kSeqWords)
-                seq[base + i] = w[i];
-        __syncwarp();
-        warp_twist(w, lane);
+        if (t < kN && base + t < kSeqWords)
+            seq[base + t] = wb[cur][t];
+        if (base + kN < kSeqWords)
+            cta_twist_oop(wb[cur], wb[cur ^ 1], t);
+        cur ^= 1;
     }
 }
-
-// Word sequences continuing each window: seq[k][0..kSeqWords) from windows[k].
-__global__ void k_window_sequence(const uint64_t* windows, uint64_t* seqs) {
-    __shared__ uint64_t w[kN];
-    int lane = threadIdx.x;
+__global__ void __launch_bounds__(kSeqThreads) k_base_sequence(uint64_t eseed, uint64_t* seq) {
+    __shared__ uint64_t wb[2][kN];
+    const int t = threadIdx.x;
+    if (t < 32)
+        warp_seed_window(wb[0], eseed, t);
+    __syncthreads();
+    cta_sequence(wb, seq, t);
+}
+__global__ void __launch_bounds__(kSeqThreads) k_window_sequence(const uint64_t* windows, uint64_t* seqs) {
+    __shared__ uint64_t wb[2][kN];
+    const int t = threadIdx.x;
     const uint64_t* src = windows + static_cast<size_t>(blockIdx.x) * kN;
-    uint64_t* seq = seqs + static_cast<size_t>(blockIdx.x) * kSeqWords;
-    for (int i = lane; i < kN; i += 32)
-        w[i] = src[i];
-    __syncwarp();
-    for (int base = 0; base < kSeqWords; base += kN) {
-        for (int i = lane; i < kN; i += 32)
-            if (base + i < kSeqWords)
-                seq[base + i] = w[i];
-        __syncwarp();
-        warp_twist(w, lane);
-    }
+    if (t < kN)
+        wb[0][t] = src[t];
+    __syncthreads();
+    cta_sequence(wb, seqs + static_cast<size_t>(blockIdx.x) * kSeqWords, t);
 }
 
 // Jump: out window t = XOR_{i : poly[i]} seq[i + j], j = 0..311.
 // Target b of block uses poly polys[(first_poly + b) % poly_mod] and base sequence
-// seqs[(b / seq_div)].
+// seqs[(b / seq_div)].  The XOR is shared-memory-bandwidth bound (~10^4 terms per word);
+// with parts > 1 the terms of one target are split over `parts` CTAs (each loads only the
+// sequence slice its terms touch) and k_jump_xor folds the partial windows: a draw of a
+// few chunks then uses the whole GPU instead of one SM per chunk.
 constexpr int kJumpThreads = 320;
 __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, uint64_t poly_mod,
                                                        const uint64_t* seqs, bool seq_single,
                                                        uint64_t c_first, int stride, uint64_t a_first,
-                                                       int ntargets, uint64_t* out) {
+                                                       int ntargets, int parts, uint64_t* out,
+                                                       uint64_t* partial) {
     extern __shared__ __align__(16) uint64_t sm[];
     uint64_t* x = sm;                                              // kSeqWords
     uint16_t* list = reinterpret_cast<uint16_t*>(sm + kSeqWords);  // up to 19937 offsets
     __shared__ int wcount[kN];
     __shared__ int total;
-    const int tgt = blockIdx.x;
+    const int tgt = blockIdx.x / parts, part = blockIdx.x - tgt * parts;
     if (tgt >= ntargets)
         return;
     // target chunk c = c_first + stride * tgt: poly c mod poly_mod applied to base sequence
@@ -272,10 +278,7 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, ui
     const uint64_t c = c_first + static_cast<uint64_t>(stride) * tgt;
     const uint64_t* poly = polys + static_cast<size_t>(c % poly_mod) * kN;
     const uint64_t* seq = seqs + (seq_single ? 0 : static_cast<size_t>(c / poly_mod - a_first) * kSeqWords);
-    out += static_cast<size_t>(c - c_first) * kN;
     const int t = threadIdx.x;
-    for (int i = t; i < kSeqWords; i += kJumpThreads)
-        x[i] = seq[i];
     uint64_t pw = 0;
     if (t < kN) {
         pw = poly[t];
@@ -285,9 +288,9 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, ui
     if (t == 0) { // exclusive scan of 312 counts (tiny)
         int acc = 0;
         for (int i = 0; i < kN; ++i) {
-            int c = wcount[i];
+            int c2 = wcount[i];
             wcount[i] = acc;
-            acc += c;
+            acc += c2;
         }
         total = acc;
     }
@@ -301,21 +304,89 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(const uint64_t* polys, ui
         }
     }
     __syncthreads();
+    const int n = total;
+    const int k_lo = static_cast<int>(static_cast<int64_t>(n) * part / parts);
+    const int k_hi = static_cast<int>(static_cast<int64_t>(n) * (part + 1) / parts);
+    // offsets ascend: this part reads seq[list[k_lo] .. list[k_hi - 1] + 311]
+    const int x_lo = k_hi > k_lo ? list[k_lo] : 0;
+    const int x_hi = k_hi > k_lo ? min(static_cast<int>(list[k_hi - 1]) + kN, kSeqWords) : 0;
+    for (int i = x_lo + t; i < x_hi; i += kJumpThreads)
+        x[i] = seq[i];
+    __syncthreads();
     if (t < kN) {
         uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-        const int n = total;
         const uint64_t* xj = x + t;
-        int k = 0;
-        for (; k + 4 <= n; k += 4) {
+        int k = k_lo;
+        for (; k < k_hi && (k & 3); ++k) // to a 4-aligned list index for the 8-byte reads
+            a0 ^= xj[list[k]];
+        for (; k + 4 <= k_hi; k += 4) {
             uint2 ids = *reinterpret_cast<const uint2*>(list + k); // 4 x u16, 8B aligned
             a0 ^= xj[ids.x & 0xffffu];
             a1 ^= xj[ids.x >> 16];
             a2 ^= xj[ids.y & 0xffffu];
             a3 ^= xj[ids.y >> 16];
         }
-        for (; k < n; ++k)
+        for (; k < k_hi; ++k)
             a0 ^= xj[list[k]];
-        out[t] = a0 ^ a1 ^ a2 ^ a3;
+        const uint64_t r = a0 ^ a1 ^ a2 ^ a3;
+        if (parts == 1)
+            out[static_cast<size_t>(c - c_first) * kN + t] = r;
+        else
+            partial[static_cast<size_t>(blockIdx.x) * kN + t] = r;
+    }
+}
+
+// out slot of target b = XOR of its `parts` partial windows
+__global__ void k_jump_xor(const uint64_t* partial, int parts, int stride, uint64_t* out) {
+    const int tgt = blockIdx.x, t = threadIdx.x;
+    if (t >= kN)
+        return;
+    uint64_t r = 0;
+    for (int p = 0; p < parts; ++p)
+        r ^= partial[(static_cast<size_t>(tgt) * parts + p) * kN + t];
+    out[static_cast<size_t>(tgt) * stride * kN + t] = r;
+}
+
+// CTA-parallel twist of one 312-word block (threads 0..311 each own one word): two phases
+// (words 0..155 from the old block, 156..311 from the new first half), two barriers.
+__device__ __forceinline__ void cta_twist_oop(const uint64_t* src, uint64_t* dst, int t) {
+    if (t < kN - kM)
+        dst[t] = twist_word(src[t], src[t + 1], src[t + kM]);
+    __syncthreads();
+    if (t >= kN - kM && t < kN)
+        dst[t] = twist_word(src[t], t + 1 < kN ? src[t + 1] : dst[0], dst[t - kM]);
+    __syncthreads();
+}
+
+// Tempered words of chunks (raw output of k_gen_chunks for Draw::RawU64), one 320-thread CTA
+// per chunk twisting with every thread: for draws of a few chunks, whose single-warp twist
+// chain would set the time.
+__global__ void __launch_bounds__(kJumpThreads) k_raw_chunks(const uint64_t* windows, uint64_t c_first,
+                                                             uint64_t nchunks, uint64_t nout, int64_t base,
+                                                             uint64_t* raw) {
+    __shared__ uint64_t wb[2][kN];
+    const int t = threadIdx.x;
+    const uint64_t ci = blockIdx.x;
+    if (ci >= nchunks)
+        return;
+    const uint64_t c = c_first + ci;
+    if (t < kN)
+        wb[1][t] = windows[ci * kN + t];
+    __syncthreads();
+    cta_twist_oop(wb[1], wb[0], t);
+    const int64_t clo = static_cast<int64_t>(c * kJ);
+    const int64_t lo = max(clo, base);
+    const int64_t hi = static_cast<int64_t>(min(nout, (c + 1) * kJ));
+    int cur = 0;
+    for (int64_t o0 = clo; o0 < hi; o0 += kN) {
+        if (t < kN) {
+            const int64_t o = o0 + t;
+            if (o >= lo && o < hi)
+                raw[o - base] = temper(wb[cur][t]);
+        }
+        if (o0 + kN < hi)
+            cta_twist_oop(wb[cur], wb[cur ^ 1], t);
+        cur ^= 1;
     }
 }
 
@@ -608,12 +679,13 @@ void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, ui
     uint64_t* l1w = base + kSeqWords;
     uint64_t* l1s = l1w + nl1 * kN;
     uint64_t* cw = ws<uint64_t>(WS_RNG2, nchunks * kN);
-    k_base_sequence<<<1, 32, 0, st>>>(eseed, base);
+    k_base_sequence<<<1, kSeqThreads, 0, st>>>(eseed, base);
     RL_LAUNCHED();
     k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(jt.d_l1, 1ULL << 40, base, true, a_first, 1,
-                                                                        a_first, static_cast<int>(nl1), l1w);
+                                                                        a_first, static_cast<int>(nl1), 1, l1w,
+                                                                        nullptr);
     RL_LAUNCHED();
-    k_window_sequence<<<static_cast<unsigned>(nl1), 32, 0, st>>>(l1w, l1s);
+    k_window_sequence<<<static_cast<unsigned>(nl1), kSeqThreads, 0, st>>>(l1w, l1s);
     RL_LAUNCHED();
     // level-2 jumps for every stride-th chunk, the others by twisting forward.  A draw of at
     // most one wave of chunks jumps to every chunk (the jumps run side by side; forward
@@ -621,9 +693,17 @@ void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, ui
     const uint64_t sms = static_cast<uint64_t>(ctx().sms);
     const int stride = nchunks <= sms ? 1 : kFwdStride;
     const uint64_t njump = (nchunks + stride - 1) / stride;
-    k_jump<<<static_cast<unsigned>(njump), kJumpThreads, kJumpSmem, st>>>(
-        jt.d_l2, static_cast<uint64_t>(jt.n_l2), l1s, false, c_first, stride, a_first, static_cast<int>(njump), cw);
+    // fewer jumps than SMs: split each jump's XOR terms over several CTAs
+    const int parts = njump * 2 <= sms ? static_cast<int>(std::min<uint64_t>(16, sms / njump)) : 1;
+    uint64_t* partial = parts > 1 ? ws<uint64_t>(WS_RNG4, njump * parts * kN) : nullptr;
+    k_jump<<<static_cast<unsigned>(njump * parts), kJumpThreads, kJumpSmem, st>>>(
+        jt.d_l2, static_cast<uint64_t>(jt.n_l2), l1s, false, c_first, stride, a_first, static_cast<int>(njump),
+        parts, cw, partial);
     RL_LAUNCHED();
+    if (parts > 1) {
+        k_jump_xor<<<static_cast<unsigned>(njump), kJumpThreads, 0, st>>>(partial, parts, stride, cw);
+        RL_LAUNCHED();
+    }
     if (stride > 1 && nchunks > 1) {
         k_window_forward<<<static_cast<unsigned>(njump), 32, 0, st>>>(cw, nchunks, stride);
         RL_LAUNCHED();
@@ -632,8 +712,8 @@ void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, ui
         // few chunks: one CTA per chunk would run the Box-Muller chain latency-bound on a
         // handful of SMs; emit the tempered words, then transform all pairs grid-wide
         uint64_t* raw = ws<uint64_t>(WS_RNG3, nend - offset);
-        GenParams pr{static_cast<int>(Draw::RawU64), 0.0, 0.0, nend, raw, static_cast<int64_t>(offset)};
-        k_gen_chunks<<<static_cast<unsigned>(nchunks), kGenThreads, 0, st>>>(cw, c_first, nchunks, nend, pr);
+        k_raw_chunks<<<static_cast<unsigned>(nchunks), kJumpThreads, 0, st>>>(cw, c_first, nchunks, nend,
+                                                                               static_cast<int64_t>(offset), raw);
         RL_LAUNCHED();
         const uint64_t npairs = (nend - offset) / 2;
         k_gaussian_pairs<<<cdiv(npairs, 128), 128, 0, st>>>(raw, npairs, p);
