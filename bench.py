@@ -10,6 +10,9 @@ solves/s; % of roofline"):
     1.4704e12 flop of SURVEY.md §8(d) (A G + LU + solves + G Y; G generation is timed but not
     counted).  Inputs resident in HBM; A (512 MiB) and G (512 MiB) exceed the 126 MB L2.
   * `batched` — config 2: 4096 systems of n = 64 with circulant +-1 multipliers (solves/s).
+  * `range_finder` — config 4: the randomized range finder on A 16384 x 4096, rho+ = 72
+    (TFLOP/s over SURVEY.md §8(d)'s 1.967e10 flop); for N > 1 the rows are sharded (TSQR of
+    the sketch + one all_reduce of B, strong scaling).
   * `e2e` — the same config-3 solve through the public host-pointer C-ABI call
     (rl_randomized_genp_ex) from pinned host buffers: H2D of A and B, D2H of X inside the timed
     region.
@@ -37,6 +40,8 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 TFLOP/s precond+GENP at n=8192; batched n=64 solves/s; % of roofline"
 N3, NRHS3 = 8192, 16
 FLOPS3 = 2 * N3 ** 3 + 2 * N3 ** 3 / 3 + 2 * N3 ** 2 * NRHS3 + 2 * N3 ** 2 * NRHS3   # 1.4704e12
+M4, N4, R4, K4 = 16384, 4096, 64, 72
+FLOPS4 = 2 * M4 * N4 * K4 * 2 + 3.4e8   # Y = A H + QR(Y) + B = Q^T A: 1.967e10
 BATCH2, N2 = 4096, 64
 FLOPS2_PER_SYS = 445035      # circulant signed sums + LU + solves + C y
 BYTES2_PER_SYS = 33800
@@ -195,6 +200,74 @@ def make_config2_inputs(torch, dev, batch):
     return A.contiguous(), b, sids
 
 
+def make_config4_rows(torch, dev, lo, hi):
+    """Rows [lo, hi) of the config-4 matrix A = U diag(logspace(0,-2,64)) V^T + 1e-10 E
+    (SURVEY.md §8(d)); U, V are the Q factors of seeded Gaussians (input construction, not
+    the measured path), identical on every rank."""
+    import paper_1212_4560_b200 as rl
+    g1 = torch.empty(M4, R4, dtype=torch.float64, device=dev)
+    g2 = torch.empty(N4, R4, dtype=torch.float64, device=dev)
+    E = torch.empty(M4, N4, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(g1, 0.0, 1.0, rl.RngStream(SEED, 61))
+    rl.dev_gaussian_matrix(g2, 0.0, 1.0, rl.RngStream(SEED, 62))
+    rl.dev_gaussian_matrix(E, 0.0, 1.0, rl.RngStream(SEED, 63))
+    U, _ = torch.linalg.qr(g1)
+    V, _ = torch.linalg.qr(g2)
+    sig = torch.logspace(0, -2, R4, dtype=torch.float64, device=dev)
+    A = ((U[lo:hi] * sig) @ V.T + 1e-10 * E[lo:hi]).contiguous()
+    del E, g1, g2
+    torch.cuda.synchronize()
+    return A
+
+
+def run_config4(torch, rl, dev, dist, rank, world, args, fp64_peak):
+    """Config 4: the randomized range finder, 16384 x 4096, rho+ = 72, rank tol 1e-8.  N = 1:
+    the fused device path (rl_dev_range_finder).  N > 1: rows sharded across ranks (strong
+    scaling), TSQR + one all_reduce (paper_1212_4560_b200/sharded.py); time = max over ranks."""
+    from paper_1212_4560_b200.sharded import DistGroup, range_finder_sharded
+    lo, hi = shard_range(M4, rank, world)
+    A = make_config4_rows(torch, dev, lo, hi)
+    st = rl.RngStream(SEED, 64)
+    Q = torch.empty(hi - lo, K4, dtype=torch.float64, device=dev)
+    B = torch.empty(K4, N4, dtype=torch.float64, device=dev)
+    group = DistGroup(dist) if dist else None
+    resid = None
+    if world == 1:
+        _, rk, resid = rl.dev_range_finder(A, K4, st, 1e-8, Q, B, want_residual=True)
+
+        def step():
+            return rl.dev_range_finder(A, K4, st, 1e-8, Q, B, want_residual=False)[1]
+    else:
+        def step():
+            return range_finder_sharded(A, K4, st, 1e-8, group)[1]
+        rk = step()
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    k4 = max(args.steps, 10)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(k4):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms4 = max_over_ranks(e0.elapsed_time(e1) / k4, dist)
+    tf4 = FLOPS4 / (ms4 * 1e-3) / 1e12
+    del A, Q, B
+    out = {"workload": "config4: range finder Y = A H, qr_positive(Y), B = Q^T A, numerical_rank(B, 1e-8); "
+                       "A 16384 x 4096, rho+ = 72",
+           "value": round(tf4, 4), "unit": "TFLOP/s", "ms_per_step": round(ms4, 4), "flop": FLOPS4,
+           "rank": rk, "parallelism": "fused" if world == 1 else f"rows{world} (TSQR + all_reduce of B)",
+           "scaling": "strong",
+           "roofline": {"bound": "fp64", "frac": round(tf4 / fp64_peak, 4), "peak": round(fp64_peak, 3),
+                        "roofline_ms": round(FLOPS4 / (fp64_peak * 1e12) * 1e3, 4)}}
+    if resid is not None:
+        out["resid_fro"] = resid
+    return out
+
+
 def load_profile_traffic():
     """Per-launch DRAM traffic of the dominant kernel from the committed ncu summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -332,6 +405,9 @@ def run_ours(args, dist, rank, world, local_rank):
     fp64_frac2 = BATCH2 * FLOPS2_PER_SYS / (ms2 * 1e-3) / 1e12 / fp64_peak
     hbm_frac2 = BATCH2 * BYTES2_PER_SYS / (ms2 * 1e-3) / 1e9 / hbm_peak
 
+    # ---- config 4: the randomized range finder (third line) ----
+    rf = run_config4(torch, rl, dev, dist, rank, world, args, fp64_peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_config3(threads=1)
@@ -373,6 +449,7 @@ def run_ours(args, dist, rank, world, local_rank):
                     "roofline": {"bound": "fp64", "frac_fp64": round(fp64_frac2, 4),
                                  "frac_hbm": round(hbm_frac2, 4), "peak_fp64": round(fp64_peak, 3),
                                  "peak_hbm_gbs": round(hbm_peak, 1)}},
+        "range_finder": rf,
         "clocks": clocks.summary(),
         "peaks_same_run": {"fp64_dmma_tflops": round(fp64_peak, 3), "hbm_copy_gbs": round(hbm_peak, 1)},
     }

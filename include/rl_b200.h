@@ -194,6 +194,11 @@ rl_status rl_project_onto_basis_left(uint64_t m, uint64_t n, uint64_t k, const d
 /* dense::numerical_rank (dense_core.cpp:161-175) + the singular values (min(m,n)). */
 rl_status rl_numerical_rank(uint64_t m, uint64_t n, const double* a, double tol, uint64_t* rank,
                             double* sigma);
+/* Device-data variants of the two above (the sharded range finder's per-rank pieces):
+ * d_y, d_q m x n, d_r n x n (n <= 128); d_a m x n with min(m, n) <= 128; sigma on the host. */
+rl_status rl_dev_qr_positive(uint64_t m, uint64_t n, const double* d_y, double* d_q, double* d_r);
+rl_status rl_dev_numerical_rank(uint64_t m, uint64_t n, const double* d_a, double tol, uint64_t* rank,
+                                double* sigma);
 /* The fused range finder on device data: Y = A H, [Q,R] = qr_positive(Y),
  * B = Q^T A, sigma(B), rank at tol, ||A - Q B||_F / ||A||_F.  d_q (m x k), d_b (k x n). */
 rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_plus,

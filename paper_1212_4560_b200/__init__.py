@@ -33,7 +33,8 @@ __all__ = [
     "multiply", "circ_mul", "circulant_multiply_matrix", "genp_factor", "genp_solve", "randomized_genp",
     "randomized_genp_batched", "approx_basis", "qr_positive", "project_onto_basis", "numerical_rank",
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
-    "dev_randomized_genp_batched", "dev_range_finder", "probe_peaks", "box_muller_fast_check", "launch_count", "LIB_PATH",
+    "dev_randomized_genp_batched", "dev_range_finder", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
+    "box_muller_fast_check", "launch_count", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -219,6 +220,8 @@ def lib() -> C.CDLL:
         "rl_project_onto_basis_left": [u64, u64, u64, _d, _d, vp, vp],
         "rl_numerical_rank": [u64, u64, _d, dbl, C.POINTER(u64), _d],
         "rl_dev_range_finder": [u64, u64, vp, u64, u64, u64, dbl, vp, vp, _d, C.POINTER(u64), C.POINTER(dbl)],
+        "rl_dev_qr_positive": [u64, u64, vp, vp, vp],
+        "rl_dev_numerical_rank": [u64, u64, vp, dbl, C.POINTER(u64), _d],
         "rl_probe_peaks": [C.POINTER(dbl), C.POINTER(dbl)],
         "rl_box_muller_fast_check": [u64, vp, u64, vp],
     }
@@ -250,6 +253,14 @@ def _ptr(t) -> int:
     if not t.is_cuda or not t.is_contiguous():
         raise InvalidArgument("device arguments must be contiguous CUDA tensors")
     return t.data_ptr()
+
+
+def _ptr64(t) -> int:
+    """Device pointer of a contiguous float64 CUDA tensor."""
+    import torch
+    if t.dtype != torch.float64:
+        raise InvalidArgument("device matrices must be float64")
+    return _ptr(t)
 
 
 def _bind_stream() -> None:
@@ -516,6 +527,23 @@ def dev_range_finder(a, rho_plus: int, stream: RngStream, rank_tol: float, q, bm
     _chk(lib().rl_dev_range_finder(m, n, _ptr(a), rho_plus, stream.seed, stream.stream_id, rank_tol, _ptr(q),
                                    _ptr(bmat), sg, C.byref(r), C.byref(res) if want_residual else None))
     return sg, int(r.value), (res.value if want_residual else None)
+
+
+def dev_qr_positive(y, q, r) -> None:
+    """dense::qr_positive on device data: q (m x n), r (n x n) with diag(r) > 0 (n <= 128)."""
+    _bind_stream()
+    m, n = y.shape
+    _chk(lib().rl_dev_qr_positive(m, n, _ptr64(y), _ptr64(q), _ptr64(r)))
+
+
+def dev_numerical_rank(a, tol: float) -> Tuple[int, np.ndarray]:
+    """dense::numerical_rank of device data -> (rank, singular values), min(m, n) <= 128."""
+    _bind_stream()
+    m, n = a.shape
+    r = u64(0)
+    sg = np.empty(min(m, n))
+    _chk(lib().rl_dev_numerical_rank(m, n, _ptr64(a), tol, C.byref(r), sg))
+    return int(r.value), sg
 
 
 def box_muller_fast_check(npairs: int, raw=None, seed: int = 0) -> Tuple[int, int, int]:

@@ -348,7 +348,8 @@ rl_status rl_matmul(uint64_t m, uint64_t k, uint64_t n, const double* a, const d
 rl_status rl_dev_gemm(int ta, int tb, uint64_t m, uint64_t n, uint64_t k, double alpha, const double* a,
                       uint64_t lda, const double* b, uint64_t ldb, double beta, double* c, uint64_t ldc) {
     API_BEGIN
-    gemm(ta != 0, tb != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+    // small outputs over a long K (Q^T A of a row block, a Gram): one split-K launch + reduction
+    gemm_splitk(ta != 0, tb != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, splits_for(m, n, k));
     API_END
 }
 
@@ -559,17 +560,15 @@ rl_status rl_approx_basis(uint64_t m, uint64_t n, const double* a, uint64_t rho,
     API_END
 }
 
-rl_status rl_qr_positive(uint64_t m, uint64_t n, const double* a, double* q, double* r) {
-    API_BEGIN
-    require_positive(m, n, "qr_positive");
+namespace {
+// dense::qr_positive on device data (dense_core.cpp:86-115): shifted CholeskyQR3, then the
+// reference's rank check min |R_ii| > 1e-13 sigma_1(R).  Returns R on the host too.
+std::vector<double> qr_positive_dev(uint64_t m, uint64_t n, const double* dy, double* dq, double* dr) {
     if (m < n)
         fail(RL_INVALID_ARGUMENT, "qr_positive: requires rows >= cols");
     if (n > 128)
         fail(RL_TOO_LARGE, "qr_positive: more than 128 columns");
-    double* da = upload(WS_H0, a, m * n);
-    double* dq = ws<double>(WS_H1, m * n);
-    double* dr = ws<double>(WS_H2, n * n);
-    if (!cholqr3(m, static_cast<int>(n), da, dq, dr))
+    if (!cholqr3(m, static_cast<int>(n), dy, dq, dr))
         fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient input");
     std::vector<double> hr(n * n);
     download(hr.data(), dr, n * n);
@@ -579,8 +578,26 @@ rl_status rl_qr_positive(uint64_t m, uint64_t n, const double* a, double* q, dou
         min_diag = std::min(min_diag, std::fabs(hr[i * n + i]));
     if (!(min_diag > 1e-13 * sg[0]))
         fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient input");
+    return hr;
+}
+} // namespace
+
+rl_status rl_qr_positive(uint64_t m, uint64_t n, const double* a, double* q, double* r) {
+    API_BEGIN
+    require_positive(m, n, "qr_positive");
+    double* da = upload(WS_H0, a, m * n);
+    double* dq = ws<double>(WS_H1, m * n);
+    double* dr = ws<double>(WS_H2, n * n);
+    std::vector<double> hr = qr_positive_dev(m, n, da, dq, dr);
     download(q, dq, m * n);
     std::memcpy(r, hr.data(), n * n * sizeof(double));
+    API_END
+}
+
+rl_status rl_dev_qr_positive(uint64_t m, uint64_t n, const double* d_y, double* d_q, double* d_r) {
+    API_BEGIN
+    require_positive(m, n, "qr_positive");
+    qr_positive_dev(m, n, d_y, d_q, d_r);
     API_END
 }
 
@@ -603,14 +620,14 @@ rl_status rl_project_onto_basis_left(uint64_t m, uint64_t n, uint64_t k, const d
     API_END
 }
 
-rl_status rl_numerical_rank(uint64_t m, uint64_t n, const double* a, double tol, uint64_t* rank, double* sigma) {
-    API_BEGIN
+namespace {
+// dense::numerical_rank (dense_core.cpp:161-175) of device data: rank and the min(m, n)
+// singular values (non-increasing).  da is not modified.
+uint64_t numerical_rank_dev(uint64_t m, uint64_t n, const double* da, double tol, std::vector<double>& sg) {
     if (!(tol > 0.0 && tol < 1.0))
         fail(RL_INVALID_ARGUMENT, "numerical_rank: tol must lie in (0, 1)");
     require_positive(m, n, "numerical_rank");
     const uint64_t l = std::min(m, n);
-    std::vector<double> sg;
-    double* da = upload(WS_H0, a, m * n);
     if (std::max(m, n) <= 128) {
         // pad to square: zero rows/columns add zero singular values only
         const uint64_t k = std::max(m, n);
@@ -640,14 +657,35 @@ rl_status rl_numerical_rank(uint64_t m, uint64_t n, const double* a, double tol,
     } else {
         fail(RL_TOO_LARGE, "numerical_rank: min(m, n) > 128 is not supported on this path");
     }
-    if (sigma)
-        std::memcpy(sigma, sg.data(), l * sizeof(double));
     uint64_t r = 0;
     if (!sg.empty() && sg[0] != 0.0)
         for (uint64_t j = 0; j < l; ++j)
             if (sg[j] >= tol * sg[0])
                 r = j + 1;
-    *rank = r;
+    return r;
+}
+} // namespace
+
+rl_status rl_numerical_rank(uint64_t m, uint64_t n, const double* a, double tol, uint64_t* rank, double* sigma) {
+    API_BEGIN
+    if (!(tol > 0.0 && tol < 1.0))
+        fail(RL_INVALID_ARGUMENT, "numerical_rank: tol must lie in (0, 1)");
+    require_positive(m, n, "numerical_rank");
+    double* da = upload(WS_H0, a, m * n);
+    std::vector<double> sg;
+    *rank = numerical_rank_dev(m, n, da, tol, sg);
+    if (sigma)
+        std::memcpy(sigma, sg.data(), sg.size() * sizeof(double));
+    API_END
+}
+
+rl_status rl_dev_numerical_rank(uint64_t m, uint64_t n, const double* d_a, double tol, uint64_t* rank,
+                                double* sigma) {
+    API_BEGIN
+    std::vector<double> sg;
+    *rank = numerical_rank_dev(m, n, d_a, tol, sg);
+    if (sigma)
+        std::memcpy(sigma, sg.data(), sg.size() * sizeof(double));
     API_END
 }
 

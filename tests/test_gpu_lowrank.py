@@ -98,3 +98,49 @@ def test_range_finder_vs_oracle(rl, oracle):
     assert np.abs(sg - so).max() <= 1e-12
     Qh = Q.cpu().numpy()
     assert np.abs(Qh.T @ Qh - np.eye(k)).max() < 1e-13
+
+
+def test_device_qr_positive_and_numerical_rank(rl, golden):
+    import torch
+    a = golden["qr/40x12/A"]
+    y = torch.tensor(a, device="cuda")
+    q = torch.empty_like(y)
+    r = torch.empty(12, 12, dtype=torch.float64, device="cuda")
+    rl.dev_qr_positive(y, q, r)
+    torch.cuda.synchronize()
+    assert np.abs(q.cpu().numpy() - golden["qr/40x12/Q"]).max() < 1e-12
+    assert np.abs(r.cpu().numpy() - golden["qr/40x12/R"]).max() < 1e-12
+    bad = torch.tensor([[i + 1.0, 2.0 * (i + 1)] for i in range(4)], dtype=torch.float64, device="cuda")
+    with pytest.raises(rl.RankDeficient):
+        rl.dev_qr_positive(bad, torch.empty_like(bad), torch.empty(2, 2, dtype=torch.float64, device="cuda"))
+    with pytest.raises(rl.InvalidArgument):  # float32 data is rejected, not reinterpreted
+        rl.dev_qr_positive(bad.float(), torch.empty_like(bad), torch.empty(2, 2, dtype=torch.float64, device="cuda"))
+    for m, n in [(3, 3), (64, 300), (300, 64), (72, 4096)]:
+        b = np.random.default_rng(m + n).standard_normal((m, n)) * np.logspace(0, -9, n)
+        rk, sg = rl.dev_numerical_rank(torch.tensor(b, device="cuda"), 1e-6)
+        rh, sh = rl.numerical_rank(b, 1e-6)
+        s_np = np.linalg.svd(b, compute_uv=False)
+        assert rk == rh and np.abs(sg - sh).max() <= 1e-15 * s_np[0]
+        assert np.abs(sg - s_np).max() <= 1e-13 * s_np[0]
+
+
+def test_sharded_range_finder_single_rank_matches_fused(rl):
+    """World size 1 through the sharded orchestration (sharded.py) with the CUDA ops: the same
+    sketch, Q, B, sigma and rank as the fused rl_dev_range_finder."""
+    import torch
+    from paper_1212_4560_b200.sharded import range_finder_sharded
+    m, n, r, k = 2048, 512, 16, 24
+    rng = np.random.default_rng(5)
+    U, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    A = (U * np.logspace(0, -2, r)) @ V.T + 1e-10 * rng.standard_normal((m, n))
+    Ad = torch.tensor(A, device="cuda")
+    Q = torch.empty(m, k, dtype=torch.float64, device="cuda")
+    B = torch.empty(k, n, dtype=torch.float64, device="cuda")
+    sg, rank, _ = rl.dev_range_finder(Ad, k, rl.RngStream(9, 9), 1e-8, Q, B)
+    sg2, rank2, q2, b2 = range_finder_sharded(Ad, k, rl.RngStream(9, 9), 1e-8)
+    torch.cuda.synchronize()
+    assert rank2 == rank
+    assert np.abs(sg2 - sg).max() <= 1e-14
+    assert (q2 - Q).abs().max().item() <= 1e-14
+    assert (b2 - B).abs().max().item() <= 1e-14 * np.abs(A).max()
