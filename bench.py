@@ -10,6 +10,10 @@ solves/s; % of roofline"):
     1.4704e12 flop of SURVEY.md §8(d) (A G + LU + solves + G Y; G generation is timed but not
     counted).  Inputs resident in HBM; A (512 MiB) and G (512 MiB) exceed the 126 MB L2.
   * `batched` — config 2: 4096 systems of n = 64 with circulant +-1 multipliers (solves/s).
+  * `config1` — n = 256 (latency): us per solve on device data and through the host-pointer call.
+  * `config5` — n = 16384, 8 RHS, with the Householder-pair, sparse +-1 and Gaussian right
+    multipliers (ms per call, attempts, backward error; 1 warm-up + 2 timed calls per arm;
+    `--skip-config5` leaves it out).
   * `range_finder` — config 4: the randomized range finder on A 16384 x 4096, rho+ = 72
     (TFLOP/s over SURVEY.md §8(d)'s 1.967e10 flop); for N > 1 the rows are sharded (TSQR of
     the sketch + one all_reduce of B, strong scaling).
@@ -40,6 +44,11 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 TFLOP/s precond+GENP at n=8192; batched n=64 solves/s; % of roofline"
 N3, NRHS3 = 8192, 16
 FLOPS3 = 2 * N3 ** 3 + 2 * N3 ** 3 / 3 + 2 * N3 ** 2 * NRHS3 + 2 * N3 ** 2 * NRHS3   # 1.4704e12
+N1 = 256
+FLOPS1 = 2 * N1 ** 3 + 2 * N1 ** 3 / 3 + 2 * N1 ** 2 + 2 * N1 ** 2   # 45.00 MFLOP
+N5, NRHS5 = 16384, 8
+FLOPS5_G = 2 * N5 ** 3 + 2 * N5 ** 3 / 3 + 2 * N5 ** 2 * NRHS5 * 2   # C5 Gaussian arm per attempt
+FLOPS5_LU = 2 * N5 ** 3 / 3
 M4, N4, R4, K4 = 16384, 4096, 64, 72
 FLOPS4 = 2 * M4 * N4 * K4 * 2 + 3.4e8   # Y = A H + QR(Y) + B = Q^T A: 1.967e10
 BATCH2, N2 = 4096, 64
@@ -198,6 +207,108 @@ def make_config2_inputs(torch, dev, batch):
     sids = torch.arange(batch, dtype=torch.int64, device=dev) + 7
     torch.cuda.synchronize()
     return A.contiguous(), b, sids
+
+
+def _timed(torch, fn, warmup, steps, dist):
+    for _ in range(warmup):
+        out = fn()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return max_over_ranks(e0.elapsed_time(e1) / steps, dist), out
+
+
+def run_config1(torch, rl, dev, dist, args, fp64_peak):
+    """Config 1: n = 256 Gaussian-preconditioned GENP, MulSide::Right, one RHS (latency-bound):
+    A with its leading 128^2 block = P Q (rank 127), x_true, b = A x_true."""
+    n, h = N1, N1 // 2
+    A = torch.empty(n, n, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(A, 0.0, 1.0, rl.RngStream(SEED, 11))
+    P = torch.empty(h, h - 1, dtype=torch.float64, device=dev)
+    Q = torch.empty(h - 1, h, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(P, 0.0, 1.0, rl.RngStream(SEED, 12))
+    rl.dev_gaussian_matrix(Q, 0.0, 1.0, rl.RngStream(SEED, 13))
+    A[:h, :h] = P @ Q
+    xt = torch.empty(n, 1, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(xt, 0.0, 1.0, rl.RngStream(SEED, 14))
+    b = (A @ xt).contiguous()
+    x = torch.empty_like(b)
+    kind = rl.MultiplierKind(rl.MultiplierTag.GAUSSIAN)
+    st = rl.RngStream(SEED, 15)
+    ms, rep = _timed(torch, lambda: rl.dev_randomized_genp(A, b, x, kind, rl.MulSide.RIGHT, 0, st,
+                                                           skip_raw_arm=True),
+                     max(args.warmup, 3), max(args.steps, 20), dist)
+    bwd = float(((A @ x - b).norm() / (A.norm() * x.norm())).item())
+    # the same solve from host buffers through the public host-pointer call
+    hA, hb, hx = A.cpu().numpy(), b.cpu().numpy().ravel(), np.empty(n)
+    t0 = time.perf_counter()
+    reps = max(args.steps, 20)
+    for _ in range(reps):
+        rl.randomized_genp(hA, hb, kind, rl.MulSide.RIGHT, 0, st)
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / reps, dist)
+    return {"workload": "config1: Gaussian-preconditioned GENP n=256, 1 RHS, MulSide::Right (latency)",
+            "value_us_per_solve": round(ms * 1e3, 2), "attempts": rep.attempts_drawn,
+            "tflops_executed": round(rep.attempts_drawn * FLOPS1 / (ms * 1e-3) / 1e12, 5),
+            "flop_per_attempt": FLOPS1, "backward_error": bwd, "residual": rep.residual,
+            "e2e_us_per_solve": round(e2e_ms * 1e3, 1),
+            "e2e_call": "rl_randomized_genp (host pointers, contrast arm included, as the reference)",
+            "roofline": {"bound": "latency", "frac_fp64": round(FLOPS1 / (ms * 1e-3) / 1e12 / fp64_peak, 6)}}
+
+
+def make_config5_inputs(torch, dev):
+    """Config 5: A 16384^2 Gaussian with its leading 8192^2 block = P Q (rank 8191), X_true
+    16384 x 8, B = A X_true; built once on the GPU, not timed."""
+    import paper_1212_4560_b200 as rl
+    n, h = N5, N5 // 2
+    A = torch.empty(n, n, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(A, 0.0, 1.0, rl.RngStream(SEED, 51))
+    P = torch.empty(h, h - 1, dtype=torch.float64, device=dev)
+    Q = torch.empty(h - 1, h, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(P, 0.0, 1.0, rl.RngStream(SEED, 52))
+    rl.dev_gaussian_matrix(Q, 0.0, 1.0, rl.RngStream(SEED, 53))
+    A[:h, :h] = P @ Q
+    del P, Q
+    Xt = torch.empty(n, NRHS5, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(Xt, 0.0, 1.0, rl.RngStream(SEED, 54))
+    B = (A @ Xt).contiguous()
+    torch.cuda.synchronize()
+    return A, B
+
+
+def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak):
+    """Config 5: n = 16384, 8 RHS, MulSide::Right with the orthogonal Householder pair, the
+    sparse +-1 and the Gaussian multipliers (contrast arm skipped as in config 3).  Short runs
+    (1 warm-up + 2 timed calls per arm: a Gaussian call is ~1 s)."""
+    A, B = make_config5_inputs(torch, dev)
+    X = torch.empty_like(B)
+    out = {"workload": "config5: GENP n=16384, 8 RHS, MulSide::Right; Householder pair / sparse +-1 / Gaussian"}
+    arms = (("householder_pair", rl.MultiplierTag.HOUSEHOLDER_PAIR, 3.0 * N5 * N5 * 8),
+            ("sparse_sign", rl.MultiplierTag.SPARSE_SIGN, 2.0 * N5 * N5 * 8),
+            ("gaussian", rl.MultiplierTag.GAUSSIAN, None))
+    for name, tag, mult_bytes in arms:
+        kind = rl.MultiplierKind(tag)
+        st = rl.RngStream(SEED, 55)
+        ms, rep = _timed(torch, lambda: rl.dev_randomized_genp(A, B, X, kind, rl.MulSide.RIGHT, 0, st,
+                                                               skip_raw_arm=True), 1, 2, dist)
+        bwd = float(((A @ X - B).norm(dim=0) / (A.norm() * X.norm(dim=0))).max().item())
+        arm = {"ms_per_call": round(ms, 2), "attempts": rep.attempts_drawn, "residual": rep.residual,
+               "backward_error_max": bwd}
+        if tag == rl.MultiplierTag.GAUSSIAN:
+            arm["tflops_executed"] = round(rep.attempts_drawn * FLOPS5_G / (ms * 1e-3) / 1e12, 3)
+            arm["frac_fp64"] = round(arm["tflops_executed"] / fp64_peak, 4)
+        else:
+            arm["lu_tflops_executed"] = round(rep.attempts_drawn * FLOPS5_LU / (ms * 1e-3) / 1e12, 3)
+            arm["multiplier_bytes_per_apply"] = mult_bytes
+        out[name] = arm
+    del A, B, X
+    torch.cuda.empty_cache()
+    return out
 
 
 def make_config4_rows(torch, dev, lo, hi):
@@ -407,6 +518,9 @@ def run_ours(args, dist, rank, world, local_rank):
 
     # ---- config 4: the randomized range finder (third line) ----
     rf = run_config4(torch, rl, dev, dist, rank, world, args, fp64_peak)
+    # ---- configs 1 and 5 (latency-bound n = 256; n = 16384 with the new multipliers) ----
+    c1 = run_config1(torch, rl, dev, dist, args, fp64_peak)
+    c5 = None if args.skip_config5 else run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -450,6 +564,8 @@ def run_ours(args, dist, rank, world, local_rank):
                                  "frac_hbm": round(hbm_frac2, 4), "peak_fp64": round(fp64_peak, 3),
                                  "peak_hbm_gbs": round(hbm_peak, 1)}},
         "range_finder": rf,
+        "config1": c1,
+        "config5": c5,
         "clocks": clocks.summary(),
         "peaks_same_run": {"fp64_dmma_tflops": round(fp64_peak, 3), "hbm_copy_gbs": round(hbm_peak, 1)},
     }
@@ -532,6 +648,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-config5", action="store_true", help="skip the n = 16384 config-5 arms (~10 s)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -35,7 +35,8 @@ constexpr uint64_t kUpper = 0xFFFFFFFF80000000ULL, kLower = 0x7FFFFFFFULL,
 constexpr int kLog2J = 15;
 constexpr uint64_t kJ = 1ULL << kLog2J;
 constexpr int kSeqWords = 19937 + kN - 1; // words x_t .. x_{t+20247} feed a jump
-constexpr uint64_t kSmallMax = 1ULL << 16; // streams this short run on one warp
+constexpr uint64_t kSmallMax = 1ULL << 12; // streams this short run on one warp (beyond ~3K draws the
+                                            // chunked path's ~0.1 ms fixed cost wins)
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {
     uint64_t z = (s += 0x9e3779b97f4a7c15ULL);

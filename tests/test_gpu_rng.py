@@ -33,7 +33,7 @@ def test_signs_uniforms_ints_bit_exact_vs_reference(rl, golden):
     assert np.array_equal(col, golden["circulant_sign/64/9_1"])
 
 
-@pytest.mark.parametrize("count", [1, 311, 312, 313, 65536, 65537, (1 << 15) * 3 + 5, (1 << 21) + 12345])
+@pytest.mark.parametrize("count", [1, 311, 312, 313, 4096, 4097, 65536, 65537, (1 << 15) * 3 + 5, (1 << 21) + 12345])
 def test_raw_stream_bit_exact_across_jump_boundaries(rl, oracle, count):
     got = rl.raw_u64(rl.RngStream(5, 9), count)
     assert np.array_equal(got, oracle.raw_u64(5, 9, count))
