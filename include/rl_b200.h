@@ -116,6 +116,10 @@ rl_status rl_householder_pair_signs(uint64_t n, uint64_t seed, uint64_t stream_i
 /* NEW: sparse +-1 multiplier, rows[n][nnz], signs[n][nnz] per column. */
 rl_status rl_sparse_sign(uint64_t n, int nnz, uint64_t seed, uint64_t stream_id, int32_t* rows,
                          double* signs);
+/* NEW: out = A S for the sparse +-1 S above (A, out n x n row-major): the multiplier stage of
+ * randomized_genp's Right side with RL_SPARSE_SIGN (genp.cpp:175-180 applies M on the right). */
+rl_status rl_sparse_apply_right(uint64_t n, int nnz, const int32_t* rows, const double* signs,
+                                const double* a, double* out);
 
 /* -------------------------------------------- matrix.hpp (matrix.cpp) ---- */
 /* Matrix::multiply(const Matrix&) (matrix.cpp:86-102): C(m x n) = A(m x k) B(k x n). */

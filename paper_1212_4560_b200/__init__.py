@@ -29,7 +29,7 @@ __all__ = [
     "Error", "DimensionMismatch", "InvalidArgument", "PivotBreakdown", "RankDeficient", "Degenerate",
     "NoConvergence", "TooLarge", "CudaError", "NoDevice", "RngStream", "MultiplierKind", "MultiplierTag",
     "MulSide", "PrecondReport", "GenpFactorization", "lib", "gaussian_matrix", "uniform_matrix",
-    "random_structured", "householder_sign", "householder_pair_signs", "sparse_sign", "rng_draws", "raw_u64",
+    "random_structured", "householder_sign", "householder_pair_signs", "sparse_sign", "sparse_apply_right", "rng_draws", "raw_u64",
     "multiply", "circ_mul", "circulant_multiply_matrix", "genp_factor", "genp_solve", "randomized_genp",
     "randomized_genp_batched", "approx_basis", "qr_positive", "project_onto_basis", "numerical_rank",
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
@@ -202,6 +202,7 @@ def lib() -> C.CDLL:
         "rl_householder_sign": [u64, u64, u64, _d],
         "rl_householder_pair_signs": [u64, u64, u64, _d, _d],
         "rl_sparse_sign": [u64, cint, u64, u64, _i32a, _d],
+        "rl_sparse_apply_right": [u64, cint, _i32a, _d, _d, _d],
         "rl_matmul": [u64, u64, u64, _d, _d, _d],
         "rl_dev_gemm": [cint, cint, u64, u64, u64, dbl, vp, u64, vp, u64, dbl, vp, u64],
         "rl_circ_mul": [u64, _d, _d, _d],
@@ -527,6 +528,18 @@ def dev_range_finder(a, rho_plus: int, stream: RngStream, rank_tol: float, q, bm
     _chk(lib().rl_dev_range_finder(m, n, _ptr(a), rho_plus, stream.seed, stream.stream_id, rank_tol, _ptr(q),
                                    _ptr(bmat), sg, C.byref(r), C.byref(res) if want_residual else None))
     return sg, int(r.value), (res.value if want_residual else None)
+
+
+def sparse_apply_right(rows, signs, a) -> np.ndarray:
+    """A S for the sparse +-1 multiplier (rows, signs: n x nnz per column of S)."""
+    rows = np.ascontiguousarray(rows, dtype=np.int32)
+    signs, a = _f64(signs), _f64(a)
+    n, nnz = rows.shape
+    if a.shape != (n, n) or signs.shape != rows.shape:
+        raise DimensionMismatch("sparse_apply_right: shape mismatch")
+    out = np.empty_like(a)
+    _chk(lib().rl_sparse_apply_right(n, nnz, rows, signs, a, out))
+    return out
 
 
 def dev_qr_positive(y, q, r) -> None:

@@ -34,6 +34,8 @@ void gemm_splitk(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double al
                  uint64_t lda, const double* b, uint64_t ldb, double beta, double* c, uint64_t ldc,
                  int splits);
 int splits_for(uint64_t m, uint64_t n, uint64_t k);
+void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs, const double* a,
+                            uint64_t lda, double* out, uint64_t ldo);
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r);
 std::vector<double> small_singular_values(int k, const double* d_a);
 double sumsq_dev(uint64_t count, const double* x);
@@ -329,6 +331,25 @@ rl_status rl_sparse_sign(uint64_t n, int nnz, uint64_t seed, uint64_t sid, int32
     rng_sparse_sign(seed, sid, n, nnz, dr, ds);
     download(rows, dr, n * nnz);
     download(signs, ds, n * nnz);
+    API_END
+}
+
+rl_status rl_sparse_apply_right(uint64_t n, int nnz, const int32_t* rows, const double* signs,
+                                const double* a, double* out) {
+    API_BEGIN
+    require_positive(n, n, "sparse_apply_right");
+    if (nnz < 1 || nnz > 8 || static_cast<uint64_t>(nnz) > n)
+        fail(RL_INVALID_ARGUMENT, "sparse_apply_right: need 1 <= nnz <= min(8, n)");
+    for (uint64_t e = 0; e < n * nnz; ++e)
+        if (rows[e] < 0 || static_cast<uint64_t>(rows[e]) >= n)
+            fail(RL_INVALID_ARGUMENT, "sparse_apply_right: row index out of range");
+    int32_t* dr = ws<int32_t>(WS_H2, n * nnz);
+    RL_CUDA(cudaMemcpyAsync(dr, rows, n * nnz * sizeof(int32_t), cudaMemcpyHostToDevice, stream()));
+    double* ds = upload(WS_H3, signs, n * nnz);
+    double* da = upload(WS_H0, a, n * n);
+    double* dout = ws<double>(WS_H1, n * n);
+    sparse_apply_right_dev(n, nnz, dr, ds, da, n, dout, n);
+    download(out, dout, n * n);
     API_END
 }
 

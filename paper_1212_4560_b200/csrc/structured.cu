@@ -160,6 +160,54 @@ __global__ void __launch_bounds__(SP_THREADS) k_sparse_right(uint64_t n, int nnz
     }
 }
 
+// The same product for nnz = 4, n <= 16384 (config 5): persistent CTAs (one per SM) keep the
+// whole S in registers — per thread 32 output columns x 4 (row, sign) entries packed as 16-bit
+// (15-bit row | sign bit), two per register — and stream the rows of A through shared memory,
+// so every byte of A and of the output crosses HBM once and S is read once per CTA (the kernel
+// above re-reads S from L2 for every row: 786 KB per 128 KB row).  Same summation order.
+constexpr int SP4_THREADS = 512, SP4_Q = 32;
+__global__ void __launch_bounds__(SP4_THREADS, 1) k_sparse_right4(uint64_t n, const double* __restrict__ a,
+                                                                  uint64_t lda, const int32_t* __restrict__ rows,
+                                                                  const double* __restrict__ signs,
+                                                                  double* __restrict__ out, uint64_t ldo) {
+    extern __shared__ __align__(16) double srow[]; // n
+    const int t = threadIdx.x;
+    uint32_t pk[SP4_Q * 2]; // output q: entries (2q, 2q+1) -> pk[2q] lo/hi, (2q+2, 2q+3) -> pk[2q+1]
+#pragma unroll
+    for (int q = 0; q < SP4_Q; ++q) {
+        const uint64_t j = t + static_cast<uint64_t>(q) * SP4_THREADS;
+        uint32_t e[4] = {0, 0, 0, 0};
+        if (j < n)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                e[u] = static_cast<uint32_t>(rows[j * 4 + u]) | (signs[j * 4 + u] < 0.0 ? 0x8000u : 0u);
+        pk[2 * q] = e[0] | (e[1] << 16);
+        pk[2 * q + 1] = e[2] | (e[3] << 16);
+    }
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const double2* src = reinterpret_cast<const double2*>(a + i * lda);
+        for (uint64_t c = t; c < n / 2; c += SP4_THREADS)
+            reinterpret_cast<double2*>(srow)[c] = __ldcs(src + c);
+        __syncthreads();
+        double* orow = out + i * ldo;
+#pragma unroll
+        for (int q = 0; q < SP4_Q; ++q) {
+            const uint64_t j = t + static_cast<uint64_t>(q) * SP4_THREADS;
+            if (j < n) {
+                double s = 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = (pk[2 * q + (u >> 1)] >> (16 * (u & 1))) & 0xffffu;
+                    const double x = srow[e & 0x7fffu];
+                    s += (e & 0x8000u) ? -x : x; // s_jt = +-1: the reference's s += s_jt A(i, r_jt)
+                }
+                __stcs(orow + j, s);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // x = S y (nrhs columns, ld nrhs) via the row-sorted transpose: x[i] = sum over
 // entries (j,t) with r_jt = i, in ascending j (deterministic).
 __global__ void k_sparse_vec(uint64_t n, uint64_t nrhs, const int32_t* row_ptr, const int32_t* col_j,
@@ -309,6 +357,20 @@ void hh2_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* u1, const double
 
 void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs,
                             const double* a, uint64_t lda, double* out, uint64_t ldo) {
+    if (nnz == 4 && n <= static_cast<uint64_t>(SP4_THREADS) * SP4_Q && n % 2 == 0 && lda % 2 == 0 &&
+        (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
+        const size_t smem = n * sizeof(double);
+        static bool attr[16] = {};
+        if (!attr[ctx().device & 15]) {
+            RL_CUDA(cudaFuncSetAttribute(k_sparse_right4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SP4_THREADS * SP4_Q * 8));
+            attr[ctx().device & 15] = true;
+        }
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, ctx().sms));
+        k_sparse_right4<<<grid, SP4_THREADS, smem, stream()>>>(n, a, lda, rows, signs, out, ldo);
+        RL_LAUNCHED();
+        return;
+    }
     int rb = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(8, (160 * 1024) / (n * 8))));
     size_t smem = static_cast<size_t>(rb) * n * sizeof(double);
     if (smem > 200 * 1024)

@@ -237,3 +237,12 @@ def test_host_pointer_path_overlapped_upload_matches_device_path(rl):
     assert np.array_equal(x_host, dX.cpu().numpy())
     assert rep_host.attempt == rep_dev.attempt and rep_host.residual == rep_dev.residual
     assert rep_host.residual <= 1e-7
+
+
+@pytest.mark.parametrize("n", [999, 1000, 4096])
+def test_sparse_apply_right_bit_exact(rl, oracle, n):
+    """A S for the sparse +-1 multiplier against the C restatement, bit for bit (n = 999 takes
+    the row-staged kernel, even n <= 16384 the register-resident-S kernel)."""
+    rows, signs = oracle.sparse_pm1(n, 5, 6)
+    a = np.random.default_rng(n).standard_normal((n, n))
+    assert np.array_equal(rl.sparse_apply_right(rows, signs, a), oracle.sparse_apply_right(rows, signs, a))
