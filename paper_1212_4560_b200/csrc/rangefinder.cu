@@ -33,6 +33,31 @@ namespace {
 
 constexpr int KMAX = 128; // largest rho+ handled by the single-CTA small kernels
 
+// Small outputs (a Gram): one warp per output element, lane l sums slices l, l+32, ... and a
+// fixed shuffle tree combines them (deterministic; enough threads to pull the partials at HBM
+// rate where one thread per element left most SMs idle).
+__global__ void k_splitk_reduce_warp(uint64_t m, uint64_t n, int splits, const double* parts, double alpha,
+                                     double beta, double* c, uint64_t ldc) {
+    const uint64_t total = m * n;
+    const uint64_t e = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= total) // whole warps exit together (e is warp-uniform)
+        return;
+    double s = 0.0;
+    for (int p = lane; p < splits; p += 32)
+        s += parts[p * total + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        const uint64_t i = e / n, j = e % n;
+        double v = alpha * s;
+        if (beta != 0.0)
+            v = fma(beta, c[i * ldc + j], v);
+        c[i * ldc + j] = v;
+    }
+}
+
 __global__ void k_splitk_reduce(uint64_t m, uint64_t n, int splits, const double* parts, double alpha,
                                 double beta, double* c, uint64_t ldc) {
     uint64_t total = m * n;
@@ -701,7 +726,10 @@ void gemm_splitk(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double al
     const int used = static_cast<int>(cdiv(k, chunk));
     double* parts = ws<double>(WS_RF6, static_cast<uint64_t>(used) * m * n);
     gemm_splitk_parts(ta, tb, m, n, k, a, lda, b, ldb, parts, used, chunk);
-    k_splitk_reduce<<<cdiv(m * n, 256), 256, 0, stream()>>>(m, n, used, parts, alpha, beta, c, ldc);
+    if (m * n * 32 <= 4ULL * 1024 * 1024 && used >= 32)
+        k_splitk_reduce_warp<<<cdiv(m * n * 32, 256), 256, 0, stream()>>>(m, n, used, parts, alpha, beta, c, ldc);
+    else
+        k_splitk_reduce<<<cdiv(m * n, 256), 256, 0, stream()>>>(m, n, used, parts, alpha, beta, c, ldc);
     RL_LAUNCHED();
 }
 
