@@ -100,34 +100,52 @@ __device__ __forceinline__ void load_A(Smem& S, const double* __restrict__ Ag, i
     }
 }
 
-// X holds A on entry; on exit X holds W = A C (row-major).
+// X holds A on entry; on exit X holds W = A C (row-major).  Two passes over the output's
+// column halves (16 accumulators each instead of 32: the kernel's register peak, which sets
+// how many systems share an SM); W goes to registers first, then over A after a barrier.
 __device__ __forceinline__ void circ_product(Smem& S, uint64_t mask, int t) {
     const int lane = t & 31, warp = t >> 5, g = lane >> 2, q = lane & 3;
-    double acc[2][8][2];
+    double keep[2][4][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int half = 0; half < 2; ++half) {
+        double acc[2][4][2];
 #pragma unroll
-        for (int jb = 0; jb < 8; ++jb)
-            acc[i][jb][0] = acc[i][jb][1] = 0.0;
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int jb = 0; jb < 4; ++jb)
+                acc[i][jb][0] = acc[i][jb][1] = 0.0;
 #pragma unroll 4
-    for (int kk = 0; kk < N; kk += 4) {
-        const int k = kk + q;
-        const double a0 = S.X[(16 * warp + g) * XP + k];
-        const double a1 = S.X[(16 * warp + 8 + g) * XP + k];
+        for (int kk = 0; kk < N; kk += 4) {
+            const int k = kk + q;
+            const double a0 = S.X[(16 * warp + g) * XP + k];
+            const double a1 = S.X[(16 * warp + 8 + g) * XP + k];
 #pragma unroll
-        for (int jb = 0; jb < 8; ++jb) {
-            const double bf = sgn(mask, k - (8 * jb + g)); // C[k][8 jb + g]
-            dmma(acc[0][jb], a0, bf);
-            dmma(acc[1][jb], a1, bf);
+            for (int jb = 0; jb < 4; ++jb) {
+                const double bf = sgn(mask, k - (8 * (4 * half + jb) + g)); // C[k][8 jb' + g]
+                dmma(acc[0][jb], a0, bf);
+                dmma(acc[1][jb], a1, bf);
+            }
+        }
+        if (half == 0) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int jb = 0; jb < 4; ++jb) {
+                    keep[i][jb][0] = acc[i][jb][0];
+                    keep[i][jb][1] = acc[i][jb][1];
+                }
+        } else {
+            __syncthreads(); // every read of A is done
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int jb = 0; jb < 4; ++jb) {
+                    double* row = S.X + (16 * warp + 8 * i + g) * XP + 2 * q;
+                    *reinterpret_cast<double2*>(row + 8 * jb) = make_double2(keep[i][jb][0], keep[i][jb][1]);
+                    *reinterpret_cast<double2*>(row + 8 * (4 + jb)) = make_double2(acc[i][jb][0], acc[i][jb][1]);
+                }
         }
     }
-    __syncthreads(); // every read of A is done
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int jb = 0; jb < 8; ++jb)
-            *reinterpret_cast<double2*>(S.X + (16 * warp + 8 * i + g) * XP + 8 * jb + 2 * q) =
-                make_double2(acc[i][jb][0], acc[i][jb][1]);
 }
 
 // Blocked no-pivot LU of the 64 x 64 working matrix in S.X (row-major, genp.cpp:20-33 per
@@ -141,49 +159,37 @@ __device__ __forceinline__ bool lu_blocked(Smem& S, double floor, int t, double&
     const int lane = t & 31, warp = t >> 5;
 #pragma unroll 1
     for (int c0 = 0; c0 < N; c0 += 16) {
-        if (warp == 0) {
-            const int r0 = c0 + lane, r1 = c0 + 32 + lane;
-            const bool v0 = r0 < N, v1 = r1 < N;
-            double a0[16], a1[16], invs[16];
+        if (warp == 0) { // (a) the 16 x 16 diagonal block: lane l < 16 holds row c0 + l
+            const bool v = lane < 16;
+            const int r = c0 + (lane & 15);
+            double a[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                a0[j] = v0 ? S.X[r0 * XP + c0 + j] : 0.0;
-                a1[j] = v1 ? S.X[r1 * XP + c0 + j] : 0.0;
-            }
+            for (int j = 0; j < 16; ++j)
+                a[j] = v ? S.X[r * XP + c0 + j] : 0.0;
             double mn = S.pm[0], mx = S.pm[1];
             bool brk = S.flag != 0;
 #pragma unroll
             for (int kk = 0; kk < 16; ++kk) {
-                const double piv = __shfl_sync(0xffffffffu, a0[kk], kk);
+                const double piv = __shfl_sync(0xffffffffu, a[kk], kk);
                 const double inv = (piv == 0.0) ? 0.0 : __drcp_rn(piv);
-                invs[kk] = inv;
+                if (lane == 0)
+                    S.rcp[c0 + kk] = inv;
                 const double ap = fabs(piv);
                 mn = (c0 + kk == 0) ? ap : min_fold(mn, ap);
                 mx = (c0 + kk == 0) ? ap : max_fold(mx, ap);
                 brk |= ap < floor;
-                const bool b0 = v0 && lane > kk;
-                const double m0 = b0 ? a0[kk] * inv : 0.0;
-                const double m1 = v1 ? a1[kk] * inv : 0.0;
-                a0[kk] = b0 ? m0 : a0[kk];
-                a1[kk] = v1 ? m1 : a1[kk];
+                const bool below = v && lane > kk;
+                const double m = below ? a[kk] * inv : 0.0;
+                a[kk] = below ? m : a[kk];
 #pragma unroll
-                for (int l = kk + 1; l < 16; ++l) {
-                    const double u = __shfl_sync(0xffffffffu, a0[l], kk);
-                    a0[l] = fma(-m0, u, a0[l]);
-                    a1[l] = fma(-m1, u, a1[l]);
-                }
+                for (int l = kk + 1; l < 16; ++l)
+                    a[l] = fma(-m, __shfl_sync(0xffffffffu, a[l], kk), a[l]);
             }
+            if (v)
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if (v0)
-                    S.X[r0 * XP + c0 + j] = a0[j];
-                if (v1)
-                    S.X[r1 * XP + c0 + j] = a1[j];
-            }
+                for (int j = 0; j < 16; ++j)
+                    S.X[r * XP + c0 + j] = a[j];
             if (lane == 0) {
-#pragma unroll
-                for (int kk = 0; kk < 16; ++kk)
-                    S.rcp[c0 + kk] = invs[kk];
                 S.pm[0] = mn;
                 S.pm[1] = mx;
                 if (brk)
@@ -194,8 +200,28 @@ __device__ __forceinline__ bool lu_blocked(Smem& S, double floor, int t, double&
         const int nc = N - c0 - 16;
         if (nc == 0)
             break;
-        if (t < nc) { // U12: column c0 + 16 + t against the unit L11 (broadcast reads)
-            const int c = c0 + 16 + t;
+        // (b) one thread per row below the block (L21 = A21 U11^-1: the same multipliers and
+        // updates, in the same order, as eliminating the rows inside the pivot loop) and one
+        // per column right of it (U12 = L11^-1 A12), warps 0-1 and 2-3
+        if (t < nc) {
+            const int i = c0 + 16 + t;
+            double y[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                y[j] = S.X[i * XP + c0 + j];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const double m = y[k] * S.rcp[c0 + k];
+                y[k] = m;
+#pragma unroll
+                for (int l = k + 1; l < 16; ++l)
+                    y[l] = fma(-m, S.X[(c0 + k) * XP + c0 + l], y[l]);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                S.X[i * XP + c0 + j] = y[j];
+        } else if (t >= 64 && t - 64 < nc) {
+            const int c = c0 + 16 + (t - 64);
             double y[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -316,7 +342,7 @@ __device__ bool circ_singular(Smem& S, uint64_t mask, int t) {
 
 // One CTA per system; the raw arm and the whole redraw protocol (8 attempts on stream
 // sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) run in-kernel.
-__global__ void __launch_bounds__(THREADS, 4) k_batched_circ64(
+__global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs0, uint64_t seed,
     const uint64_t* __restrict__ sids, int refine, double* __restrict__ X, rl_precond_report* __restrict__ rep,
     int* __restrict__ status) {
