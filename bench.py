@@ -252,7 +252,9 @@ def run_config1(torch, rl, dev, dist, args, fp64_peak):
     for _ in range(reps):
         rl.randomized_genp(hA, hb, kind, rl.MulSide.RIGHT, 0, st)
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / reps, dist)
+    cpu1 = cpu_baseline_config1(hA, hb) if (not dist and not args.no_cpu_baseline) else None
     return {"workload": "config1: Gaussian-preconditioned GENP n=256, 1 RHS, MulSide::Right (latency)",
+            "cpu_baseline": cpu1,
             "value_us_per_solve": round(ms * 1e3, 2), "attempts": rep.attempts_drawn,
             "tflops_executed": round(rep.attempts_drawn * FLOPS1 / (ms * 1e-3) / 1e12, 5),
             "flop_per_attempt": FLOPS1, "backward_error": bwd, "residual": rep.residual,
@@ -366,6 +368,11 @@ def run_config4(torch, rl, dev, dist, rank, world, args, fp64_peak):
     torch.cuda.synchronize()
     ms4 = max_over_ranks(e0.elapsed_time(e1) / k4, dist)
     tf4 = FLOPS4 / (ms4 * 1e-3) / 1e12
+    cpu4 = None
+    if world == 1 and not args.no_cpu_baseline:
+        H = torch.empty(N4, K4, dtype=torch.float64, device=dev)
+        rl.dev_gaussian_matrix(H, 0.0, 1.0, st)
+        cpu4 = cpu_baseline_config4(A[:2048].cpu().numpy(), H.cpu().numpy())
     del A, Q, B
     out = {"workload": "config4: range finder Y = A H, qr_positive(Y), B = Q^T A, numerical_rank(B, 1e-8); "
                        "A 16384 x 4096, rho+ = 72",
@@ -376,6 +383,8 @@ def run_config4(torch, rl, dev, dist, rank, world, args, fp64_peak):
                         "roofline_ms": round(FLOPS4 / (fp64_peak * 1e12) * 1e3, 4)}}
     if resid is not None:
         out["resid_fro"] = resid
+    if cpu4 is not None:
+        out["cpu_baseline"] = cpu4
     return out
 
 
@@ -515,6 +524,9 @@ def run_ours(args, dist, rank, world, local_rank):
     bwd2 = float((res2.norm(dim=1) / (A2.flatten(1).norm(dim=1) * x2.norm(dim=1))).max())
     fp64_frac2 = BATCH2 * FLOPS2_PER_SYS / (ms2 * 1e-3) / 1e12 / fp64_peak
     hbm_frac2 = BATCH2 * BYTES2_PER_SYS / (ms2 * 1e-3) / 1e9 / hbm_peak
+    cpu2 = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu2 = cpu_baseline_config2(A2[:256].cpu().numpy(), b2[:256].cpu().numpy())
 
     # ---- config 4: the randomized range finder (third line) ----
     rf = run_config4(torch, rl, dev, dist, rank, world, args, fp64_peak)
@@ -562,7 +574,8 @@ def run_ours(args, dist, rank, world, local_rank):
                     "backward_error_max": bwd2,
                     "roofline": {"bound": "fp64", "frac_fp64": round(fp64_frac2, 4),
                                  "frac_hbm": round(hbm_frac2, 4), "peak_fp64": round(fp64_peak, 3),
-                                 "peak_hbm_gbs": round(hbm_peak, 1)}},
+                                 "peak_hbm_gbs": round(hbm_peak, 1)},
+                    "cpu_baseline": cpu2},
         "range_finder": rf,
         "config1": c1,
         "config5": c5,
@@ -606,6 +619,64 @@ def cpu_baseline_config3(threads: int = 1):
             "sample": f"Matrix::multiply {rows_per * threads}x{N3} slab x {N3}^2 G ({threads} thread(s)) "
                       f"+ genp_factor n={nl} (1 thread); {t_mm + t_lu:.2f} s",
             "host": _host_cpu()}
+
+
+def _ref_lib():
+    from oracle.pyoracle import Reference, Restated
+    kind = "reference" if Reference.available() else "port"
+    return kind, (Reference() if kind == "reference" else Restated())
+
+
+def cpu_baseline_config1(A, b):
+    """The reference's randomized_genp (Gaussian, Right, refine 0; its contrast arm included,
+    as the reference always runs it) on the config-1 system, 1 thread: us per solve."""
+    kind, lib = _ref_lib()
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        lib.randomized_genp(A, b, "gaussian", "right", 0, seed=SEED, sid=15)
+    us = (time.perf_counter() - t0) * 1e6 / reps
+    return {"value": round(us, 1), "unit": "us/solve", "cores": 1, "kind": kind,
+            "sample": f"randomized_genp n=256 x {reps} (contrast arm included)"}
+
+
+def cpu_baseline_config2(A, b, nsys: int = 256):
+    """The reference's randomized_genp (CirculantSign, Right) per system, as table1_genp loops it,
+    on the first `nsys` config-2 systems: 1 thread and all host threads (solves/s)."""
+    kind, lib = _ref_lib()
+
+    def run(lo, hi):
+        for t in range(lo, hi):
+            lib.randomized_genp(A[t], b[t], "circulant_sign", "right", 0, seed=SEED, sid=7 + t)
+    t0 = time.perf_counter()
+    run(0, nsys)
+    one = nsys / (time.perf_counter() - t0)
+    th = os.cpu_count() or 1
+    chunks = [(i * nsys // th, (i + 1) * nsys // th) for i in range(th)]
+    t0 = time.perf_counter()
+    ts = [threading.Thread(target=run, args=c) for c in chunks]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    allc = nsys / (time.perf_counter() - t0)
+    return {"value": round(allc, 1), "unit": "solves/s", "cores": th, "kind": kind,
+            "value_1_thread": round(one, 1),
+            "sample": f"{nsys} systems, randomized_genp per system (contrast arm included)"}
+
+
+def cpu_baseline_config4(A_slab, H):
+    """The reference's Matrix::multiply for Y = A H on a row slab of the config-4 A (the
+    dominant CPU cost; the QR and SVD are Eigen in the reference and not compiled here):
+    TFLOP/s, 1 thread."""
+    kind, lib = _ref_lib()
+    t0 = time.perf_counter()
+    lib.matmul(A_slab, H)
+    dt = time.perf_counter() - t0
+    fl = 2.0 * A_slab.shape[0] * A_slab.shape[1] * H.shape[1]
+    return {"value": round(fl / dt / 1e12, 6), "unit": "TFLOP/s", "cores": 1, "kind": kind,
+            "sample": f"Matrix::multiply {A_slab.shape[0]}x{A_slab.shape[1]} slab x H {H.shape[0]}x{H.shape[1]}; "
+                      f"{dt:.2f} s"}
 
 
 def _host_cpu():
