@@ -96,7 +96,9 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // memory (k padded to KP = 8 ceil(k/8) with an identity corner), 8-column blocks J, three
 // barriers per block:
 //   A  warp 0 factors the 8 x 8 diagonal block in registers (lane c holds column c, pivot
-//      rows by shuffle) and inverts it (X_JJ);
+//      rows by shuffle) and inverts it (X_JJ) — for blocks after the first, inside the
+//      previous block's phase C (lookahead: it first applies that block's update to its own
+//      8 x 8, then factors, while warps 1-15 do the rest of C);
 //   B  one thread per trailing column solves the block's panel row R_J,rest; the others form
 //      T = R_0:J,J X_JJ;
 //   C  rank-8 update of the trailing upper triangle; X_0:J,J = -X_0:J,0:J T.
@@ -105,6 +107,55 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // g <- R (upper, zeros below), rinv <- R^-1.  *bad is sticky: a kernel whose earlier pass
 // failed returns at once; a non-positive pivot sets it.
 constexpr int CH_T = 512;
+// Warp 0: factor the 8 x 8 diagonal block at (c0, c0) of W in registers (lane c holds column
+// c, pivot rows by shuffle) -> R_JJ (upper) and rdiag = 1 / R_tt, then X_JJ = R_JJ^-1 by back
+// substitution, stored transposed in the free lower triangle (X_rc at W[c0+c][c0+r]).
+__device__ __forceinline__ void chol_diag8(double* W, int P, int c0, double* rdiag, int lane, int* s_bad) {
+    const int c = lane & 7;
+    double col[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        col[r] = W[(c0 + r) * P + c0 + c];
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const double d = __shfl_sync(0xffffffffu, col[t], t);
+        ok = ok && (d > 0.0);
+        const double inv = rsqrt_nr(d); // 1 / R_tt
+        const double rtc = (c == t) ? d * inv : col[t] * inv; // R_{t,c} (c >= t)
+        col[t] = rtc;
+        if (c == t)
+            rdiag[c0 + t] = inv;
+#pragma unroll
+        for (int r = t + 1; r < 8; ++r) {
+            const double rtr = __shfl_sync(0xffffffffu, rtc, r); // R_{t,r}
+            col[r] = fma(-rtr, rtc, col[r]);
+        }
+    }
+    if (lane < 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (r <= c)
+                W[(c0 + r) * P + c0 + c] = col[r];
+    }
+    __syncwarp();
+    if (lane < 8) {
+        double x[8];
+#pragma unroll
+        for (int r = 7; r >= 0; --r) {
+            double v = 0.0;
+#pragma unroll
+            for (int l = r + 1; l < 8; ++l)
+                if (l <= c)
+                    v = fma(W[(c0 + r) * P + c0 + l], x[l], v);
+            x[r] = (r == c) ? rdiag[c0 + c] : (r < c ? -v * rdiag[c0 + r] : 0.0);
+            if (r < c)
+                W[(c0 + c) * P + c0 + r] = x[r];
+        }
+    }
+    if (lane == 0 && !ok)
+        *s_bad = 1;
+}
 __global__ void __launch_bounds__(CH_T) k_chol_inv(int k, double* g, const double* shift_part, int nshift,
                                                    double shift_coef, double* rinv, int* bad) {
     extern __shared__ double W[]; // KP x (KP + 1)
@@ -140,61 +191,16 @@ __global__ void __launch_bounds__(CH_T) k_chol_inv(int k, double* g, const doubl
         W[i * P + l] = v;
     }
     __syncthreads();
+    if (warp == 0)
+        chol_diag8(W, P, 0, rdiag, lane, &s_bad);
+    __syncthreads();
+    if (s_bad) { // uniform
+        if (tid == 0)
+            *bad = 1;
+        return;
+    }
     for (int c0 = 0; c0 < KP; c0 += 8) {
-        // ---- A: R_JJ and X_JJ
-        if (warp == 0) {
-            const int c = lane & 7;
-            double col[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r)
-                col[r] = W[(c0 + r) * P + c0 + c];
-            bool ok = true;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const double d = __shfl_sync(0xffffffffu, col[t], t);
-                ok = ok && (d > 0.0);
-                const double inv = rsqrt_nr(d); // 1 / R_tt
-                const double rtc = (c == t) ? d * inv : col[t] * inv; // R_{t,c} (c >= t)
-                col[t] = rtc;
-                if (c == t)
-                    rdiag[c0 + t] = inv;
-#pragma unroll
-                for (int r = t + 1; r < 8; ++r) {
-                    const double rtr = __shfl_sync(0xffffffffu, rtc, r); // R_{t,r}
-                    col[r] = fma(-rtr, rtc, col[r]);
-                }
-            }
-            if (lane < 8) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r)
-                    if (r <= c)
-                        W[(c0 + r) * P + c0 + c] = col[r];
-            }
-            __syncwarp();
-            if (lane < 8) { // X_JJ column c: back substitution, X_rc at W[c0+c][c0+r] (r < c)
-                double x[8];
-#pragma unroll
-                for (int r = 7; r >= 0; --r) {
-                    double v = 0.0;
-#pragma unroll
-                    for (int l = r + 1; l < 8; ++l)
-                        if (l <= c)
-                            v = fma(W[(c0 + r) * P + c0 + l], x[l], v);
-                    x[r] = (r == c) ? rdiag[c0 + c] : (r < c ? -v * rdiag[c0 + r] : 0.0);
-                    if (r < c)
-                        W[(c0 + c) * P + c0 + r] = x[r];
-                }
-            }
-            if (lane == 0 && !ok)
-                s_bad = 1;
-        }
-        __syncthreads();
-        if (s_bad) { // uniform
-            if (tid == 0)
-                *bad = 1;
-            return;
-        }
-        // ---- B: panel row of R; T = R_0:J,J X_JJ
+        // ---- B: panel row of R; T = R_0:J,J X_JJ   (R_JJ, X_JJ: the previous step's lookahead)
         const int rest = KP - c0 - 8;
         if (tid < rest) { // R_{c0+t, l} = (W_{c0+t, l} - sum_{s<t} R_{c0+s, c0+t} R_{c0+s, l}) / R_tt
             const int l = c0 + 8 + tid;
@@ -221,40 +227,64 @@ __global__ void __launch_bounds__(CH_T) k_chol_inv(int k, double* g, const doubl
             T[c][l] = v;
         }
         __syncthreads();
-        // ---- C: trailing update; X_0:J,J
-        if (rest > 0) {
-            const int ty = tid >> 5, tx = tid & 31;
-            for (int i = c0 + 8 + ty; i < KP; i += 16) {
-                double pi[8];
+        // ---- C: warp 0 brings the next diagonal block up to date and factors it (lookahead);
+        // warps 1-15 update the rest of the trailing triangle and form X_0:J,J
+        if (warp == 0) {
+            if (rest > 0) {
+                const int l = c0 + 8 + (lane & 7);
 #pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    pi[t] = W[(c0 + t) * P + i];
-                for (int l = c0 + 8 + tx; l < KP; l += 32) {
-                    if (l < i)
-                        continue;
-                    double v = W[i * P + l];
+                for (int r = 0; r < 2; ++r) {
+                    const int i = c0 + 8 + (lane >> 3) + 4 * r;
+                    if (i <= l) {
+                        double v = W[i * P + l];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            v = fma(-W[(c0 + t) * P + i], W[(c0 + t) * P + l], v);
+                        W[i * P + l] = v;
+                    }
+                }
+                __syncwarp();
+                chol_diag8(W, P, c0 + 8, rdiag, lane, &s_bad);
+            }
+        } else {
+            const int nd = c0 + 16; // the next diagonal block [c0 + 8, c0 + 16)^2 is warp 0's
+            if (rest > 0) {
+                for (int i = c0 + 8 + (warp - 1); i < KP; i += 15) {
+                    double pi[8];
 #pragma unroll
                     for (int t = 0; t < 8; ++t)
-                        v = fma(-pi[t], W[(c0 + t) * P + l], v);
-                    W[i * P + l] = v;
+                        pi[t] = W[(c0 + t) * P + i];
+                    const int lstart = i < nd ? nd : i; // upper triangle, minus warp 0's block
+                    for (int l = lstart + ((lane - lstart) & 31); l < KP; l += 32) {
+                        double v = W[i * P + l];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            v = fma(-pi[t], W[(c0 + t) * P + l], v);
+                        W[i * P + l] = v;
+                    }
                 }
             }
-        }
-        for (int e = tid; e < 8 * c0; e += CH_T) { // X_{i, c0+c} = -sum_{l=i}^{c0-1} X_il T[l][c]
-            const int i = e >> 3, c = e & 7;
-            double v0 = rdiag[i] * T[c][i], v1 = 0.0, v2 = 0.0, v3 = 0.0;
-            int l = i + 1;
-            for (; l + 3 < c0; l += 4) { // four chains: the loads pipeline
-                v0 = fma(W[l * P + i], T[c][l], v0);
-                v1 = fma(W[(l + 1) * P + i], T[c][l + 1], v1);
-                v2 = fma(W[(l + 2) * P + i], T[c][l + 2], v2);
-                v3 = fma(W[(l + 3) * P + i], T[c][l + 3], v3);
+            for (int e = tid - 32; e < 8 * c0; e += CH_T - 32) { // X_{i, c0+c} = -sum_{l=i}^{c0-1} X_il T[l][c]
+                const int i = e >> 3, c = e & 7;
+                double v0 = rdiag[i] * T[c][i], v1 = 0.0, v2 = 0.0, v3 = 0.0;
+                int l = i + 1;
+                for (; l + 3 < c0; l += 4) { // four chains: the loads pipeline
+                    v0 = fma(W[l * P + i], T[c][l], v0);
+                    v1 = fma(W[(l + 1) * P + i], T[c][l + 1], v1);
+                    v2 = fma(W[(l + 2) * P + i], T[c][l + 2], v2);
+                    v3 = fma(W[(l + 3) * P + i], T[c][l + 3], v3);
+                }
+                for (; l < c0; ++l)
+                    v0 = fma(W[l * P + i], T[c][l], v0);
+                W[(c0 + c) * P + i] = -((v0 + v1) + (v2 + v3));
             }
-            for (; l < c0; ++l)
-                v0 = fma(W[l * P + i], T[c][l], v0);
-            W[(c0 + c) * P + i] = -((v0 + v1) + (v2 + v3));
         }
         __syncthreads();
+        if (s_bad) { // uniform
+            if (tid == 0)
+                *bad = 1;
+            return;
+        }
     }
     for (int e = tid; e < k * k; e += CH_T) {
         const int i = e / k, l = e - i * k;
