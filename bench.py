@@ -283,6 +283,41 @@ def make_config5_inputs(torch, dev):
     return A, B
 
 
+def hbm_reference_peak(hbm_same_run):
+    """HBM roofline denominator: MEASURED_PEAKS.json's driver-measured copy bandwidth when the
+    file is present, else this run's own copy probe."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (torch copy)"
+    except (OSError, KeyError, ValueError):
+        return hbm_same_run, "same-run copy probe (rl_probe_peaks)"
+
+
+def time_multiplier_apply(torch, rl, dev, dist, tag, A, mult_bytes, hbm_peak):
+    """The structured multiplier stage alone (the HBM-bound kernels of config 5): A S with its
+    gather plan (k_sparse_plan + k_sparse_right4), or A H1 H2 (k_hh2_rowdots + k_hh2_apply),
+    at n = 16384 through the device C-ABI; A (2 GiB) and the output exceed L2, so no flush
+    is needed between calls.  Algorithmic bytes: 2 n^2 8 (sparse) / 3 n^2 8 (pair)."""
+    n = A.shape[0]
+    out = torch.empty_like(A)
+    if tag == rl.MultiplierTag.SPARSE_SIGN:
+        rows_h, signs_h = rl.sparse_sign(n, rl.RngStream(SEED, 56))
+        rows, signs = torch.from_numpy(rows_h).to(dev), torch.from_numpy(signs_h).to(dev)
+        fn = lambda: rl.dev_sparse_apply_right(rows, signs, A, out)  # noqa: E731
+        kernels = "k_sparse_plan + k_sparse_right4"
+    else:
+        u = torch.from_numpy(rl.rng_draws(rl.RngStream(SEED, 57), "sign", 2 * n)).to(dev)
+        u1, u2 = u[:n].contiguous(), u[n:].contiguous()
+        fn = lambda: rl.dev_householder_pair_apply_right(u1, u2, A, out)  # noqa: E731
+        kernels = "k_hh2_rowdots + k_hh2_apply"
+    ms, _ = _timed(torch, fn, 3, 20, dist)
+    peak, src = hbm_reference_peak(hbm_peak)
+    gbs = mult_bytes / (ms * 1e-3) / 1e9
+    del out
+    return {"kernels": kernels, "ms": round(ms, 4), "achieved_gbs": round(gbs, 1), "peak_gbs": peak,
+            "frac": round(gbs / peak, 4), "peak_source": src, "frac_same_run_copy": round(gbs / hbm_peak, 4)}
+
+
 def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak):
     """Config 5: n = 16384, 8 RHS, MulSide::Right with the orthogonal Householder pair, the
     sparse +-1 and the Gaussian multipliers (contrast arm skipped as in config 3).  Short runs
@@ -307,6 +342,7 @@ def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak):
         else:
             arm["lu_tflops_executed"] = round(rep.attempts_drawn * FLOPS5_LU / (ms * 1e-3) / 1e12, 3)
             arm["multiplier_bytes_per_apply"] = mult_bytes
+            arm["multiplier_apply"] = time_multiplier_apply(torch, rl, dev, dist, tag, A, mult_bytes, hbm_peak)
         out[name] = arm
     del A, B, X
     torch.cuda.empty_cache()

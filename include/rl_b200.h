@@ -120,6 +120,13 @@ rl_status rl_sparse_sign(uint64_t n, int nnz, uint64_t seed, uint64_t stream_id,
  * randomized_genp's Right side with RL_SPARSE_SIGN (genp.cpp:175-180 applies M on the right). */
 rl_status rl_sparse_apply_right(uint64_t n, int nnz, const int32_t* rows, const double* signs,
                                 const double* a, double* out);
+/* Device-pointer variants of the two matrix-free right multipliers (calling thread's stream):
+ * out = A S (sparse +-1, d_rows/d_signs n x nnz) and out = A H1 H2 (Householder pair,
+ * H_i = I - (2/n) u_i u_i^T, d_u1/d_u2 n signs).  out may alias a only for the pair. */
+rl_status rl_dev_sparse_apply_right(uint64_t n, int nnz, const int32_t* d_rows, const double* d_signs,
+                                    const double* d_a, double* d_out);
+rl_status rl_dev_householder_pair_apply_right(uint64_t n, const double* d_u1, const double* d_u2,
+                                              const double* d_a, double* d_out);
 
 /* -------------------------------------------- matrix.hpp (matrix.cpp) ---- */
 /* Matrix::multiply(const Matrix&) (matrix.cpp:86-102): C(m x n) = A(m x k) B(k x n). */

@@ -543,15 +543,24 @@ void rlo_hh2_apply_vec(uint64_t n, const double* u1, const double* u2, const dou
     free(v);
 }
 
-/* NEW: (A S)(i,j) = sum_t s_jt A(i, r_jt), t ascending. */
+/* Pairwise sum of v[0..m): sum(v[0:h]) + sum(v[h:m]), h = ceil(m / 2) — the defined order
+ * of the sparse product (for nnz = 4: (v0 + v1) + (v2 + v3)). */
+static double rlo_pairwise(const double* v, int m) {
+    if (m == 1)
+        return v[0];
+    int h = (m + 1) / 2;
+    return rlo_pairwise(v, h) + rlo_pairwise(v + h, m - h);
+}
+
+/* NEW: (A S)(i,j) = sum_t s_jt A(i, r_jt), summed pairwise over t (rlo_pairwise). */
 void rlo_sparse_apply_right(uint64_t n, int nnz, const int32_t* rows, const double* signs,
                             const double* a, double* out) {
+    double v[64];
     for (uint64_t i = 0; i < n; ++i)
         for (uint64_t j = 0; j < n; ++j) {
-            double s = 0.0;
             for (int t = 0; t < nnz; ++t)
-                s += signs[j * nnz + t] * a[i * n + (uint64_t)rows[j * nnz + t]];
-            out[i * n + j] = s;
+                v[t] = signs[j * nnz + t] * a[i * n + (uint64_t)rows[j * nnz + t]];
+            out[i * n + j] = rlo_pairwise(v, nnz);
         }
 }
 

@@ -33,7 +33,8 @@ __all__ = [
     "multiply", "circ_mul", "circulant_multiply_matrix", "genp_factor", "genp_solve", "randomized_genp",
     "randomized_genp_batched", "approx_basis", "qr_positive", "project_onto_basis", "numerical_rank",
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
-    "dev_randomized_genp_batched", "dev_range_finder", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
+    "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
+    "dev_householder_pair_apply_right", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
     "box_muller_fast_check", "launch_count", "LIB_PATH",
 ]
 
@@ -203,6 +204,8 @@ def lib() -> C.CDLL:
         "rl_householder_pair_signs": [u64, u64, u64, _d, _d],
         "rl_sparse_sign": [u64, cint, u64, u64, _i32a, _d],
         "rl_sparse_apply_right": [u64, cint, _i32a, _d, _d, _d],
+        "rl_dev_sparse_apply_right": [u64, cint, vp, vp, vp, vp],
+        "rl_dev_householder_pair_apply_right": [u64, vp, vp, vp, vp],
         "rl_matmul": [u64, u64, u64, _d, _d, _d],
         "rl_dev_gemm": [cint, cint, u64, u64, u64, dbl, vp, u64, vp, u64, dbl, vp, u64],
         "rl_circ_mul": [u64, _d, _d, _d],
@@ -540,6 +543,24 @@ def sparse_apply_right(rows, signs, a) -> np.ndarray:
     out = np.empty_like(a)
     _chk(lib().rl_sparse_apply_right(n, nnz, rows, signs, a, out))
     return out
+
+
+def dev_sparse_apply_right(rows, signs, a, out) -> None:
+    """out = A S on device tensors (rows int32 n x nnz, signs/a/out float64)."""
+    _bind_stream()
+    n, nnz = rows.shape
+    if a.shape != (n, n) or out.shape != (n, n) or signs.shape != rows.shape:
+        raise DimensionMismatch("sparse_apply_right: shape mismatch")
+    _chk(lib().rl_dev_sparse_apply_right(n, nnz, _ptr(rows), _ptr(signs), _ptr(a), _ptr(out)))
+
+
+def dev_householder_pair_apply_right(u1, u2, a, out) -> None:
+    """out = A H1 H2 on device tensors, H_i = I - (2/n) u_i u_i^T (u_i +-1 vectors)."""
+    _bind_stream()
+    n = a.shape[0]
+    if a.shape != (n, n) or out.shape != (n, n) or u1.shape[0] != n or u2.shape[0] != n:
+        raise DimensionMismatch("householder_pair_apply_right: shape mismatch")
+    _chk(lib().rl_dev_householder_pair_apply_right(n, _ptr(u1), _ptr(u2), _ptr(a), _ptr(out)))
 
 
 def dev_qr_positive(y, q, r) -> None:

@@ -36,6 +36,8 @@ void gemm_splitk(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double al
 int splits_for(uint64_t m, uint64_t n, uint64_t k);
 void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs, const double* a,
                             uint64_t lda, double* out, uint64_t ldo);
+void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
+                         double s12, double* out, uint64_t ldo);
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r);
 std::vector<double> small_singular_values(int k, const double* d_a);
 double sumsq_dev(uint64_t count, const double* x);
@@ -350,6 +352,31 @@ rl_status rl_sparse_apply_right(uint64_t n, int nnz, const int32_t* rows, const 
     double* dout = ws<double>(WS_H1, n * n);
     sparse_apply_right_dev(n, nnz, dr, ds, da, n, dout, n);
     download(out, dout, n * n);
+    API_END
+}
+
+rl_status rl_dev_sparse_apply_right(uint64_t n, int nnz, const int32_t* d_rows, const double* d_signs,
+                                    const double* d_a, double* d_out) {
+    API_BEGIN
+    require_positive(n, n, "sparse_apply_right");
+    if (nnz < 1 || nnz > 8 || static_cast<uint64_t>(nnz) > n)
+        fail(RL_INVALID_ARGUMENT, "sparse_apply_right: need 1 <= nnz <= min(8, n)");
+    sparse_apply_right_dev(n, nnz, d_rows, d_signs, d_a, n, d_out, n);
+    API_END
+}
+
+rl_status rl_dev_householder_pair_apply_right(uint64_t n, const double* d_u1, const double* d_u2,
+                                              const double* d_a, double* d_out) {
+    API_BEGIN
+    require_positive(n, n, "householder_pair_apply_right");
+    // s12 = u1^T u2: an exact integer for +-1 entries (as randomized_genp's draw computes it)
+    std::vector<double> h1(n), h2(n);
+    download(h1.data(), d_u1, n);
+    download(h2.data(), d_u2, n);
+    double s12 = 0.0;
+    for (uint64_t i = 0; i < n; ++i)
+        s12 += h1[i] * h2[i];
+    hh2_apply_right_dev(n, d_a, n, d_u1, d_u2, s12, d_out, n);
     API_END
 }
 

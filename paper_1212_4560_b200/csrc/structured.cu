@@ -11,6 +11,8 @@
 //    double2 loads, no tensor work — an HBM-bound kernel.
 //  * NEW sparse +-1 S (nnz per column): (A S)(i,j) = sum_t s_jt A(i, r_jt), a row-tiled
 //    gather (row of A in shared memory, index/sign table from L2): 2 n^2 doubles.
+#include <cstdio>
+
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -128,6 +130,21 @@ __global__ void k_hh2_vec(uint64_t n, uint64_t nrhs, const double* u1, const dou
         x[i * nrhs + col] = x[i * nrhs + col] - (c * d1) * u1[i];
 }
 
+// The sparse product's defined summation order (oracle rlo_pairwise): sum(v[0:h]) +
+// sum(v[h:m]), h = ceil(m / 2); for nnz = 4 that is (v0 + v1) + (v2 + v3).
+__device__ __forceinline__ double pairwise8(const double (&v)[8], int m) {
+    switch (m) {
+    case 1: return v[0];
+    case 2: return v[0] + v[1];
+    case 3: return (v[0] + v[1]) + v[2];
+    case 4: return (v[0] + v[1]) + (v[2] + v[3]);
+    case 5: return ((v[0] + v[1]) + v[2]) + (v[3] + v[4]);
+    case 6: return ((v[0] + v[1]) + v[2]) + ((v[3] + v[4]) + v[5]);
+    case 7: return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + v[6]);
+    default: return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+    }
+}
+
 // (A S)(i,j) = sum_t s_jt A(i, r_jt): one CTA per row block of RB rows staged in smem
 constexpr int SP_THREADS = 512;
 __global__ void __launch_bounds__(SP_THREADS) k_sparse_right(uint64_t n, int nnz, const double* __restrict__ a,
@@ -152,10 +169,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_sparse_right(uint64_t n, int nnz
             sg[t] = signs[j * nnz + t];
         }
         for (int r = 0; r < nr; ++r) {
-            double s = 0.0;
+            double v[8];
             for (int t = 0; t < nnz; ++t)
-                s += sg[t] * srow[r * n + idx[t]];
-            out[(r0 + r) * ldo + j] = s;
+                v[t] = sg[t] * srow[r * n + idx[t]];
+            out[(r0 + r) * ldo + j] = pairwise8(v, nnz);
         }
     }
 }
@@ -165,47 +182,262 @@ __global__ void __launch_bounds__(SP_THREADS) k_sparse_right(uint64_t n, int nnz
 // (15-bit row | sign bit), two per register — and stream the rows of A through shared memory,
 // so every byte of A and of the output crosses HBM once and S is read once per CTA (the kernel
 // above re-reads S from L2 for every row: 786 KB per 128 KB row).  Same summation order.
-constexpr int SP4_THREADS = 512, SP4_Q = 32;
-__global__ void __launch_bounds__(SP4_THREADS, 1) k_sparse_right4(uint64_t n, const double* __restrict__ a,
-                                                                  uint64_t lda, const int32_t* __restrict__ rows,
-                                                                  const double* __restrict__ signs,
-                                                                  double* __restrict__ out, uint64_t ldo) {
-    extern __shared__ __align__(16) double srow[]; // n
-    const int t = threadIdx.x;
-    uint32_t pk[SP4_Q * 2]; // output q: entries (2q, 2q+1) -> pk[2q] lo/hi, (2q+2, 2q+3) -> pk[2q+1]
+constexpr int SP4_THREADS = 512, SP4_Q = 32, SP4_CH = 1024, SP4_SLOTS = 27, SP4_GROUP = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// Gather plan for k_sparse_right4.  A warp's 64-bit shared loads are served per half-warp;
+// 16 random row indices collide on the 16 eight-byte bank pairs (index mod 16) in ~3.1
+// wavefronts per half-warp instead of 1.  The gathers can be regrouped without touching the
+// result: inside each (warp, q) group of 32 output columns, the lanes l and l ^ 16 may trade
+// columns (the store stays inside the same 256 B), and a column's four entries may be gathered
+// in any order of the symmetry group of (v0 + v1) + (v2 + v3) (swap inside either pair, swap
+// the pairs: 8 orders, all giving the same bits).  One thread per group chooses, pair by pair,
+// the trade and the orders that add the fewest same-bank-pair collisions to what the group
+// already placed (~2.1 instead of ~3.1 wavefronts per half-warp, 33% fewer).  Slot (q, t) = 4 x
+// 16 bits in gather order: row (14 bits) | trade bit (entry 2 only) | sign.
+constexpr int SPP_GROUPS = 4; // groups per 32-thread CTA; lane o = t & 7 evaluates gather order o
+__global__ void __launch_bounds__(32) k_sparse_plan(uint64_t n, const int32_t* __restrict__ rows,
+                                                    const double* __restrict__ signs, uint32_t* __restrict__ plan) {
+    __shared__ uint8_t cnt[SPP_GROUPS][2 * 4 * 16]; // [half][gather][bank pair] per group
+    __shared__ uint8_t cls[SPP_GROUPS][32 * 4];     // bank pair of entry e of the group's column c
+    __shared__ uint8_t pick[SPP_GROUPS][32];        // lane l: column << 3 | order
+    const int t = threadIdx.x, g = t >> 3, o = t & 7;
+    const int grp = blockIdx.x * SPP_GROUPS + g; // (warp, q) = (grp % 16, grp / 16)
+    const int warp = grp % (SP4_THREADS / 32), q = grp / (SP4_THREADS / 32);
+    const uint64_t col0 = static_cast<uint64_t>(q) * SP4_THREADS + warp * 32;
+    for (int c = o; c < 2 * 4 * 16; c += 8)
+        cnt[g][c] = 0;
+    for (int c = o; c < 32 * 4; c += 8)
+        cls[g][c] = (col0 + c / 4 < n) ? static_cast<uint8_t>(rows[col0 * 4 + c] & 15) : 0;
+    __syncwarp();
+    // gather order o (bit 0: swap v0/v1, bit 1: swap v2/v3, bit 2: swap the pairs): gather u
+    // reads entry ord(o, u) — the 8 orders that leave (v0 + v1) + (v2 + v3) unchanged
+    auto ord = [](uint32_t oo, int u) -> uint32_t {
+        const uint32_t e = static_cast<uint32_t>(u) ^ ((oo & 4u) >> 1);
+        return e ^ ((e < 2u ? oo : (oo >> 1)) & 1u);
+    };
+    // (collisions added << 3) | order, minimised over the group's 8 lanes
+    auto best_ord = [&](int c, int h, bool valid) -> uint32_t {
+        uint32_t v = 0;
 #pragma unroll
-    for (int q = 0; q < SP4_Q; ++q) {
-        const uint64_t j = t + static_cast<uint64_t>(q) * SP4_THREADS;
+        for (int u = 0; u < 4; ++u)
+            v += cnt[g][(h * 4 + u) * 16 + cls[g][c * 4 + ord(o, u)]];
+        uint32_t b = valid ? (v << 3) | static_cast<uint32_t>(o) : 0u;
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1)
+            b = min(b, __shfl_xor_sync(0xffffffffu, b, m));
+        return b;
+    };
+    auto place = [&](int c, int h, uint32_t oo, int d, bool valid) { // lanes 0..3: gather u = lane
+        __syncwarp();
+        if (valid && o < 4) {
+            const int i = (h * 4 + o) * 16 + cls[g][c * 4 + ord(oo, o)];
+            cnt[g][i] = static_cast<uint8_t>(cnt[g][i] + d);
+        }
+        __syncwarp();
+    };
+    for (int p = 0; p < 16; ++p) {
+        uint32_t o_lo[2] = {0, 0}, o_hi[2] = {0, 0}, cost[2] = {0, 0};
+        const bool two = col0 + p + 16 < n; // a pair with a missing column keeps its lanes
+        for (int sw = 0; sw < 2; ++sw) {     // uniform trip count: shuffles need the whole warp
+            const int c_lo = sw ? p + 16 : p, c_hi = sw ? p : p + 16; // column of lane p / p + 16
+            const bool ok = sw == 0 || two;
+            const bool v_lo = ok && col0 + c_lo < n, v_hi = ok && col0 + c_hi < n;
+            uint32_t b = best_ord(c_lo, 0, v_lo);
+            o_lo[sw] = b & 7u;
+            uint32_t v = b >> 3;
+            place(c_lo, 0, o_lo[sw], 1, v_lo);
+            b = best_ord(c_hi, 1, v_hi);
+            o_hi[sw] = b & 7u;
+            v += b >> 3;
+            place(c_lo, 0, o_lo[sw], -1, v_lo);
+            cost[sw] = ok ? v : 0xffffffffu;
+        }
+        const int sw = cost[1] < cost[0] ? 1 : 0;
+        const int c_lo = sw ? p + 16 : p, c_hi = sw ? p : p + 16;
+        place(c_lo, 0, o_lo[sw], 1, col0 + c_lo < n);
+        place(c_hi, 1, o_hi[sw], 1, col0 + c_hi < n);
+        if (o == 0) {
+            pick[g][p] = static_cast<uint8_t>(c_lo << 3 | o_lo[sw]);
+            pick[g][p + 16] = static_cast<uint8_t>(c_hi << 3 | o_hi[sw]);
+        }
+    }
+    __syncwarp();
+    // slots: lane l computes column pick[l] >> 3, gathering its entries in order pick[l] & 7
+    for (int l = o; l < 32; l += 8) {
+        const int c = pick[g][l] >> 3;
+        const uint32_t oo = pick[g][l] & 7u;
+        const uint64_t j = col0 + c;
         uint32_t e[4] = {0, 0, 0, 0};
         if (j < n)
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                e[u] = static_cast<uint32_t>(rows[j * 4 + u]) | (signs[j * 4 + u] < 0.0 ? 0x8000u : 0u);
-        pk[2 * q] = e[0] | (e[1] << 16);
-        pk[2 * q + 1] = e[2] | (e[3] << 16);
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t x = j * 4 + ord(oo, u);
+                e[u] = static_cast<uint32_t>(rows[x]) | (signs[x] < 0.0 ? 0x8000u : 0u);
+            }
+        e[2] |= static_cast<uint32_t>(c != l) << 14; // lane trade bit
+        const uint64_t slot = static_cast<uint64_t>(q) * SP4_THREADS + warp * 32 + l;
+        reinterpret_cast<uint2*>(plan)[slot] = make_uint2(e[0] | (e[1] << 16), e[2] | (e[3] << 16));
     }
-    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const double2* src = reinterpret_cast<const double2*>(a + i * lda);
-        for (uint64_t c = t; c < n / 2; c += SP4_THREADS)
-            reinterpret_cast<double2*>(srow)[c] = __ldcs(src + c);
-        __syncthreads();
-        double* orow = out + i * ldo;
+}
+
+template <bool PLAN>
+__global__ void __launch_bounds__(SP4_THREADS, 1) k_sparse_right4(uint64_t n, const double* __restrict__ a,
+                                                                  uint64_t lda, const int32_t* __restrict__ rows,
+                                                                  const double* __restrict__ signs,
+                                                                  const uint32_t* __restrict__ plan,
+                                                                  double* __restrict__ out, uint64_t ldo) {
+    extern __shared__ __align__(128) double srow[]; // SP4_SLOTS x SP4_CH ring + barriers
+    const int t = threadIdx.x;
+#ifdef RL_SP_TRACE
+    long long tr0 = clock64(), tr_wait = 0, tr_comp = 0, tr_sync = 0;
+#endif
+    // slot q: 4 x 16-bit entries, row (14 bits) | spare | sign; in draw order, or (PLAN) in
+    // the plan's gather order with the rotation / lane trade in the spare bits
+    uint32_t pk[SP4_Q * 2];
+    if constexpr (PLAN) {
+        const uint2* pl = reinterpret_cast<const uint2*>(plan);
+#pragma unroll
+        for (int q = 0; q < SP4_Q; ++q) {
+            const uint2 v = pl[q * SP4_THREADS + t];
+            pk[2 * q] = v.x;
+            pk[2 * q + 1] = v.y;
+        }
+    } else {
 #pragma unroll
         for (int q = 0; q < SP4_Q; ++q) {
             const uint64_t j = t + static_cast<uint64_t>(q) * SP4_THREADS;
+            uint32_t e[4] = {0, 0, 0, 0};
+            if (j < n)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    e[u] = static_cast<uint32_t>(rows[j * 4 + u]) | (signs[j * 4 + u] < 0.0 ? 0x8000u : 0u);
+            pk[2 * q] = e[0] | (e[1] << 16);
+            pk[2 * q + 1] = e[2] | (e[3] << 16);
+        }
+    }
+    // Shared memory holds [head buffer 0 | tail | head buffer 1], SP4_SLOTS = 2 H + T chunks of
+    // SP4_CH doubles.  Row r's first H chunks (its head) arrive by bulk async copies (TMA
+    // engine, one mbarrier per chunk) into head buffer r & 1 while row r - 1 is gathered; its
+    // last T chunks (the tail, prefetched into L2 one row ahead) are copied by all threads
+    // with cp.async into the single tail buffer once row r - 1 is done.  Row r's element col
+    // sits at col (even r: head 0 then tail) or, for odd r, at col + (H + T) SP4_CH when it is
+    // in the head, so only a short L2 read of each row's tail is exposed.
+    double* sm = srow;
+    constexpr uint32_t H = (SP4_SLOTS - 5) / 2, T = SP4_SLOTS - 2 * H; // 11 + 5 + 11 for n = 16384
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SP4_SLOTS * SP4_CH); // 2 H head barriers
+    const uint32_t cpr = static_cast<uint32_t>((n + SP4_CH - 1) / SP4_CH); // chunks per row (<= H + T)
+    const uint32_t nh = cpr < H ? cpr : H;                                 // head chunks per row
+    const uint32_t my_rows = blockIdx.x < n ? static_cast<uint32_t>((n - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+    if (t == 0) {
+        for (uint32_t s = 0; s < 2 * H; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + s)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto row_ptr = [&](uint32_t r) { return a + (blockIdx.x + static_cast<uint64_t>(r) * gridDim.x) * lda; };
+    auto chunk_bytes = [&](uint32_t c) {
+        const uint64_t left = n - static_cast<uint64_t>(c) * SP4_CH;
+        return static_cast<uint32_t>(left < SP4_CH ? left : SP4_CH) * 8u;
+    };
+    auto issue_head = [&](uint32_t r) { // thread 0: row r's head into buffer r & 1
+        const double* src = row_ptr(r);
+        const uint32_t buf = (r & 1u) ? H + T : 0u;
+        for (uint32_t c = 0; c < nh; ++c) {
+            const uint32_t bytes = chunk_bytes(c), mb = smem_u32(bar + (r & 1u) * H + c);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sm + (buf + c) * SP4_CH)),
+                "l"(src + static_cast<uint64_t>(c) * SP4_CH), "r"(bytes), "r"(mb)
+                : "memory");
+        }
+        for (uint32_t c = nh; c < cpr; ++c) // the tail: into L2 now, into shared memory a row later
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + static_cast<uint64_t>(c) * SP4_CH),
+                         "r"(chunk_bytes(c))
+                         : "memory");
+    };
+    const uint32_t tail_elems = n > nh * SP4_CH ? static_cast<uint32_t>(n) - nh * SP4_CH : 0u; // even (n even)
+    if (t == 0 && my_rows > 0)
+        issue_head(0);
+    for (uint32_t r = 0; r < my_rows; ++r) {
+#ifdef RL_SP_TRACE
+        long long ta = clock64();
+        tr_sync += ta - tr0;
+#endif
+        if (t == 0 && r + 1 < my_rows)
+            issue_head(r + 1); // buffer (r + 1) & 1 was freed by row r - 1
+        {                      // row r's tail: 16-byte cp.async by every thread
+            const double* src = row_ptr(r) + nh * SP4_CH;
+            for (uint32_t e = 2 * t; e < tail_elems; e += 2 * SP4_THREADS)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sm + (H * SP4_CH + e))),
+                             "l"(src + e)
+                             : "memory");
+            asm volatile("cp.async.commit_group;\n cp.async.wait_all;" ::: "memory");
+        }
+        for (uint32_t c = 0; c < nh; ++c) { // row r's head
+            const uint32_t mb = smem_u32(bar + (r & 1u) * H + c), par = (r >> 1) & 1u;
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                             " selp.u32 %0, 1, 0, p;\n}"
+                             : "=r"(done)
+                             : "r"(mb), "r"(par)
+                             : "memory");
+        }
+        __syncthreads(); // every thread's tail pieces are visible
+#ifdef RL_SP_TRACE
+        long long tb = clock64();
+        tr_wait += tb - ta;
+#endif
+        // element col of row r at col + (col < head_end ? head_off : 0)
+        const uint32_t head_end = nh * SP4_CH, head_off = (r & 1u) ? (H + T) * SP4_CH : 0u;
+        uint32_t tr; // t, opaque to the compiler: keeps the 32 column offsets from being hoisted into registers
+        asm volatile("mov.u32 %0, %1;" : "=r"(tr) : "r"(static_cast<uint32_t>(t)));
+        const uint64_t i = blockIdx.x + static_cast<uint64_t>(r) * gridDim.x;
+        double* orow = out + i * ldo;
+#pragma unroll
+        for (int q = 0; q < SP4_Q; ++q) {
+            uint32_t p0, p1; // opaque copies: keeps the compiler from hoisting the unpacked entries (spills)
+            asm volatile("mov.b32 %0, %1;" : "=r"(p0) : "r"(pk[2 * q]));
+            asm volatile("mov.b32 %0, %1;" : "=r"(p1) : "r"(pk[2 * q + 1]));
+            // PLAN: lane pair (l, l ^ 16) may trade columns
+            const uint32_t j = static_cast<uint32_t>(q) * SP4_THREADS +
+                               (PLAN ? (tr & ~31u) + ((tr & 31u) ^ ((p1 >> 10) & 16u)) : tr);
             if (j < n) {
-                double s = 0.0;
+                double y[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const uint32_t e = (pk[2 * q + (u >> 1)] >> (16 * (u & 1))) & 0xffffu;
-                    const double x = srow[e & 0x7fffu];
-                    s += (e & 0x8000u) ? -x : x; // s_jt = +-1: the reference's s += s_jt A(i, r_jt)
+                    const uint32_t w = u < 2 ? p0 : p1;
+                    const uint32_t e = (u & 1) ? (w >> 16) : (w & 0xffffu);
+                    const uint32_t col = e & 0x3fffu;
+                    const double x = sm[col + (col < head_end ? head_off : 0u)];
+                    // s_jt = +-1: flip the sign bit (the reference's s_jt * A(i, r_jt) is exact)
+                    const uint32_t sbit = (u & 1) ? (w & 0x80000000u) : ((w << 16) & 0x80000000u);
+                    y[u] = __hiloint2double(__double2hiint(x) ^ static_cast<int>(sbit), __double2loint(x));
                 }
+                // the defined order (v0 + v1) + (v2 + v3); the plan's gather orders all preserve it
+                const double s = (y[0] + y[1]) + (y[2] + y[3]);
                 __stcs(orow + j, s);
             }
+            if (q % SP4_GROUP == SP4_GROUP - 1)
+                asm volatile("" ::: "memory"); // bounds the compiler's load hoisting (register budget)
         }
-        __syncthreads();
+#ifdef RL_SP_TRACE
+        tr0 = clock64();
+        tr_comp += tr0 - tb;
+#endif
+        __syncthreads(); // row r's slots are free
     }
+#ifdef RL_SP_TRACE
+    if (t % 32 == 0) { // per warp: cycles waiting for the row, gathering, at the row barrier
+        atomicAdd(reinterpret_cast<unsigned long long*>(const_cast<uint32_t*>(plan)), static_cast<unsigned long long>(tr_wait));
+        atomicAdd(reinterpret_cast<unsigned long long*>(const_cast<uint32_t*>(plan)) + 1, static_cast<unsigned long long>(tr_comp));
+        atomicAdd(reinterpret_cast<unsigned long long*>(const_cast<uint32_t*>(plan)) + 2, static_cast<unsigned long long>(tr_sync));
+    }
+#endif
 }
 
 // x = S y (nrhs columns, ld nrhs) via the row-sorted transpose: x[i] = sum over
@@ -359,15 +591,40 @@ void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const doub
                             const double* a, uint64_t lda, double* out, uint64_t ldo) {
     if (nnz == 4 && n <= static_cast<uint64_t>(SP4_THREADS) * SP4_Q && n % 2 == 0 && lda % 2 == 0 &&
         (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
-        const size_t smem = n * sizeof(double);
+        constexpr size_t smem = SP4_SLOTS * SP4_CH * sizeof(double) + SP4_SLOTS * sizeof(uint64_t); // + barriers
         static bool attr[16] = {};
         if (!attr[ctx().device & 15]) {
-            RL_CUDA(cudaFuncSetAttribute(k_sparse_right4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SP4_THREADS * SP4_Q * 8));
+            RL_CUDA(cudaFuncSetAttribute(k_sparse_right4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            RL_CUDA(cudaFuncSetAttribute(k_sparse_right4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
             attr[ctx().device & 15] = true;
         }
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, ctx().sms));
-        k_sparse_right4<<<grid, SP4_THREADS, smem, stream()>>>(n, a, lda, rows, signs, out, ldo);
+        static const bool use_plan = [] {
+            const char* e = getenv("RL_SPARSE_PLAN"); // 0: draw-order gathers (dev comparison)
+            return e == nullptr || e[0] != '0';
+        }();
+        if (use_plan) {
+            uint32_t* plan = ws<uint32_t>(WS_SPLAN, 2 * SP4_THREADS * SP4_Q);
+            k_sparse_plan<<<SP4_THREADS / 32 * SP4_Q / SPP_GROUPS, 32, 0, stream()>>>(n, rows, signs, plan);
+            RL_LAUNCHED();
+#ifdef RL_SP_TRACE
+            unsigned long long h0[3], h1[3];
+            RL_CUDA(cudaMemcpyAsync(h0, plan, sizeof h0, cudaMemcpyDeviceToHost, stream()));
+            RL_CUDA(cudaStreamSynchronize(stream()));
+#endif
+            k_sparse_right4<true><<<grid, SP4_THREADS, smem, stream()>>>(n, a, lda, rows, signs, plan, out, ldo);
+#ifdef RL_SP_TRACE
+            RL_CUDA(cudaMemcpyAsync(h1, plan, sizeof h1, cudaMemcpyDeviceToHost, stream()));
+            RL_CUDA(cudaStreamSynchronize(stream()));
+            const double warps = static_cast<double>(grid) * SP4_THREADS / 32 * (static_cast<double>(n) / grid);
+            fprintf(stderr, "sparse trace (cycles per warp-row): wait %.0f gather %.0f barrier %.0f\n",
+                    (h1[0] - h0[0]) / warps, (h1[1] - h0[1]) / warps, (h1[2] - h0[2]) / warps);
+#endif
+        } else {
+            k_sparse_right4<false><<<grid, SP4_THREADS, smem, stream()>>>(n, a, lda, rows, signs, nullptr, out, ldo);
+        }
         RL_LAUNCHED();
         return;
     }
