@@ -127,6 +127,12 @@ rl_status rl_dev_sparse_apply_right(uint64_t n, int nnz, const int32_t* d_rows, 
                                     const double* d_a, double* d_out);
 rl_status rl_dev_householder_pair_apply_right(uint64_t n, const double* d_u1, const double* d_u2,
                                               const double* d_a, double* d_out);
+/* out = A C for the circulant C(i,j) = c[(i-j) mod n] (structured::circulant, structured.cpp:54-68;
+ * randomized_genp's Right side with CirculantSign / CirculantGaussian, genp.cpp:175-180):
+ * A, out m x n row-major on the device, out != a.  Power-of-two 64 <= n <= 8192 go through the
+ * FFT (matrix-free, O(m n log n)); other n through a dense product. */
+rl_status rl_dev_circulant_apply_right(uint64_t m, uint64_t n, const double* d_c, const double* d_a,
+                                       double* d_out);
 
 /* -------------------------------------------- matrix.hpp (matrix.cpp) ---- */
 /* Matrix::multiply(const Matrix&) (matrix.cpp:86-102): C(m x n) = A(m x k) B(k x n). */

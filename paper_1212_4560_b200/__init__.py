@@ -34,7 +34,7 @@ __all__ = [
     "randomized_genp_batched", "approx_basis", "qr_positive", "project_onto_basis", "numerical_rank",
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
     "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
-    "dev_householder_pair_apply_right", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
+    "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
     "box_muller_fast_check", "launch_count", "LIB_PATH",
 ]
 
@@ -206,6 +206,7 @@ def lib() -> C.CDLL:
         "rl_sparse_apply_right": [u64, cint, _i32a, _d, _d, _d],
         "rl_dev_sparse_apply_right": [u64, cint, vp, vp, vp, vp],
         "rl_dev_householder_pair_apply_right": [u64, vp, vp, vp, vp],
+        "rl_dev_circulant_apply_right": [u64, u64, vp, vp, vp],
         "rl_matmul": [u64, u64, u64, _d, _d, _d],
         "rl_dev_gemm": [cint, cint, u64, u64, u64, dbl, vp, u64, vp, u64, dbl, vp, u64],
         "rl_circ_mul": [u64, _d, _d, _d],
@@ -561,6 +562,16 @@ def dev_householder_pair_apply_right(u1, u2, a, out) -> None:
     if a.shape != (n, n) or out.shape != (n, n) or u1.shape[0] != n or u2.shape[0] != n:
         raise DimensionMismatch("householder_pair_apply_right: shape mismatch")
     _chk(lib().rl_dev_householder_pair_apply_right(n, _ptr(u1), _ptr(u2), _ptr(a), _ptr(out)))
+
+
+def dev_circulant_apply_right(c, a, out) -> None:
+    """out = A C on device tensors for the circulant with first column c (FFT for power-of-two
+    64 <= n <= 8192)."""
+    _bind_stream()
+    m, n = a.shape
+    if c.shape[0] != n or out.shape != (m, n):
+        raise DimensionMismatch("circulant_apply_right: shape mismatch")
+    _chk(lib().rl_dev_circulant_apply_right(m, n, _ptr(c), _ptr(a), _ptr(out)))
 
 
 def dev_qr_positive(y, q, r) -> None:

@@ -38,6 +38,9 @@ void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const doub
                             uint64_t lda, double* out, uint64_t ldo);
 void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
                          double s12, double* out, uint64_t ldo);
+bool circ_fft_supported(uint64_t n);
+void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
+                              uint64_t ldo);
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r);
 std::vector<double> small_singular_values(int k, const double* d_a);
 double sumsq_dev(uint64_t count, const double* x);
@@ -377,6 +380,22 @@ rl_status rl_dev_householder_pair_apply_right(uint64_t n, const double* d_u1, co
     for (uint64_t i = 0; i < n; ++i)
         s12 += h1[i] * h2[i];
     hh2_apply_right_dev(n, d_a, n, d_u1, d_u2, s12, d_out, n);
+    API_END
+}
+
+rl_status rl_dev_circulant_apply_right(uint64_t m, uint64_t n, const double* d_c, const double* d_a,
+                                       double* d_out) {
+    API_BEGIN
+    require_positive(m, n, "circulant_apply_right");
+    if (d_a == d_out)
+        fail(RL_INVALID_ARGUMENT, "circulant_apply_right: out must not alias a");
+    if (circ_fft_supported(n)) {
+        circ_apply_right_fft_dev(m, n, d_c, d_a, n, d_out, n);
+    } else {
+        double* dense = ws<double>(WS_TMP2, n * n);
+        circulant_dense_dev(n, d_c, dense);
+        gemm(false, false, m, n, n, 1.0, d_a, n, dense, n, 0.0, d_out, n);
+    }
     API_END
 }
 

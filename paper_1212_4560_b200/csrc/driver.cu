@@ -33,6 +33,9 @@ void hh2_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* u1, const double
                        double* x);
 void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs,
                             const double* a, uint64_t lda, double* out, uint64_t ldo);
+bool circ_fft_supported(uint64_t n);
+void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
+                              uint64_t ldo);
 struct SparseT {
     int32_t* row_ptr;
     int32_t* col_j;
@@ -185,6 +188,13 @@ void apply_right(const Mult& m, const double* sys, double* out) {
     case RL_SPARSE_SIGN:
         sparse_apply_right_dev(n, 4, m.rows, m.signs, sys, n, out, n);
         return;
+    case RL_CIRCULANT_SIGN:
+    case RL_CIRCULANT_GAUSSIAN:
+        if (!m.dense) {
+            circ_apply_right_fft_dev(n, n, m.c, sys, n, out, n);
+            return;
+        }
+        [[fallthrough]];
     default:
         gemm(false, false, n, n, n, 1.0, sys, n, m.dense, n, 0.0, out, n);
     }
@@ -340,8 +350,11 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
                 RL_CUDA(cudaStreamWaitEvent(st, sp.done, 0));
                 spec_attempt = -1;
             } else {
+                // circulant multipliers of power-of-two n <= 8192 are applied on the right through
+                // the FFT (matrix-free); everything else is densified
+                const bool fft = (tag == RL_CIRCULANT_SIGN || tag == RL_CIRCULANT_GAUSSIAN) && circ_fft_supported(n);
                 draw(right, tag, mu, sigma, n, seed, ds ^ 0x5000000000000000ULL,
-                     use_left ? WS_RF1 : (speculate ? mult_slot[attempt & 1] : WS_MULT), WS_RF2, true);
+                     use_left ? WS_RF1 : (speculate ? mult_slot[attempt & 1] : WS_MULT), WS_RF2, !fft);
             }
         }
         const double* src = A;

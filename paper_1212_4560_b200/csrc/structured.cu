@@ -677,4 +677,274 @@ void circ_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* c, const double
     RL_LAUNCHED();
 }
 
+
+// ------------------------------------------- circulant right product through the FFT ----
+// out = A C for the circulant C(i, j) = c[(i - j) mod n] (random_structured CirculantSign /
+// CirculantGaussian, random_gen.cpp:90-123; the reference applies it on the Right as
+// (C^T A^T)^T with an FFT per column, genp.cpp:175-180 and structured.cpp:132-189).  Row r of
+// A C is the cyclic cross-correlation of A(r, :) with c, so FFT(out_r) = FFT(A_r) . conj(FFT(c)).
+// Matrix-free: O(n^2 log n) instead of the dense 2 n^3, one read of A and one write of A C.
+//   * two real rows per complex sequence z = A_r + i A_{r+1} (c is real, so the imaginary
+//     part carries row r + 1 through the product untouched);
+//   * one persistent CTA per SM, a row pair's n complex values in shared memory (n <= 8192:
+//     128 KB), padded by one element per n / 8 so that the bit-reversed load / store are
+//     conflict-free;
+//   * forward: bit-reversed load, decimation-in-time radix-2 stages fused two at a time in
+//     registers (radix-2^2: the same operations, half the shared-memory passes); the product
+//     with conj(FFT(c)) / n; inverse: decimation-in-frequency stages (natural in, bit-reversed
+//     out), read back in bit-reversed order for a coalesced store;
+//   * twiddles w^m = exp(-2 pi i m / n) from two small exact tables (w^m = hi[m / 64] lo[m % 64]).
+namespace {
+
+constexpr int CF_THREADS = 512, CF_L = 64, CF_MAXN = 8192;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+struct CfPlan {
+    int n, lg, sh; // n = 2^lg; shared index i lives at i + (i >> 3) + (i >> sh)
+    const double2* lo;
+    const double2* hi;
+    __device__ __forceinline__ int at(int i) const { return i + (i >> 3) + (i >> sh); }
+    __device__ __forceinline__ int brev(int j) const { return static_cast<int>(__brev(static_cast<unsigned>(j)) >> (32 - lg)); }
+    __device__ __forceinline__ double2 w(int m) const { return cmul(hi[m / CF_L], lo[m % CF_L]); } // exp(-2 pi i m / n)
+};
+
+// x (-i) exactly; x exp(-i pi / 4) (one rounding); x exp(-3 i pi / 4)
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }
+__device__ __forceinline__ double2 mul_w8(double2 a) {
+    constexpr double r = 0.70710678118654752440;
+    return make_double2((a.x + a.y) * r, (a.y - a.x) * r);
+}
+__device__ __forceinline__ double2 mul_w8_3(double2 a) { return mul_mi(mul_w8(a)); }
+
+// One shared-memory pass of R fused DIT stages (spans h, 2h, ..., 2^(R-1) h) on a group of 2^R
+// elements I_e = base + j + e h held in registers.  The stage with span S = 2^s h pairs e with
+// e + 2^s (bit s of e clear) and twiddles by w^((j + (e mod 2^s) h) n / (2S)) =
+// w^(j n / (2S)) exp(-2 pi i (e mod 2^s) / 2^(s+1)): one table twiddle per stage, the rest
+// exact or one-rounding powers of the 8th root.
+template <int R>
+__device__ __forceinline__ void cf_dit_pass(double2* z, const CfPlan& P, int h, int g) {
+    constexpr int E = 1 << R;
+    const int n = P.n, j = g % h, i0 = (g / h) * E * h + j;
+    double2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        v[e] = z[P.at(i0 + e * h)];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+        const int S = h << s;
+        const double2 tw = P.w(j * (n / (2 * S)));
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e >> s) & 1)
+                continue;
+            const int r = e & ((1 << s) - 1);
+            double2 t = cmul(tw, v[e + (1 << s)]);
+            if (s == 1 && r == 1)
+                t = mul_mi(t);
+            if (s == 2 && r == 1)
+                t = mul_w8(t);
+            if (s == 2 && r == 2)
+                t = mul_mi(t);
+            if (s == 2 && r == 3)
+                t = mul_w8_3(t);
+            v[e + (1 << s)] = csub(v[e], t);
+            v[e] = cadd(v[e], t);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        z[P.at(i0 + e * h)] = v[e];
+}
+
+// One pass of R fused DIF stages with conjugate twiddles (spans 2^(R-1) q, ..., q) on a group
+// I_e = base + j + e q: the stage with span S = 2^s q pairs e with e + 2^s and multiplies the
+// difference by conj(w)^((j + (e mod 2^s) q) n / (2S)).
+template <int R>
+__device__ __forceinline__ void cf_dif_pass(double2* z, const CfPlan& P, int q, int g) {
+    constexpr int E = 1 << R;
+    const int n = P.n, j = g % q, i0 = (g / q) * E * q + j;
+    double2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        v[e] = z[P.at(i0 + e * q)];
+#pragma unroll
+    for (int s = R - 1; s >= 0; --s) {
+        const int S = q << s;
+        const double2 tw = cconj(P.w(j * (n / (2 * S))));
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e >> s) & 1)
+                continue;
+            const int r = e & ((1 << s) - 1);
+            double2 d = csub(v[e], v[e + (1 << s)]);
+            v[e] = cadd(v[e], v[e + (1 << s)]);
+            d = cmul(d, tw);
+            if (s == 1 && r == 1)
+                d = cconj(mul_mi(cconj(d)));
+            if (s == 2 && r == 1)
+                d = cconj(mul_w8(cconj(d)));
+            if (s == 2 && r == 2)
+                d = cconj(mul_mi(cconj(d)));
+            if (s == 2 && r == 3)
+                d = cconj(mul_w8_3(cconj(d)));
+            v[e + (1 << s)] = d;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        z[P.at(i0 + e * q)] = v[e];
+}
+
+// forward DFT (w = exp(-2 pi i / n)) in place: bit-reversed input, natural output
+__device__ void cf_dit(double2* z, const CfPlan& P, int t) {
+    const int n = P.n;
+    int h = 1, left = P.lg;
+    while (left > 0) {
+        const int R = left >= 3 ? 3 : left;
+        if (R == 3) {
+            for (int g = t; g < n / 8; g += CF_THREADS)
+                cf_dit_pass<3>(z, P, h, g);
+        } else if (R == 2) {
+            for (int g = t; g < n / 4; g += CF_THREADS)
+                cf_dit_pass<2>(z, P, h, g);
+        } else {
+            for (int g = t; g < n / 2; g += CF_THREADS)
+                cf_dit_pass<1>(z, P, h, g);
+        }
+        h <<= R;
+        left -= R;
+        __syncthreads();
+    }
+}
+
+// inverse DFT without the 1/n (conjugate twiddles) in place: natural input, bit-reversed output
+__device__ void cf_dif_inv(double2* z, const CfPlan& P, int t) {
+    const int n = P.n;
+    int left = P.lg, hs = n; // the remaining stages have spans below hs
+    while (left > 0) {
+        const int R = left >= 3 ? 3 : left;
+        const int q = hs >> R; // smallest span of this pass
+        if (R == 3) {
+            for (int g = t; g < n / 8; g += CF_THREADS)
+                cf_dif_pass<3>(z, P, q, g);
+        } else if (R == 2) {
+            for (int g = t; g < n / 4; g += CF_THREADS)
+                cf_dif_pass<2>(z, P, q, g);
+        } else {
+            for (int g = t; g < n / 2; g += CF_THREADS)
+                cf_dif_pass<1>(z, P, q, g);
+        }
+        hs = q;
+        left -= R;
+        __syncthreads();
+    }
+}
+
+__device__ CfPlan cf_setup(int n, double2* tabs, int t) {
+    CfPlan P;
+    P.n = n;
+    P.lg = 31 - __clz(n);
+    P.sh = P.lg - 3;
+    double2* lo = tabs;
+    double2* hi = tabs + CF_L;
+    for (int m = t; m < CF_L; m += CF_THREADS) { // exact argument 2m/n: sincospi
+        double s, c;
+        sincospi(2.0 * m / n, &s, &c);
+        lo[m] = make_double2(c, -s);
+    }
+    for (int m = t; m < n / (2 * CF_L) || m == 0; m += CF_THREADS) {
+        if (m >= CF_L)
+            break;
+        double s, c;
+        sincospi(2.0 * (static_cast<double>(m) * CF_L) / n, &s, &c);
+        hi[m] = make_double2(c, -s);
+    }
+    P.lo = lo;
+    P.hi = hi;
+    return P;
+}
+
+// chat[k] = conj(FFT(c))_k / n  (one CTA)
+__global__ void __launch_bounds__(CF_THREADS) k_circ_fft_prep(int n, const double* __restrict__ c,
+                                                              double2* __restrict__ chat) {
+    extern __shared__ double2 cz[];
+    __shared__ double2 tabs[2 * CF_L];
+    const int t = threadIdx.x;
+    const CfPlan P = cf_setup(n, tabs, t);
+    for (int j = t; j < n; j += CF_THREADS)
+        cz[P.at(P.brev(j))] = make_double2(c[j], 0.0);
+    __syncthreads();
+    cf_dit(cz, P, t);
+    const double inv_n = 1.0 / n; // a power of two: exact
+    for (int k = t; k < n; k += CF_THREADS) {
+        const double2 v = cz[P.at(k)];
+        chat[k] = make_double2(v.x * inv_n, -v.y * inv_n);
+    }
+}
+
+// out (m x n, ldo) = A (m x n, lda) C; persistent CTAs over row pairs
+__global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, int n, const double* __restrict__ a,
+                                                                  uint64_t lda, const double2* __restrict__ chat,
+                                                                  double* __restrict__ out, uint64_t ldo) {
+    extern __shared__ double2 cz[];
+    __shared__ double2 tabs[2 * CF_L];
+    const int t = threadIdx.x;
+    const CfPlan P = cf_setup(n, tabs, t);
+    __syncthreads();
+    const uint64_t pairs = (m + 1) / 2;
+    for (uint64_t pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+        const uint64_t r = 2 * pr;
+        const bool two = r + 1 < m;
+        const double* a0 = a + r * lda;
+        const double* a1 = a0 + lda;
+        for (int j = t; j < n; j += CF_THREADS)
+            cz[P.at(P.brev(j))] = make_double2(__ldcs(a0 + j), two ? __ldcs(a1 + j) : 0.0);
+        __syncthreads();
+        cf_dit(cz, P, t);
+        for (int k = t; k < n; k += CF_THREADS)
+            cz[P.at(k)] = cmul(cz[P.at(k)], chat[k]);
+        __syncthreads();
+        cf_dif_inv(cz, P, t);
+        double* o0 = out + r * ldo;
+        double* o1 = o0 + ldo;
+        for (int j = t; j < n; j += CF_THREADS) {
+            const double2 v = cz[P.at(P.brev(j))];
+            __stcs(o0 + j, v.x);
+            if (two)
+                __stcs(o1 + j, v.y);
+        }
+        __syncthreads();
+    }
+}
+
+} // namespace
+
+// true when the FFT path handles n (a power of two, 64 <= n <= 8192)
+bool circ_fft_supported(uint64_t n) { return n >= 64 && n <= CF_MAXN && (n & (n - 1)) == 0; }
+
+// out = A C for the circulant with first column c; A, out m x n (out != A)
+void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
+                              uint64_t ldo) {
+    const size_t smem = (n + n / 8 + 8) * sizeof(double2);
+    static bool attr[16] = {};
+    if (!attr[ctx().device & 15]) {
+        const int mx = static_cast<int>((CF_MAXN + CF_MAXN / 8 + 8) * sizeof(double2));
+        RL_CUDA(cudaFuncSetAttribute(k_circ_fft_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        RL_CUDA(cudaFuncSetAttribute(k_circ_right_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        attr[ctx().device & 15] = true;
+    }
+    double2* chat = ws<double2>(WS_SPLAN, n); // k_sparse_plan's slot: not live at the same time
+    k_circ_fft_prep<<<1, CF_THREADS, smem, stream()>>>(static_cast<int>(n), c, chat);
+    RL_LAUNCHED();
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((m + 1) / 2, ctx().sms));
+    k_circ_right_fft<<<grid, CF_THREADS, smem, stream()>>>(m, static_cast<int>(n), a, lda, chat, out, ldo);
+    RL_LAUNCHED();
+}
+
 } // namespace rl

@@ -246,3 +246,40 @@ def test_sparse_apply_right_bit_exact(rl, oracle, n):
     rows, signs = oracle.sparse_pm1(n, 5, 6)
     a = np.random.default_rng(n).standard_normal((n, n))
     assert np.array_equal(rl.sparse_apply_right(rows, signs, a), oracle.sparse_apply_right(rows, signs, a))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(64, 64), (255, 256), (1024, 1024), (3, 2048), (8192, 8192), (100, 96)])
+def test_circulant_apply_right_fft(rl, m, n):
+    """A C for a circulant multiplier (C(i,j) = c[(i-j) mod n], structured.cpp:54-68) through the
+    FFT path (power-of-two n <= 8192; n = 96 takes the dense fallback) against the dense product
+    in numpy: relative error within 1e-13 (FFT rounding grows like log2 n eps)."""
+    import torch
+    rng = np.random.default_rng(n + m)
+    for c in (np.where(rng.random(n) < 0.5, -1.0, 1.0), rng.standard_normal(n)):
+        a = rng.standard_normal((m, n))
+        idx = (np.arange(n)[:, None] - np.arange(n)[None, :]) % n
+        want = a @ c[idx]
+        dev = torch.device("cuda", 0)
+        out = torch.empty(m, n, dtype=torch.float64, device=dev)
+        rl.dev_circulant_apply_right(torch.from_numpy(c).to(dev), torch.from_numpy(a).to(dev), out)
+        got = out.cpu().numpy()
+        assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max() * max(1.0, np.log2(n) / 4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["circulant_sign", "circulant_gaussian"])
+def test_randomized_genp_circulant_fft_path(rl, oracle, kind):
+    """randomized_genp with a circulant Right multiplier at n = 512 (FFT path) against the C
+    restatement (dense circulant): same accepted attempt, x and backward error within tolerance."""
+    n = 512
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((n, n))
+    A[:128, :128] = rng.standard_normal((128, 127)) @ rng.standard_normal((127, 128))
+    b = A @ rng.standard_normal(n)
+    tag = getattr(rl.MultiplierTag, kind.upper())
+    x, rep = rl.randomized_genp(A, b, rl.MultiplierKind(tag), rl.MulSide.RIGHT, 0, rl.RngStream(5, 3))
+    xo, ro, eo = oracle.randomized_genp(A, b, kind, "right", 0, seed=5, sid=3)
+    assert rep.attempt == eo[0]
+    assert rel(x, xo) < 1e-8
+    assert bwd(A, x, b) <= 4 * bwd(A, xo, b) + 1e-15
