@@ -318,6 +318,32 @@ def time_multiplier_apply(torch, rl, dev, dist, tag, A, mult_bytes, hbm_peak):
             "frac": round(gbs / peak, 4), "peak_source": src, "frac_same_run_copy": round(gbs / hbm_peak, 4)}
 
 
+def run_circulant_fft(torch, rl, dev, dist, hbm_peak):
+    """a circulant +-1 right multiplier at n = 8192 applied matrix-free
+    (randomized_genp's Right-side A C through k_circ_fft_prep + k_circ_right_fft) against the
+    dense DMMA product it replaces; HBM roofline over 2 n^2 8 bytes (A read once, A C written
+    once; A and A C exceed L2)."""
+    n = 8192
+    A = torch.empty(n, n, dtype=torch.float64, device=dev)
+    rl.dev_gaussian_matrix(A, 0.0, 1.0, rl.RngStream(SEED, 71))
+    c = torch.from_numpy(rl.rng_draws(rl.RngStream(SEED, 72), "sign", n)).to(dev)
+    out = torch.empty_like(A)
+    ms, _ = _timed(torch, lambda: rl.dev_circulant_apply_right(c, A, out), 3, 20, dist)
+    idx = (torch.arange(n, device=dev)[:, None] - torch.arange(n, device=dev)[None, :]) % n
+    C = c[idx]
+    ref = torch.empty_like(A)
+    ms_dense, _ = _timed(torch, lambda: rl.dev_gemm(A, C, ref), 1, 2, dist)
+    diff = float((out - ref).abs().max() / ref.abs().max())
+    peak, src = hbm_reference_peak(hbm_peak)
+    gbs = 2.0 * n * n * 8 / (ms * 1e-3) / 1e9
+    del A, out, C, ref
+    torch.cuda.empty_cache()
+    return {"workload": "A C, circulant +-1 right multiplier, n = 8192 (FFT path)", "ms": round(ms, 4),
+            "dense_dmma_ms": round(ms_dense, 3), "max_rel_diff_vs_dense": diff,
+            "roofline": {"bound": "hbm", "achieved_gbs": round(gbs, 1), "peak_gbs": peak, "frac": round(gbs / peak, 4),
+                         "peak_source": src}}
+
+
 def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak):
     """Config 5: n = 16384, 8 RHS, MulSide::Right with the orthogonal Householder pair, the
     sparse +-1 and the Gaussian multipliers (contrast arm skipped as in config 3).  Short runs
@@ -569,6 +595,7 @@ def run_ours(args, dist, rank, world, local_rank):
     # ---- configs 1 and 5 (latency-bound n = 256; n = 16384 with the new multipliers) ----
     c1 = run_config1(torch, rl, dev, dist, args, fp64_peak)
     c5 = None if args.skip_config5 else run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak)
+    circ = run_circulant_fft(torch, rl, dev, dist, hbm_peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -615,6 +642,7 @@ def run_ours(args, dist, rank, world, local_rank):
         "range_finder": rf,
         "config1": c1,
         "config5": c5,
+        "circulant_fft": circ,
         "clocks": clocks.summary(),
         "peaks_same_run": {"fp64_dmma_tflops": round(fp64_peak, 3), "hbm_copy_gbs": round(hbm_peak, 1)},
     }
