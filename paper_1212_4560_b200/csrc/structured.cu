@@ -903,6 +903,14 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, in
         const bool two = r + 1 < m;
         const double* a0 = a + r * lda;
         const double* a1 = a0 + lda;
+        if (t == 0 && pr + gridDim.x < pairs) { // the next row pair into L2 while this one is transformed
+            const double* nx = a + 2 * (pr + gridDim.x) * lda;
+            const uint64_t rows = (2 * (pr + gridDim.x) + 1 < m) ? 2 : 1;
+            for (uint64_t q = 0; q < rows; ++q)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + q * lda),
+                             "r"(static_cast<uint32_t>(n * sizeof(double)))
+                             : "memory");
+        }
         for (int j = t; j < n; j += CF_THREADS)
             cz[P.at(P.brev(j))] = make_double2(__ldcs(a0 + j), two ? __ldcs(a1 + j) : 0.0);
         __syncthreads();
