@@ -727,8 +727,9 @@ __device__ __forceinline__ double2 mul_w8_3(double2 a) { return mul_mi(mul_w8(a)
 // e + 2^s (bit s of e clear) and twiddles by w^((j + (e mod 2^s) h) n / (2S)) =
 // w^(j n / (2S)) exp(-2 pi i (e mod 2^s) / 2^(s+1)): one table twiddle per stage, the rest
 // exact or one-rounding powers of the 8th root.
-template <int R>
-__device__ __forceinline__ void cf_dit_pass(double2* z, const CfPlan& P, int h, int g) {
+template <int R, bool MUL = false>
+__device__ __forceinline__ void cf_dit_pass(double2* z, const CfPlan& P, int h, int g,
+                                            const double2* __restrict__ chat = nullptr) {
     constexpr int E = 1 << R;
     const int n = P.n, j = g % h, i0 = (g / h) * E * h + j;
     double2 v[E];
@@ -759,7 +760,85 @@ __device__ __forceinline__ void cf_dit_pass(double2* z, const CfPlan& P, int h, 
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        z[P.at(i0 + e * h)] = v[e];
+        z[P.at(i0 + e * h)] = MUL ? cmul(v[e], chat[i0 + e * h]) : v[e]; // MUL: the last pass, natural order
+}
+
+// The first three DIT stages (spans 1, 2, 4: every twiddle a power of the 8th root) straight
+// from the two input rows: bit-reversed position 8g + e holds x[jj + brev3(e) n / 8] for
+// g = brev(jj), so consecutive threads load consecutive columns (coalesced) and, thanks to the
+// padding's i >> sh term, store to distinct bank groups.
+__device__ __forceinline__ void cf_dit_first(double2* z, const CfPlan& P, int jj, const double* __restrict__ a0,
+                                             const double* __restrict__ a1, bool two) {
+    const int n8 = P.n >> 3;
+    const int g = static_cast<int>(__brev(static_cast<unsigned>(jj)) >> (35 - P.lg));
+    double2 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int src = jj + ((((e & 1) << 2) | (e & 2) | ((e >> 2) & 1)) * n8); // brev3(e) n / 8
+        v[e] = make_double2(__ldcs(a0 + src), two ? __ldcs(a1 + src) : 0.0);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if ((e >> s) & 1)
+                continue;
+            const int r = e & ((1 << s) - 1);
+            double2 t = v[e + (1 << s)];
+            if (s == 1 && r == 1)
+                t = mul_mi(t);
+            if (s == 2 && r == 1)
+                t = mul_w8(t);
+            if (s == 2 && r == 2)
+                t = mul_mi(t);
+            if (s == 2 && r == 3)
+                t = mul_w8_3(t);
+            v[e + (1 << s)] = csub(v[e], t);
+            v[e] = cadd(v[e], t);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+        z[P.at(8 * g + e)] = v[e];
+}
+
+// The last three DIF stages (spans 4, 2, 1) straight to the two output rows: bit-reversed
+// position 8g + e is natural column jj + brev3(e) n / 8 (coalesced stores).
+__device__ __forceinline__ void cf_dif_last(const double2* z, const CfPlan& P, int jj, double* __restrict__ o0,
+                                            double* __restrict__ o1, bool two) {
+    const int n8 = P.n >> 3;
+    const int g = static_cast<int>(__brev(static_cast<unsigned>(jj)) >> (35 - P.lg));
+    double2 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+        v[e] = z[P.at(8 * g + e)];
+#pragma unroll
+    for (int s = 2; s >= 0; --s) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if ((e >> s) & 1)
+                continue;
+            const int r = e & ((1 << s) - 1);
+            double2 d = csub(v[e], v[e + (1 << s)]);
+            v[e] = cadd(v[e], v[e + (1 << s)]);
+            if (s == 1 && r == 1)
+                d = cconj(mul_mi(cconj(d)));
+            if (s == 2 && r == 1)
+                d = cconj(mul_w8(cconj(d)));
+            if (s == 2 && r == 2)
+                d = cconj(mul_mi(cconj(d)));
+            if (s == 2 && r == 3)
+                d = cconj(mul_w8_3(cconj(d)));
+            v[e + (1 << s)] = d;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int dst = jj + ((((e & 1) << 2) | (e & 2) | ((e >> 2) & 1)) * n8);
+        __stcs(o0 + dst, v[e].x);
+        if (two)
+            __stcs(o1 + dst, v[e].y);
+    }
 }
 
 // One pass of R fused DIF stages with conjugate twiddles (spans 2^(R-1) q, ..., q) on a group
@@ -801,21 +880,24 @@ __device__ __forceinline__ void cf_dif_pass(double2* z, const CfPlan& P, int q, 
         z[P.at(i0 + e * q)] = v[e];
 }
 
-// forward DFT (w = exp(-2 pi i / n)) in place: bit-reversed input, natural output
-__device__ void cf_dit(double2* z, const CfPlan& P, int t) {
+// forward DFT (w = exp(-2 pi i / n)) in place: bit-reversed input, natural output; stages from
+// span h0 on (h0 = 8 after cf_dit_first); MUL: multiply by chat in the last pass
+template <bool MUL>
+__device__ void cf_dit(double2* z, const CfPlan& P, int t, int h0, const double2* __restrict__ chat) {
     const int n = P.n;
-    int h = 1, left = P.lg;
+    int h = h0, left = P.lg - (31 - __clz(h0));
     while (left > 0) {
         const int R = left >= 3 ? 3 : left;
+        const bool last = left == R;
         if (R == 3) {
             for (int g = t; g < n / 8; g += CF_THREADS)
-                cf_dit_pass<3>(z, P, h, g);
+                last && MUL ? cf_dit_pass<3, true>(z, P, h, g, chat) : cf_dit_pass<3>(z, P, h, g);
         } else if (R == 2) {
             for (int g = t; g < n / 4; g += CF_THREADS)
-                cf_dit_pass<2>(z, P, h, g);
+                last && MUL ? cf_dit_pass<2, true>(z, P, h, g, chat) : cf_dit_pass<2>(z, P, h, g);
         } else {
             for (int g = t; g < n / 2; g += CF_THREADS)
-                cf_dit_pass<1>(z, P, h, g);
+                last && MUL ? cf_dit_pass<1, true>(z, P, h, g, chat) : cf_dit_pass<1>(z, P, h, g);
         }
         h <<= R;
         left -= R;
@@ -823,12 +905,14 @@ __device__ void cf_dit(double2* z, const CfPlan& P, int t) {
     }
 }
 
-// inverse DFT without the 1/n (conjugate twiddles) in place: natural input, bit-reversed output
-__device__ void cf_dif_inv(double2* z, const CfPlan& P, int t) {
+// inverse DFT without the 1/n (conjugate twiddles) in place: natural input, bit-reversed output;
+// the lg mod 3 largest spans first, then radix-2^3 passes; stops `stop` stages early (3: the
+// last pass is cf_dif_last)
+__device__ void cf_dif_inv(double2* z, const CfPlan& P, int t, int stop) {
     const int n = P.n;
-    int left = P.lg, hs = n; // the remaining stages have spans below hs
+    int left = P.lg - stop, hs = n; // the remaining stages have spans below hs
     while (left > 0) {
-        const int R = left >= 3 ? 3 : left;
+        const int R = (left % 3) ? left % 3 : 3;
         const int q = hs >> R; // smallest span of this pass
         if (R == 3) {
             for (int g = t; g < n / 8; g += CF_THREADS)
@@ -880,7 +964,7 @@ __global__ void __launch_bounds__(CF_THREADS) k_circ_fft_prep(int n, const doubl
     for (int j = t; j < n; j += CF_THREADS)
         cz[P.at(P.brev(j))] = make_double2(c[j], 0.0);
     __syncthreads();
-    cf_dit(cz, P, t);
+    cf_dit<false>(cz, P, t, 1, nullptr);
     const double inv_n = 1.0 / n; // a power of two: exact
     for (int k = t; k < n; k += CF_THREADS) {
         const double2 v = cz[P.at(k)];
@@ -911,22 +995,15 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, in
                              "r"(static_cast<uint32_t>(n * sizeof(double)))
                              : "memory");
         }
-        for (int j = t; j < n; j += CF_THREADS)
-            cz[P.at(P.brev(j))] = make_double2(__ldcs(a0 + j), two ? __ldcs(a1 + j) : 0.0);
+        for (int jj = t; jj < n / 8; jj += CF_THREADS)
+            cf_dit_first(cz, P, jj, a0, a1, two);
         __syncthreads();
-        cf_dit(cz, P, t);
-        for (int k = t; k < n; k += CF_THREADS)
-            cz[P.at(k)] = cmul(cz[P.at(k)], chat[k]);
-        __syncthreads();
-        cf_dif_inv(cz, P, t);
+        cf_dit<true>(cz, P, t, 8, chat); // the rest of the forward transform, then x conj(FFT(c)) / n
+        cf_dif_inv(cz, P, t, 3);
         double* o0 = out + r * ldo;
         double* o1 = o0 + ldo;
-        for (int j = t; j < n; j += CF_THREADS) {
-            const double2 v = cz[P.at(P.brev(j))];
-            __stcs(o0 + j, v.x);
-            if (two)
-                __stcs(o1 + j, v.y);
-        }
+        for (int jj = t; jj < n / 8; jj += CF_THREADS)
+            cf_dif_last(cz, P, jj, o0, o1, two);
         __syncthreads();
     }
 }
