@@ -504,6 +504,28 @@ int rlo_circ_apply_right(uint64_t n, const double* c, const double* a, double* o
     return st;
 }
 
+/* structured.cpp:156-176: T x for the m x n Toeplitz (first column col, first row row), via
+ * the circulant of power-of-two order len >= m + n - 1 whose first column is col followed by the
+ * reversed strict first row in the wrap-around positions; y = the first m entries. */
+int rlo_toeplitz_mul(uint64_t m, uint64_t n, const double* col, const double* row, const double* x, double* y) {
+    uint64_t len = 1;
+    while (len < m + n - 1)
+        len <<= 1;
+    double* buf = (double*)calloc(3 * len, sizeof(double));
+    double *ce = buf, *xp = buf + len, *full = buf + 2 * len;
+    for (uint64_t i = 0; i < m; ++i)
+        ce[i] = col[i];
+    for (uint64_t j = 1; j < n; ++j)
+        ce[len - j] = row[j];
+    for (uint64_t i = 0; i < n; ++i)
+        xp[i] = x[i];
+    int st = rlo_circ_mul(len, ce, xp, full);
+    for (uint64_t i = 0; i < m; ++i)
+        y[i] = full[i];
+    free(buf);
+    return st;
+}
+
 /* NEW: A*H1*H2, H_i = I - (2/n) u_i u_i^T, u_i in {+-1}^n:
  *   w1 = A u1, t1 = (2/n) w1, w2 = A u2 - t1 (u1^T u2), t2 = (2/n) w2,
  *   out(i,j) = (A(i,j) - t1(i) u1(j)) - t2(i) u2(j). */
@@ -612,6 +634,44 @@ static int draw(mult_t* m, int tag, double mu, double sigma, uint64_t n, uint64_
             m->v1[i] = mu + sigma * rlo_gaussian(&r);
         return 0;
     }
+    case TAG_TOEPLITZ: { /* random_gen.cpp:94-103: col[0], col[1..n-1], row[1..n-1]; row[0] = col[0] */
+        m->v1 = (double*)malloc(n * sizeof(double));
+        m->v2 = (double*)malloc(n * sizeof(double));
+        rlo_rng r;
+        rlo_rng_init(&r, seed, sid);
+        m->v1[0] = mu + sigma * rlo_gaussian(&r);
+        m->v2[0] = m->v1[0];
+        for (uint64_t i = 1; i < n; ++i)
+            m->v1[i] = mu + sigma * rlo_gaussian(&r);
+        for (uint64_t j = 1; j < n; ++j)
+            m->v2[j] = mu + sigma * rlo_gaussian(&r);
+        return 0;
+    }
+    case TAG_HH_SIGN: { /* random_gen.cpp:125-143: I - u v^T / (u^T v), resampled while u^T v == 0 */
+        double* u = (double*)malloc(2 * n * sizeof(double));
+        double* v = u + n;
+        rlo_rng r;
+        rlo_rng_init(&r, seed, sid);
+        for (int attempt = 0; attempt < 64; ++attempt) {
+            for (uint64_t i = 0; i < n; ++i)
+                u[i] = rlo_sign(&r);
+            for (uint64_t i = 0; i < n; ++i)
+                v[i] = rlo_sign(&r);
+            double uv = 0.0;
+            for (uint64_t i = 0; i < n; ++i)
+                uv += u[i] * v[i];
+            if (uv == 0.0)
+                continue;
+            m->dense = (double*)malloc(n * n * sizeof(double));
+            for (uint64_t i = 0; i < n; ++i)
+                for (uint64_t j = 0; j < n; ++j)
+                    m->dense[i * n + j] = (i == j ? 1.0 : 0.0) - u[i] * v[j] / uv;
+            free(u);
+            return 0;
+        }
+        free(u);
+        return 9; /* Degenerate */
+    }
     case TAG_HH_PAIR:
         m->v1 = (double*)malloc(n * sizeof(double));
         m->v2 = (double*)malloc(n * sizeof(double));
@@ -639,11 +699,25 @@ static int apply_left_mat(const mult_t* m, const double* a, double* out) {
     switch (m->tag) {
     case TAG_GAUSSIAN:
     case TAG_UNIFORM:
+    case TAG_HH_SIGN:
         rlo_matmul(n, n, n, m->dense, a, out);
         return 0;
     case TAG_CIRC_SIGN:
     case TAG_CIRC_GAUSS:
         return rlo_circ_apply_left(n, m->v1, n, a, out);
+    case TAG_TOEPLITZ: { /* structured.cpp:178-189: column by column */
+        double* col = (double*)malloc(2 * n * sizeof(double));
+        int st = 0;
+        for (uint64_t j = 0; j < n && !st; ++j) {
+            for (uint64_t i = 0; i < n; ++i)
+                col[i] = a[i * n + j];
+            st = rlo_toeplitz_mul(n, n, m->v1, m->v2, col, col + n);
+            for (uint64_t i = 0; i < n; ++i)
+                out[i * n + j] = col[n + i];
+        }
+        free(col);
+        return st;
+    }
     default:
         return 2; /* new kinds: Right side only */
     }
@@ -655,11 +729,18 @@ static int apply_right_mat(const mult_t* m, const double* a, double* out) {
     switch (m->tag) {
     case TAG_GAUSSIAN:
     case TAG_UNIFORM:
+    case TAG_HH_SIGN:
         rlo_matmul(n, n, n, a, m->dense, out);
         return 0;
     case TAG_CIRC_SIGN:
     case TAG_CIRC_GAUSS:
         return rlo_circ_apply_right(n, m->v1, a, out);
+    case TAG_TOEPLITZ: { /* genp.cpp:175-180: row i of A T = toeplitz_mul(T^T, row i), T^T = toeplitz(row, col) */
+        int st = 0;
+        for (uint64_t i = 0; i < n && !st; ++i)
+            st = rlo_toeplitz_mul(n, n, m->v2, m->v1, a + i * n, out + i * n);
+        return st;
+    }
     case TAG_HH_PAIR:
         rlo_hh2_apply_right(n, m->v1, m->v2, a, out);
         return 0;
@@ -677,11 +758,14 @@ static int apply_vec(const mult_t* m, const double* v, double* out) {
     switch (m->tag) {
     case TAG_GAUSSIAN:
     case TAG_UNIFORM:
+    case TAG_HH_SIGN:
         rlo_matvec(n, n, m->dense, v, out);
         return 0;
     case TAG_CIRC_SIGN:
     case TAG_CIRC_GAUSS:
         return rlo_circ_mul(n, m->v1, v, out);
+    case TAG_TOEPLITZ:
+        return rlo_toeplitz_mul(n, n, m->v1, m->v2, v, out);
     case TAG_HH_PAIR:
         rlo_hh2_apply_vec(n, m->v1, m->v2, v, out);
         return 0;

@@ -27,6 +27,7 @@ void axpy_dev(uint64_t count, double alpha, const double* x, double* y);
 // structured.cu
 void circulant_dense_dev(uint64_t n, const double* c, double* out);
 void rank1_dense_dev(uint64_t n, const double* u, const double* v, double inv_uv, double* out);
+void toeplitz_dense_dev(uint64_t n, const double* g, double* out);
 void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
                          double s12, double* out, uint64_t ldo);
 void hh2_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* u1, const double* u2, const double* y,
@@ -114,6 +115,16 @@ void draw(Mult& m, int tag, double mu, double sigma, uint64_t n, uint64_t seed, 
             circulant_dense_dev(n, m.c, m.dense);
         }
         break;
+    case RL_TOEPLITZ_GAUSSIAN: {
+        // random_structured (random_gen.cpp:94-103): n x n, col[0], col[1..n-1], row[1..n-1]
+        // on one stream (row[0] = col[0]); applied densified (the reference's FFT products,
+        // structured.cpp:156-189, equal it up to rounding)
+        double* g = ws<double>(slot_vec, 2 * n);
+        rng_generate(seed, sid, Draw::Gaussian, 2 * n - 1, mu, sigma, g);
+        m.dense = ws<double>(slot_dense, n * n);
+        toeplitz_dense_dev(n, g, m.dense);
+        break;
+    }
     case RL_HOUSEHOLDER_SIGN: {
         // random_gen.cpp:125-143: u, v signs; resample while u^T v == 0 (<= 64)
         double* uv = ws<double>(slot_vec, 2 * n * 64);
@@ -278,8 +289,6 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
         fail(RL_INVALID_ARGUMENT, "randomized_genp: refine must be in {0, 1, 2}");
     if (side < 0 || side > 2)
         fail(RL_INVALID_ARGUMENT, "randomized_genp: bad side");
-    if (tag == RL_TOEPLITZ_GAUSSIAN)
-        fail(RL_INVALID_ARGUMENT, "randomized_genp: ToeplitzGaussian needs m x n specs (not a square multiplier)");
     if ((tag == RL_HOUSEHOLDER_PAIR || tag == RL_SPARSE_SIGN) && side != RL_RIGHT)
         fail(RL_INVALID_ARGUMENT, "randomized_genp: the new multiplier kinds are applied on the right");
     const bool use_left = side == RL_LEFT || side == RL_BOTH;

@@ -28,6 +28,17 @@ __global__ void k_circulant_dense(uint64_t n, const double* c, double* out) {
     }
 }
 
+// T(i, j) = col[i - j] (i >= j) or row[j - i] (j > i) with g = col[0..n-1], row[1..n-1]
+// (random_structured's draw order, random_gen.cpp:94-103; densify, structured.cpp:70-83)
+__global__ void k_toeplitz_dense(uint64_t n, const double* g, double* out) {
+    uint64_t total = n * n;
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t i = e / n, j = e % n;
+        out[e] = i >= j ? g[i - j] : g[n - 1 + (j - i)];
+    }
+}
+
 __global__ void k_rank1_dense(uint64_t n, const double* u, const double* v, double inv_uv, double* out) {
     uint64_t total = n * n;
     for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -562,6 +573,11 @@ unsigned grid_for(uint64_t total, int threads) {
 
 void circulant_dense_dev(uint64_t n, const double* c, double* out) {
     k_circulant_dense<<<grid_for(n * n, 256), 256, 0, stream()>>>(n, c, out);
+    RL_LAUNCHED();
+}
+
+void toeplitz_dense_dev(uint64_t n, const double* g, double* out) {
+    k_toeplitz_dense<<<grid_for(n * n, 256), 256, 0, stream()>>>(n, g, out);
     RL_LAUNCHED();
 }
 

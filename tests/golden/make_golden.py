@@ -67,6 +67,12 @@ y, rep = R.randomized_genp(A, b, "gaussian", "left", 0, seed=seed, sid=11)
 g["c1/gaussian/left/y"], g["c1/gaussian/left/report"] = y, rep
 y, rep = R.randomized_genp(A, b, "circulant_sign", "both", 1, seed=seed, sid=11)
 g["c1/circulant_sign/both/y"], g["c1/circulant_sign/both/report"] = y, rep
+# the other reference multiplier kinds of draw_multiplier (genp.cpp:183-203) on every side
+for kind in ("toeplitz_gaussian", "householder_sign"):
+    for side in ("right", "left", "both"):
+        for refine in (0, 1):
+            y, rep = R.randomized_genp(A, b, kind, side, refine, seed=seed, sid=11)
+            g[f"c1/{kind}/{side}/r{refine}/y"], g[f"c1/{kind}/{side}/r{refine}/report"] = y, rep
 
 # --- config 2 shape (n = 64 systems, circulant sign, Right) --------------------------
 batch, n2, seed2 = 48, 64, 4096

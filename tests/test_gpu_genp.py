@@ -283,3 +283,35 @@ def test_randomized_genp_circulant_fft_path(rl, oracle, kind):
     assert rep.attempt == eo[0]
     assert rel(x, xo) < 1e-8
     assert bwd(A, x, b) <= 4 * bwd(A, xo, b) + 1e-15
+
+
+@pytest.mark.parametrize("side", ["right", "left", "both"])
+@pytest.mark.parametrize("refine", [0, 1])
+def test_randomized_genp_toeplitz(rl, golden, side, refine):
+    """randomized_genp with the ToeplitzGaussian multiplier (random_structured n x n, draw order
+    col[0], col[1..n-1], row[1..n-1]) on every side against the reference's fixtures: same
+    accepted attempt, x and backward error within the config-1 tolerances, pivots within 1e-6."""
+    A, b = golden["c1/A"], golden["c1/b"]
+    sd = getattr(rl.MulSide, side.upper())
+    x, rep = rl.randomized_genp(A, b, rl.MultiplierKind(rl.MultiplierTag.TOEPLITZ_GAUSSIAN), sd, refine,
+                                rl.RngStream(20260825, 11))
+    y_ref = golden[f"c1/toeplitz_gaussian/{side}/r{refine}/y"]
+    rep_ref = golden[f"c1/toeplitz_gaussian/{side}/r{refine}/report"]
+    assert rep.attempt == 0 and rep.residual <= 1e-7
+    assert rel(x, y_ref) < 1e-7
+    assert bwd(A, x, b) <= 4 * bwd(A, y_ref, b) + 1e-16
+    assert rel(np.array([rep.pivot_min, rep.pivot_max]), rep_ref[2:4]) < 1e-6
+
+
+@pytest.mark.parametrize("side", ["right", "left"])
+def test_randomized_genp_householder_sign(rl, golden, side):
+    """The singular Householder sign multiplier I - u v^T/(u^T v) (idempotent, rank n - 1): no
+    attempt reaches 1e-7 on either implementation; all 8 draws are used and the best residual
+    is of the reference's magnitude."""
+    A, b = golden["c1/A"], golden["c1/b"]
+    sd = getattr(rl.MulSide, side.upper())
+    x, rep = rl.randomized_genp(A, b, rl.MultiplierKind(rl.MultiplierTag.HOUSEHOLDER_SIGN), sd, 0,
+                                rl.RngStream(20260825, 11))
+    rep_ref = golden[f"c1/householder_sign/{side}/r0/report"]
+    assert rep.attempts_drawn == 8 and rep.residual > 1e-7
+    assert rep_ref[0] / 10 < rep.residual < rep_ref[0] * 10
