@@ -133,6 +133,12 @@ rl_status rl_dev_householder_pair_apply_right(uint64_t n, const double* d_u1, co
  * FFT (matrix-free, O(m n log n)); other n through a dense product. */
 rl_status rl_dev_circulant_apply_right(uint64_t m, uint64_t n, const double* d_c, const double* d_a,
                                        double* d_out);
+/* out = A T for the n x n Toeplitz T(i,j) = col[i-j] (i >= j), row[j-i] (j > i) (structured::toeplitz,
+ * structured.cpp:61-68; toeplitz_mul's circulant embedding, :156-176): d_g = col[0..n-1] followed by
+ * row[1..n-1] (random_structured's draw order).  FFT of the embedding for next_pow2(2n-1) <= 8192,
+ * a dense product otherwise; out != a. */
+rl_status rl_dev_toeplitz_apply_right(uint64_t m, uint64_t n, const double* d_g, const double* d_a,
+                                      double* d_out);
 
 /* -------------------------------------------- matrix.hpp (matrix.cpp) ---- */
 /* Matrix::multiply(const Matrix&) (matrix.cpp:86-102): C(m x n) = A(m x k) B(k x n). */

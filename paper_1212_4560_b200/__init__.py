@@ -34,7 +34,7 @@ __all__ = [
     "randomized_genp_batched", "approx_basis", "qr_positive", "project_onto_basis", "numerical_rank",
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
     "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
-    "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
+    "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_toeplitz_apply_right", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
     "box_muller_fast_check", "launch_count", "LIB_PATH",
 ]
 
@@ -207,6 +207,7 @@ def lib() -> C.CDLL:
         "rl_dev_sparse_apply_right": [u64, cint, vp, vp, vp, vp],
         "rl_dev_householder_pair_apply_right": [u64, vp, vp, vp, vp],
         "rl_dev_circulant_apply_right": [u64, u64, vp, vp, vp],
+        "rl_dev_toeplitz_apply_right": [u64, u64, vp, vp, vp],
         "rl_matmul": [u64, u64, u64, _d, _d, _d],
         "rl_dev_gemm": [cint, cint, u64, u64, u64, dbl, vp, u64, vp, u64, dbl, vp, u64],
         "rl_circ_mul": [u64, _d, _d, _d],
@@ -572,6 +573,19 @@ def dev_circulant_apply_right(c, a, out) -> None:
     if c.shape[0] != n or out.shape != (m, n):
         raise DimensionMismatch("circulant_apply_right: shape mismatch")
     _chk(lib().rl_dev_circulant_apply_right(m, n, _ptr(c), _ptr(a), _ptr(out)))
+
+
+def dev_toeplitz_apply_right(col, row, a, out) -> None:
+    """out = A T on device tensors for the Toeplitz with first column col and first row row
+    (row[0] == col[0]); FFT of the circulant embedding when next_pow2(2n - 1) <= 8192."""
+    import torch
+    _bind_stream()
+    m, n = a.shape
+    if col.shape[0] != n or row.shape[0] != n or out.shape != (m, n):
+        raise DimensionMismatch("toeplitz_apply_right: shape mismatch")
+    g = torch.cat([col, row[1:]]).contiguous()
+    _chk(lib().rl_dev_toeplitz_apply_right(m, n, _ptr(g), _ptr(a), _ptr(out)))
+    torch.cuda.current_stream().synchronize()  # g is a temporary
 
 
 def dev_qr_positive(y, q, r) -> None:

@@ -39,6 +39,10 @@ void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const doub
 void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
                          double s12, double* out, uint64_t ldo);
 bool circ_fft_supported(uint64_t n);
+uint64_t toeplitz_fft_len(uint64_t n);
+void toeplitz_apply_right_fft_dev(uint64_t m, uint64_t n, const double* g, const double* a, uint64_t lda,
+                                  double* out, uint64_t ldo);
+void toeplitz_dense_dev(uint64_t n, const double* g, double* out);
 void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
                               uint64_t ldo);
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r);
@@ -394,6 +398,22 @@ rl_status rl_dev_circulant_apply_right(uint64_t m, uint64_t n, const double* d_c
     } else {
         double* dense = ws<double>(WS_TMP2, n * n);
         circulant_dense_dev(n, d_c, dense);
+        gemm(false, false, m, n, n, 1.0, d_a, n, dense, n, 0.0, d_out, n);
+    }
+    API_END
+}
+
+rl_status rl_dev_toeplitz_apply_right(uint64_t m, uint64_t n, const double* d_g, const double* d_a,
+                                      double* d_out) {
+    API_BEGIN
+    require_positive(m, n, "toeplitz_apply_right");
+    if (d_a == d_out)
+        fail(RL_INVALID_ARGUMENT, "toeplitz_apply_right: out must not alias a");
+    if (toeplitz_fft_len(n) != 0) {
+        toeplitz_apply_right_fft_dev(m, n, d_g, d_a, n, d_out, n);
+    } else {
+        double* dense = ws<double>(WS_TMP2, n * n);
+        toeplitz_dense_dev(n, d_g, dense);
         gemm(false, false, m, n, n, 1.0, d_a, n, dense, n, 0.0, d_out, n);
     }
     API_END

@@ -37,6 +37,10 @@ void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const doub
 bool circ_fft_supported(uint64_t n);
 void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
                               uint64_t ldo);
+uint64_t toeplitz_fft_len(uint64_t n);
+void toeplitz_apply_right_fft_dev(uint64_t m, uint64_t n, const double* g, const double* a, uint64_t lda,
+                                  double* out, uint64_t ldo);
+void toeplitz_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* g, const double* z, double* y);
 struct SparseT {
     int32_t* row_ptr;
     int32_t* col_j;
@@ -71,7 +75,7 @@ struct Mult {
     int tag = 0;
     uint64_t n = 0;
     double* dense = nullptr; // n x n (dense kinds; circulant densified for the left product)
-    double* c = nullptr;     // circulant first column
+    double* c = nullptr;     // circulant first column; Toeplitz col[0..n-1], row[1..n-1]
     double* u1 = nullptr;
     double* u2 = nullptr;
     double s12 = 0.0;
@@ -117,12 +121,16 @@ void draw(Mult& m, int tag, double mu, double sigma, uint64_t n, uint64_t seed, 
         break;
     case RL_TOEPLITZ_GAUSSIAN: {
         // random_structured (random_gen.cpp:94-103): n x n, col[0], col[1..n-1], row[1..n-1]
-        // on one stream (row[0] = col[0]); applied densified (the reference's FFT products,
-        // structured.cpp:156-189, equal it up to rounding)
+        // on one stream (row[0] = col[0]); on the Right through the FFT of its circulant
+        // embedding when next_pow2(2n - 1) <= 8192 (as toeplitz_mul, structured.cpp:156-176),
+        // densified otherwise
         double* g = ws<double>(slot_vec, 2 * n);
         rng_generate(seed, sid, Draw::Gaussian, 2 * n - 1, mu, sigma, g);
-        m.dense = ws<double>(slot_dense, n * n);
-        toeplitz_dense_dev(n, g, m.dense);
+        m.c = g;
+        if (want_dense) {
+            m.dense = ws<double>(slot_dense, n * n);
+            toeplitz_dense_dev(n, g, m.dense);
+        }
         break;
     }
     case RL_HOUSEHOLDER_SIGN: {
@@ -206,6 +214,12 @@ void apply_right(const Mult& m, const double* sys, double* out) {
             return;
         }
         [[fallthrough]];
+    case RL_TOEPLITZ_GAUSSIAN:
+        if (!m.dense) {
+            toeplitz_apply_right_fft_dev(n, n, m.c, sys, n, out, n);
+            return;
+        }
+        [[fallthrough]];
     default:
         gemm(false, false, n, n, n, 1.0, sys, n, m.dense, n, 0.0, out, n);
     }
@@ -225,6 +239,13 @@ void apply_vec(const Mult& m, const double* v, uint64_t nrhs, double* out) {
     case RL_CIRCULANT_SIGN:
     case RL_CIRCULANT_GAUSSIAN:
         circ_apply_vec_dev(n, nrhs, m.c, v, out);
+        return;
+    case RL_TOEPLITZ_GAUSSIAN:
+        if (!m.dense) {
+            toeplitz_apply_vec_dev(n, nrhs, m.c, v, out);
+            return;
+        }
+        gemm(false, false, n, nrhs, n, 1.0, m.dense, n, v, nrhs, 0.0, out, nrhs);
         return;
     case RL_HOUSEHOLDER_PAIR:
         hh2_apply_vec_dev(n, nrhs, m.u1, m.u2, v, out);
@@ -361,7 +382,8 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
             } else {
                 // circulant multipliers of power-of-two n <= 8192 are applied on the right through
                 // the FFT (matrix-free); everything else is densified
-                const bool fft = (tag == RL_CIRCULANT_SIGN || tag == RL_CIRCULANT_GAUSSIAN) && circ_fft_supported(n);
+                const bool fft = ((tag == RL_CIRCULANT_SIGN || tag == RL_CIRCULANT_GAUSSIAN) && circ_fft_supported(n)) ||
+                                 (tag == RL_TOEPLITZ_GAUSSIAN && toeplitz_fft_len(n) != 0);
                 draw(right, tag, mu, sigma, n, seed, ds ^ 0x5000000000000000ULL,
                      use_left ? WS_RF1 : (speculate ? mult_slot[attempt & 1] : WS_MULT), WS_RF2, !fft);
             }

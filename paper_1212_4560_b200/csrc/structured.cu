@@ -784,14 +784,15 @@ __device__ __forceinline__ void cf_dit_pass(double2* z, const CfPlan& P, int h, 
 // g = brev(jj), so consecutive threads load consecutive columns (coalesced) and, thanks to the
 // padding's i >> sh term, store to distinct bank groups.
 __device__ __forceinline__ void cf_dit_first(double2* z, const CfPlan& P, int jj, const double* __restrict__ a0,
-                                             const double* __restrict__ a1, bool two) {
+                                             const double* __restrict__ a1, bool two, int n_in) {
     const int n8 = P.n >> 3;
     const int g = static_cast<int>(__brev(static_cast<unsigned>(jj)) >> (35 - P.lg));
     double2 v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int src = jj + ((((e & 1) << 2) | (e & 2) | ((e >> 2) & 1)) * n8); // brev3(e) n / 8
-        v[e] = make_double2(__ldcs(a0 + src), two ? __ldcs(a1 + src) : 0.0);
+        const bool in = src < n_in; // columns past n_in are the zero padding of an embedding
+        v[e] = make_double2(in ? __ldcs(a0 + src) : 0.0, (in && two) ? __ldcs(a1 + src) : 0.0);
     }
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
@@ -821,7 +822,7 @@ __device__ __forceinline__ void cf_dit_first(double2* z, const CfPlan& P, int jj
 // The last three DIF stages (spans 4, 2, 1) straight to the two output rows: bit-reversed
 // position 8g + e is natural column jj + brev3(e) n / 8 (coalesced stores).
 __device__ __forceinline__ void cf_dif_last(const double2* z, const CfPlan& P, int jj, double* __restrict__ o0,
-                                            double* __restrict__ o1, bool two) {
+                                            double* __restrict__ o1, bool two, int n_out) {
     const int n8 = P.n >> 3;
     const int g = static_cast<int>(__brev(static_cast<unsigned>(jj)) >> (35 - P.lg));
     double2 v[8];
@@ -851,9 +852,11 @@ __device__ __forceinline__ void cf_dif_last(const double2* z, const CfPlan& P, i
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int dst = jj + ((((e & 1) << 2) | (e & 2) | ((e >> 2) & 1)) * n8);
-        __stcs(o0 + dst, v[e].x);
-        if (two)
-            __stcs(o1 + dst, v[e].y);
+        if (dst < n_out) {
+            __stcs(o0 + dst, v[e].x);
+            if (two)
+                __stcs(o1 + dst, v[e].y);
+        }
     }
 }
 
@@ -989,7 +992,11 @@ __global__ void __launch_bounds__(CF_THREADS) k_circ_fft_prep(int n, const doubl
 }
 
 // out (m x n, ldo) = A (m x n, lda) C; persistent CTAs over row pairs
-__global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, int n, const double* __restrict__ a,
+// n: the transform length; rows of A hold n_in <= n columns (zero padding beyond), the first
+// n_out <= n columns of the product are written (n_in = n_out = n for a circulant; n_in =
+// n_out = the Toeplitz order inside its circulant embedding)
+__global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, int n, int n_in, int n_out,
+                                                                  const double* __restrict__ a,
                                                                   uint64_t lda, const double2* __restrict__ chat,
                                                                   double* __restrict__ out, uint64_t ldo) {
     extern __shared__ double2 cz[];
@@ -1008,18 +1015,18 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, in
             const uint64_t rows = (2 * (pr + gridDim.x) + 1 < m) ? 2 : 1;
             for (uint64_t q = 0; q < rows; ++q)
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + q * lda),
-                             "r"(static_cast<uint32_t>(n * sizeof(double)))
+                             "r"(static_cast<uint32_t>(n_in * sizeof(double)))
                              : "memory");
         }
         for (int jj = t; jj < n / 8; jj += CF_THREADS)
-            cf_dit_first(cz, P, jj, a0, a1, two);
+            cf_dit_first(cz, P, jj, a0, a1, two, n_in);
         __syncthreads();
         cf_dit<true>(cz, P, t, 8, chat); // the rest of the forward transform, then x conj(FFT(c)) / n
         cf_dif_inv(cz, P, t, 3);
         double* o0 = out + r * ldo;
         double* o1 = o0 + ldo;
         for (int jj = t; jj < n / 8; jj += CF_THREADS)
-            cf_dif_last(cz, P, jj, o0, o1, two);
+            cf_dif_last(cz, P, jj, o0, o1, two, n_out);
         __syncthreads();
     }
 }
@@ -1030,8 +1037,10 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, in
 bool circ_fft_supported(uint64_t n) { return n >= 64 && n <= CF_MAXN && (n & (n - 1)) == 0; }
 
 // out = A C for the circulant with first column c; A, out m x n (out != A)
-void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
-                              uint64_t ldo) {
+namespace {
+// the transform for rows of n_in columns against the length-n circulant c (n a power of two)
+void circ_right_fft_launch(uint64_t m, uint64_t n, uint64_t n_in, uint64_t n_out, const double* c, const double* a,
+                           uint64_t lda, double* out, uint64_t ldo) {
     const size_t smem = (n + n / 8 + 8) * sizeof(double2);
     static bool attr[16] = {};
     if (!attr[ctx().device & 15]) {
@@ -1044,7 +1053,58 @@ void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const dou
     k_circ_fft_prep<<<1, CF_THREADS, smem, stream()>>>(static_cast<int>(n), c, chat);
     RL_LAUNCHED();
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((m + 1) / 2, ctx().sms));
-    k_circ_right_fft<<<grid, CF_THREADS, smem, stream()>>>(m, static_cast<int>(n), a, lda, chat, out, ldo);
+    k_circ_right_fft<<<grid, CF_THREADS, smem, stream()>>>(m, static_cast<int>(n), static_cast<int>(n_in),
+                                                           static_cast<int>(n_out), a, lda, chat, out, ldo);
+    RL_LAUNCHED();
+}
+
+// circulant embedding of the n x n Toeplitz (g = col[0..n-1], row[1..n-1]): c2[k] = col[k],
+// c2[len - j] = row[j], zero elsewhere (structured.cpp:156-176)
+__global__ void k_toeplitz_embed(uint64_t n, uint64_t len, const double* g, double* c2) {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < len;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        c2[k] = k < n ? g[k] : (k > len - n ? g[n - 1 + (len - k)] : 0.0);
+}
+
+// x = T z (nrhs columns, ld nrhs), T(i, j) = col[i - j] / row[j - i], ascending j
+__global__ void k_toeplitz_vec(uint64_t n, uint64_t nrhs, const double* g, const double* z, double* y) {
+    uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (e >= n * nrhs)
+        return;
+    uint64_t i = e / nrhs, col = e % nrhs;
+    double s = 0.0;
+    for (uint64_t j = 0; j < n; ++j)
+        s = fma(i >= j ? g[i - j] : g[n - 1 + (j - i)], z[j * nrhs + col], s);
+    y[e] = s;
+}
+} // namespace
+
+void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
+                              uint64_t ldo) {
+    circ_right_fft_launch(m, n, n, n, c, a, lda, out, ldo);
+}
+
+// the embedding length when the Toeplitz product can take the FFT path (0 otherwise)
+uint64_t toeplitz_fft_len(uint64_t n) {
+    uint64_t len = 1;
+    while (len < 2 * n - 1)
+        len <<= 1;
+    return (n >= 2 && circ_fft_supported(len)) ? len : 0;
+}
+
+// out = A T for the n x n Toeplitz of g (A, out m x n, out != A): the circulant of order
+// len = next_pow2(2n - 1) on zero-padded rows, first n columns kept
+void toeplitz_apply_right_fft_dev(uint64_t m, uint64_t n, const double* g, const double* a, uint64_t lda,
+                                  double* out, uint64_t ldo) {
+    const uint64_t len = toeplitz_fft_len(n);
+    double* c2 = ws<double>(WS_TMP2, len);
+    k_toeplitz_embed<<<cdiv(len, 256), 256, 0, stream()>>>(n, len, g, c2);
+    RL_LAUNCHED();
+    circ_right_fft_launch(m, len, n, n, c2, a, lda, out, ldo);
+}
+
+void toeplitz_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* g, const double* z, double* y) {
+    k_toeplitz_vec<<<cdiv(n * nrhs, 256), 256, 0, stream()>>>(n, nrhs, g, z, y);
     RL_LAUNCHED();
 }
 

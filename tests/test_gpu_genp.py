@@ -315,3 +315,24 @@ def test_randomized_genp_householder_sign(rl, golden, side):
     rep_ref = golden[f"c1/householder_sign/{side}/r0/report"]
     assert rep.attempts_drawn == 8 and rep.residual > 1e-7
     assert rep_ref[0] / 10 < rep.residual < rep_ref[0] * 10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(256, 256), (77, 1000), (4096, 4096), (30, 5000)])
+def test_toeplitz_apply_right(rl, m, n):
+    """A T for a Toeplitz multiplier (T(i,j) = col[i-j] / row[j-i], structured.cpp:70-83) through
+    the FFT of its circulant embedding (toeplitz_mul, structured.cpp:156-176; order
+    next_pow2(2n - 1) <= 8192) or the dense fallback (n = 5000), against numpy's dense product."""
+    import torch
+    rng = np.random.default_rng(n)
+    col, row = rng.standard_normal(n), rng.standard_normal(n)
+    row[0] = col[0]
+    a = rng.standard_normal((m, n))
+    i, j = np.arange(n)[:, None], np.arange(n)[None, :]
+    T = np.where(i >= j, col[np.abs(i - j)], row[np.abs(j - i)])
+    want = a @ T
+    dev = torch.device("cuda", 0)
+    out = torch.empty(m, n, dtype=torch.float64, device=dev)
+    rl.dev_toeplitz_apply_right(torch.from_numpy(col).to(dev), torch.from_numpy(row).to(dev),
+                                torch.from_numpy(a).to(dev), out)
+    assert np.abs(out.cpu().numpy() - want).max() <= 1e-13 * np.abs(want).max() * max(1.0, np.log2(n) / 4)
