@@ -41,6 +41,8 @@ uint64_t toeplitz_fft_len(uint64_t n);
 void toeplitz_apply_right_fft_dev(uint64_t m, uint64_t n, const double* g, const double* a, uint64_t lda,
                                   double* out, uint64_t ldo);
 void toeplitz_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* g, const double* z, double* y);
+void spec_transpose_dev(uint64_t n, bool toeplitz, const double* g, double* out);
+void transpose_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, double* t, uint64_t ldt);
 struct SparseT {
     int32_t* row_ptr;
     int32_t* col_j;
@@ -229,6 +231,22 @@ void apply_right(const Mult& m, const double* sys, double* out) {
 void apply_left(const Mult& m, const double* sys, uint64_t cols, double* out) {
     const uint64_t n = m.n;
     wait_upload(sys);
+    if (!m.dense && (m.tag == RL_CIRCULANT_SIGN || m.tag == RL_CIRCULANT_GAUSSIAN || m.tag == RL_TOEPLITZ_GAUSSIAN)) {
+        // M A = (A^T M^T)^T with M^T = transpose_spec(M) (structured.cpp:85-94): the Right-side
+        // FFT product between two transposes
+        const bool tp = m.tag == RL_TOEPLITZ_GAUSSIAN;
+        double* t1 = ws<double>(WS_T1, n * cols);
+        double* t2 = ws<double>(WS_T2, n * cols + 2 * n);
+        double* spec = t2 + n * cols;
+        transpose_dev(n, cols, sys, cols, t1, n);
+        spec_transpose_dev(n, tp, m.c, spec);
+        if (tp)
+            toeplitz_apply_right_fft_dev(cols, n, spec, t1, n, t2, n);
+        else
+            circ_apply_right_fft_dev(cols, n, spec, t1, n, t2, n);
+        transpose_dev(cols, n, t2, n, out, cols);
+        return;
+    }
     gemm(false, false, n, cols, n, 1.0, m.dense, n, sys, cols, 0.0, out, cols);
 }
 
@@ -370,8 +388,10 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
         const uint64_t ds = sid + 7919ULL * static_cast<uint64_t>(attempt);
         rep.attempts_drawn = attempt + 1;
         Mult left, right;
-        if (use_left)
-            draw(left, tag, mu, sigma, n, seed, ds, WS_MULT, WS_LVEC, true);
+        if (use_left) // circulant / Toeplitz multipliers stay matrix-free when the FFT path takes them
+            draw(left, tag, mu, sigma, n, seed, ds, WS_MULT, WS_LVEC,
+                 !(((tag == RL_CIRCULANT_SIGN || tag == RL_CIRCULANT_GAUSSIAN) && circ_fft_supported(n)) ||
+                   (tag == RL_TOEPLITZ_GAUSSIAN && toeplitz_fft_len(n) != 0)));
         if (use_right) {
             if (spec_attempt == attempt) {
                 right.tag = tag;

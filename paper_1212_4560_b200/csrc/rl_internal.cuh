@@ -60,7 +60,7 @@ struct Ctx {
     int device = -1;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr; // what rl_dev_* calls launch on
-    DevBuf ws[32];                 // named scratch slots (see WS_* below)
+    DevBuf ws[40];                 // named scratch slots (see WS_* below)
     uint64_t launches = 0;
     int sms = 148;
     PendingUpload upload;          // set only inside a host-pointer call
@@ -73,7 +73,7 @@ void wait_upload(const double* dev);
 enum WsSlot {
     WS_IN_A = 0, WS_IN_B, WS_OUT, WS_MULT, WS_SYS, WS_RHS, WS_TMP1, WS_TMP2, WS_RNG,
     WS_RNG2, WS_SMALL, WS_LU_AUX, WS_BATCH, WS_RF1, WS_RF2, WS_RF3, WS_LVEC, WS_RESID, WS_RF4,
-    WS_RF5, WS_RF6, WS_H0, WS_H1, WS_H2, WS_H3, WS_WAVE, WS_MULT2, WS_RNG3, WS_RNG4, WS_SPLAN
+    WS_RF5, WS_RF6, WS_H0, WS_H1, WS_H2, WS_H3, WS_WAVE, WS_MULT2, WS_RNG3, WS_RNG4, WS_SPLAN, WS_T1, WS_T2
 };
 
 Ctx& ctx();          // thread-local context (initialises the device on first use)

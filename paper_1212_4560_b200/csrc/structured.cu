@@ -1103,6 +1103,27 @@ void toeplitz_apply_right_fft_dev(uint64_t m, uint64_t n, const double* g, const
     circ_right_fft_launch(m, len, n, n, c2, a, lda, out, ldo);
 }
 
+namespace {
+// transpose_spec (structured.cpp:85-94) of a circulant (c'[k] = c[(n - k) mod n]) and of the
+// n x n Toeplitz (g' = row[0..n-1], col[1..n-1] from g = col[0..n-1], row[1..n-1])
+__global__ void k_spec_transpose(uint64_t n, int toeplitz, const double* g, double* out) {
+    const uint64_t len = toeplitz ? 2 * n - 1 : n;
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < len;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (!toeplitz)
+            out[k] = g[(n - k) % n];
+        else
+            out[k] = k == 0 ? g[0] : (k < n ? g[n - 1 + k] : g[k - n + 1]);
+    }
+}
+} // namespace
+
+void spec_transpose_dev(uint64_t n, bool toeplitz, const double* g, double* out) {
+    const uint64_t len = toeplitz ? 2 * n - 1 : n;
+    k_spec_transpose<<<cdiv(len, 256), 256, 0, stream()>>>(n, toeplitz ? 1 : 0, g, out);
+    RL_LAUNCHED();
+}
+
 void toeplitz_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* g, const double* z, double* y) {
     k_toeplitz_vec<<<cdiv(n * nrhs, 256), 256, 0, stream()>>>(n, nrhs, g, z, y);
     RL_LAUNCHED();
