@@ -42,6 +42,7 @@ struct Smem {
     uint64_t mask, mask0;
     unsigned bal[2];
     int flag;
+    rl_precond_report rp; // the system's report (thread 0), kept out of the register budget
 };
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
@@ -367,8 +368,11 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
     const double bsq = cta_sum(S, bt * bt, t);
     const uint64_t sid = sids[sys];
     double* xg = X + sys * N;
-    rl_precond_report rp{};
-    rp.attempt = -1;
+    rl_precond_report& rp = S.rp; // written by thread 0 only
+    if (t == 0) {
+        rp = rl_precond_report{};
+        rp.attempt = -1;
+    }
     int st = RL_PIVOT_BREAKDOWN;
     // pass 0: raw arm (a = -1) + pre-screened protocol; pass 1 (rare): exact protocol
     for (int pass = 0; pass < 2; ++pass) {
@@ -440,23 +444,28 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
             const double res = sqrt(cta_sum(S, e * e, t)) / sqrt(bsq);
             if (a < 0) { // contrast arm: non-finite solution -> +inf (genp.cpp:226-231)
                 const int fin = __syncthreads_and(!vt || isfinite(y));
-                rp.raw_residual = fin ? res : INFINITY;
-                rp.raw_pivot_min = pmn;
-                rp.raw_pivot_max = pmx;
+                if (t == 0) {
+                    rp.raw_residual = fin ? res : INFINITY;
+                    rp.raw_pivot_min = pmn;
+                    rp.raw_pivot_max = pmx;
+                }
                 continue;
             }
             const bool acc = res <= 1e-7;
             if (acc || !have_best || res < best_res) {
                 if (vt)
                     xg[t] = y;
-                rp.residual = res;
-                rp.pivot_min = pmn;
-                rp.pivot_max = pmx;
-                rp.attempt = a;
+                if (t == 0) {
+                    rp.residual = res;
+                    rp.pivot_min = pmn;
+                    rp.pivot_max = pmx;
+                    rp.attempt = a;
+                }
                 best_res = res;
                 have_best = true;
             }
-            rp.attempts_drawn = a + 1;
+            if (t == 0)
+                rp.attempts_drawn = a + 1;
             if (acc) {
                 accepted = true;
                 break;
