@@ -2,7 +2,7 @@ import sys, time
 sys.path.insert(0, ".")
 import torch, bench
 import paper_1212_4560_b200 as rl
-class A: warmup=3; steps=20
+class A: warmup=3; steps=20; no_cpu_baseline=True
 print(bench.run_config1(torch, rl, torch.device("cuda",0), None, A, 37.0))
 if len(sys.argv) > 1 and sys.argv[1] == "timeline":
     from torch.profiler import ProfilerActivity, profile
