@@ -1063,6 +1063,184 @@ void rlo_singular_values(uint64_t m, uint64_t n, const double* a, double* sigma)
     free(w);
 }
 
+/* Thin SVD of the m x n (m >= n) matrix a by the one-sided Jacobi above: sigma (descending) and
+ * the left singular vectors u (m x n row-major, column j for sigma_j; columns of zero singular
+ * values are left zero).  dense::svd (dense_core.cpp:117-136) is Eigen's; its rounding and the
+ * signs of the vectors are unpinned upstream, so the restatement fixes its own (the Jacobi
+ * result). */
+void rlo_svd_left(uint64_t m, uint64_t n, const double* a, double* sigma, double* u) {
+    double* w = (double*)malloc(m * n * sizeof(double));
+    for (uint64_t i = 0; i < m; ++i)
+        for (uint64_t j = 0; j < n; ++j)
+            w[j * m + i] = a[i * n + j];
+    for (int sweep = 0; sweep < 80; ++sweep) {
+        double off = 0.0;
+        for (uint64_t p = 0; p + 1 < n; ++p)
+            for (uint64_t q = p + 1; q < n; ++q) {
+                double *wp = w + p * m, *wq = w + q * m;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (uint64_t i = 0; i < m; ++i) {
+                    al += wp[i] * wp[i];
+                    be += wq[i] * wq[i];
+                    ga += wp[i] * wq[i];
+                }
+                if (ga == 0.0)
+                    continue;
+                double rel = fabs(ga) / sqrt(al * be);
+                if (!(rel > 1e-15))
+                    continue;
+                if (rel > off)
+                    off = rel;
+                double zeta = (be - al) / (2.0 * ga);
+                double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+                for (uint64_t i = 0; i < m; ++i) {
+                    double x = wp[i], yv = wq[i];
+                    wp[i] = c * x - sn * yv;
+                    wq[i] = sn * x + c * yv;
+                }
+            }
+        if (off <= 1e-15)
+            break;
+    }
+    /* order by descending norm (stable: ties keep column order) */
+    uint64_t* ord = (uint64_t*)malloc(n * sizeof(uint64_t));
+    double* nr = (double*)malloc(n * sizeof(double));
+    for (uint64_t j = 0; j < n; ++j) {
+        ord[j] = j;
+        nr[j] = vnorm2(m, w + j * m);
+    }
+    for (uint64_t i = 1; i < n; ++i)
+        for (uint64_t k = i; k > 0 && nr[ord[k]] > nr[ord[k - 1]]; --k) {
+            uint64_t tmp = ord[k];
+            ord[k] = ord[k - 1];
+            ord[k - 1] = tmp;
+        }
+    for (uint64_t j = 0; j < n; ++j) {
+        const double sg = nr[ord[j]];
+        sigma[j] = sg;
+        for (uint64_t i = 0; i < m; ++i)
+            u[i * n + j] = sg > 0.0 ? w[ord[j] * m + i] / sg : 0.0;
+    }
+    free(ord);
+    free(nr);
+    free(w);
+}
+
+/* lowrank::proto_lowrank (lowrank.cpp:108-177) for the Gaussian kind, RightSpace sketches
+ * (approx_basis, lowrank.cpp:67-106: sketch = A^T G, G = gaussian_matrix(m, rho_plus)), with
+ * the restated SVD above.  Outputs rho, basis (n x rho, ld rho_plus), approx (m x n), residual,
+ * ok.  Returns 2 on a bad argument. */
+int rlo_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus, double tau, double tau_prime,
+                      double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out, double* basis,
+                      double* approx, double* residual, int* ok) {
+    if (!(tau_prime > 0.0 && tau_prime < 1.0) || (tau > 0.0 && !(tau < 1.0)))
+        return 2;
+    if (rho_plus < 1 || rho_plus > (m < n ? m : n))
+        return 2;
+    const uint64_t k = m < n ? m : n;
+    double* sg = (double*)malloc((k + rho_plus) * sizeof(double));
+    double* ua = (double*)malloc(m * n * sizeof(double));
+    /* ||A||_2 = sigma_1(A) */
+    if (m >= n)
+        rlo_svd_left(m, n, a, sg, ua);
+    else {
+        double* at = (double*)malloc(m * n * sizeof(double));
+        rlo_transpose(m, n, a, at);
+        rlo_svd_left(n, m, at, sg, ua);
+        free(at);
+    }
+    const double norm_a = sg[0];
+    *rho_out = 0;
+    *residual = 0.0;
+    *ok = 0;
+    memset(approx, 0, m * n * sizeof(double));
+    if (norm_a == 0.0) {
+        *ok = 1;
+        free(sg);
+        free(ua);
+        return 0;
+    }
+    double* g = (double*)malloc(m * rho_plus * sizeof(double));
+    double* sk = (double*)malloc(n * rho_plus * sizeof(double));
+    double* us = (double*)malloc(n * rho_plus * sizeof(double));
+    double* ss = sg + k;
+    double* at = (double*)malloc(m * n * sizeof(double));
+    double* ab = (double*)malloc(m * rho_plus * sizeof(double));
+    double* diff = (double*)malloc(m * n * sizeof(double));
+    rlo_transpose(m, n, a, at);
+    for (int attempt = 0; attempt <= 3; ++attempt) {
+        const uint64_t ds = sid + 104729ULL * (uint64_t)attempt;
+        rlo_gaussian_matrix(m, rho_plus, mu, sig_g, seed, ds, g);
+        rlo_matmul(n, m, rho_plus, at, g, sk); /* A^T G */
+        rlo_svd_left(n, rho_plus, sk, ss, us);
+        double tau_eff = tau;
+        if (tau_eff <= 0.0) { /* lowrank.cpp:132-147 */
+            tau_eff = 1e-6;
+            double best_gap = 1.0;
+            for (uint64_t j = 1; j < rho_plus; ++j) {
+                if (ss[j] >= 1e-3 * ss[0])
+                    continue;
+                double gap = ss[j] / fmax(ss[j - 1], 1e-300);
+                if (gap < best_gap) {
+                    best_gap = gap;
+                    tau_eff = sqrt(fmax(ss[j] * ss[j - 1], 1e-300)) / norm_a;
+                }
+            }
+        }
+        uint64_t s = rho_plus;
+        while (s > 0 && ss[s - 1] <= tau_eff * norm_a)
+            --s;
+        if (s == 0) { /* only the zero matrix passes (handled above) */
+            *rho_out = 0;
+            memset(approx, 0, m * n * sizeof(double));
+            *residual = 1.0;
+            *ok = 0;
+            continue;
+        }
+        for (uint64_t i = 0; i < n; ++i)
+            for (uint64_t j = 0; j < rho_plus; ++j)
+                basis[i * rho_plus + j] = j < s ? us[i * rho_plus + j] : 0.0;
+        /* project_onto_basis (lowrank.cpp:45-65), Right, orthonormal: (A T) T^T */
+        for (uint64_t i = 0; i < m; ++i)
+            for (uint64_t j = 0; j < s; ++j) {
+                double acc = 0.0;
+                for (uint64_t l = 0; l < n; ++l)
+                    acc += a[i * n + l] * basis[l * rho_plus + j];
+                ab[i * rho_plus + j] = acc;
+            }
+        for (uint64_t i = 0; i < m; ++i)
+            for (uint64_t l = 0; l < n; ++l) {
+                double acc = 0.0;
+                for (uint64_t j = 0; j < s; ++j)
+                    acc += ab[i * rho_plus + j] * basis[l * rho_plus + j];
+                approx[i * n + l] = acc;
+                diff[i * n + l] = a[i * n + l] - acc;
+            }
+        if (m >= n)
+            rlo_svd_left(m, n, diff, sg, ua);
+        else {
+            rlo_transpose(m, n, diff, at);
+            rlo_svd_left(n, m, at, sg, ua);
+            rlo_transpose(m, n, a, at);
+        }
+        *rho_out = s;
+        *residual = sg[0] / norm_a;
+        *ok = *residual <= tau_prime;
+        if (*ok)
+            break;
+    }
+    free(g);
+    free(sk);
+    free(us);
+    free(at);
+    free(ab);
+    free(diff);
+    free(sg);
+    free(ua);
+    return 0;
+}
+
 /* dense_core.cpp:161-169 */
 uint64_t rlo_numerical_rank(uint64_t l, const double* sigma, double tol) {
     if (l == 0 || sigma[0] == 0.0)

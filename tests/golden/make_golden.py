@@ -104,5 +104,7 @@ qq, rr = R.qr_positive(M)
 g["qr/40x12/A"], g["qr/40x12/Q"], g["qr/40x12/R"] = M, qq, rr
 g["nrank/profile64"] = R.profile_matrix_paper(64, 8, 42, 90)
 
+# proto_lowrank test matrix (tests/test_lowrank.cpp:80-91): paper profile, rank 8 of 64
+g["proto/A"] = R.profile_matrix_paper(64, 8, 41, 10)
 np.savez_compressed(os.path.join(OUT, "golden.npz"), **g)
 print("wrote", os.path.join(OUT, "golden.npz"), len(g), "arrays")
