@@ -34,7 +34,7 @@ __all__ = [
     "randomized_genp_batched", "approx_basis", "qr_positive", "project_onto_basis", "numerical_rank",
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
     "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
-    "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_toeplitz_apply_right", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
+    "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_toeplitz_apply_right", "proto_lowrank", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
     "box_muller_fast_check", "launch_count", "LIB_PATH",
 ]
 
@@ -208,6 +208,8 @@ def lib() -> C.CDLL:
         "rl_dev_householder_pair_apply_right": [u64, vp, vp, vp, vp],
         "rl_dev_circulant_apply_right": [u64, u64, vp, vp, vp],
         "rl_dev_toeplitz_apply_right": [u64, u64, vp, vp, vp],
+        "rl_proto_lowrank": [u64, u64, _d, u64, dbl, dbl, dbl, dbl, u64, u64, C.POINTER(C.c_uint64), _d, _d,
+                             C.POINTER(C.c_double), C.POINTER(C.c_int)],
         "rl_matmul": [u64, u64, u64, _d, _d, _d],
         "rl_dev_gemm": [cint, cint, u64, u64, u64, dbl, vp, u64, vp, u64, dbl, vp, u64],
         "rl_circ_mul": [u64, _d, _d, _d],
@@ -586,6 +588,20 @@ def dev_toeplitz_apply_right(col, row, a, out) -> None:
     g = torch.cat([col, row[1:]]).contiguous()
     _chk(lib().rl_dev_toeplitz_apply_right(m, n, _ptr(g), _ptr(a), _ptr(out)))
     torch.cuda.current_stream().synchronize()  # g is a temporary
+
+
+def proto_lowrank(a, rho_plus: int, tau: float, tau_prime: float, kind: MultiplierKind, stream: RngStream):
+    """lowrank::proto_lowrank (lowrank.cpp:108-177), Gaussian kind: (rho, basis n x rho, approx,
+    residual, ok)."""
+    if kind.tag != MultiplierTag.GAUSSIAN:
+        raise InvalidArgument("proto_lowrank: only the Gaussian kind is on the B200 path")
+    a = _f64(a)
+    m, n = a.shape
+    basis, approx = np.empty((n, rho_plus)), np.empty((m, n))
+    rho, res, ok = C.c_uint64(0), C.c_double(0.0), C.c_int(0)
+    _chk(lib().rl_proto_lowrank(m, n, a, rho_plus, tau, tau_prime, kind.mu, kind.sigma, stream.seed,
+                                stream.stream_id, C.byref(rho), basis, approx, C.byref(res), C.byref(ok)))
+    return rho.value, basis[:, :rho.value].copy(), approx, res.value, bool(ok.value)
 
 
 def dev_qr_positive(y, q, r) -> None:

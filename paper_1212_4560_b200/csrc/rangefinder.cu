@@ -920,3 +920,231 @@ double sumsq_dev(uint64_t count, const double* x) {
 }
 
 } // namespace rl
+
+// ------------------------------------------------------------- proto_lowrank ----
+namespace rl {
+void transpose_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, double* t, uint64_t ldt);
+}
+// lowrank::proto_lowrank (lowrank.cpp:108-177), small n (the reference's own tests use 64):
+// Gaussian RightSpace sketches (approx_basis, lowrank.cpp:67-106), the thin SVD of the sketch
+// with left singular vectors (span_basis = its leading s left vectors), the auto-tau rule
+// (:132-147), projection A T T^T (project_onto_basis, :45-65) and ||A - A T T^T||_2 / ||A||_2.
+namespace rl {
+namespace {
+
+constexpr int PJ_T = 512, PJ_MAXC = 64, PJ_MAXR = 256;
+
+// One-sided Jacobi on the R x C matrix W (row-major, ld C, R >= C, C <= 64, R C <= 16384):
+// columns orthogonalised by round-robin rotations (C/2 disjoint pairs per step, one warp per
+// pair, warp-shuffle reductions in a fixed order), sweeps until every pair is orthogonal to
+// 1e-15 relative; sigma_j = ||w_j|| sorted descending (stable), u = normalised columns.
+__global__ void __launch_bounds__(PJ_T) k_jacobi_left(int R, int C, const double* __restrict__ w_in,
+                                                      double* __restrict__ sigma, double* __restrict__ u) {
+    extern __shared__ double W[]; // column-major: W[j * R + i]
+    __shared__ int perm[PJ_MAXC], order[PJ_MAXC];
+    __shared__ double nrm[PJ_MAXC];
+    __shared__ int rotated;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int e = t; e < R * C; e += PJ_T)
+        W[(e % C) * R + e / C] = w_in[e];
+    const int Ce = C + (C & 1); // even count: a dummy column when C is odd
+    if (t < Ce)
+        perm[t] = t;
+    __syncthreads();
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (t == 0)
+            rotated = 0;
+        __syncthreads();
+        for (int step = 0; step < Ce - 1; ++step) {
+            for (int pr = warp; pr < Ce / 2; pr += PJ_T / 32) {
+                int p = perm[pr], q = perm[Ce - 1 - pr];
+                if (p > q) {
+                    const int x = p;
+                    p = q;
+                    q = x;
+                }
+                if (q >= C)
+                    continue; // the dummy
+                double* wp = W + p * R;
+                double* wq = W + q * R;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = lane; i < R; i += 32) {
+                    al = fma(wp[i], wp[i], al);
+                    be = fma(wq[i], wq[i], be);
+                    ga = fma(wp[i], wq[i], ga);
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
+                if (ga == 0.0 || !(fabs(ga) > 1e-15 * sqrt(al * be)))
+                    continue;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+                for (int i = lane; i < R; i += 32) {
+                    const double x = wp[i], y = wq[i];
+                    wp[i] = c * x - s * y;
+                    wq[i] = s * x + c * y;
+                }
+                if (lane == 0)
+                    rotated = 1;
+            }
+            __syncthreads();
+            if (t == 0) { // round-robin: position 0 fixed, the others rotate
+                const int last = perm[Ce - 1];
+                for (int k = Ce - 1; k > 1; --k)
+                    perm[k] = perm[k - 1];
+                perm[1] = last;
+            }
+            __syncthreads();
+        }
+        if (!rotated)
+            break;
+        __syncthreads();
+    }
+    for (int j = warp; j < C; j += PJ_T / 32) {
+        double s2 = 0.0;
+        for (int i = lane; i < R; i += 32)
+            s2 = fma(W[j * R + i], W[j * R + i], s2);
+        for (int o = 16; o > 0; o >>= 1)
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (lane == 0)
+            nrm[j] = sqrt(s2);
+    }
+    __syncthreads();
+    if (t == 0) { // stable insertion sort, descending
+        for (int j = 0; j < C; ++j)
+            order[j] = j;
+        for (int i = 1; i < C; ++i)
+            for (int k = i; k > 0 && nrm[order[k]] > nrm[order[k - 1]]; --k) {
+                const int x = order[k];
+                order[k] = order[k - 1];
+                order[k - 1] = x;
+            }
+    }
+    __syncthreads();
+    for (int e = t; e < R * C; e += PJ_T) {
+        const int i = e / C, j = e % C, src = order[j];
+        const double sg = nrm[src];
+        if (u)
+            u[e] = sg > 0.0 ? W[src * R + i] / sg : 0.0;
+        if (i == 0)
+            sigma[j] = sg;
+    }
+}
+
+__global__ void k_sub(uint64_t count, const double* a, const double* b, double* c) {
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < count;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        c[e] = a[e] - b[e];
+}
+
+// sigma (and u) of the m x n device matrix a (row-major): the taller orientation goes in
+std::vector<double> jacobi_svd_dev(uint64_t m, uint64_t n, const double* a, double* d_sigma, double* d_u,
+                                   double* scratch) {
+    const double* src = a;
+    uint64_t R = m, C = n;
+    if (m < n) {
+        transpose_dev(m, n, a, n, scratch, m);
+        src = scratch;
+        R = n;
+        C = m;
+    }
+    static bool attr[16] = {};
+    if (!attr[ctx().device & 15]) {
+        RL_CUDA(cudaFuncSetAttribute(k_jacobi_left, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     PJ_MAXR * PJ_MAXC * 8));
+        attr[ctx().device & 15] = true;
+    }
+    k_jacobi_left<<<1, PJ_T, R * C * sizeof(double), stream()>>>(static_cast<int>(R), static_cast<int>(C), src,
+                                                                  d_sigma, d_u);
+    RL_LAUNCHED();
+    std::vector<double> h(C);
+    RL_CUDA(cudaMemcpyAsync(h.data(), d_sigma, C * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+    return h;
+}
+
+} // namespace
+
+bool proto_lowrank_supported(uint64_t m, uint64_t n, uint64_t rho_plus) {
+    const uint64_t k = m < n ? m : n, l = m < n ? n : m;
+    return k <= PJ_MAXC && l <= PJ_MAXR && rho_plus <= PJ_MAXC && n <= PJ_MAXR;
+}
+
+// d_a: m x n on the device.  basis: n x rho_plus (first rho columns valid), approx: m x n.
+void proto_lowrank_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_plus, double tau, double tau_prime,
+                       double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out, double* d_basis,
+                       double* d_approx, double* residual, int* ok) {
+    double* sc = ws<double>(WS_RF5, 4 * m * n + 2 * n * rho_plus + m * rho_plus + 2 * (m + n + rho_plus) + 64);
+    double* g = sc;                      // m x rho_plus
+    double* sk = g + m * rho_plus;       // n x rho_plus
+    double* ab = sk + n * rho_plus;      // m x rho_plus
+    double* diff = ab + m * rho_plus;    // m x n
+    double* scratch = diff + m * n;      // m x n (transposes)
+    double* usv = scratch + m * n;       // m x n (left vectors of A / diff, unused)
+    double* sg = usv + m * n;            // sigma scratch
+    const std::vector<double> sa = jacobi_svd_dev(m, n, d_a, sg, nullptr, scratch);
+    const double norm_a = sa[0];
+    *rho_out = 0;
+    *residual = 0.0;
+    *ok = 0;
+    RL_CUDA(cudaMemsetAsync(d_approx, 0, m * n * sizeof(double), stream()));
+    RL_CUDA(cudaMemsetAsync(d_basis, 0, n * rho_plus * sizeof(double), stream()));
+    if (norm_a == 0.0) {
+        *ok = 1;
+        RL_CUDA(cudaStreamSynchronize(stream()));
+        return;
+    }
+    for (int attempt = 0; attempt <= 3; ++attempt) {
+        const uint64_t ds = sid + 104729ULL * static_cast<uint64_t>(attempt);
+        rng_generate(seed, ds, Draw::Gaussian, m * rho_plus, mu, sig_g, g);
+        gemm(true, false, n, rho_plus, m, 1.0, d_a, n, g, rho_plus, 0.0, sk, rho_plus); // A^T G
+        const std::vector<double> ss = jacobi_svd_dev(n, rho_plus, sk, sg, d_basis, scratch);
+        double tau_eff = tau;
+        if (tau_eff <= 0.0) { // the auto rule (lowrank.cpp:132-147)
+            tau_eff = 1e-6;
+            double best_gap = 1.0;
+            for (size_t j = 1; j < ss.size(); ++j) {
+                if (ss[j] >= 1e-3 * ss[0])
+                    continue;
+                const double gap = ss[j] / std::max(ss[j - 1], 1e-300);
+                if (gap < best_gap) {
+                    best_gap = gap;
+                    tau_eff = std::sqrt(std::max(ss[j] * ss[j - 1], 1e-300)) / norm_a;
+                }
+            }
+        }
+        uint64_t s = ss.size();
+        while (s > 0 && ss[s - 1] <= tau_eff * norm_a)
+            --s;
+        if (s == 0) {
+            *rho_out = 0;
+            RL_CUDA(cudaMemsetAsync(d_approx, 0, m * n * sizeof(double), stream()));
+            *residual = 1.0;
+            *ok = 0;
+            continue;
+        }
+        // (A T) T^T with T the first s columns of the n x rho_plus basis
+        gemm(false, false, m, s, n, 1.0, d_a, n, d_basis, rho_plus, 0.0, ab, rho_plus);
+        gemm(false, true, m, n, s, 1.0, ab, rho_plus, d_basis, rho_plus, 0.0, d_approx, n);
+        k_sub<<<cdiv(m * n, 256), 256, 0, stream()>>>(m * n, d_a, d_approx, diff);
+        RL_LAUNCHED();
+        const std::vector<double> sd = jacobi_svd_dev(m, n, diff, sg, nullptr, scratch);
+        *rho_out = s;
+        *residual = sd[0] / norm_a;
+        *ok = *residual <= tau_prime;
+        if (*ok)
+            break;
+    }
+    // columns beyond rho are not part of the basis
+    if (*rho_out < rho_plus)
+        for (uint64_t i = 0; i < n; ++i)
+            RL_CUDA(cudaMemsetAsync(d_basis + i * rho_plus + *rho_out, 0, (rho_plus - *rho_out) * sizeof(double),
+                                    stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+}
+
+} // namespace rl
