@@ -262,6 +262,17 @@ int main() {
         CHECK(rel_diff(lowrank::project_onto_basis(A, Y, false, dense::Side::Left), A) < 1e-12);
         Matrix Z = lowrank::approx_basis(A, 8, {rnd::MultiplierTag::Gaussian}, lowrank::SpaceSide::RightSpace, {50, 4});
         CHECK(Z.rows() == 60 && Z.cols() == 8);
+        // proto_lowrank (test_lowrank.cpp:72-91): the zero matrix, and a rank-8 matrix recovered
+        auto z = lowrank::proto_lowrank(Matrix(4, 4), 2, 1e-8, 1e-6, {rnd::MultiplierTag::Gaussian, 0.0, 1.0},
+                                        {41, 9});
+        CHECK(z.ok && z.rho == 0);
+        Matrix A2 = rnd::gaussian_matrix(64, 8, 0.0, 1.0, {50, 5}).multiply(rnd::gaussian_matrix(8, 48, 0.0, 1.0, {50, 6}));
+        auto pl = lowrank::proto_lowrank(A2, 12, 1e-6, 1e-6, {rnd::MultiplierTag::Gaussian, 0.0, 1.0}, {41, 11});
+        CHECK(pl.ok && pl.rho == 8 && pl.residual < 1e-6);
+        CHECK(pl.basis.rows() == 48 && pl.basis.cols() == 8);
+        CHECK(rel_diff(pl.approx, A2) < 1e-12);
+        CHECK_THROWS_AS(lowrank::proto_lowrank(A2, 12, 1e-6, 2.0, {rnd::MultiplierTag::Gaussian, 0.0, 1.0}, {41, 11}),
+                        InvalidArgument);
     }
     std::printf("drop-in checks: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
