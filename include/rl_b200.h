@@ -137,12 +137,12 @@ rl_status rl_dev_circulant_apply_right(uint64_t m, uint64_t n, const double* d_c
  * structured.cpp:61-68; toeplitz_mul's circulant embedding, :156-176): d_g = col[0..n-1] followed by
  * row[1..n-1] (random_structured's draw order).  FFT of the embedding for next_pow2(2n-1) <= 8192,
  * a dense product otherwise; out != a. */
-/* lowrank::proto_lowrank (lowrank.cpp:108-177) for the Gaussian kind (RightSpace sketches
- * A^T G on stream stream_id + 104729 a, a = 0..3): host pointers, a m x n; basis n x rho_plus
+/* lowrank::proto_lowrank (lowrank.cpp:108-177) for the Gaussian and ToeplitzGaussian kinds
+ * (RightSpace sketches A^T G on stream stream_id + 104729 a, a = 0..3): host pointers, a m x n; basis n x rho_plus
  * (its first *rho columns are the orthonormal basis), approx m x n; small matrices only
  * (min(m, n) <= 64, max(m, n) <= 256, rho_plus <= 64; RL_TOO_LARGE otherwise). */
 rl_status rl_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus, double tau,
-                           double tau_prime, double mu, double sigma, uint64_t seed, uint64_t stream_id,
+                           double tau_prime, int tag, double mu, double sigma, uint64_t seed, uint64_t stream_id,
                            uint64_t* rho, double* basis, double* approx, double* residual, int* ok);
 rl_status rl_dev_toeplitz_apply_right(uint64_t m, uint64_t n, const double* d_g, const double* d_a,
                                       double* d_out);

@@ -79,7 +79,7 @@ class Restated:
         L.rlo_randomized_genp.argtypes = [u64, _d, _d, cint, dbl, dbl, cint, cint, u64, u64, _d, _d, _ip]
         L.rlo_qr_positive.argtypes = [u64, u64, _d, _d, _d]
         L.rlo_singular_values.argtypes = [u64, u64, _d, _d]
-        L.rlo_proto_lowrank.argtypes = [u64, u64, _d, u64, dbl, dbl, dbl, dbl, u64, u64, C.POINTER(C.c_uint64), _d, _d,
+        L.rlo_proto_lowrank.argtypes = [u64, u64, _d, u64, dbl, dbl, cint, dbl, dbl, u64, u64, C.POINTER(C.c_uint64), _d, _d,
                                         C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.rlo_numerical_rank.argtypes = [u64, _d, dbl]
         L.rlo_numerical_rank.restype = u64
@@ -182,13 +182,13 @@ class Restated:
                                       np.ascontiguousarray(signs), np.ascontiguousarray(y, float), x)
         return x
 
-    def proto_lowrank(self, a, rho_plus, tau, tau_prime, seed, sid, mu=0.0, sigma=1.0):
-        """lowrank::proto_lowrank, Gaussian kind: (rho, basis n x rho, approx, residual, ok)."""
+    def proto_lowrank(self, a, rho_plus, tau, tau_prime, seed, sid, mu=0.0, sigma=1.0, kind="gaussian"):
+        """lowrank::proto_lowrank, Gaussian / ToeplitzGaussian: (rho, basis n x rho, approx, residual, ok)."""
         a = np.ascontiguousarray(a, float)
         m, n = a.shape
         basis, approx = np.zeros((n, rho_plus)), np.empty((m, n))
         rho, res, ok = C.c_uint64(0), C.c_double(0.0), C.c_int(0)
-        _chk(self.lib.rlo_proto_lowrank(m, n, a, rho_plus, tau, tau_prime, mu, sigma, seed, sid, C.byref(rho), basis,
+        _chk(self.lib.rlo_proto_lowrank(m, n, a, rho_plus, tau, tau_prime, TAGS[kind], mu, sigma, seed, sid, C.byref(rho), basis,
                                         approx, C.byref(res), C.byref(ok)), "proto_lowrank")
         return rho.value, basis[:, :rho.value], approx, res.value, bool(ok.value)
 

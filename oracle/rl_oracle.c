@@ -1132,8 +1132,10 @@ void rlo_svd_left(uint64_t m, uint64_t n, const double* a, double* sigma, double
  * the restated SVD above.  Outputs rho, basis (n x rho, ld rho_plus), approx (m x n), residual,
  * ok.  Returns 2 on a bad argument. */
 int rlo_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus, double tau, double tau_prime,
-                      double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out, double* basis,
-                      double* approx, double* residual, int* ok) {
+                      int tag, double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out,
+                      double* basis, double* approx, double* residual, int* ok) {
+    if (tag != TAG_GAUSSIAN && tag != TAG_TOEPLITZ)
+        return 2;
     if (!(tau_prime > 0.0 && tau_prime < 1.0) || (tau > 0.0 && !(tau < 1.0)))
         return 2;
     if (rho_plus < 1 || rho_plus > (m < n ? m : n))
@@ -1171,7 +1173,19 @@ int rlo_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus
     rlo_transpose(m, n, a, at);
     for (int attempt = 0; attempt <= 3; ++attempt) {
         const uint64_t ds = sid + 104729ULL * (uint64_t)attempt;
-        rlo_gaussian_matrix(m, rho_plus, mu, sig_g, seed, ds, g);
+        if (tag == TAG_TOEPLITZ) { /* random_structured(kind, m, rho_plus): col[0..m-1], row[1..rho_plus-1] */
+            rlo_rng r;
+            rlo_rng_init(&r, seed, ds);
+            double* gv = (double*)malloc((m + rho_plus) * sizeof(double));
+            for (uint64_t i = 0; i < m + rho_plus - 1; ++i)
+                gv[i] = mu + sig_g * rlo_gaussian(&r);
+            for (uint64_t i = 0; i < m; ++i)
+                for (uint64_t j = 0; j < rho_plus; ++j)
+                    g[i * rho_plus + j] = i >= j ? gv[i - j] : gv[m - 1 + (j - i)];
+            free(gv);
+        } else {
+            rlo_gaussian_matrix(m, rho_plus, mu, sig_g, seed, ds, g);
+        }
         rlo_matmul(n, m, rho_plus, at, g, sk); /* A^T G */
         rlo_svd_left(n, rho_plus, sk, ss, us);
         double tau_eff = tau;

@@ -59,8 +59,8 @@ int rlo_fft(uint64_t n, double* re, double* im, int inverse);
 int rlo_circ_mul(uint64_t n, const double* c, const double* x, double* y);
 void rlo_svd_left(uint64_t m, uint64_t n, const double* a, double* sigma, double* u);
 int rlo_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus, double tau, double tau_prime,
-                      double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out, double* basis,
-                      double* approx, double* residual, int* ok);
+                      int tag, double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out,
+                      double* basis, double* approx, double* residual, int* ok);
 int rlo_toeplitz_mul(uint64_t m, uint64_t n, const double* col, const double* row, const double* x, double* y);
 int rlo_circ_apply_left(uint64_t n, const double* c, uint64_t cols, const double* a, double* out);
 int rlo_circ_apply_right(uint64_t n, const double* c, const double* a, double* out);

@@ -208,7 +208,7 @@ def lib() -> C.CDLL:
         "rl_dev_householder_pair_apply_right": [u64, vp, vp, vp, vp],
         "rl_dev_circulant_apply_right": [u64, u64, vp, vp, vp],
         "rl_dev_toeplitz_apply_right": [u64, u64, vp, vp, vp],
-        "rl_proto_lowrank": [u64, u64, _d, u64, dbl, dbl, dbl, dbl, u64, u64, C.POINTER(C.c_uint64), _d, _d,
+        "rl_proto_lowrank": [u64, u64, _d, u64, dbl, dbl, cint, dbl, dbl, u64, u64, C.POINTER(C.c_uint64), _d, _d,
                              C.POINTER(C.c_double), C.POINTER(C.c_int)],
         "rl_matmul": [u64, u64, u64, _d, _d, _d],
         "rl_dev_gemm": [cint, cint, u64, u64, u64, dbl, vp, u64, vp, u64, dbl, vp, u64],
@@ -591,15 +591,13 @@ def dev_toeplitz_apply_right(col, row, a, out) -> None:
 
 
 def proto_lowrank(a, rho_plus: int, tau: float, tau_prime: float, kind: MultiplierKind, stream: RngStream):
-    """lowrank::proto_lowrank (lowrank.cpp:108-177), Gaussian kind: (rho, basis n x rho, approx,
-    residual, ok)."""
-    if kind.tag != MultiplierTag.GAUSSIAN:
-        raise InvalidArgument("proto_lowrank: only the Gaussian kind is on the B200 path")
+    """lowrank::proto_lowrank (lowrank.cpp:108-177), Gaussian / ToeplitzGaussian kinds: (rho,
+    basis n x rho, approx, residual, ok)."""
     a = _f64(a)
     m, n = a.shape
     basis, approx = np.empty((n, rho_plus)), np.empty((m, n))
     rho, res, ok = C.c_uint64(0), C.c_double(0.0), C.c_int(0)
-    _chk(lib().rl_proto_lowrank(m, n, a, rho_plus, tau, tau_prime, kind.mu, kind.sigma, stream.seed,
+    _chk(lib().rl_proto_lowrank(m, n, a, rho_plus, tau, tau_prime, kind.tag, kind.mu, kind.sigma, stream.seed,
                                 stream.stream_id, C.byref(rho), basis, approx, C.byref(res), C.byref(ok)))
     return rho.value, basis[:, :rho.value].copy(), approx, res.value, bool(ok.value)
 

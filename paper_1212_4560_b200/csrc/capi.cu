@@ -41,8 +41,8 @@ void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double
 bool circ_fft_supported(uint64_t n);
 bool proto_lowrank_supported(uint64_t m, uint64_t n, uint64_t rho_plus);
 void proto_lowrank_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_plus, double tau, double tau_prime,
-                       double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out, double* d_basis,
-                       double* d_approx, double* residual, int* ok);
+                       int tag, double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out,
+                       double* d_basis, double* d_approx, double* residual, int* ok);
 uint64_t toeplitz_fft_len(uint64_t n);
 void toeplitz_apply_right_fft_dev(uint64_t m, uint64_t n, const double* g, const double* a, uint64_t lda,
                                   double* out, uint64_t ldo);
@@ -424,9 +424,11 @@ rl_status rl_dev_toeplitz_apply_right(uint64_t m, uint64_t n, const double* d_g,
 }
 
 rl_status rl_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus, double tau,
-                           double tau_prime, double mu, double sigma, uint64_t seed, uint64_t sid, uint64_t* rho,
-                           double* basis, double* approx, double* residual, int* ok) {
+                           double tau_prime, int tag, double mu, double sigma, uint64_t seed, uint64_t sid,
+                           uint64_t* rho, double* basis, double* approx, double* residual, int* ok) {
     API_BEGIN
+    if (tag != RL_GAUSSIAN && tag != RL_TOEPLITZ_GAUSSIAN)
+        fail(RL_INVALID_ARGUMENT, "proto_lowrank: the B200 path takes the Gaussian and ToeplitzGaussian kinds");
     require_positive(m, n, "proto_lowrank");
     if (!(tau_prime > 0.0 && tau_prime < 1.0))
         fail(RL_INVALID_ARGUMENT, "proto_lowrank: tau_prime must lie in (0, 1)");
@@ -434,14 +436,14 @@ rl_status rl_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho
         fail(RL_INVALID_ARGUMENT, "proto_lowrank: tau must lie in (0, 1) or <= 0 for auto");
     if (rho_plus < 1 || rho_plus > std::min(m, n))
         fail(RL_INVALID_ARGUMENT, "approx_basis: rho_plus out of range");
-    if (!(sigma > 0.0))
+    if (tag == RL_GAUSSIAN && !(sigma > 0.0))
         fail(RL_INVALID_ARGUMENT, "gaussian_matrix: sigma must be positive");
     if (!proto_lowrank_supported(m, n, rho_plus))
         fail(RL_TOO_LARGE, "proto_lowrank: the B200 path takes min(m, n) <= 64, max(m, n) <= 256, rho_plus <= 64");
     double* da = upload(WS_H0, a, m * n);
     double* db = ws<double>(WS_H1, n * rho_plus);
     double* dx = ws<double>(WS_H2, m * n);
-    proto_lowrank_dev(m, n, da, rho_plus, tau, tau_prime, mu, sigma, seed, sid, rho, db, dx, residual, ok);
+    proto_lowrank_dev(m, n, da, rho_plus, tau, tau_prime, tag, mu, sigma, seed, sid, rho, db, dx, residual, ok);
     download(basis, db, n * rho_plus);
     download(approx, dx, m * n);
     API_END

@@ -1035,6 +1035,16 @@ __global__ void __launch_bounds__(PJ_T) k_jacobi_left(int R, int C, const double
     }
 }
 
+// m x k Toeplitz from g = col[0..m-1], row[1..k-1] (random_structured's draw order,
+// random_gen.cpp:94-103; densify, structured.cpp:70-83)
+__global__ void k_toeplitz_rect(uint64_t m, uint64_t k, const double* g, double* out) {
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < m * k;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t i = e / k, j = e % k;
+        out[e] = i >= j ? g[i - j] : g[m - 1 + (j - i)];
+    }
+}
+
 __global__ void k_sub(uint64_t count, const double* a, const double* b, double* c) {
     for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < count;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -1076,9 +1086,9 @@ bool proto_lowrank_supported(uint64_t m, uint64_t n, uint64_t rho_plus) {
 
 // d_a: m x n on the device.  basis: n x rho_plus (first rho columns valid), approx: m x n.
 void proto_lowrank_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_plus, double tau, double tau_prime,
-                       double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out, double* d_basis,
-                       double* d_approx, double* residual, int* ok) {
-    double* sc = ws<double>(WS_RF5, 4 * m * n + 2 * n * rho_plus + m * rho_plus + 2 * (m + n + rho_plus) + 64);
+                       int tag, double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out,
+                       double* d_basis, double* d_approx, double* residual, int* ok) {
+    double* sc = ws<double>(WS_RF5, 4 * m * n + 2 * n * rho_plus + 2 * m * rho_plus + 2 * (m + n + rho_plus) + 64);
     double* g = sc;                      // m x rho_plus
     double* sk = g + m * rho_plus;       // n x rho_plus
     double* ab = sk + n * rho_plus;      // m x rho_plus
@@ -1086,6 +1096,7 @@ void proto_lowrank_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_p
     double* scratch = diff + m * n;      // m x n (transposes)
     double* usv = scratch + m * n;       // m x n (left vectors of A / diff, unused)
     double* sg = usv + m * n;            // sigma scratch
+    double* gv = sg + (m + n + rho_plus); // Toeplitz generators (m + rho_plus - 1)
     const std::vector<double> sa = jacobi_svd_dev(m, n, d_a, sg, nullptr, scratch);
     const double norm_a = sa[0];
     *rho_out = 0;
@@ -1100,7 +1111,13 @@ void proto_lowrank_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_p
     }
     for (int attempt = 0; attempt <= 3; ++attempt) {
         const uint64_t ds = sid + 104729ULL * static_cast<uint64_t>(attempt);
-        rng_generate(seed, ds, Draw::Gaussian, m * rho_plus, mu, sig_g, g);
+        if (tag == RL_TOEPLITZ_GAUSSIAN) { // the m x rho_plus Toeplitz sketching matrix (approx_basis, lowrank.cpp:93-101)
+            rng_generate(seed, ds, Draw::Gaussian, m + rho_plus - 1, mu, sig_g, gv);
+            k_toeplitz_rect<<<cdiv(m * rho_plus, 256), 256, 0, stream()>>>(m, rho_plus, gv, g);
+            RL_LAUNCHED();
+        } else {
+            rng_generate(seed, ds, Draw::Gaussian, m * rho_plus, mu, sig_g, g);
+        }
         gemm(true, false, n, rho_plus, m, 1.0, d_a, n, g, rho_plus, 0.0, sk, rho_plus); // A^T G
         const std::vector<double> ss = jacobi_svd_dev(n, rho_plus, sk, sg, d_basis, scratch);
         double tau_eff = tau;

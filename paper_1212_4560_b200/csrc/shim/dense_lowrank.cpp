@@ -112,15 +112,16 @@ Matrix approx_basis(const Matrix& a, std::size_t rho_plus, rnd::MultiplierKind k
 
 LowRankResult proto_lowrank(const Matrix& a, std::size_t rho_plus, double tau, double tau_prime,
                             rnd::MultiplierKind kind, rnd::RngStream stream) {
-    if (kind.tag != rnd::MultiplierTag::Gaussian)
-        throw InvalidArgument("proto_lowrank: only the Gaussian kind is on the B200 path");
+    if (kind.tag != rnd::MultiplierTag::Gaussian && kind.tag != rnd::MultiplierTag::ToeplitzGaussian)
+        throw InvalidArgument("proto_lowrank: the B200 path takes the Gaussian and ToeplitzGaussian kinds");
     const std::size_t m = a.rows(), n = a.cols();
     Matrix basis(n, std::max<std::size_t>(rho_plus, 1));
     Matrix approx(m, n);
     uint64_t rho = 0;
     double residual = 0.0;
     int ok = 0;
-    check(rl_proto_lowrank(m, n, a.data().data(), rho_plus, tau, tau_prime, kind.mu, kind.sigma, stream.seed,
+    check(rl_proto_lowrank(m, n, a.data().data(), rho_plus, tau, tau_prime, static_cast<int>(kind.tag), kind.mu,
+                           kind.sigma, stream.seed,
                            stream.stream_id, &rho, basis.data().data(), approx.data().data(), &residual, &ok));
     LowRankResult r;
     r.rho = rho;

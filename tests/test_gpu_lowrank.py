@@ -146,18 +146,18 @@ def test_sharded_range_finder_single_rank_matches_fused(rl):
     assert (b2 - B).abs().max().item() <= 1e-14 * np.abs(A).max()
 
 
-@pytest.mark.parametrize("tau", [1e-6, 0.0])
-def test_proto_lowrank(rl, oracle, golden, tau):
+@pytest.mark.parametrize("tau,kind", [(1e-6, "gaussian"), (0.0, "gaussian"), (1e-6, "toeplitz_gaussian")])
+def test_proto_lowrank(rl, oracle, golden, tau, kind):
     """lowrank::proto_lowrank's own cases (tests/test_lowrank.cpp:72-91) on the GPU against the
     restatement: the zero matrix (ok, rank 0) and the paper profile (rank 8 of 64, rho+ = 12,
     explicit and automatic tau): same rank and verdict, approximation within 1e-12 of the
     restatement's (the basis is unique up to signs; A T T^T is not), residual < 1e-6."""
-    kind = rl.MultiplierKind(rl.MultiplierTag.GAUSSIAN)
-    rho, _, _, _, ok = rl.proto_lowrank(np.zeros((4, 4)), 2, 1e-8, 1e-6, kind, rl.RngStream(41, 9))
+    mk = rl.MultiplierKind(getattr(rl.MultiplierTag, kind.upper()))
+    rho, _, _, _, ok = rl.proto_lowrank(np.zeros((4, 4)), 2, 1e-8, 1e-6, mk, rl.RngStream(41, 9))
     assert ok and rho == 0
     a = golden["proto/A"]
-    rho, basis, approx, res, ok = rl.proto_lowrank(a, 12, tau, 1e-6, kind, rl.RngStream(41, 11))
-    rho_o, basis_o, approx_o, res_o, ok_o = oracle.proto_lowrank(a, 12, tau, 1e-6, 41, 11)
+    rho, basis, approx, res, ok = rl.proto_lowrank(a, 12, tau, 1e-6, mk, rl.RngStream(41, 11))
+    rho_o, basis_o, approx_o, res_o, ok_o = oracle.proto_lowrank(a, 12, tau, 1e-6, 41, 11, kind=kind)
     assert ok and ok_o and rho == rho_o == 8 and res < 1e-6
     assert np.abs(approx - approx_o).max() <= 1e-12 * np.abs(a).max()
     assert np.abs(basis.T @ basis - np.eye(rho)).max() < 1e-13
