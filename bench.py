@@ -13,7 +13,10 @@ solves/s; % of roofline"):
   * `config1` — n = 256 (latency): us per solve on device data and through the host-pointer call.
   * `config5` — n = 16384, 8 RHS, with the Householder-pair, sparse +-1 and Gaussian right
     multipliers (ms per call, attempts, backward error; 1 warm-up + 2 timed calls per arm;
-    `--skip-config5` leaves it out).
+    `--skip-config5` leaves it out); the structured arms add `multiplier_apply`, the matrix-free
+    multiplier stage alone with its HBM fraction.
+  * `circulant_fft` — A C for a circulant +-1 right multiplier at n = 8192 through the FFT path,
+    beside the dense DMMA product it replaces.
   * `range_finder` — config 4: the randomized range finder on A 16384 x 4096, rho+ = 72
     (TFLOP/s over SURVEY.md §8(d)'s 1.967e10 flop); for N > 1 the rows are sharded (TSQR of
     the sketch + one all_reduce of B, strong scaling).
