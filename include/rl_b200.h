@@ -243,11 +243,11 @@ rl_status rl_rng_block(uint64_t seed, uint64_t stream_id, uint64_t offset, uint6
 /* Box-Muller of npairs consecutive raw pairs (random_gen.cpp:46-52): out[2q] = r cos a,
  * out[2q+1] = r sin a. */
 rl_status rl_box_muller(uint64_t npairs, const uint64_t* raw, double* out);
-/* Diagnostic for the Gaussian generator's fast path: runs the fast (Ziv) and the
- * double-double Box-Muller on npairs raw pairs (raw == NULL: splitmix64 pairs from seed);
- * counts[0] = pairs the fast path accepted, counts[1] = of those, pairs whose bits differ
- * from the double-double result (0 is the contract), counts[2] = pairs it deferred. */
-rl_status rl_box_muller_fast_check(uint64_t npairs, const uint64_t* raw, uint64_t seed, uint64_t* counts);
+/* Checksums of the GPU Box-Muller over npairs splitmix64 pairs (pair q: raw words
+ * splitmix64 of seed + 2q, twice): hashes[c] = wrapping sum over q in chunk c of
+ * pair_hash(q, bits(g0), bits(g1)) (csrc/glibc_math.cuh). Lets a host program check 2^30 pairs
+ * against its own libm without moving the outputs (tests/cpp/bm_libm_check.cpp). */
+rl_status rl_box_muller_hash(uint64_t seed, uint64_t npairs, uint64_t chunk, uint64_t* hashes);
 /* structured::fft (structured.cpp:96-130): complex interleaved (re, im), n a power of two,
  * inverse scaled by 1/n. */
 rl_status rl_dft(uint64_t n, const double* in, int inverse, double* out);

@@ -35,7 +35,7 @@ __all__ = [
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
     "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
     "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_toeplitz_apply_right", "proto_lowrank", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
-    "box_muller_fast_check", "launch_count", "LIB_PATH",
+    "box_muller", "box_muller_hash", "launch_count", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -231,7 +231,8 @@ def lib() -> C.CDLL:
         "rl_dev_qr_positive": [u64, u64, vp, vp, vp],
         "rl_dev_numerical_rank": [u64, u64, vp, dbl, C.POINTER(u64), _d],
         "rl_probe_peaks": [C.POINTER(dbl), C.POINTER(dbl)],
-        "rl_box_muller_fast_check": [u64, vp, u64, vp],
+        "rl_box_muller": [u64, vp, vp],
+        "rl_box_muller_hash": [u64, u64, u64, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -619,14 +620,20 @@ def dev_numerical_rank(a, tol: float) -> Tuple[int, np.ndarray]:
     return int(r.value), sg
 
 
-def box_muller_fast_check(npairs: int, raw=None, seed: int = 0) -> Tuple[int, int, int]:
-    """(fast-path pairs, of those bitwise different from the double-double path, deferred)."""
-    counts = np.zeros(3, dtype=np.uint64)
-    if raw is not None:
-        raw = np.ascontiguousarray(raw, dtype=np.uint64)
-        npairs = raw.size // 2
-    _chk(lib().rl_box_muller_fast_check(npairs, None if raw is None else raw.ctypes.data, seed, counts.ctypes.data))
-    return int(counts[0]), int(counts[1]), int(counts[2])
+def box_muller(raw) -> np.ndarray:
+    """Rng::gaussian's Box-Muller (random_gen.cpp:46-52) of consecutive raw u64 pairs on the GPU:
+    out[2q] = r cos a, out[2q + 1] = r sin a."""
+    raw = np.ascontiguousarray(raw, dtype=np.uint64)
+    out = np.empty(raw.size, dtype=np.float64)
+    _chk(lib().rl_box_muller(raw.size // 2, raw.ctypes.data, out.ctypes.data))
+    return out
+
+
+def box_muller_hash(seed: int, npairs: int, chunk: int = 1 << 20) -> np.ndarray:
+    """Per-chunk checksums of the GPU Box-Muller over splitmix64 pairs (rl_b200.h)."""
+    out = np.zeros((npairs + chunk - 1) // chunk, dtype=np.uint64)
+    _chk(lib().rl_box_muller_hash(seed, npairs, chunk, out.ctypes.data))
+    return out
 
 
 def probe_peaks() -> Tuple[float, float]:

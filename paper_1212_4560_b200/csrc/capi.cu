@@ -871,12 +871,14 @@ rl_status rl_box_muller(uint64_t npairs, const uint64_t* raw, double* out) {
     API_END
 }
 
-rl_status rl_box_muller_fast_check(uint64_t npairs, const uint64_t* raw, uint64_t seed, uint64_t* counts) {
+rl_status rl_box_muller_hash(uint64_t seed, uint64_t npairs, uint64_t chunk, uint64_t* hashes) {
     API_BEGIN
-    const uint64_t* d = raw ? upload(WS_H0, raw, 2 * npairs) : nullptr;
-    unsigned long long* dc = ws<unsigned long long>(WS_H1, 3);
-    box_muller_fast_check_dev(d, npairs, seed, dc);
-    download(reinterpret_cast<unsigned long long*>(counts), dc, 3);
+    if (chunk == 0)
+        fail(RL_INVALID_ARGUMENT, "box_muller_hash: chunk must be positive");
+    const uint64_t nchunks = (npairs + chunk - 1) / chunk;
+    unsigned long long* dh = ws<unsigned long long>(WS_H1, nchunks ? nchunks : 1);
+    box_muller_hash_dev(seed, npairs, chunk, dh);
+    download(reinterpret_cast<unsigned long long*>(hashes), dh, nchunks);
     API_END
 }
 

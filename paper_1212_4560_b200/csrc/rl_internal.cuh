@@ -100,7 +100,7 @@ void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, ui
                      double sigma, void* d_out);
 // Box-Muller of consecutive raw pairs (random_gen.cpp:46-52).
 void box_muller_pairs_dev(const uint64_t* d_raw, uint64_t npairs, double* d_out);
-void box_muller_fast_check_dev(const uint64_t* d_raw, uint64_t npairs, uint64_t seed, unsigned long long* d_counts);
+void box_muller_hash_dev(uint64_t seed, uint64_t npairs, uint64_t chunk, unsigned long long* d_hashes);
 // One stream per element of d_sids (seed shared, stream id ^ xor_mask + add): n sign
 // draws each into d_out[t*n ...]  (batched circulant first columns).
 void rng_sign_vectors_batched(uint64_t seed, const uint64_t* d_sids, uint64_t add, uint64_t xor_mask,

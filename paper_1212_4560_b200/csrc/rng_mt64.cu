@@ -20,7 +20,7 @@
 #include <string>
 #include <vector>
 
-#include "dd_math.cuh"
+#include "glibc_math.cuh"
 #include <algorithm>
 
 #include "rl_internal.cuh"
@@ -123,32 +123,17 @@ struct GenParams {
 };
 
 // Box-Muller pair of random_gen.cpp:46-52 from two raw draws; returns (cos, sin) entries.
+// log and sincos are glibc 2.39's FMA builds step for step (glibc_math.cuh), so every entry
+// carries the reference's exact bits; the rest are single IEEE operations in source order.
 __device__ __forceinline__ void box_muller(uint64_t r1, uint64_t r2, double mu, double sigma,
                                            double* g0, double* g1) {
-    double u1 = __dsub_rn(1.0, __dmul_rn(static_cast<double>(r1 >> 11), 0x1.0p-53));
-    double u2 = __dmul_rn(static_cast<double>(r2 >> 11), 0x1.0p-53);
-    double lg = cr_log_unit(u1);
-    double r = __dsqrt_rn(__dmul_rn(-2.0, lg));
-    double a = __dmul_rn(2.0 * 3.14159265358979323846, u2);
-    double s, c;
-    cr_sincos(a, &s, &c);
-    *g0 = __dadd_rn(mu, __dmul_rn(sigma, __dmul_rn(r, c)));
-    *g1 = __dadd_rn(mu, __dmul_rn(sigma, __dmul_rn(r, s)));
-}
-
-// Fast-path Box-Muller: false when log / sin / cos could not be rounded with certainty from
-// the fast estimates (the caller then runs box_muller; both give identical bits).
-__device__ __forceinline__ bool box_muller_fast(uint64_t r1, uint64_t r2, double mu, double sigma,
-                                                double* g0, double* g1) {
     const double u1 = __dsub_rn(1.0, __dmul_rn(static_cast<double>(r1 >> 11), 0x1.0p-53));
     const double u2 = __dmul_rn(static_cast<double>(r2 >> 11), 0x1.0p-53);
-    double lg, s, c;
-    const bool ok1 = fast_log_unit(u1, &lg);
-    const bool ok2 = fast_sincos(__dmul_rn(2.0 * 3.14159265358979323846, u2), &s, &c);
-    const double r = __dsqrt_rn(__dmul_rn(-2.0, lg));
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, glm::log_fma(u1)));
+    double s, c;
+    glm::sincos_fma(__dmul_rn(2.0 * 3.14159265358979323846, u2), &s, &c);
     *g0 = __dadd_rn(mu, __dmul_rn(sigma, __dmul_rn(r, c)));
     *g1 = __dadd_rn(mu, __dmul_rn(sigma, __dmul_rn(r, s)));
-    return ok1 & ok2;
 }
 
 // Emit the outputs carried by one freshly twisted window whose word 0 is stream
@@ -457,7 +442,6 @@ __device__ void warp_twist_oop(const uint64_t* src, uint64_t* dst, int lane) {
 // thread for Gaussians), one barrier per block: five warps per chunk keep the FP64 pipe
 // fed where one warp per chunk left it latency-bound.
 constexpr int kGenThreads = 160;
-constexpr int kSlowCap = 512; // deferred slow-path pairs per chunk (~1% of 16384 expected)
 
 __device__ __forceinline__ void store_pair(const GenParams& p, int64_t o, double g0, double g1) {
     double* out = static_cast<double*>(p.out) - p.base;
@@ -469,13 +453,8 @@ __device__ __forceinline__ void store_pair(const GenParams& p, int64_t o, double
 __global__ void __launch_bounds__(kGenThreads) k_gen_chunks(const uint64_t* windows, uint64_t c_first,
                                                             uint64_t nchunks, uint64_t nout, GenParams p) {
     __shared__ uint64_t wb[2][kN];
-    __shared__ ulonglong2 slow_w[kSlowCap];
-    __shared__ int64_t slow_o[kSlowCap];
-    __shared__ int nslow;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ci = blockIdx.x;
-    if (tid == 0)
-        nslow = 0;
     if (ci >= nchunks)
         return;
     const uint64_t c = c_first + ci;
@@ -501,18 +480,8 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_chunks(const uint64_t* wind
                     if (o >= lo && o < hi) {
                         const uint64_t w0 = temper(w[2 * q]), w1 = temper(w[2 * q + 1]);
                         double g0, g1;
-                        if (box_muller_fast(w0, w1, p.mu, p.sigma, &g0, &g1)) {
-                            store_pair(p, o, g0, g1);
-                        } else { // rare: defer to the accurate path after the chunk
-                            const int slot = atomicAdd(&nslow, 1);
-                            if (slot < kSlowCap) {
-                                slow_o[slot] = o;
-                                slow_w[slot] = make_ulonglong2(w0, w1);
-                            } else {
-                                box_muller(w0, w1, p.mu, p.sigma, &g0, &g1);
-                                store_pair(p, o, g0, g1);
-                            }
-                        }
+                        box_muller(w0, w1, p.mu, p.sigma, &g0, &g1);
+                        store_pair(p, o, g0, g1);
                     }
                 }
             } else {
@@ -543,12 +512,6 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_chunks(const uint64_t* wind
         __syncthreads();
         cur ^= 1;
     }
-    const int ns = min(nslow, kSlowCap);
-    for (int k = tid; k < ns; k += kGenThreads) {
-        double g0, g1;
-        box_muller(slow_w[k].x, slow_w[k].y, p.mu, p.sigma, &g0, &g1);
-        store_pair(p, slow_o[k], g0, g1);
-    }
 }
 
 // Gaussian pairs from tempered words: pair q = entries base + 2q (cos), base + 2q + 1 (sin).
@@ -558,8 +521,7 @@ __global__ void k_gaussian_pairs(const uint64_t* raw, uint64_t npairs, GenParams
         return;
     const ulonglong2 w = reinterpret_cast<const ulonglong2*>(raw)[q];
     double g0, g1;
-    if (!box_muller_fast(w.x, w.y, p.mu, p.sigma, &g0, &g1))
-        box_muller(w.x, w.y, p.mu, p.sigma, &g0, &g1);
+    box_muller(w.x, w.y, p.mu, p.sigma, &g0, &g1);
     store_pair(p, p.base + static_cast<int64_t>(2 * q), g0, g1);
 }
 
@@ -898,45 +860,31 @@ void rng_sparse_sign(uint64_t seed, uint64_t sid, uint64_t n, int nnz, int32_t* 
 
 
 namespace {
-// Fast vs accurate Box-Muller on the same raw pairs (raw == nullptr: splitmix pairs of seed):
-// counts[0] fast path taken, counts[1] fast path taken but bits differ (must stay 0),
-// counts[2] deferred to the accurate path.
-__global__ void k_bm_check(const uint64_t* raw, uint64_t npairs, uint64_t seed, unsigned long long* counts) {
-    unsigned long long ok = 0, bad = 0, slow = 0;
+// Per-chunk checksums of Box-Muller outputs for the pairs (splitmix64(seed + 2q),
+// splitmix64(seed + 2q + 1)), q < npairs: hashes[q / chunk] += mix(q, bits(r cos a),
+// bits(r sin a)) (wrapping integer sums: independent of the summation order). The host side
+// (tests/cpp/bm_libm_check.cpp) forms the same sums with the installed libm.
+__global__ void k_bm_hash(uint64_t seed, uint64_t npairs, uint64_t chunk, unsigned long long* hashes) {
     for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < npairs;
          q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        uint64_t w0, w1;
-        if (raw) {
-            w0 = raw[2 * q];
-            w1 = raw[2 * q + 1];
-        } else {
-            uint64_t st = seed + 2 * q;
-            w0 = splitmix64(st);
-            w1 = splitmix64(st);
-        }
-        double f0, f1, a0, a1;
-        const bool fast = box_muller_fast(w0, w1, 0.0, 1.0, &f0, &f1);
-        box_muller(w0, w1, 0.0, 1.0, &a0, &a1);
-        if (fast) {
-            ++ok;
-            if (__double_as_longlong(f0) != __double_as_longlong(a0) ||
-                __double_as_longlong(f1) != __double_as_longlong(a1))
-                ++bad;
-        } else {
-            ++slow;
-        }
+        uint64_t st = seed + 2 * q;
+        const uint64_t w0 = splitmix64(st);
+        const uint64_t w1 = splitmix64(st);
+        double g0, g1;
+        box_muller(w0, w1, 0.0, 1.0, &g0, &g1);
+        const uint64_t h = glm::pair_hash(q, static_cast<uint64_t>(__double_as_longlong(g0)),
+                                        static_cast<uint64_t>(__double_as_longlong(g1)));
+        atomicAdd(&hashes[q / chunk], static_cast<unsigned long long>(h));
     }
-    atomicAdd(&counts[0], ok);
-    atomicAdd(&counts[1], bad);
-    atomicAdd(&counts[2], slow);
 }
 } // namespace
 
-void box_muller_fast_check_dev(const uint64_t* d_raw, uint64_t npairs, uint64_t seed, unsigned long long* d_counts) {
+void box_muller_hash_dev(uint64_t seed, uint64_t npairs, uint64_t chunk, unsigned long long* d_hashes) {
     cudaStream_t st = stream();
-    RL_CUDA(cudaMemsetAsync(d_counts, 0, 3 * sizeof(unsigned long long), st));
-    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((npairs + 255) / 256, 148ULL * 8));
-    k_bm_check<<<blocks, 256, 0, st>>>(d_raw, npairs, seed, d_counts);
+    const uint64_t nchunks = (npairs + chunk - 1) / chunk;
+    RL_CUDA(cudaMemsetAsync(d_hashes, 0, nchunks * sizeof(unsigned long long), st));
+    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((npairs + 255) / 256, 148ULL * 16));
+    k_bm_hash<<<blocks, 256, 0, st>>>(seed, npairs, chunk, d_hashes);
     RL_LAUNCHED();
 }
 } // namespace rl

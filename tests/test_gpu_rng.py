@@ -1,8 +1,11 @@
 """GPU: the multiplier streams (K1) against the reference's draws (golden fixtures) and the
 C restatement.  Signs, uniforms, uniform_int and raw outputs are bit-exact everywhere,
-including across jump-ahead chunk (2^15) and level-1 (2^21) boundaries.  Gaussians use
-correctly rounded log/sin/cos: bit-exact except where glibc itself is not correctly
-rounded (~0.16% of entries), and then within 2 ulp."""
+including across jump-ahead chunk (2^15) and level-1 (2^21) boundaries.  Gaussians run
+glibc 2.39's own log/sincos operation sequences (csrc/glibc_math.cuh) and are bit-exact too."""
+import ctypes
+import os
+import subprocess
+
 import numpy as np
 import pytest
 
@@ -46,22 +49,17 @@ def test_gaussian_golden_and_rate(rl, golden, oracle):
     assert g.ravel().tolist() == [0.49698630815925782, 0.47268287749077509, -0.26078844461327677,
                                   0.27389602589300449]
     got = rl.gaussian_matrix(33, 31, 0.5, 2.0, rl.RngStream(3, 9))
-    ref = golden["gaussian_matrix/33x31/mu_sigma"]
-    assert np.max(np.abs(got - ref) / np.spacing(np.abs(ref))) <= 4
+    assert np.array_equal(got, golden["gaussian_matrix/33x31/mu_sigma"])
     for key, seed, sid in _streams(golden, "gaussian"):
         got = rl.rng_draws(rl.RngStream(seed, sid), "gaussian", len(golden[key]))
-        ulp = np.abs(got - golden[key]) / np.spacing(np.abs(golden[key]))
-        assert ulp.max() <= 2, key
+        assert np.array_equal(got, golden[key]), key
 
 
-def test_gaussian_matrix_large_bit_rate(rl, oracle):
+def test_gaussian_matrix_large_bit_exact(rl, oracle):
     m = n = 1536  # 2.36 M entries: crosses level-1 jump windows
     got = rl.gaussian_matrix(m, n, 0.0, 1.0, rl.RngStream(20260825, 99))
     ref = oracle.gaussian_matrix(m, n, 20260825, 99)
-    exact = np.mean(got == ref)
-    ulp = np.abs(got - ref) / np.spacing(np.abs(ref))
-    assert exact >= 0.9975, exact
-    assert ulp.max() <= 2
+    assert np.array_equal(got, ref), int(np.sum(got != ref))
 
 
 def test_new_multiplier_streams_bit_exact(rl, oracle):
@@ -86,17 +84,40 @@ def test_determinism_and_stream_independence(rl):
     assert np.array_equal(a, b) and not np.array_equal(a, c)
 
 
-def test_box_muller_fast_path_is_exact(rl):
-    """The generator's Ziv fast path must return exactly the double-double path's bits
-    whenever it accepts: random pairs, plus the edges (u1 -> 1 and 0, angles at k pi/2)."""
-    ok, bad, slow = rl.box_muller_fast_check(1 << 22, seed=12345)
-    assert bad == 0 and ok + slow == 1 << 22 and slow < (1 << 22) // 20
-    edge = []
-    for k in range(0, 1 << 12):
-        lo = k << 11                              # u1 = 1 - k 2^-53 -> log u1 ~ 0
+def _libm_pair(raw0, raw1):
+    """Rng::gaussian (random_gen.cpp:46-52) with this host's libm log and sincos."""
+    libm = ctypes.CDLL("libm.so.6")
+    libm.log.restype = ctypes.c_double
+    libm.log.argtypes = [ctypes.c_double]
+    libm.sincos.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    u1 = 1.0 - float(raw0 >> 11) * 2.0 ** -53
+    u2 = float(raw1 >> 11) * 2.0 ** -53
+    r = np.sqrt(-2.0 * libm.log(u1))
+    s, c = ctypes.c_double(), ctypes.c_double()
+    libm.sincos(2.0 * np.pi * u2, ctypes.byref(s), ctypes.byref(c))
+    return r * c.value, r * s.value
+
+
+def test_box_muller_edges_match_host_libm(rl):
+    """Box-Muller at the ends of its domain: u1 -> 1 (log near 0, the near-one polynomial),
+    u1 -> 2^-53, and angles within a few ulp of k pi/2 (glibc's branch points)."""
+    raw = []
+    for k in list(range(0, 64)) + [1 << 40, (1 << 45) + 3, (1 << 49) - 1]:
+        lo = k << 11                              # u1 = 1 - k 2^-53
         hi = ((1 << 53) - 1 - k) << 11            # u1 = (k + 1) 2^-53
         for q in range(5):                        # u2 near q/4 -> angle near q pi/2
-            u2 = ((q * (1 << 51) + k - 2048) % (1 << 53)) << 11
-            edge += [lo, u2, hi, u2]
-    ok, bad, slow = rl.box_muller_fast_check(0, raw=np.array(edge, dtype=np.uint64))
-    assert bad == 0
+            u2 = ((q * (1 << 51) + k - 32) % (1 << 53)) << 11
+            raw += [lo, u2, hi, u2]
+    raw = np.array(raw, dtype=np.uint64)
+    got = rl.box_muller(raw)
+    want = np.array([g for i in range(0, raw.size, 2) for g in _libm_pair(int(raw[i]), int(raw[i + 1]))])
+    assert np.array_equal(got, want), int(np.sum(got != want))
+
+
+def test_box_muller_matches_host_libm_2e24(rl):
+    """2^24 random pairs: GPU checksums against the host libm's (tests/cpp/bm_libm_check.cpp).
+    tools/bm_full.sh runs the same check on 2^30 pairs (profiles/r02_bm_libm_2e30.txt)."""
+    exe = os.path.join(os.path.dirname(rl.LIB_PATH), "bm_libm_check")
+    r = subprocess.run([exe, "24"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert '"mismatched_chunks": 0' in r.stdout
