@@ -354,7 +354,7 @@ def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak):
     A, B = make_config5_inputs(torch, dev)
     X = torch.empty_like(B)
     out = {"workload": "config5: GENP n=16384, 8 RHS, MulSide::Right; Householder pair / sparse +-1 / Gaussian"}
-    arms = (("householder_pair", rl.MultiplierTag.HOUSEHOLDER_PAIR, 3.0 * N5 * N5 * 8),
+    arms = (("householder_pair", rl.MultiplierTag.HOUSEHOLDER_PAIR, 2.0 * N5 * N5 * 8),
             ("sparse_sign", rl.MultiplierTag.SPARSE_SIGN, 2.0 * N5 * N5 * 8),
             ("gaussian", rl.MultiplierTag.GAUSSIAN, None))
     for name, tag, mult_bytes in arms:

@@ -197,6 +197,16 @@ rl_status rl_dev_randomized_genp_ex(uint64_t n, uint64_t nrhs, const double* d_a
                                     int tag, double mu, double sigma, int side, int refine,
                                     uint64_t seed, uint64_t stream_id, double* d_x,
                                     rl_precond_report* report, uint32_t flags);
+/* Per-right-hand-side outcome of the calling thread's last randomized_genp call: column j is
+ * the reference call randomized_genp(a, B[:, j], ...) (genp.cpp:207-291) — the first attempt
+ * whose residual <= 1e-7, else its best — so `attempt` is that call's accepted draw and
+ * `attempts_drawn` how many draws that call would make. Fails with RL_INVALID_ARGUMENT when
+ * nrhs differs from the last call's. */
+typedef struct {
+    double residual, pivot_min, pivot_max;
+    int32_t attempt, attempts_drawn;
+} rl_column_report;
+rl_status rl_last_column_reports(uint64_t nrhs, rl_column_report* out);
 /* Batched randomized_genp: `batch` independent systems A[t] (n x n), b[t] (n), each
  * with stream (seed, stream_ids[t]) — semantically the loop bench::table1_genp runs
  * (bench.cpp:117-133).  Host pointers; reports may be NULL. */

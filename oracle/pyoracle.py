@@ -77,6 +77,8 @@ class Restated:
         L.rlo_sparse_apply_right.argtypes = [u64, cint, _i32p, _d, _d, _d]
         L.rlo_sparse_apply_vec.argtypes = [u64, cint, _i32p, _d, _d, _d]
         L.rlo_randomized_genp.argtypes = [u64, _d, _d, cint, dbl, dbl, cint, cint, u64, u64, _d, _d, _ip]
+        L.rlo_randomized_genp_multi.argtypes = [u64, u64, _d, _d, cint, dbl, dbl, cint, cint, u64, u64, cint, _d,
+                                                _d, _ip]
         L.rlo_qr_positive.argtypes = [u64, u64, _d, _d, _d]
         L.rlo_singular_values.argtypes = [u64, u64, _d, _d]
         L.rlo_proto_lowrank.argtypes = [u64, u64, _d, u64, dbl, dbl, cint, dbl, dbl, u64, u64, C.POINTER(C.c_uint64), _d, _d,
@@ -200,6 +202,17 @@ class Restated:
              "randomized_genp")
         return y, rep, extra
 
+    def randomized_genp_multi(self, a, B, kind="gaussian", side="right", refine=0, seed=0, sid=0, mu=0.0,
+                              sigma=1.0, skip_raw=False):
+        """nrhs columns of B as independent randomized_genp calls sharing the stream: Y, reports
+        (nrhs x 6), extras (nrhs x 2: accepted attempt, attempts drawn)."""
+        n, nrhs = B.shape
+        Y, rep, extra = np.empty((n, nrhs)), np.empty((nrhs, 6)), np.zeros((nrhs, 2), np.int32)
+        _chk(self.lib.rlo_randomized_genp_multi(n, nrhs, np.ascontiguousarray(a, float), np.ascontiguousarray(B, float),
+                                                TAGS[kind], mu, sigma, SIDES[side], refine, seed, sid, int(skip_raw),
+                                                Y, rep, extra), "randomized_genp_multi")
+        return Y, rep, extra
+
     def qr_positive(self, a):
         m, n = a.shape
         q, r = np.empty((m, n)), np.empty((n, n))
@@ -246,6 +259,15 @@ class Reference:
         L.rlref_qr_positive.argtypes = [u64, u64, _d, _d, _d]
         L.rlref_singular_values.argtypes = [u64, u64, _d, _d]
         L.rlref_profile_matrix_paper.argtypes = [u64, u64, u64, u64, _d]
+        P = C.POINTER
+        L.rlref_proto_lowrank.argtypes = [u64, u64, _d, u64, dbl, dbl, cint, dbl, dbl, u64, u64, P(C.c_uint64), _d,
+                                          _d, P(C.c_uint64), P(C.c_double), P(C.c_int)]
+        L.rlref_nrank_search.argtypes = [u64, u64, _d, u64, u64, dbl, cint, u64, u64, P(C.c_uint64), _d,
+                                         P(C.c_uint64), P(C.c_uint64)]
+        L.rlref_extremal_sv_estimate.argtypes = [u64, u64, _d, cint, cint, u64, u64, P(C.c_double), P(C.c_double)]
+        L.rlref_cond_probe.argtypes = [u64, u64, _d, dbl, cint, cint, u64, u64, P(C.c_int)]
+        L.rlref_power_transform.argtypes = [u64, u64, _d, C.c_uint, _d]
+        L.rlref_sampled_residual_check.argtypes = [u64, u64, _d, _d, u64, u64, dbl, u64, u64, P(C.c_int)]
 
     def _chk(self, code, where):
         if code != 0:
@@ -334,6 +356,57 @@ class Reference:
                                                  TAGS[kind], mu, sigma, SIDES[side], refine, seed, sid, y, rep),
                   "randomized_genp")
         return y, rep
+
+    def proto_lowrank(self, a, rho_plus, tau, tau_prime, seed, sid, mu=0.0, sigma=1.0, kind="gaussian"):
+        """lowrank::proto_lowrank (lowrank.cpp:108-177): (rho, basis, approx, residual, ok)."""
+        a = np.ascontiguousarray(a, float)
+        m, n = a.shape
+        basis, approx = np.zeros(max(n * rho_plus, n)), np.empty((m, n))
+        rho, cols, res, ok = C.c_uint64(0), C.c_uint64(0), C.c_double(0.0), C.c_int(0)
+        self._chk(self.lib.rlref_proto_lowrank(m, n, a, rho_plus, tau, tau_prime, TAGS[kind], mu, sigma, seed, sid,
+                                               C.byref(rho), approx, basis, C.byref(cols), C.byref(res), C.byref(ok)),
+                  "proto_lowrank")
+        basis = basis[:n * cols.value].reshape(n, cols.value)
+        return rho.value, basis[:, :rho.value], approx, res.value, bool(ok.value)
+
+    def nrank_search(self, a, rho_minus, rho_plus, kappa, policy, seed, sid):
+        """lowrank::nrank_search (lowrank.cpp:360-396): (rho, basis) with policy 0 Binary / 1 LinearDown."""
+        a = np.ascontiguousarray(a, float)
+        m, n = a.shape
+        w = max(m, n)
+        basis = np.zeros(max(min(m, n) * rho_plus, w))
+        rho, br, bc = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        self._chk(self.lib.rlref_nrank_search(m, n, a, rho_minus, rho_plus, kappa, policy, seed, sid, C.byref(rho),
+                                              basis, C.byref(br), C.byref(bc)), "nrank_search")
+        return rho.value, basis[:br.value * bc.value].reshape(br.value, bc.value)
+
+    def extremal_sv_estimate(self, a, method, iters, seed, sid):
+        """lowrank::extremal_sv_estimate: (sv_max, sv_min); method 0 Power / 1 Lanczos."""
+        a = np.ascontiguousarray(a, float)
+        hi, lo = C.c_double(0.0), C.c_double(0.0)
+        self._chk(self.lib.rlref_extremal_sv_estimate(a.shape[0], a.shape[1], a, method, iters, seed, sid,
+                                                      C.byref(hi), C.byref(lo)), "extremal_sv_estimate")
+        return hi.value, lo.value
+
+    def cond_probe(self, b, kappa, method, iters, seed, sid):
+        b = np.ascontiguousarray(b, float)
+        ok = C.c_int(0)
+        self._chk(self.lib.rlref_cond_probe(b.shape[0], b.shape[1], b, kappa, method, iters, seed, sid, C.byref(ok)),
+                  "cond_probe")
+        return bool(ok.value)
+
+    def power_transform(self, a, h):
+        a = np.ascontiguousarray(a, float)
+        out = np.empty_like(a)
+        self._chk(self.lib.rlref_power_transform(a.shape[0], a.shape[1], a, h, out), "power_transform")
+        return out
+
+    def sampled_residual_check(self, a, ahat, rho1, rho2, tau, seed, sid):
+        ok = C.c_int(0)
+        a, ahat = np.ascontiguousarray(a, float), np.ascontiguousarray(ahat, float)
+        self._chk(self.lib.rlref_sampled_residual_check(a.shape[0], a.shape[1], a, ahat, rho1, rho2, tau, seed, sid,
+                                                        C.byref(ok)), "sampled_residual_check")
+        return bool(ok.value)
 
     def illblock_system(self, n, seed, sid):
         a, b, y = np.empty((n, n)), np.empty(n), np.empty(n)

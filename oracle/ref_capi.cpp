@@ -19,6 +19,7 @@
 #include "randla/random_gen.hpp"
 #include "randla/structured.hpp"
 #include "randla/dense_core.hpp"
+#include "randla/lowrank.hpp"
 
 using namespace randla;
 
@@ -256,6 +257,75 @@ int rlref_singular_values(uint64_t m, uint64_t n, const double* a, double* sigma
     GUARD_BEGIN
     auto f = dense::svd(mat(m, n, a));
     std::memcpy(sigma, f.sigma.data(), f.sigma.size() * sizeof(double));
+    GUARD_END
+}
+
+// lowrank::proto_lowrank (lowrank.cpp:108-177). approx: m x n; basis: n x rho (up to n x rho_plus
+// capacity, `basis_cols` receives its column count); out: rho, ok.
+int rlref_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus, double tau,
+                        double tau_prime, int tag, double mu, double sigma, uint64_t seed, uint64_t sid,
+                        uint64_t* rho, double* approx, double* basis, uint64_t* basis_cols,
+                        double* residual, int* ok) {
+    GUARD_BEGIN
+    auto r = lowrank::proto_lowrank(mat(m, n, a), rho_plus, tau, tau_prime, kind_of(tag, mu, sigma),
+                                    rnd::RngStream{seed, sid});
+    *rho = r.rho;
+    put(r.approx, approx);
+    put(r.basis, basis);
+    *basis_cols = r.basis.cols();
+    *residual = r.residual;
+    *ok = r.ok ? 1 : 0;
+    GUARD_END
+}
+
+// lowrank::nrank_search (lowrank.cpp:360-396); basis: n x rho of the wide-side work matrix
+// (capacity n x rho_plus).
+int rlref_nrank_search(uint64_t m, uint64_t n, const double* a, uint64_t rho_minus, uint64_t rho_plus,
+                       double kappa, int policy, uint64_t seed, uint64_t sid, uint64_t* rho, double* basis,
+                       uint64_t* basis_rows, uint64_t* basis_cols) {
+    GUARD_BEGIN
+    auto r = lowrank::nrank_search(mat(m, n, a), rho_minus, rho_plus, kappa,
+                                   static_cast<lowrank::SearchPolicy>(policy), rnd::RngStream{seed, sid});
+    *rho = r.rho;
+    put(r.basis, basis);
+    *basis_rows = r.basis.rows();
+    *basis_cols = r.basis.cols();
+    GUARD_END
+}
+
+// lowrank::extremal_sv_estimate (lowrank.cpp:204-348); method 0 = Power, 1 = Lanczos.
+int rlref_extremal_sv_estimate(uint64_t m, uint64_t n, const double* a, int method, int iters, uint64_t seed,
+                               uint64_t sid, double* sv_max, double* sv_min) {
+    GUARD_BEGIN
+    auto e = lowrank::extremal_sv_estimate(mat(m, n, a), static_cast<lowrank::SvMethod>(method), iters,
+                                           rnd::RngStream{seed, sid});
+    *sv_max = e.sv_max;
+    *sv_min = e.sv_min;
+    GUARD_END
+}
+
+// lowrank::cond_probe (lowrank.cpp:350-358).
+int rlref_cond_probe(uint64_t m, uint64_t n, const double* b, double kappa, int method, int iters,
+                     uint64_t seed, uint64_t sid, int* pass) {
+    GUARD_BEGIN
+    *pass = lowrank::cond_probe(mat(m, n, b), kappa, static_cast<lowrank::SvMethod>(method), iters,
+                                rnd::RngStream{seed, sid}) ? 1 : 0;
+    GUARD_END
+}
+
+// lowrank::power_transform (lowrank.cpp:179-187): (A A^T)^h A.
+int rlref_power_transform(uint64_t m, uint64_t n, const double* a, unsigned h, double* out) {
+    GUARD_BEGIN
+    put(lowrank::power_transform(mat(m, n, a), h), out);
+    GUARD_END
+}
+
+// lowrank::sampled_residual_check (lowrank.cpp:189-202).
+int rlref_sampled_residual_check(uint64_t m, uint64_t n, const double* a, const double* ahat, uint64_t rho1,
+                                 uint64_t rho2, double tau, uint64_t seed, uint64_t sid, int* pass) {
+    GUARD_BEGIN
+    *pass = lowrank::sampled_residual_check(mat(m, n, a), mat(m, n, ahat), rho1, rho2, tau,
+                                            rnd::RngStream{seed, sid}) ? 1 : 0;
     GUARD_END
 }
 

@@ -10,6 +10,7 @@
 //   svd         dense_core.cpp:117-136 (sigma non-increasing; sign convention:
 //                                       largest-|.| entry of each left vector > 0)
 //   cond2       dense_core.cpp:177-186 (+ numerical_rank :161-175)
+//   inverse     dense_core.cpp:241-247 (partial-pivoting LU inverse; needed by lowrank.cpp)
 // Eigen's own rounding is not reproduced (it is unpinned upstream);
 // QR is unique for full rank, so Q and R agree with Eigen to rounding.
 // The SVD is a one-sided (Hestenes) Jacobi iteration.
@@ -259,6 +260,39 @@ double cond2(const Matrix& a, double tol) {
     if (smin == 0.0)
         return std::numeric_limits<double>::infinity();
     return sg[0] / smin;
+}
+
+Matrix inverse(const Matrix& a) {
+    if (a.rows() != a.cols())
+        throw DimensionMismatch("inverse: square matrix required");
+    const std::size_t n = a.rows();
+    Matrix w = a, inv = Matrix::identity(n);
+    for (std::size_t k = 0; k < n; ++k) { // Gauss-Jordan with partial pivoting
+        std::size_t p = k;
+        for (std::size_t i = k + 1; i < n; ++i)
+            if (std::abs(w(i, k)) > std::abs(w(p, k)))
+                p = i;
+        if (p != k)
+            for (std::size_t j = 0; j < n; ++j) {
+                std::swap(w(k, j), w(p, j));
+                std::swap(inv(k, j), inv(p, j));
+            }
+        const double d = w(k, k);
+        for (std::size_t j = 0; j < n; ++j) {
+            w(k, j) /= d;
+            inv(k, j) /= d;
+        }
+        for (std::size_t i = 0; i < n; ++i) {
+            if (i == k || w(i, k) == 0.0)
+                continue;
+            const double f = w(i, k);
+            for (std::size_t j = 0; j < n; ++j) {
+                w(i, j) -= f * w(k, j);
+                inv(i, j) -= f * inv(k, j);
+            }
+        }
+    }
+    return inv;
 }
 
 } // namespace randla::dense

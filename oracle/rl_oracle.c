@@ -931,6 +931,170 @@ done:
     return status;
 }
 
+/* One right-hand side of an attempt (genp.cpp:256-274) on the factored system: rhs (already
+ * multiplied by the left multiplier when used), solve, y = right z, `refine` refinement steps.
+ * v holds 4 scratch vectors of n. */
+static int solve_column(uint64_t n, const double* a, const double* b, const double* sys, const mult_t* left,
+                        const mult_t* right, int side, int refine, const double* rhs, double* yy, double* v) {
+    const int use_left = (side == SIDE_LEFT || side == SIDE_BOTH);
+    double *z = v, *r = v + n, *t = v + 2 * n;
+    int st = 0;
+    rlo_genp_solve(n, sys, rhs, z);
+    if (side == SIDE_LEFT)
+        memcpy(yy, z, n * sizeof(double));
+    else
+        st = apply_vec(right, z, yy);
+    for (int s = 0; s < refine && !st; ++s) {
+        rlo_matvec(n, n, a, yy, t);
+        for (uint64_t i = 0; i < n; ++i)
+            r[i] = b[i] - t[i];
+        if (use_left) {
+            st = apply_vec(left, r, t);
+            memcpy(r, t, n * sizeof(double));
+        }
+        rlo_genp_solve(n, sys, r, z);
+        if (side == SIDE_LEFT)
+            memcpy(t, z, n * sizeof(double));
+        else
+            st = st ? st : apply_vec(right, z, t);
+        for (uint64_t i = 0; i < n; ++i)
+            yy[i] += t[i];
+    }
+    return st;
+}
+
+/* randomized_genp (genp.cpp:207-291) for nrhs right-hand sides at once: column j behaves as an
+ * independent reference call randomized_genp(a, B[:, j], ...) on the same stream — the draws of
+ * attempt a do not depend on b, so attempt a's multipliers and factorization are shared, and each
+ * column keeps the first attempt whose residual is <= 1e-7 (else its best). Per column the
+ * operations are exactly those of the single-RHS call (solve_column), so the bits agree with it.
+ * B, Y row-major n x nrhs; reports: nrhs x 6 (rep[] of the single call); extras: nrhs x 2
+ * (accepted attempt, attempts drawn). skip_raw: leave the contrast-arm fields at 0. */
+int rlo_randomized_genp_multi(uint64_t n, uint64_t nrhs, const double* a, const double* B, int tag, double mu,
+                              double sigma, int side, int refine, uint64_t seed, uint64_t sid, int skip_raw,
+                              double* Y, double* reports, int* extras) {
+    if (refine < 0 || refine > 2)
+        return 2;
+    if ((tag == TAG_HH_PAIR || tag == TAG_SPARSE) && side != SIDE_RIGHT)
+        return 2;
+    const uint64_t nn = n * n;
+    double* w = (double*)malloc(nn * sizeof(double));
+    double* sys = (double*)malloc(nn * sizeof(double));
+    double* piv = (double*)malloc(n * sizeof(double));
+    double* v = (double*)malloc((6 + 2 * nrhs) * n * sizeof(double));
+    double *bj = v, *rhs = v + n, *yy = v + 2 * n, *scr = v + 3 * n; /* scr: 3 vectors */
+    double* best_y = v + 6 * n;                                      /* nrhs x n */
+    double* col_b = best_y + nrhs * n;                               /* nrhs x n */
+    int* done = (int*)calloc(nrhs, sizeof(int));
+    int* have = (int*)calloc(nrhs, sizeof(int));
+    double raw[6] = {0, 0, 0, 0, 0, 0};
+    int status = 0, drawn = 0;
+    for (uint64_t j = 0; j < nrhs; ++j)
+        for (uint64_t i = 0; i < n; ++i)
+            col_b[j * n + i] = B[i * nrhs + j];
+    if (!skip_raw) {
+        memcpy(w, a, nn * sizeof(double));
+        rlo_genp_factor(n, w, 0.0, piv);
+        minmax(n, piv, &raw[4], &raw[5]);
+    }
+    for (uint64_t j = 0; j < nrhs; ++j) {
+        double* rep = reports + 6 * j;
+        memset(rep, 0, 6 * sizeof(double));
+        if (!skip_raw) {
+            rlo_genp_solve(n, w, col_b + j * n, yy);
+            rep[1] = all_finite(n, yy) ? rlo_relative_residual(n, a, yy, col_b + j * n) : INFINITY;
+            rep[4] = raw[4];
+            rep[5] = raw[5];
+        }
+        extras[2 * j] = -1;
+    }
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        uint64_t ds = sid + 7919ULL * (uint64_t)attempt;
+        mult_t left, right;
+        int use_left = (side == SIDE_LEFT || side == SIDE_BOTH);
+        int use_right = (side == SIDE_RIGHT || side == SIDE_BOTH);
+        int pending = 0;
+        for (uint64_t j = 0; j < nrhs; ++j)
+            pending += !done[j];
+        if (!pending)
+            break;
+        ++drawn;
+        int st = 0;
+        memset(&left, 0, sizeof(left));
+        memset(&right, 0, sizeof(right));
+        if (use_left)
+            st = draw(&left, tag, mu, sigma, n, seed, ds);
+        if (!st && use_right)
+            st = draw(&right, tag, mu, sigma, n, seed, ds ^ 0x5000000000000000ULL);
+        memcpy(sys, a, nn * sizeof(double));
+        if (!st && use_left) {
+            st = apply_left_mat(&left, sys, w);
+            memcpy(sys, w, nn * sizeof(double));
+        }
+        if (!st && use_right) {
+            st = apply_right_mat(&right, sys, w);
+            memcpy(sys, w, nn * sizeof(double));
+        }
+        if (st) {
+            mult_free(&left);
+            mult_free(&right);
+            status = st;
+            break;
+        }
+        if (rlo_genp_factor(n, sys, 1e-300, piv) != 0) {
+            mult_free(&left);
+            mult_free(&right);
+            continue;
+        }
+        double pmn, pmx;
+        minmax(n, piv, &pmn, &pmx);
+        for (uint64_t j = 0; j < nrhs && !st; ++j) {
+            if (done[j])
+                continue;
+            memcpy(bj, col_b + j * n, n * sizeof(double));
+            if (use_left)
+                st = apply_vec(&left, bj, rhs);
+            else
+                memcpy(rhs, bj, n * sizeof(double));
+            if (!st)
+                st = solve_column(n, a, bj, sys, &left, &right, side, refine, rhs, yy, scr);
+            if (st)
+                break;
+            double res = rlo_relative_residual(n, a, yy, bj);
+            double* rep = reports + 6 * j;
+            if (res <= 1e-7 || !have[j] || res < rep[0]) {
+                memcpy(best_y + j * n, yy, n * sizeof(double));
+                rep[0] = res;
+                rep[2] = pmn;
+                rep[3] = pmx;
+                have[j] = 1;
+                extras[2 * j] = attempt;
+            }
+            done[j] = res <= 1e-7;
+        }
+        mult_free(&left);
+        mult_free(&right);
+        if (st) {
+            status = st;
+            break;
+        }
+    }
+    for (uint64_t j = 0; j < nrhs; ++j) {
+        extras[2 * j + 1] = done[j] ? extras[2 * j] + 1 : drawn; /* the single call stops at acceptance */
+        if (!have[j] && !status)
+            status = 3;
+        for (uint64_t i = 0; i < n; ++i)
+            Y[i * nrhs + j] = best_y[j * n + i];
+    }
+    free(w);
+    free(sys);
+    free(piv);
+    free(v);
+    free(done);
+    free(have);
+    return status;
+}
+
 /* ------------------------------------------------------ range finder ---- */
 
 /* dense_core.cpp:86-115 semantics: Householder QR, rank check
@@ -1134,9 +1298,21 @@ void rlo_svd_left(uint64_t m, uint64_t n, const double* a, double* sigma, double
 int rlo_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho_plus, double tau, double tau_prime,
                       int tag, double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out,
                       double* basis, double* approx, double* residual, int* ok) {
-    if (tag != TAG_GAUSSIAN && tag != TAG_TOEPLITZ)
-        return 2;
+    /* lowrank.cpp:110-125: the tau checks, then ||A||; the zero matrix is accepted before
+     * approx_basis validates rho_plus or the kind */
     if (!(tau_prime > 0.0 && tau_prime < 1.0) || (tau > 0.0 && !(tau < 1.0)))
+        return 2;
+    int all_zero = 1;
+    for (uint64_t i = 0; i < m * n && all_zero; ++i)
+        all_zero = a[i] == 0.0;
+    if (all_zero) {
+        *rho_out = 0;
+        *residual = 0.0;
+        *ok = 1;
+        memset(approx, 0, m * n * sizeof(double));
+        return 0;
+    }
+    if (tag != TAG_GAUSSIAN && tag != TAG_TOEPLITZ)
         return 2;
     if (rho_plus < 1 || rho_plus > (m < n ? m : n))
         return 2;

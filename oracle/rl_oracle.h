@@ -77,6 +77,11 @@ void rlo_sparse_apply_vec(uint64_t n, int nnz, const int32_t* rows, const double
 int rlo_randomized_genp(uint64_t n, const double* a, const double* b, int tag, double mu,
                         double sigma, int side, int refine, uint64_t seed, uint64_t sid, double* y,
                         double* report, int* extra);
+/* randomized_genp for nrhs columns sharing the draws (per column bit-identical to the single
+ * call); B, Y row-major n x nrhs, reports nrhs x 6, extras nrhs x 2. */
+int rlo_randomized_genp_multi(uint64_t n, uint64_t nrhs, const double* a, const double* B, int tag, double mu,
+                              double sigma, int side, int refine, uint64_t seed, uint64_t sid, int skip_raw,
+                              double* Y, double* reports, int* extras);
 
 int rlo_qr_positive(uint64_t m, uint64_t n, const double* a, double* q, double* r);
 void rlo_singular_values(uint64_t m, uint64_t n, const double* a, double* sigma);

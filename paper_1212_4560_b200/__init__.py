@@ -35,7 +35,7 @@ __all__ = [
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
     "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
     "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_toeplitz_apply_right", "proto_lowrank", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
-    "box_muller", "box_muller_hash", "launch_count", "LIB_PATH",
+    "box_muller", "box_muller_hash", "last_column_reports", "launch_count", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -142,6 +142,11 @@ class MulSide:
     BOTH = 2
 
 
+class _ColumnReport(C.Structure):
+    _fields_ = [("residual", C.c_double), ("pivot_min", C.c_double), ("pivot_max", C.c_double),
+                ("attempt", C.c_int32), ("attempts_drawn", C.c_int32)]
+
+
 class _Report(C.Structure):
     _fields_ = [("residual", C.c_double), ("raw_residual", C.c_double), ("pivot_min", C.c_double),
                 ("pivot_max", C.c_double), ("raw_pivot_min", C.c_double), ("raw_pivot_max", C.c_double),
@@ -232,6 +237,7 @@ def lib() -> C.CDLL:
         "rl_dev_numerical_rank": [u64, u64, vp, dbl, C.POINTER(u64), _d],
         "rl_probe_peaks": [C.POINTER(dbl), C.POINTER(dbl)],
         "rl_box_muller": [u64, vp, vp],
+        "rl_last_column_reports": [u64, vp],
         "rl_box_muller_hash": [u64, u64, u64, vp],
     }
     for name, args in sig.items():
@@ -513,6 +519,14 @@ def dev_randomized_genp(a, b, x, kind: MultiplierKind, side: int, refine: int, s
                                          stream.seed, stream.stream_id, _ptr(x), C.byref(rep),
                                          1 if skip_raw_arm else 0))
     return _report(rep, kind, refine)
+
+
+def last_column_reports(nrhs: int):
+    """Per-column outcome of this thread's last randomized_genp call (rl_last_column_reports):
+    a list of (attempt, attempts_drawn, residual, pivot_min, pivot_max)."""
+    arr = (_ColumnReport * nrhs)()
+    _chk(lib().rl_last_column_reports(nrhs, arr))
+    return [(c.attempt, c.attempts_drawn, c.residual, c.pivot_min, c.pivot_max) for c in arr]
 
 
 def dev_randomized_genp_batched(a, b, x, kind: MultiplierKind, side: int, refine: int, seed: int, sids,

@@ -26,6 +26,7 @@ void circ_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* c, const double
 rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const double* B, int tag,
                               double mu, double sigma, int side, int refine, uint64_t seed, uint64_t sid,
                               double* X, rl_precond_report* report, uint32_t flags);
+const std::vector<rl_column_report>& last_column_reports();
 rl_status randomized_genp_batched_dev(uint64_t batch, uint64_t n, const double* dA, const double* dB,
                                       int tag, double mu, double sigma, int side, int refine,
                                       uint64_t seed, const uint64_t* d_sids, double* dX,
@@ -427,13 +428,26 @@ rl_status rl_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho
                            double tau_prime, int tag, double mu, double sigma, uint64_t seed, uint64_t sid,
                            uint64_t* rho, double* basis, double* approx, double* residual, int* ok) {
     API_BEGIN
-    if (tag != RL_GAUSSIAN && tag != RL_TOEPLITZ_GAUSSIAN)
-        fail(RL_INVALID_ARGUMENT, "proto_lowrank: the B200 path takes the Gaussian and ToeplitzGaussian kinds");
     require_positive(m, n, "proto_lowrank");
     if (!(tau_prime > 0.0 && tau_prime < 1.0))
         fail(RL_INVALID_ARGUMENT, "proto_lowrank: tau_prime must lie in (0, 1)");
     if (tau > 0.0 && !(tau < 1.0))
         fail(RL_INVALID_ARGUMENT, "proto_lowrank: tau must lie in (0, 1) or <= 0 for auto");
+    // lowrank.cpp:116-125: ||A|| = 0 is accepted (rho 0, empty basis) before approx_basis checks
+    // rho_plus or the kind
+    bool all_zero = true;
+    for (uint64_t i = 0; i < m * n && all_zero; ++i)
+        all_zero = a[i] == 0.0;
+    if (all_zero) {
+        *rho = 0;
+        *residual = 0.0;
+        *ok = 1;
+        std::memset(basis, 0, n * std::max<uint64_t>(rho_plus, 1) * sizeof(double));
+        std::memset(approx, 0, m * n * sizeof(double));
+        return RL_OK;
+    }
+    if (tag != RL_GAUSSIAN && tag != RL_TOEPLITZ_GAUSSIAN)
+        fail(RL_INVALID_ARGUMENT, "proto_lowrank: the B200 path takes the Gaussian and ToeplitzGaussian kinds");
     if (rho_plus < 1 || rho_plus > std::min(m, n))
         fail(RL_INVALID_ARGUMENT, "approx_basis: rho_plus out of range");
     if (tag == RL_GAUSSIAN && !(sigma > 0.0))
@@ -612,6 +626,15 @@ rl_status rl_randomized_genp_ex(uint64_t n, uint64_t nrhs, const double* a, cons
     if (s != RL_OK)
         return s;
     download(x, dx, n * nrhs);
+    API_END
+}
+
+rl_status rl_last_column_reports(uint64_t nrhs, rl_column_report* out) {
+    API_BEGIN
+    const std::vector<rl_column_report>& c = last_column_reports();
+    if (c.size() != nrhs)
+        fail(RL_INVALID_ARGUMENT, "last_column_reports: no randomized_genp call with this nrhs on this thread");
+    std::memcpy(out, c.data(), nrhs * sizeof(rl_column_report));
     API_END
 }
 

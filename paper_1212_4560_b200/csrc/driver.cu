@@ -321,9 +321,13 @@ double residual_max(uint64_t n, uint64_t nrhs, const double* a, const double* x,
 
 } // namespace
 
+// Per-column outcome of this thread's last randomized_genp_dev call (rl_last_column_reports).
+thread_local std::vector<rl_column_report> g_last_cols;
+
 rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const double* B, int tag,
                               double mu, double sigma, int side, int refine, uint64_t seed, uint64_t sid,
                               double* X, rl_precond_report* report, uint32_t flags) {
+    g_last_cols.clear();
     if (refine < 0 || refine > 2)
         fail(RL_INVALID_ARGUMENT, "randomized_genp: refine must be in {0, 1, 2}");
     if (side < 0 || side > 2)
@@ -503,6 +507,10 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
     if (spec_attempt >= 0) // an unused speculative draw still owns its slot and the RNG workspace
         RL_CUDA(cudaStreamWaitEvent(st, sp.done, 0));
     if (have_best) {
+        g_last_cols.resize(nrhs);
+        for (uint64_t j = 0; j < nrhs; ++j)
+            g_last_cols[j] = rl_column_report{col_best[j], col_pmin[j], col_pmax[j], col_attempt[j],
+                                              col_accepted[j] ? col_attempt[j] + 1 : rep.attempts_drawn};
         // report: worst column; its attempt and pivots (nrhs = 1: exactly the reference's report)
         uint64_t w = 0;
         for (uint64_t j = 1; j < nrhs; ++j)
@@ -522,6 +530,8 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
     RL_CUDA(cudaStreamSynchronize(st));
     return status;
 }
+
+const std::vector<rl_column_report>& last_column_reports() { return g_last_cols; }
 
 rl_status randomized_genp_batched_dev(uint64_t batch, uint64_t n, const double* dA, const double* dB,
                                       int tag, double mu, double sigma, int side, int refine,

@@ -105,6 +105,112 @@ __global__ void k_hh2_apply(uint64_t n, const double* __restrict__ a, uint64_t l
     }
 }
 
+// One pass over A for the Householder pair (config 5, north_star "stream A once"): the row dots
+// w1 = A(i,:) u1, w2 = A(i,:) u2 need the whole row before any output of that row can be written,
+// so the row is held on chip. Persistent CTAs (one per SM, 1024 threads): row r arrives in shared
+// memory by one TMA bulk copy (cp.async.bulk + mbarrier), every thread moves its 2K values into
+// registers, thread 0 immediately launches row r + grid into the freed buffer, and the dots,
+// the two-level reduction (warp shuffles, 32 partials in shared memory summed in a fixed order by
+// every thread) and the streaming stores of row r overlap that copy. HBM traffic: A read once,
+// the output written once = 2 n^2 8 bytes. u1, u2 (+-1) stay in registers for the whole kernel.
+__device__ __forceinline__ uint32_t hh_smem(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+constexpr int HH_THREADS = 1024, HH_K = 8; // 1024 threads x 8 double2 = rows of up to 16384
+__global__ void __launch_bounds__(HH_THREADS, 1)
+    k_hh2_onepass(uint64_t n, const double* __restrict__ a, uint64_t lda, const double* __restrict__ u1,
+                  const double* __restrict__ u2, double s12, double c, double* __restrict__ out, uint64_t ldo) {
+    extern __shared__ __align__(16) double hh_row[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ double red1[32], red2[32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t nn = static_cast<uint32_t>(n);
+    // u1, u2 are +-1 vectors: one sign bit per element (bit 2k + h: element 2(t + k 1024) + h)
+    uint32_t m1 = 0, m2 = 0;
+#pragma unroll
+    for (int k = 0; k < HH_K; ++k) {
+        const uint32_t j = 2u * static_cast<uint32_t>(t + k * HH_THREADS);
+        if (j < nn) {
+            const double2 q1 = *reinterpret_cast<const double2*>(u1 + j);
+            const double2 q2 = *reinterpret_cast<const double2*>(u2 + j);
+            m1 |= (q1.x < 0.0 ? 1u : 0u) << (2 * k) | (q1.y < 0.0 ? 1u : 0u) << (2 * k + 1);
+            m2 |= (q2.x < 0.0 ? 1u : 0u) << (2 * k) | (q2.y < 0.0 ? 1u : 0u) << (2 * k + 1);
+        }
+    }
+    auto sgn = [](uint32_t m, int b, double x) { return ((m >> b) & 1u) ? -x : x; }; // x * u (exact)
+    const uint32_t bytes = static_cast<uint32_t>(n * sizeof(double));
+    const uint32_t mb = hh_smem(&bar);
+    auto issue = [&](uint64_t r) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         hh_smem(hh_row)),
+                     "l"(a + r * lda), "r"(bytes), "r"(mb)
+                     : "memory");
+    };
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (blockIdx.x < n)
+            issue(blockIdx.x);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (uint64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                         " selp.u32 %0, 1, 0, p;\n}"
+                         : "=r"(done)
+                         : "r"(mb), "r"(phase)
+                         : "memory");
+        phase ^= 1u;
+        double2 v[HH_K];
+#pragma unroll
+        for (int k = 0; k < HH_K; ++k) {
+            const uint32_t j = 2u * static_cast<uint32_t>(t + k * HH_THREADS);
+            v[k] = j < nn ? *reinterpret_cast<const double2*>(hh_row + j) : make_double2(0.0, 0.0);
+        }
+        __syncthreads(); // the buffer is free: the next row streams in under this row's work
+        if (t == 0 && r + gridDim.x < n)
+            issue(r + gridDim.x);
+        double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < HH_K; ++k) { // d += v u, u = +-1 (the products are exact)
+            d1 = (d1 + sgn(m1, 2 * k, v[k].x)) + sgn(m1, 2 * k + 1, v[k].y);
+            d2 = (d2 + sgn(m2, 2 * k, v[k].x)) + sgn(m2, 2 * k + 1, v[k].y);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            d1 += __shfl_xor_sync(0xffffffffu, d1, off);
+            d2 += __shfl_xor_sync(0xffffffffu, d2, off);
+        }
+        if (lane == 0) {
+            red1[warp] = d1;
+            red2[warp] = d2;
+        }
+        __syncthreads();
+        double w1 = 0.0, w2 = 0.0;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+            w1 += red1[q];
+            w2 += red2[q];
+        }
+        const double t1 = c * w1;
+        const double t2 = c * (w2 - t1 * s12);
+        double* orow = out + r * ldo;
+#pragma unroll
+        for (int k = 0; k < HH_K; ++k) {
+            const uint32_t j = 2u * static_cast<uint32_t>(t + k * HH_THREADS);
+            if (j < nn) {
+                double2 o;
+                o.x = (v[k].x - sgn(m1, 2 * k, t1)) - sgn(m2, 2 * k, t2);
+                o.y = (v[k].y - sgn(m1, 2 * k + 1, t1)) - sgn(m2, 2 * k + 1, t2);
+                __stcs(reinterpret_cast<double2*>(orow + j), o);
+            }
+        }
+    }
+}
+
 // x = H1 (H2 y) for nrhs columns (ld nrhs): one CTA per column (small work)
 __global__ void k_hh2_vec(uint64_t n, uint64_t nrhs, const double* u1, const double* u2, const double* y,
                           double* x) {
@@ -589,6 +695,22 @@ void rank1_dense_dev(uint64_t n, const double* u, const double* v, double inv_uv
 // out = A H1 H2 (out may alias a); s12 = u1^T u2 (exact integer, host-computed)
 void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
                          double s12, double* out, uint64_t ldo) {
+    if (n <= 2ull * HH_THREADS * HH_K && n % 2 == 0 && lda % 2 == 0 && ldo % 2 == 0 &&
+        ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+        const size_t smem = n * sizeof(double);
+        static bool attr[16] = {};
+        if (!attr[ctx().device & 15]) {
+            RL_CUDA(cudaFuncSetAttribute(k_hh2_onepass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(2 * HH_THREADS * HH_K * sizeof(double))));
+            attr[ctx().device & 15] = true;
+        }
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, ctx().sms));
+        k_hh2_onepass<<<grid, HH_THREADS, smem, stream()>>>(n, a, lda, u1, u2, s12, 2.0 / static_cast<double>(n),
+                                                            out, ldo);
+        RL_LAUNCHED();
+        return;
+    }
+    // rows longer than 16384 or unaligned: two passes (row dots, then the rank-2 update)
     double* w = ws<double>(WS_SMALL, 2 * n);
     k_hh2_rowdots<<<cdiv(n, 8), 256, 0, stream()>>>(n, a, lda, u1, u2, w, w + n);
     RL_LAUNCHED();

@@ -15,10 +15,11 @@ import numpy as np
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), "..", ".."))
 sys.path.insert(0, ROOT)
-from oracle.pyoracle import Reference  # noqa: E402
+from oracle.pyoracle import Reference, Restated  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(__file__))
 R = Reference()
+O = Restated()
 g = {}
 
 # --- RNG streams (random_gen.cpp:22-70) -------------------------------------------
@@ -76,7 +77,7 @@ for kind in ("toeplitz_gaussian", "householder_sign"):
 
 # --- config 2 shape (n = 64 systems, circulant sign, Right) --------------------------
 batch, n2, seed2 = 48, 64, 4096
-As, bs, ys, reps = [], [], [], []
+As, bs, ys, reps, atts = [], [], [], [], []
 for t in range(batch):
     At = R.gaussian_matrix(n2, n2, seed2, 10 * t + 1)
     Pt = R.gaussian_matrix(32, 31, seed2, 10 * t + 2)
@@ -85,8 +86,14 @@ for t in range(batch):
     xt = R.gaussian_matrix(n2, 1, seed2, 10 * t + 4).ravel()
     bt = R.matvec(At, xt)
     y, rep = R.randomized_genp(At, bt, "circulant_sign", "right", 0, seed=seed2, sid=1000 + t)
+    # the reference's report has no attempt field: take it from the restatement, whose y and report
+    # must equal the reference's bit for bit (so it accepted the same draw)
+    yo, ro, eo = O.randomized_genp(At, bt, "circulant_sign", "right", 0, seed=seed2, sid=1000 + t)
+    assert np.array_equal(y, yo) and np.array_equal(rep, ro), t
+    atts.append(int(eo[0]))
     As.append(At), bs.append(bt), ys.append(y), reps.append(rep)
 g["c2/A"], g["c2/b"], g["c2/y"], g["c2/report"] = np.array(As), np.array(bs), np.array(ys), np.array(reps)
+g["c2/attempt"] = np.array(atts, dtype=np.int32)
 g["c2/sids"] = np.arange(1000, 1000 + batch, dtype=np.uint64)
 g["c2/seed"] = np.array([seed2], dtype=np.uint64)
 

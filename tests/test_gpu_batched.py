@@ -7,21 +7,36 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def test_config2_golden(rl, golden):
+def test_config2_golden(rl, golden, oracle):
+    """48 config-2-shaped systems against the reference's fixtures: the same accepted attempt for
+    every system (golden c2/attempt), x within 1e-8, and the backward error within 2x of the
+    reference's band — the largest backward error the reference itself shows on that system over
+    three 1-ulp perturbations of A (its per-system rounding scatter reaches ~10x on these
+    ill-conditioned n = 64 systems: profiles/r02_pin_c2.json) — per system and for the worst."""
     A, b, y_ref, rep_ref = golden["c2/A"], golden["c2/b"], golden["c2/y"], golden["c2/report"]
     seed = int(golden["c2/seed"][0])
+    sids = golden["c2/sids"]
     x, reps = rl.randomized_genp_batched(A, b, rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN),
-                                         rl.MulSide.RIGHT, 0, seed, golden["c2/sids"])
-    worst, worst_ref = 0.0, 0.0
+                                         rl.MulSide.RIGHT, 0, seed, sids)
+    rng = np.random.default_rng(48)
+
+    def be(a, v, bb):
+        return np.linalg.norm(a @ v - bb) / (np.linalg.norm(a) * np.linalg.norm(v))
+
+    worst, worst_band = 0.0, 0.0
     for t in range(A.shape[0]):
-        assert np.abs(x[t] - y_ref[t]).max() / np.abs(y_ref[t]).max() < 1e-8, t
-        be = np.linalg.norm(A[t] @ x[t] - b[t]) / (np.linalg.norm(A[t]) * np.linalg.norm(x[t]))
-        be_ref = np.linalg.norm(A[t] @ y_ref[t] - b[t]) / (np.linalg.norm(A[t]) * np.linalg.norm(y_ref[t]))
-        worst, worst_ref = max(worst, be), max(worst_ref, be_ref)
-        assert be <= 4 * be_ref + 16 * 2.2e-16, t  # per system: eps-level noise floor
-        assert reps[t].attempt == int(rep_ref[t][6]) if rep_ref.shape[1] > 6 else True
+        assert reps[t].attempt == int(golden["c2/attempt"][t]), t
         assert reps[t].residual <= 1e-7 and rep_ref[t][0] <= 1e-7
-    assert worst <= 2 * worst_ref  # config 2 reports the worst backward error
+        assert np.abs(x[t] - y_ref[t]).max() / np.abs(y_ref[t]).max() < 1e-8, t
+        band = be(A[t], y_ref[t], b[t])
+        for _ in range(3):
+            Ap = A[t] * (1.0 + 2.220446049250313e-16 * rng.standard_normal(A[t].shape))
+            yp, _, _ = oracle.randomized_genp(Ap, b[t], "circulant_sign", "right", 0, seed=seed, sid=int(sids[t]))
+            band = max(band, be(A[t], yp, b[t]))
+        g = be(A[t], x[t], b[t])
+        assert g <= 2 * band + 16 * 2.2e-16, (t, g, band)
+        worst, worst_band = max(worst, g), max(worst_band, band)
+    assert worst <= 2 * worst_band  # config 2 reports the worst backward error
 
 
 def test_redraw_protocol_matches_oracle(rl, oracle):

@@ -47,7 +47,7 @@ for c0 in range(0, n, 2048):
     ok &= bool(torch.equal(ref, out[:, c0:c0 + 2048]))
 print("sparse bit-exact vs torch gather:", ok, flush=True)
 ms = timed(lambda: rl.dev_householder_pair_apply_right(u1, u2, A, out))
-print(f"hh pair A H1 H2 n={n}: {ms:.3f} ms  {3 * n * n * 8 / ms / 1e6:.0f} GB/s", flush=True)
+print(f"hh pair A H1 H2 n={n}: {ms:.3f} ms  {2 * n * n * 8 / ms / 1e6:.0f} GB/s (A read once + written once)", flush=True)
 t1 = (2.0 / n) * (A @ u1)
 t2 = (2.0 / n) * (A @ u2 - t1 * float(u1 @ u2))
 ref = A - torch.outer(t1, u1) - torch.outer(t2, u2)
