@@ -156,11 +156,22 @@ rl_status rl_dev_gemm(int trans_a, int trans_b, uint64_t m, uint64_t n, uint64_t
                       double* d_c, uint64_t ldc);
 
 /* ------------------------------------ structured.hpp (structured.cpp) ---- */
-/* structured::circ_mul (structured.cpp:132-154): y = C x, C circulant with first column c. */
+/* The structured products are the reference's FFT algorithms executed step for step on the GPU
+ * (csrc/fft_exact.cu): the same bits as the reference, O(n log n), matrix-free. A column whose
+ * imaginary residue fails take_real's test (structured.cpp:39-50) returns RL_ERROR
+ * ("structured product: imaginary residue exceeds tolerance", randla::Error).
+ * structured::circ_mul (structured.cpp:132-154): y = C x, C circulant with first column c. */
 rl_status rl_circ_mul(uint64_t n, const double* c, const double* x, double* y);
-/* structured::multiply_matrix for a circulant spec (structured.cpp:178-189): out = C A. */
+/* structured::multiply_matrix for a circulant spec (structured.cpp:178-189): out = C A, A n x cols. */
 rl_status rl_circulant_multiply_matrix(uint64_t n, const double* c, uint64_t cols, const double* a,
                                        double* out);
+/* structured::toeplitz_mul (structured.cpp:156-176): y = T x, T m x n with first column col (m)
+ * and first row row (n), col[0] == row[0]. */
+rl_status rl_toeplitz_mul(uint64_t m, uint64_t n, const double* col, const double* row, const double* x,
+                          double* y);
+/* structured::multiply_matrix for a Toeplitz spec: out = T A, A n x cols, out m x cols. */
+rl_status rl_toeplitz_multiply_matrix(uint64_t m, uint64_t n, const double* col, const double* row, uint64_t cols,
+                                      const double* a, double* out);
 
 /* ---------------------------------------------------- genp.hpp (genp.cpp) ---- */
 /* genp::genp_factor (genp.cpp:11-41): separate unit-lower L and upper U, |pivots|,
@@ -258,9 +269,9 @@ rl_status rl_box_muller(uint64_t npairs, const uint64_t* raw, double* out);
  * pair_hash(q, bits(g0), bits(g1)) (csrc/glibc_math.cuh). Lets a host program check 2^30 pairs
  * against its own libm without moving the outputs (tests/cpp/bm_libm_check.cpp). */
 rl_status rl_box_muller_hash(uint64_t seed, uint64_t npairs, uint64_t chunk, uint64_t* hashes);
-/* structured::fft (structured.cpp:96-130): complex interleaved (re, im), n a power of two,
- * inverse scaled by 1/n. */
-rl_status rl_dft(uint64_t n, const double* in, int inverse, double* out);
+/* structured::fft (structured.cpp:96-130), bit for bit: complex interleaved (re, im), n a power
+ * of two (else RL_LENGTH_NOT_POW2), inverse scaled by 1/n. O(n log n) on the GPU. */
+rl_status rl_fft(uint64_t n, const double* in, int inverse, double* out);
 /* dense::norm (dense_core.cpp:48-84): kind 0 One, 1 Two, 2 Inf, 3 Frobenius. */
 rl_status rl_norm(uint64_t m, uint64_t n, const double* a, int kind, double* out);
 

@@ -251,6 +251,8 @@ class Reference:
         L.rlref_circulant_multiply_matrix.argtypes = [u64, _d, u64, _d, _d]
         L.rlref_circ_mul.argtypes = [u64, _d, _d, _d]
         L.rlref_fft.argtypes = [u64, _d, cint, _d]
+        L.rlref_toeplitz_mul.argtypes = [u64, u64, _d, _d, _d, _d]
+        L.rlref_toeplitz_multiply_matrix.argtypes = [u64, u64, _d, _d, u64, _d, _d]
         L.rlref_genp_factor.argtypes = [u64, _d, dbl, _d, _d, _d, _d]
         L.rlref_block_ge.argtypes = [u64, _d, u64, _d, _d, _d, _d]
         L.rlref_genp_solve.argtypes = [u64, _d, _d, _d, _d]
@@ -322,6 +324,27 @@ class Reference:
         self._chk(self.lib.rlref_circ_mul(len(c), np.ascontiguousarray(c, float), np.ascontiguousarray(x, float), y),
                   "circ_mul")
         return y
+
+    def fft(self, x, inverse=False):
+        """structured::fft on a complex vector."""
+        z = np.ascontiguousarray(np.asarray(x, np.complex128)).view(np.float64)
+        out = np.empty_like(z)
+        self._chk(self.lib.rlref_fft(len(z) // 2, z, int(inverse), out), "fft")
+        return out.view(np.complex128)
+
+    def toeplitz_mul(self, col, row, x):
+        y = np.empty(len(col))
+        self._chk(self.lib.rlref_toeplitz_mul(len(col), len(row), np.ascontiguousarray(col, float),
+                                              np.ascontiguousarray(row, float), np.ascontiguousarray(x, float), y),
+                  "toeplitz_mul")
+        return y
+
+    def toeplitz_multiply_matrix(self, col, row, a):
+        out = np.empty((len(col), a.shape[1]))
+        self._chk(self.lib.rlref_toeplitz_multiply_matrix(len(col), len(row), np.ascontiguousarray(col, float),
+                                                          np.ascontiguousarray(row, float), a.shape[1],
+                                                          np.ascontiguousarray(a, float), out), "multiply_matrix")
+        return out
 
     def circulant_multiply_matrix(self, c, a):
         out = np.empty_like(a)

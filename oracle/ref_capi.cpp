@@ -170,6 +170,15 @@ int rlref_toeplitz_mul(uint64_t m, uint64_t n, const double* col, const double* 
     GUARD_END
 }
 
+int rlref_toeplitz_multiply_matrix(uint64_t m, uint64_t n, const double* col, const double* row, uint64_t cols,
+                                   const double* a, double* out) {
+    GUARD_BEGIN
+    auto spec = structured::StructuredSpec::toeplitz(std::vector<double>(col, col + m),
+                                                     std::vector<double>(row, row + n));
+    put(structured::multiply_matrix(spec, mat(n, cols, a)), out);
+    GUARD_END
+}
+
 // Complex interleaved (re, im) in/out; dir 0 forward, 1 inverse.
 int rlref_fft(uint64_t n, const double* in, int dir, double* out) {
     GUARD_BEGIN

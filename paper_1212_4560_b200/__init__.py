@@ -35,7 +35,7 @@ __all__ = [
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
     "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
     "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_toeplitz_apply_right", "proto_lowrank", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
-    "box_muller", "box_muller_hash", "last_column_reports", "launch_count", "LIB_PATH",
+    "box_muller", "box_muller_hash", "last_column_reports", "fft", "toeplitz_mul", "toeplitz_multiply_matrix", "launch_count", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -219,6 +219,9 @@ def lib() -> C.CDLL:
         "rl_dev_gemm": [cint, cint, u64, u64, u64, dbl, vp, u64, vp, u64, dbl, vp, u64],
         "rl_circ_mul": [u64, _d, _d, _d],
         "rl_circulant_multiply_matrix": [u64, _d, u64, _d, _d],
+        "rl_toeplitz_mul": [u64, u64, _d, _d, _d, _d],
+        "rl_toeplitz_multiply_matrix": [u64, u64, _d, _d, u64, _d, _d],
+        "rl_fft": [u64, vp, cint, vp],
         "rl_genp_factor": [u64, _d, dbl, _d, _d, _d, _d, C.POINTER(C.c_int64)],
         "rl_dev_genp_factor": [u64, vp, u64, dbl, vp, C.POINTER(C.c_int64)],
         "rl_genp_solve": [u64, u64, _d, _d, _d, _d],
@@ -370,6 +373,34 @@ def circulant_multiply_matrix(first_col, a) -> np.ndarray:
         raise DimensionMismatch("multiply_matrix: inner dimensions differ")
     out = np.empty_like(a)
     _chk(lib().rl_circulant_multiply_matrix(len(c), c, a.shape[1], a, out))
+    return out
+
+
+def toeplitz_mul(first_col, first_row, x) -> np.ndarray:
+    """structured::toeplitz_mul (structured.cpp:156-176): T x, T m x n."""
+    c, r, x = _f64(first_col), _f64(first_row), _f64(x)
+    if len(x) != len(r):
+        raise DimensionMismatch("toeplitz_mul: vector length mismatch")
+    y = np.empty(len(c))
+    _chk(lib().rl_toeplitz_mul(len(c), len(r), c, r, x, y))
+    return y
+
+
+def toeplitz_multiply_matrix(first_col, first_row, a) -> np.ndarray:
+    """structured::multiply_matrix for a Toeplitz spec: T A."""
+    c, r, a = _f64(first_col), _f64(first_row), _f64(a)
+    if a.shape[0] != len(r):
+        raise DimensionMismatch("multiply_matrix: inner dimensions differ")
+    out = np.empty((len(c), a.shape[1]))
+    _chk(lib().rl_toeplitz_multiply_matrix(len(c), len(r), c, r, a.shape[1], a, out))
+    return out
+
+
+def fft(x, inverse: bool = False) -> np.ndarray:
+    """structured::fft (structured.cpp:96-130), bit-identical to the reference, on the GPU."""
+    z = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+    out = np.empty_like(z)
+    _chk(lib().rl_fft(len(z), z.ctypes.data, int(inverse), out.ctypes.data))
     return out
 
 

@@ -57,7 +57,9 @@ void uniform_int_dev(uint64_t seed, uint64_t sid, uint64_t count, int64_t lo, in
 void unpack_lu_dev(uint64_t n, const double* lu, double* l, double* u);
 void pack_lu_dev(uint64_t n, const double* l, const double* u, double* lu);
 rl_status probe_peaks(double* fp64, double* hbm);
-void dft_dev(uint64_t n, const double* in, int inverse, double* out);
+void fft_exact_dev(uint64_t n, uint64_t batch, const double2* src, double2* dst, int inverse);
+void structured_multiply_dev(uint64_t m, uint64_t n, const double* first_col, const double* first_row,
+                             uint64_t cols, const double* a, double* out);
 void abs_sums_dev(uint64_t m, uint64_t n, const double* a, int rows, double* out);
 } // namespace rl
 
@@ -486,14 +488,7 @@ rl_status rl_dev_gemm(int ta, int tb, uint64_t m, uint64_t n, uint64_t k, double
 
 // ------------------------------------------------------------ structured ----
 rl_status rl_circ_mul(uint64_t n, const double* c, const double* x, double* y) {
-    API_BEGIN
-    require_positive(n, n, "circ_mul");
-    double* dc = upload(WS_H0, c, n);
-    double* dx = upload(WS_H1, x, n);
-    double* dy = ws<double>(WS_H2, n);
-    circ_apply_vec_dev(n, 1, dc, dx, dy);
-    download(y, dy, n);
-    API_END
+    return rl_circulant_multiply_matrix(n, c, 1, x, y);
 }
 
 rl_status rl_circulant_multiply_matrix(uint64_t n, const double* c, uint64_t cols, const double* a,
@@ -502,11 +497,28 @@ rl_status rl_circulant_multiply_matrix(uint64_t n, const double* c, uint64_t col
     require_positive(n, cols, "multiply_matrix");
     double* dc = upload(WS_H0, c, n);
     double* da = upload(WS_H1, a, n * cols);
-    double* dC = ws<double>(WS_H2, n * n);
-    double* dout = ws<double>(WS_H3, n * cols);
-    circulant_dense_dev(n, dc, dC);
-    gemm(false, false, n, cols, n, 1.0, dC, n, da, cols, 0.0, dout, cols);
+    double* dout = ws<double>(WS_H2, n * cols);
+    structured_multiply_dev(n, n, dc, nullptr, cols, da, dout);
     download(out, dout, n * cols);
+    API_END
+}
+
+rl_status rl_toeplitz_mul(uint64_t m, uint64_t n, const double* col, const double* row, const double* x,
+                          double* y) {
+    return rl_toeplitz_multiply_matrix(m, n, col, row, 1, x, y);
+}
+
+rl_status rl_toeplitz_multiply_matrix(uint64_t m, uint64_t n, const double* col, const double* row, uint64_t cols,
+                                      const double* a, double* out) {
+    API_BEGIN
+    require_positive(m, n, "toeplitz_mul");
+    require_positive(cols, 1, "multiply_matrix");
+    double* dc = upload(WS_H0, col, m);
+    double* dr = upload(WS_H3, row, n);
+    double* da = upload(WS_H1, a, n * cols);
+    double* dout = ws<double>(WS_H2, m * cols);
+    structured_multiply_dev(m, n, dc, dr, cols, da, dout);
+    download(out, dout, m * cols);
     API_END
 }
 
@@ -905,13 +917,13 @@ rl_status rl_box_muller_hash(uint64_t seed, uint64_t npairs, uint64_t chunk, uin
     API_END
 }
 
-rl_status rl_dft(uint64_t n, const double* in, int inverse, double* out) {
+rl_status rl_fft(uint64_t n, const double* in, int inverse, double* out) {
     API_BEGIN
     if (n == 0 || (n & (n - 1)))
         fail(RL_LENGTH_NOT_POW2, "fft: length must be a power of two");
     double* d = upload(WS_H0, in, 2 * n);
     double* o = ws<double>(WS_H1, 2 * n);
-    dft_dev(n, d, inverse, o);
+    fft_exact_dev(n, 1, reinterpret_cast<const double2*>(d), reinterpret_cast<double2*>(o), inverse);
     download(out, o, 2 * n);
     API_END
 }

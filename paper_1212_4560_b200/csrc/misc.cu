@@ -79,27 +79,6 @@ __global__ void k_probe_copy(const double4* __restrict__ in, double4* __restrict
         out[i] = in[i];
 }
 
-__global__ void k_dft(uint64_t n, const double2* in, int inverse, double2* out) {
-    uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (k >= n)
-        return;
-    const double sgn = inverse ? 1.0 : -1.0;
-    double re = 0.0, im = 0.0;
-    for (uint64_t j = 0; j < n; ++j) {
-        double s, c;
-        // angle 2 pi jk / n reduced exactly modulo n
-        sincospi(2.0 * static_cast<double>((j * k) % n) / static_cast<double>(n), &s, &c);
-        s *= sgn;
-        re += in[j].x * c - in[j].y * s;
-        im += in[j].x * s + in[j].y * c;
-    }
-    if (inverse) {
-        re /= static_cast<double>(n);
-        im /= static_cast<double>(n);
-    }
-    out[k] = make_double2(re, im);
-}
-
 // kind 0 One (max column abs sum), 1 Inf (max row abs sum), 3 Frobenius partial sums
 __global__ void k_norm_cols(uint64_t m, uint64_t n, const double* a, double* out) {
     uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -123,11 +102,6 @@ __global__ void k_norm_rows(uint64_t m, uint64_t n, const double* a, double* out
 
 } // namespace
 
-void dft_dev(uint64_t n, const double* in, int inverse, double* out) {
-    k_dft<<<cdiv(n, 128), 128, 0, stream()>>>(n, reinterpret_cast<const double2*>(in), inverse,
-                                              reinterpret_cast<double2*>(out));
-    RL_LAUNCHED();
-}
 
 // One / Inf norm partial vectors (host takes the max of n or m values)
 void abs_sums_dev(uint64_t m, uint64_t n, const double* a, int rows, double* out) {

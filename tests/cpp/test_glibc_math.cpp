@@ -61,7 +61,8 @@ int main(int argc, char** argv) {
         const char* name;
         int kind;
     } fams[] = {{"box_muller_log", 0}, {"box_muller_sincos", 1}, {"log_unit_by_exponent", 2},
-                {"sincos_0_2pi", 3},   {"sincos_branch_points", 4}, {"log_near_one", 5}};
+                {"sincos_0_2pi", 3},   {"sincos_branch_points", 4}, {"log_near_one", 5},
+                {"sincos_signed", 6}};
     int fail = 0;
     for (const Fam& f : fams) {
         Counts c;
@@ -104,6 +105,9 @@ int main(int argc, char** argv) {
                         check_log(x, c);
                         break;
                     }
+                    case 6: // negative and positive arguments (the FFT's forward twiddles are < 0)
+                        check_sincos(14.0 * ((double)(r >> 11) * 0x1.0p-53) - 7.0, c);
+                        break;
                     }
                 }
             });
@@ -119,6 +123,10 @@ int main(int argc, char** argv) {
         check_log((double)(k + 1) * 0x1.0p-53, e);
         check_sincos(two_pi * ((double)k * 0x1.0p-53), e);
         check_sincos(two_pi * (1.0 - (double)(k + 1) * 0x1.0p-53), e);
+    }
+    for (int k = 1; k < 40; ++k) { // structured::fft's wlen angles: +-(2 pi) / 2^k
+        check_sincos(2.0 * 3.14159265358979323846 / ldexp(1.0, k), e);
+        check_sincos(-2.0 * 3.14159265358979323846 / ldexp(1.0, k), e);
     }
     check_log(0x1p-1074, e);
     check_log(0x1.fffffffffffffp-1023, e);

@@ -113,5 +113,49 @@ g["nrank/profile64"] = R.profile_matrix_paper(64, 8, 42, 90)
 
 # proto_lowrank test matrix (tests/test_lowrank.cpp:80-91): paper profile, rank 8 of 64
 g["proto/A"] = R.profile_matrix_paper(64, 8, 41, 10)
+# --- structured products through the reference's own FFT (structured.cpp:20-189) -------
+rs = np.random.default_rng(1212)
+for n in (1, 2, 8, 64, 1024, 2048, 4096, 16384):
+    z = rs.standard_normal(n) + 1j * rs.standard_normal(n)
+    g[f"fft/{n}/x"] = z
+    g[f"fft/{n}/fwd"] = R.fft(z, False)
+    g[f"fft/{n}/inv"] = R.fft(z, True)
+for n in (8, 48, 64, 1000, 4096):
+    c, x = rs.standard_normal(n), rs.standard_normal(n)
+    g[f"circ_mul/{n}/c"], g[f"circ_mul/{n}/x"] = c, x
+    g[f"circ_mul/{n}/y"] = R.circ_mul(c, x)
+for m, n in ((5, 3), (64, 64), (100, 37), (1000, 1000), (3, 700)):
+    col, row, x = rs.standard_normal(m), rs.standard_normal(n), rs.standard_normal(n)
+    row[0] = col[0]
+    g[f"toeplitz_mul/{m}x{n}/col"], g[f"toeplitz_mul/{m}x{n}/row"], g[f"toeplitz_mul/{m}x{n}/x"] = col, row, x
+    g[f"toeplitz_mul/{m}x{n}/y"] = R.toeplitz_mul(col, row, x)
+for n, cols in ((48, 7), (64, 5), (300, 33)):
+    c, a = rs.standard_normal(n), rs.standard_normal((n, cols))
+    g[f"circ_mm/{n}x{cols}/c"], g[f"circ_mm/{n}x{cols}/a"] = c, a
+    g[f"circ_mm/{n}x{cols}/out"] = R.circulant_multiply_matrix(c, a)
+col, row, a = rs.standard_normal(30), rs.standard_normal(20), rs.standard_normal((20, 6))
+row[0] = col[0]
+g["toep_mm/col"], g["toep_mm/row"], g["toep_mm/a"] = col, row, a
+g["toep_mm/out"] = R.toeplitz_multiply_matrix(col, row, a)
+# take_real's imaginary-residue Error (structured.cpp:39-50) and non-finite propagation: inputs
+# found by searching extreme values with the reference; the error cases raise, the others return
+# inf/nan patterns
+errs = [([-1e154, 1e-300, -1e154, 1e154], [-1e154, -1e154, 1.0, 1e-300]),
+        ([1e154, 1e154, -1e154, -1e154], [1e-300, -1e154, 1e300, 1e308]),
+        ([1.0, 1e-300, 1e-300, 0.0, 0.0], [-1e154, 0.0, -1e154, -1e308, 1e154]),
+        ([1.0, 1e154, 1e154, -1e154], [1.0, 1e300, 1e300, 1e154])]
+for k, (c, x) in enumerate(errs):
+    try:
+        R.circ_mul(np.array(c), np.array(x))
+        raise SystemExit("expected the reference to raise")
+    except Exception as e:  # OracleError with the Error status
+        assert "imaginary residue" in str(e), e
+    g[f"circ_err/{k}/c"], g[f"circ_err/{k}/x"] = np.array(c), np.array(x)
+nonfinite = [([np.inf, 0, 0, 0], [1, 0, 0, 0]), ([np.inf, 1, 2, 3], [1, 1, 1, 1]),
+             ([1e300, 1e300, -1e300, 1e-300], [1e300, 1, 1, 1]), ([1, 2, 3], [np.inf, 1, 1])]
+for k, (c, x) in enumerate(nonfinite):
+    c, x = np.array(c, float), np.array(x, float)
+    g[f"circ_nf/{k}/c"], g[f"circ_nf/{k}/x"], g[f"circ_nf/{k}/y"] = c, x, R.circ_mul(c, x)
+
 np.savez_compressed(os.path.join(OUT, "golden.npz"), **g)
 print("wrote", os.path.join(OUT, "golden.npz"), len(g), "arrays")

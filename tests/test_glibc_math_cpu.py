@@ -18,4 +18,4 @@ def test_glibc_math_host_matches_libm(tmp_path):
                         "-o", exe, os.path.join(HERE, "cpp", "test_glibc_math.cpp"), "-lm"], check=True)
     r = subprocess.run([exe, "21"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count(" 0 mismatches") == 7, r.stdout
+    assert r.stdout.count(" 0 mismatches") == 8, r.stdout
