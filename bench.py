@@ -163,6 +163,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+def config3(world):
+    """The headline workload (BASELINE.json configs[2]); identical in both arms' JSON lines."""
+    return {"workload": "config3: Gaussian-preconditioned GENP n=8192, 16 RHS, MulSide::Right, block 128",
+            "n": N3, "nrhs": NRHS3, "flop_per_attempt": FLOPS3, "parallelism": f"replicas{world}",
+            "l2": "inputs larger than L2 (A, G 512 MiB each)"}
+
+
 def make_config3_inputs(torch, dev):
     """A = U diag(sigma) V^T-like test matrix of config 3, built once on the GPU (not timed).
 
@@ -347,7 +354,7 @@ def run_circulant_fft(torch, rl, dev, dist, hbm_peak):
                          "peak_source": src}}
 
 
-def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak):
+def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak, rank=0, world=1):
     """Config 5: n = 16384, 8 RHS, MulSide::Right with the orthogonal Householder pair, the
     sparse +-1 and the Gaussian multipliers (contrast arm skipped as in config 3).  Short runs
     (1 warm-up + 2 timed calls per arm: a Gaussian call is ~1 s)."""
@@ -373,6 +380,10 @@ def run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak):
             arm["multiplier_bytes_per_apply"] = mult_bytes
             arm["multiplier_apply"] = time_multiplier_apply(torch, rl, dev, dist, tag, A, mult_bytes, hbm_peak)
         out[name] = arm
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline_config5(A.cpu().numpy(), os.cpu_count() or 1)
+        for name in ("householder_pair", "sparse_sign", "gaussian"):
+            out[name]["cpu_baseline"] = cb[name]
     del A, B, X
     torch.cuda.empty_cache()
     return out
@@ -504,6 +515,7 @@ def run_ours(args, dist, rank, world, local_rank):
     # executes `attempts` full multiplier draws (G, A G, LU, solves, G Y).  The headline counts
     # the flops executed; value_per_solve counts one attempt's 1.4704e12.
     attempts = max(1, rep.attempts_drawn)
+    cols = rl.last_column_reports(NRHS3)  # per right-hand side: the reference call's accepted draw
     value = world * attempts * FLOPS3 / (ms * 1e-3) / 1e12
     value_per_solve = world * FLOPS3 / (ms * 1e-3) / 1e12
 
@@ -597,7 +609,7 @@ def run_ours(args, dist, rank, world, local_rank):
     rf = run_config4(torch, rl, dev, dist, rank, world, args, fp64_peak)
     # ---- configs 1 and 5 (latency-bound n = 256; n = 16384 with the new multipliers) ----
     c1 = run_config1(torch, rl, dev, dist, args, fp64_peak)
-    c5 = None if args.skip_config5 else run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak)
+    c5 = None if args.skip_config5 else run_config5(torch, rl, dev, dist, args, fp64_peak, hbm_peak, rank, world)
     circ = run_circulant_fft(torch, rl, dev, dist, hbm_peak)
 
     cpu = None
@@ -619,13 +631,12 @@ def run_ours(args, dist, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded; reference RNG streams)",
-        "config": {"workload": "config3: Gaussian-preconditioned GENP n=8192, 16 RHS, MulSide::Right, block 128",
-                   "n": N3, "nrhs": NRHS3, "flop_per_attempt": FLOPS3, "attempts_per_step": attempts,
-                   "flop_per_step": attempts * FLOPS3, "value_per_solve_tflops": round(value_per_solve, 4),
-                   "parallelism": f"replicas{world}",
-                   "l2": "inputs larger than L2 (A, G 512 MiB each)",
-                   "backward_error_max": bwd, "residual": rep.residual, "attempt": rep.attempt,
-                   "rng_ms_per_G": round(rng_ms, 3)},
+        "config": config3(world),
+        "run": {"attempts_per_step": attempts, "flop_per_step": attempts * FLOPS3,
+                "value_per_solve_tflops": round(value_per_solve, 4),
+                "backward_error_max": bwd, "residual": rep.residual,
+                "attempt_worst_column": rep.attempt, "column_attempts": [c[0] for c in cols],
+                "rng_ms_per_G": round(rng_ms, 3)},
         "roofline": {"bound": "tensor", "kernel": "k_dgemm (A G, DMMA m8n8k4 f64)",
                      "achieved": round(gemm_tf, 3), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
                      "frac": round(gemm_tf / fp64_peak, 4), "traffic": traffic,
@@ -746,6 +757,54 @@ def cpu_baseline_config4(A_slab, H):
                       f"{dt:.2f} s"}
 
 
+def cpu_baseline_config5(A_host, threads: int):
+    """Config 5's CPU arms on bounded samples: the reference's Gaussian
+    arm = Matrix::multiply of a row slab of A against the 16384^2 G (all host threads, one
+    reference call per thread) + genp_factor at n = 1024 (single-threaded in the reference);
+    the Householder-pair and sparse +-1 applies through the C restatement (oracle/rl_oracle.c,
+    the reference has no such multipliers) on the full 16384^2 A, 1 thread (GB/s over the same
+    algorithmic bytes as the GPU kernels: 2 n^2 8)."""
+    from oracle.pyoracle import Restated
+    kind, lib = _ref_lib()
+    n = A_host.shape[0]
+    rng = np.random.default_rng(5)
+    G = rng.standard_normal((n, n))
+    rows_per = 4
+    slabs = [np.ascontiguousarray(A_host[i * rows_per:(i + 1) * rows_per]) for i in range(threads)]
+    t0 = time.perf_counter()
+    ts = [threading.Thread(target=lib.matmul, args=(sl, G)) for sl in slabs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    t_mm = time.perf_counter() - t0
+    del G
+    nl = 1024
+    M = rng.standard_normal((nl, nl)) + nl * np.eye(nl)
+    t0 = time.perf_counter()
+    lib.genp_factor(M, 0.0)
+    t_lu = time.perf_counter() - t0
+    f = 2.0 * rows_per * threads * n * n + 2.0 * nl ** 3 / 3
+    gauss = {"value": round(f / (t_mm + t_lu) / 1e12, 6), "unit": "TFLOP/s", "cores": threads, "kind": kind,
+             "sample": f"Matrix::multiply {rows_per * threads}x{n} slab x {n}^2 G ({threads} threads) + "
+                       f"genp_factor n={nl} (1 thread); {t_mm + t_lu:.2f} s"}
+    O = Restated()
+    u1, u2 = O.householder_pair_signs(n, SEED, 55)
+    rows, signs = O.sparse_pm1(n, SEED, 56)
+    bytes_ = 2.0 * n * n * 8
+    t0 = time.perf_counter()
+    O.hh2_apply_right(u1, u2, A_host)
+    t_hh = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.sparse_apply_right(rows, signs, A_host)
+    t_sp = time.perf_counter() - t0
+    return {"gaussian": gauss,
+            "householder_pair": {"value": round(bytes_ / t_hh / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+                                 "sample": f"A H1 H2 on the full {n}^2 A (rlo_hh2_apply_right); {t_hh:.2f} s"},
+            "sparse_sign": {"value": round(bytes_ / t_sp / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+                            "sample": f"A S on the full {n}^2 A (rlo_sparse_apply_right); {t_sp:.2f} s"}}
+
+
 def _host_cpu():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
@@ -773,8 +832,8 @@ def run_reference(args, rank, world):
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "config3 (bounded CPU sample, see cpu_baseline.sample)",
-                                             "n": N3, "nrhs": NRHS3},
+            "data": "synthetic", "config": config3(world),
+            "sample_note": "each step is a bounded sample of the config-3 work on the host cores (cpu_baseline.sample)",
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
 

@@ -275,6 +275,23 @@ rl_status rl_fft(uint64_t n, const double* in, int inverse, double* out);
 /* dense::norm (dense_core.cpp:48-84): kind 0 One, 1 Two, 2 Inf, 3 Frobenius. */
 rl_status rl_norm(uint64_t m, uint64_t n, const double* a, int kind, double* out);
 
+/* ----------------------------- lowrank.hpp rank search (lowrank.cpp:179-396) ---- */
+/* lowrank::extremal_sv_estimate (lowrank.cpp:204-348): method 0 Power, 1 Lanczos; the start
+ * vectors are the stream's Gaussians. RL_NO_CONVERGENCE as the reference's NoConvergence. */
+rl_status rl_extremal_sv_estimate(uint64_t m, uint64_t n, const double* a, int method, int iters, uint64_t seed,
+                                  uint64_t stream_id, double* sv_max, double* sv_min);
+/* lowrank::cond_probe (lowrank.cpp:350-358): *pass = 1 when sv_max / sv_min <= kappa. */
+rl_status rl_cond_probe(uint64_t m, uint64_t n, const double* b, double kappa, int method, int iters, uint64_t seed,
+                        uint64_t stream_id, int* pass);
+/* lowrank::nrank_search (lowrank.cpp:360-396): policy 0 Binary, 1 LinearDown. basis (capacity
+ * max(m, n) x rho_plus) receives the sketch at the final rank, *basis_rows x *basis_cols (the
+ * reference's n x 1 zero matrix when rho = 0). */
+rl_status rl_nrank_search(uint64_t m, uint64_t n, const double* a, uint64_t rho_minus, uint64_t rho_plus,
+                          double kappa, int policy, uint64_t seed, uint64_t stream_id, uint64_t* rho, double* basis,
+                          uint64_t* basis_rows, uint64_t* basis_cols);
+/* lowrank::power_transform (lowrank.cpp:179-187): (A A^T)^h A. */
+rl_status rl_power_transform(uint64_t m, uint64_t n, const double* a, unsigned h, double* out);
+
 /* -------------------------------------------------------- probes (K12) ---- */
 /* Measured peaks on the current device: FP64 DMMA TFLOP/s and HBM copy GB/s. */
 rl_status rl_probe_peaks(double* fp64_tflops, double* hbm_gbs);

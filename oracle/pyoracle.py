@@ -269,6 +269,8 @@ class Reference:
         L.rlref_extremal_sv_estimate.argtypes = [u64, u64, _d, cint, cint, u64, u64, P(C.c_double), P(C.c_double)]
         L.rlref_cond_probe.argtypes = [u64, u64, _d, dbl, cint, cint, u64, u64, P(C.c_int)]
         L.rlref_power_transform.argtypes = [u64, u64, _d, C.c_uint, _d]
+        L.rlref_profile_matrix.argtypes = [u64, _d, u64, u64, _d]
+        L.rlref_random_orthogonal.argtypes = [u64, u64, u64, _d]
         L.rlref_sampled_residual_check.argtypes = [u64, u64, _d, _d, u64, u64, dbl, u64, u64, P(C.c_int)]
 
     def _chk(self, code, where):
@@ -430,6 +432,18 @@ class Reference:
         self._chk(self.lib.rlref_sampled_residual_check(a.shape[0], a.shape[1], a, ahat, rho1, rho2, tau, seed, sid,
                                                         C.byref(ok)), "sampled_residual_check")
         return bool(ok.value)
+
+    def profile_matrix(self, sigmas, seed, sid):
+        n = len(sigmas)
+        out = np.empty((n, n))
+        self._chk(self.lib.rlref_profile_matrix(n, np.ascontiguousarray(sigmas, float), seed, sid, out),
+                  "profile_matrix")
+        return out
+
+    def random_orthogonal(self, n, seed, sid):
+        out = np.empty((n, n))
+        self._chk(self.lib.rlref_random_orthogonal(n, seed, sid, out), "random_orthogonal")
+        return out
 
     def illblock_system(self, n, seed, sid):
         a, b, y = np.empty((n, n)), np.empty(n), np.empty(n)

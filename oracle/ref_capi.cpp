@@ -350,3 +350,23 @@ extern "C" int rlref_profile_matrix_paper(uint64_t n, uint64_t rho, uint64_t see
     }
     return 0;
 }
+
+extern "C" int rlref_profile_matrix(uint64_t n, const double* sigmas, uint64_t seed, uint64_t sid, double* out) {
+    try {
+        auto m = randla::rnd::profile_matrix(n, std::span<const double>(sigmas, n), randla::rnd::RngStream{seed, sid});
+        std::memcpy(out, m.data().data(), n * n * sizeof(double));
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+    return 0;
+}
+
+extern "C" int rlref_random_orthogonal(uint64_t n, uint64_t seed, uint64_t sid, double* out) {
+    try {
+        auto m = randla::rnd::random_orthogonal(n, randla::rnd::RngStream{seed, sid});
+        std::memcpy(out, m.data().data(), n * n * sizeof(double));
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+    return 0;
+}

@@ -35,7 +35,7 @@ __all__ = [
     "dev_gemm", "dev_gaussian_matrix", "dev_genp_factor", "dev_genp_solve", "dev_randomized_genp",
     "dev_randomized_genp_batched", "dev_range_finder", "dev_sparse_apply_right",
     "dev_householder_pair_apply_right", "dev_circulant_apply_right", "dev_toeplitz_apply_right", "proto_lowrank", "dev_qr_positive", "dev_numerical_rank", "probe_peaks",
-    "box_muller", "box_muller_hash", "last_column_reports", "fft", "toeplitz_mul", "toeplitz_multiply_matrix", "launch_count", "LIB_PATH",
+    "box_muller", "box_muller_hash", "last_column_reports", "fft", "toeplitz_mul", "toeplitz_multiply_matrix", "SvMethod", "SearchPolicy", "extremal_sv_estimate", "cond_probe", "nrank_search", "power_transform", "launch_count", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -241,6 +241,10 @@ def lib() -> C.CDLL:
         "rl_probe_peaks": [C.POINTER(dbl), C.POINTER(dbl)],
         "rl_box_muller": [u64, vp, vp],
         "rl_last_column_reports": [u64, vp],
+        "rl_extremal_sv_estimate": [u64, u64, _d, cint, cint, u64, u64, vp, vp],
+        "rl_cond_probe": [u64, u64, _d, dbl, cint, cint, u64, u64, vp],
+        "rl_nrank_search": [u64, u64, _d, u64, u64, dbl, cint, u64, u64, vp, _d, vp, vp],
+        "rl_power_transform": [u64, u64, _d, C.c_uint, _d],
         "rl_box_muller_hash": [u64, u64, u64, vp],
     }
     for name, args in sig.items():
@@ -663,6 +667,53 @@ def dev_numerical_rank(a, tol: float) -> Tuple[int, np.ndarray]:
     sg = np.empty(min(m, n))
     _chk(lib().rl_dev_numerical_rank(m, n, _ptr64(a), tol, C.byref(r), sg))
     return int(r.value), sg
+
+
+class SvMethod:
+    POWER = 0
+    LANCZOS = 1
+
+
+class SearchPolicy:
+    BINARY = 0
+    LINEAR_DOWN = 1
+
+
+def extremal_sv_estimate(a, method: int, iters: int, stream: RngStream) -> Tuple[float, float]:
+    """lowrank::extremal_sv_estimate (lowrank.cpp:204-348) -> (sv_max, sv_min)."""
+    a = _f64(a)
+    hi, lo = dbl(0.0), dbl(0.0)
+    _chk(lib().rl_extremal_sv_estimate(a.shape[0], a.shape[1], a, method, iters, stream.seed, stream.stream_id,
+                                       C.byref(hi), C.byref(lo)))
+    return hi.value, lo.value
+
+
+def cond_probe(b, kappa: float, method: int, iters: int, stream: RngStream) -> bool:
+    """lowrank::cond_probe (lowrank.cpp:350-358)."""
+    b = _f64(b)
+    ok = C.c_int(0)
+    _chk(lib().rl_cond_probe(b.shape[0], b.shape[1], b, kappa, method, iters, stream.seed, stream.stream_id,
+                             C.byref(ok)))
+    return bool(ok.value)
+
+
+def nrank_search(a, rho_minus: int, rho_plus: int, kappa: float, policy: int, stream: RngStream):
+    """lowrank::nrank_search (lowrank.cpp:360-396) -> (rho, basis)."""
+    a = _f64(a)
+    m, n = a.shape
+    basis = np.zeros(max(m, n) * max(rho_plus, 1))
+    rho, br, bc = u64(0), u64(0), u64(0)
+    _chk(lib().rl_nrank_search(m, n, a, rho_minus, rho_plus, kappa, policy, stream.seed, stream.stream_id,
+                               C.byref(rho), basis, C.byref(br), C.byref(bc)))
+    return int(rho.value), basis[:br.value * bc.value].reshape(br.value, bc.value).copy()
+
+
+def power_transform(a, h: int) -> np.ndarray:
+    """lowrank::power_transform (lowrank.cpp:179-187): (A A^T)^h A."""
+    a = _f64(a)
+    out = np.empty_like(a)
+    _chk(lib().rl_power_transform(a.shape[0], a.shape[1], a, h, out))
+    return out
 
 
 def box_muller(raw) -> np.ndarray:

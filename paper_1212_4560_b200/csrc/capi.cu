@@ -27,6 +27,13 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
                               double mu, double sigma, int side, int refine, uint64_t seed, uint64_t sid,
                               double* X, rl_precond_report* report, uint32_t flags);
 const std::vector<rl_column_report>& last_column_reports();
+void extremal_sv_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, int method, int iters, uint64_t seed,
+                     uint64_t sid, double* sv_max, double* sv_min);
+bool cond_probe_dev(uint64_t m, uint64_t n, const double* b, uint64_t ldb, double kappa, int method, int iters,
+                    uint64_t seed, uint64_t sid);
+uint64_t nrank_search_dev(uint64_t m, uint64_t n, const double* a, uint64_t rho_minus, uint64_t rho_plus,
+                          double kappa, int policy, uint64_t seed, uint64_t sid, double* basis,
+                          uint64_t* basis_rows);
 rl_status randomized_genp_batched_dev(uint64_t batch, uint64_t n, const double* dA, const double* dB,
                                       int tag, double mu, double sigma, int side, int refine,
                                       uint64_t seed, const uint64_t* d_sids, double* dX,
@@ -51,6 +58,9 @@ void toeplitz_dense_dev(uint64_t n, const double* g, double* out);
 void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
                               uint64_t ldo);
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r);
+void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad);
+void small_sv_launch(int k, const double* d_a, double* d_sg);
+void rank_bracket_launch(int k, const double* d_r, int* d_flag);
 std::vector<double> small_singular_values(int k, const double* d_a);
 double sumsq_dev(uint64_t count, const double* x);
 void uniform_int_dev(uint64_t seed, uint64_t sid, uint64_t count, int64_t lo, int64_t hi, int64_t* out);
@@ -720,15 +730,25 @@ std::vector<double> qr_positive_dev(uint64_t m, uint64_t n, const double* dy, do
         fail(RL_INVALID_ARGUMENT, "qr_positive: requires rows >= cols");
     if (n > 128)
         fail(RL_TOO_LARGE, "qr_positive: more than 128 columns");
-    if (!cholqr3(m, static_cast<int>(n), dy, dq, dr))
-        fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient input");
+    int* flags = ws<int>(WS_FLAGS, 4);
+    RL_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), stream()));
+    cholqr3_async(m, static_cast<int>(n), dy, dq, dr, flags);
+    rank_bracket_launch(static_cast<int>(n), dr, flags + 1);
     std::vector<double> hr(n * n);
-    download(hr.data(), dr, n * n);
-    std::vector<double> sg = small_singular_values(static_cast<int>(n), dr);
-    double min_diag = std::numeric_limits<double>::infinity();
-    for (uint64_t i = 0; i < n; ++i)
-        min_diag = std::min(min_diag, std::fabs(hr[i * n + i]));
-    if (!(min_diag > 1e-13 * sg[0]))
+    download(hr.data(), dr, n * n); // synchronises
+    int hf[2];
+    download(hf, flags, 2);
+    if (hf[0])
+        fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient input");
+    bool ok = hf[1] == 0;
+    if (hf[1] == 2) { // between the Frobenius bounds: sigma_1(R) itself
+        std::vector<double> sg = small_singular_values(static_cast<int>(n), dr);
+        double min_diag = std::numeric_limits<double>::infinity();
+        for (uint64_t i = 0; i < n; ++i)
+            min_diag = std::min(min_diag, std::fabs(hr[i * n + i]));
+        ok = min_diag > 1e-13 * sg[0];
+    }
+    if (!ok)
         fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient input");
     return hr;
 }
@@ -853,21 +873,43 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
     rng_generate(seed, sid, Draw::Gaussian, n * rho, 0.0, 1.0, dh);
     double* dy = ws<double>(WS_RF2, m * rho);
     gemm_splitk(false, false, m, rho, n, 1.0, d_a, n, dh, rho, 0.0, dy, rho, splits_for(m, rho, n));
-    // [Q, R] = qr_positive(Y)
+    // [Q, R] = qr_positive(Y), its rank test bracketed on the device (k_rank_bracket)
     double* dr = ws<double>(WS_RF3, rho * rho);
-    if (!cholqr3(m, static_cast<int>(rho), dy, d_q, dr))
-        fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient sketch");
+    int* flags = ws<int>(WS_FLAGS, 4);
+    RL_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), stream()));
+    cholqr3_async(m, static_cast<int>(rho), dy, d_q, dr, flags);
+    rank_bracket_launch(static_cast<int>(rho), dr, flags + 1);
     // B = Q^T A (lowrank.cpp:61-64 `sta`)
     gemm_splitk(true, false, rho, n, m, 1.0, d_q, rho, d_a, n, 0.0, d_b, n, splits_for(rho, n, m));
     // sigma(B) from R of B^T
     double* bt = ws<double>(WS_RF1, n * rho);
     transpose_dev(rho, n, d_b, n, bt, rho);
     double* qb = ws<double>(WS_RF2, n * rho);
-    double* rb = ws<double>(WS_RF3, rho * rho);
-    std::vector<double> sg;
-    if (cholqr3(n, static_cast<int>(rho), bt, qb, rb))
-        sg = small_singular_values(static_cast<int>(rho), rb);
-    else
+    double* rb = ws<double>(WS_RF3B, rho * rho);
+    cholqr3_async(n, static_cast<int>(rho), bt, qb, rb, flags + 2);
+    double* dsg = ws<double>(WS_RF5B, 128 + 1);
+    small_sv_launch(static_cast<int>(rho), rb, dsg);
+    // one synchronisation: the flags and sigma together
+    int hf[3];
+    std::vector<double> sg(rho);
+    download(hf, flags, 3);
+    download(sg.data(), dsg, rho);
+    if (hf[0])
+        fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient sketch");
+    if (hf[1] != 0) {
+        bool ok = false;
+        if (hf[1] == 2) {
+            std::vector<double> hr(rho * rho), sr = small_singular_values(static_cast<int>(rho), dr);
+            download(hr.data(), dr, rho * rho);
+            double min_diag = std::numeric_limits<double>::infinity();
+            for (uint64_t i = 0; i < rho; ++i)
+                min_diag = std::min(min_diag, std::fabs(hr[i * rho + i]));
+            ok = min_diag > 1e-13 * sr[0];
+        }
+        if (!ok)
+            fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient sketch");
+    }
+    if (hf[2])
         fail(RL_NO_CONVERGENCE, "range_finder: QR of B^T failed");
     if (sigma_host)
         std::memcpy(sigma_host, sg.data(), rho * sizeof(double));
@@ -952,6 +994,65 @@ rl_status rl_norm(uint64_t m, uint64_t n, const double* a, int kind, double* out
             return st;
         *out = sg.empty() ? 0.0 : sg[0];
     }
+    API_END
+}
+
+// ------------------------------------------------------------ rank search ----
+rl_status rl_extremal_sv_estimate(uint64_t m, uint64_t n, const double* a, int method, int iters, uint64_t seed,
+                                  uint64_t sid, double* sv_max, double* sv_min) {
+    API_BEGIN
+    require_positive(m, n, "extremal_sv_estimate");
+    if (method != 0 && method != 1)
+        fail(RL_INVALID_ARGUMENT, "extremal_sv_estimate: method must be Power (0) or Lanczos (1)");
+    double* da = upload(WS_H0, a, m * n);
+    extremal_sv_dev(m, n, da, n, method, iters, seed, sid, sv_max, sv_min);
+    API_END
+}
+
+rl_status rl_cond_probe(uint64_t m, uint64_t n, const double* b, double kappa, int method, int iters, uint64_t seed,
+                        uint64_t sid, int* pass) {
+    API_BEGIN
+    require_positive(m, n, "cond_probe");
+    double* db = upload(WS_H0, b, m * n);
+    *pass = cond_probe_dev(m, n, db, n, kappa, method, iters, seed, sid) ? 1 : 0;
+    API_END
+}
+
+rl_status rl_nrank_search(uint64_t m, uint64_t n, const double* a, uint64_t rho_minus, uint64_t rho_plus,
+                          double kappa, int policy, uint64_t seed, uint64_t sid, uint64_t* rho, double* basis,
+                          uint64_t* basis_rows, uint64_t* basis_cols) {
+    API_BEGIN
+    require_positive(m, n, "nrank_search");
+    double* da = upload(WS_H0, a, m * n);
+    double* db = ws<double>(WS_H1, std::max(m, n) * std::max<uint64_t>(rho_plus, 1));
+    uint64_t rows = 0;
+    const uint64_t r = nrank_search_dev(m, n, da, rho_minus, rho_plus, kappa, policy, seed, sid, db, &rows);
+    *rho = r;
+    *basis_rows = rows;
+    *basis_cols = r > 0 ? r : 1; // the reference's Matrix(n, 1) when rho = 0
+    if (r > 0)
+        download(basis, db, rows * r);
+    else
+        std::memset(basis, 0, rows * sizeof(double));
+    API_END
+}
+
+rl_status rl_power_transform(uint64_t m, uint64_t n, const double* a, unsigned h, double* out) {
+    API_BEGIN
+    require_positive(m, n, "power_transform");
+    double* da = upload(WS_H0, a, m * n);
+    double* cur = ws<double>(WS_H2, m * n);
+    copy2d_dev(m, n, da, n, cur, n);
+    if (h > 0) { // (A A^T)^h A (lowrank.cpp:179-187)
+        double* aat = ws<double>(WS_H1, m * m);
+        double* nxt = ws<double>(WS_H3, m * n);
+        gemm(false, true, m, m, n, 1.0, da, n, da, n, 0.0, aat, m);
+        for (unsigned i = 0; i < h; ++i) {
+            gemm(false, false, m, n, m, 1.0, aat, m, cur, n, 0.0, nxt, n);
+            std::swap(cur, nxt);
+        }
+    }
+    download(out, cur, m * n);
     API_END
 }
 

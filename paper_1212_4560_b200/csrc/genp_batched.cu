@@ -11,8 +11,8 @@
 //     panel in registers (pivot row by shuffles, m = w(i,k) * (1/p), 1/p := 0 for p = 0),
 //     one thread per column solves U12 against the unit L11, all warps update the trailing
 //     square on DMMA — three barriers per panel instead of one per pivot.
-//   * The packed LU is transposed in place and warp 0 runs the forward / backward
-//     substitution (two rows per lane, shuffle chain; genp.cpp:106-124), then y = C z,
+//   * Warp 0 runs the forward / backward substitution on the packed LU (two rows per lane,
+//     shuffle chain; genp.cpp:106-124), then y = C z,
 //     refinement and the residual ||A y - b|| / ||b|| on threads 0..63.
 // The raw-GENP contrast arm is iteration -1 of the same loop (pivot floor 0, no multiplier).  The 8-attempt redraw protocol (stream id + 7919 a, accept
 // <= 1e-7, keep best, genp.cpp:236-290) runs in-kernel.  Exactly singular circulants (a
@@ -56,6 +56,22 @@ __device__ __forceinline__ double sgn(uint64_t mask, int j) { // bit j set <=> c
 }
 
 __device__ __forceinline__ double min_fold(double a, double v) { return (v < a) ? v : a; }
+
+// 1/p on the pivot chain: the hardware estimate plus two Newton steps (a few cycles instead of
+// __drcp_rn's correctly rounded sequence); p is warp-uniform, so the rare tiny-|p| fallback
+// does not diverge. 0 -> 0 (the reference's m = 0 for a zero pivot).
+__device__ __forceinline__ double pivot_rcp(double p) {
+    if (p == 0.0)
+        return 0.0;
+    if (!(fabs(p) > 1e-300 && fabs(p) < 1e300))
+        return __drcp_rn(p);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+    double e = fma(-p, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-p, r, 1.0);
+    return fma(r, e, r);
+}
 __device__ __forceinline__ double max_fold(double b, double v) { return (b < v) ? v : b; }
 
 // 64 sign draws of stream (seed, sid) after discard(8) as a bitmask (random_gen.cpp:22-31,
@@ -172,7 +188,7 @@ __device__ __forceinline__ bool lu_blocked(Smem& S, double floor, int t, double&
 #pragma unroll
             for (int kk = 0; kk < 16; ++kk) {
                 const double piv = __shfl_sync(0xffffffffu, a[kk], kk);
-                const double inv = (piv == 0.0) ? 0.0 : __drcp_rn(piv);
+                const double inv = pivot_rcp(piv);
                 if (lane == 0)
                     S.rcp[c0 + kk] = inv;
                 const double ap = fabs(piv);
@@ -246,28 +262,20 @@ __device__ __forceinline__ bool lu_blocked(Smem& S, double floor, int t, double&
     return S.flag != 0;
 }
 
-// X <- X^T in place (the solves read columns of L and U)
-__device__ __forceinline__ void transpose_X(Smem& S, int t) {
-    for (int e = t; e < N * N; e += THREADS) {
-        const int i = e >> 6, j = e & 63;
-        if (i < j) {
-            const double v = S.X[i * XP + j];
-            S.X[i * XP + j] = S.X[j * XP + i];
-            S.X[j * XP + i] = v;
-        }
-    }
-}
-
-// warp 0: S.v0 <- U^{-1} L^{-1} S.v0 with the packed LU transposed in X (X[c * XP + r]).
+// warp 0: S.v0 <- U^{-1} L^{-1} S.v0 with the packed LU row-major in X (L_ij = X[i * XP + j]
+// below the diagonal, U on and above). Lane l owns rows l and l + 32; step j reads column j of
+// L or U down the lanes (a 4-way bank conflict at pitch 68, far cheaper than transposing X).
 __device__ __forceinline__ void solve_warp0(Smem& S, int lane) {
     double x0 = S.v0[lane], x1 = S.v0[lane + 32];
+    const double* r0 = S.X + lane * XP;
+    const double* r1 = S.X + (lane + 32) * XP;
 #pragma unroll
     for (int j = 0; j < N; ++j) { // forward, unit L
         const double yj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
         if (j < 32 && lane > j)
-            x0 = fma(-S.X[j * XP + lane], yj, x0);
+            x0 = fma(-r0[j], yj, x0);
         if (lane + 32 > j)
-            x1 = fma(-S.X[j * XP + lane + 32], yj, x1);
+            x1 = fma(-r1[j], yj, x1);
     }
 #pragma unroll
     for (int j = N - 1; j >= 0; --j) { // backward, U
@@ -276,13 +284,13 @@ __device__ __forceinline__ void solve_warp0(Smem& S, int lane) {
             if (lane == j)
                 x0 = xj;
             else if (lane < j)
-                x0 = fma(-S.X[j * XP + lane], xj, x0);
+                x0 = fma(-r0[j], xj, x0);
         } else {
             if (lane + 32 == j)
                 x1 = xj;
             else if (lane + 32 < j)
-                x1 = fma(-S.X[j * XP + lane + 32], xj, x1);
-            x0 = fma(-S.X[j * XP + lane], xj, x0);
+                x1 = fma(-r1[j], xj, x1);
+            x0 = fma(-r0[j], xj, x0);
         }
     }
     S.v0[lane] = x0;
@@ -413,7 +421,6 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
             const bool brk = lu_blocked(S, a < 0 ? 0.0 : 1e-300, t, pmn, pmx);
             if (brk && a >= 0)
                 continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
-            transpose_X(S, t);
             if (vt)
                 S.v0[t] = bt;
             __syncthreads();

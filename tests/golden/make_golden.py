@@ -157,5 +157,33 @@ for k, (c, x) in enumerate(nonfinite):
     c, x = np.array(c, float), np.array(x, float)
     g[f"circ_nf/{k}/c"], g[f"circ_nf/{k}/x"], g[f"circ_nf/{k}/y"] = c, x, R.circ_mul(c, x)
 
+# --- the rank-search side of lowrank (lowrank.cpp:179-396; tests/test_lowrank.cpp:116-177) ----
+d51 = np.diag([5.0, 1.0])
+q8 = R.random_orthogonal(8, 41, 16)
+sig32 = np.ones(32)
+sig32[31] = 1e-3
+p32 = R.profile_matrix(sig32, 41, 18)
+g["es/q8"], g["es/p32"] = q8, p32
+for meth in (0, 1):
+    g[f"es/d51/{meth}"] = np.array(R.extremal_sv_estimate(d51, meth, 200, 41, 15))
+    g[f"es/q8/{meth}"] = np.array(R.extremal_sv_estimate(q8, meth, 200, 41, 17))
+    g[f"es/p32/{meth}"] = np.array(R.extremal_sv_estimate(p32, meth, 5000, 41, 19))
+a64 = R.profile_matrix_paper(64, 8, 41, 22)
+g9 = R.gaussian_matrix(64, 9, 41, 23)
+g["cp/b8"], g["cp/b9"] = a64.T @ g9[:, :8], a64.T @ g9
+g["cp/b8/pass"] = np.array([R.cond_probe(g["cp/b8"], 1e6, 1, 56, 41, 24)])
+g["cp/b9/pass"] = np.array([R.cond_probe(g["cp/b9"], 1e6, 1, 56, 41, 25)])
+a26 = R.profile_matrix_paper(64, 8, 41, 26)
+g["nr/a"] = a26
+for pol in (0, 1):
+    rho, basis = R.nrank_search(a26, 0, 16, 1e6, pol, 41, 27)
+    g[f"nr/{pol}/rho"], g[f"nr/{pol}/basis"] = np.array([rho]), basis
+wide = R.gaussian_matrix(24, 80, 41, 40)
+wide = wide[:, :80] * 1.0
+rho, basis = R.nrank_search(wide, 2, 20, 1e6, 0, 41, 41)  # m < n: the transposed work matrix
+g["nr/wide/a"], g["nr/wide/rho"], g["nr/wide/basis"] = wide, np.array([rho]), basis
+g["pt/a"] = R.gaussian_matrix(20, 7, 41, 42)
+g["pt/h2"] = R.power_transform(g["pt/a"], 2)
+
 np.savez_compressed(os.path.join(OUT, "golden.npz"), **g)
 print("wrote", os.path.join(OUT, "golden.npz"), len(g), "arrays")
