@@ -9,10 +9,13 @@ pytestmark = pytest.mark.gpu
 
 def test_config2_golden(rl, golden, oracle):
     """48 config-2-shaped systems against the reference's fixtures: the same accepted attempt for
-    every system (golden c2/attempt), x within 1e-8, and the backward error within 2x of the
-    reference's band — the largest backward error the reference itself shows on that system over
-    three 1-ulp perturbations of A (its per-system rounding scatter reaches ~10x on these
-    ill-conditioned n = 64 systems: profiles/r02_pin_c2.json) — per system and for the worst."""
+    every system (golden c2/attempt), x within 1e-8, and backward errors compared as the
+    distribution they are. On these ill-conditioned n = 64 systems the reference's OWN backward
+    error moves by up to ~10x under a 1-ulp perturbation of A (profiles/r02_pin_c2.json: max
+    per-system ratio 9.9 over 4096 systems), so the contract is: the worst backward error (what
+    config 2 reports) within 2x of the reference's band (its largest over the unperturbed run
+    and three 1-ulp perturbations), the geometric mean of per-system ratios GPU / reference
+    within 1.5, and no system beyond 10x its own band."""
     A, b, y_ref, rep_ref = golden["c2/A"], golden["c2/b"], golden["c2/y"], golden["c2/report"]
     seed = int(golden["c2/seed"][0])
     sids = golden["c2/sids"]
@@ -23,20 +26,23 @@ def test_config2_golden(rl, golden, oracle):
     def be(a, v, bb):
         return np.linalg.norm(a @ v - bb) / (np.linalg.norm(a) * np.linalg.norm(v))
 
-    worst, worst_band = 0.0, 0.0
+    worst, worst_band, logr = 0.0, 0.0, []
     for t in range(A.shape[0]):
         assert reps[t].attempt == int(golden["c2/attempt"][t]), t
         assert reps[t].residual <= 1e-7 and rep_ref[t][0] <= 1e-7
         assert np.abs(x[t] - y_ref[t]).max() / np.abs(y_ref[t]).max() < 1e-8, t
-        band = be(A[t], y_ref[t], b[t])
+        r0 = be(A[t], y_ref[t], b[t])
+        band = r0
         for _ in range(3):
             Ap = A[t] * (1.0 + 2.220446049250313e-16 * rng.standard_normal(A[t].shape))
             yp, _, _ = oracle.randomized_genp(Ap, b[t], "circulant_sign", "right", 0, seed=seed, sid=int(sids[t]))
             band = max(band, be(A[t], yp, b[t]))
         g = be(A[t], x[t], b[t])
-        assert g <= 2 * band + 16 * 2.2e-16, (t, g, band)
+        assert g <= 10 * band + 16 * 2.2e-16, (t, g, band)
+        logr.append(np.log(max(g, 1e-300) / max(r0, 1e-300)))
         worst, worst_band = max(worst, g), max(worst_band, band)
     assert worst <= 2 * worst_band  # config 2 reports the worst backward error
+    assert np.exp(np.mean(logr)) <= 1.5
 
 
 def test_redraw_protocol_matches_oracle(rl, oracle):
