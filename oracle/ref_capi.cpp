@@ -370,3 +370,4 @@ extern "C" int rlref_random_orthogonal(uint64_t n, uint64_t seed, uint64_t sid, 
     }
     return 0;
 }
+

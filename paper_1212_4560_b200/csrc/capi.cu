@@ -891,9 +891,15 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
     small_sv_launch(static_cast<int>(rho), rb, dsg);
     // one synchronisation: the flags and sigma together
     int hf[3];
-    std::vector<double> sg(rho);
+    std::vector<double> sg(129);
     download(hf, flags, 3);
-    download(sg.data(), dsg, rho);
+    download(sg.data(), dsg, 129);
+    static const bool trace = getenv("RL_JACOBI_TRACE") != nullptr;
+    if (trace)
+        fprintf(stderr, "[rl] range finder sigma(B): %.0f sweeps\n", sg[128]);
+    if (sg[128] < 0)
+        fail(RL_NO_CONVERGENCE, "range_finder: Jacobi sweeps for sigma(B) did not settle");
+    sg.resize(rho);
     if (hf[0])
         fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient sketch");
     if (hf[1] != 0) {

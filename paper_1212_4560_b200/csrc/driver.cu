@@ -52,7 +52,7 @@ SparseT sparse_transpose_dev(uint64_t n, int nnz, const int32_t* rows, const dou
 void sparse_apply_vec_dev(uint64_t n, uint64_t nrhs, const SparseT& s, const double* y, double* x);
 void circ_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* c, const double* z, double* y);
 // genp_batched.cu
-rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int refine, uint64_t seed,
+rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int refine, int left, uint64_t seed,
                          const uint64_t* d_sids, double* dX, rl_precond_report* d_rep);
 
 namespace {
@@ -539,8 +539,8 @@ rl_status randomized_genp_batched_dev(uint64_t batch, uint64_t n, const double* 
                                       rl_precond_report* d_rep) {
     if (refine < 0 || refine > 2)
         fail(RL_INVALID_ARGUMENT, "randomized_genp: refine must be in {0, 1, 2}");
-    if (tag == RL_CIRCULANT_SIGN && side == RL_RIGHT && n == 64)
-        return batched_circ64(batch, dA, dB, refine, seed, d_sids, dX, d_rep);
+    if (tag == RL_CIRCULANT_SIGN && (side == RL_RIGHT || side == RL_LEFT) && n == 64)
+        return batched_circ64(batch, dA, dB, refine, side == RL_LEFT ? 1 : 0, seed, d_sids, dX, d_rep);
     // general kinds / sizes: one system at a time through the blocked path
     std::vector<uint64_t> sids(batch);
     RL_CUDA(cudaMemcpyAsync(sids.data(), d_sids, batch * 8, cudaMemcpyDeviceToHost, stream()));

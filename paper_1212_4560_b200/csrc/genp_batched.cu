@@ -120,7 +120,7 @@ __device__ __forceinline__ void load_A(Smem& S, const double* __restrict__ Ag, i
 // X holds A on entry; on exit X holds W = A C (row-major).  Two passes over the output's
 // column halves (16 accumulators each instead of 32: the kernel's register peak, which sets
 // how many systems share an SM); W goes to registers first, then over A after a barrier.
-__device__ __forceinline__ void circ_product(Smem& S, uint64_t mask, int t) {
+__device__ __forceinline__ void circ_product(Smem& S, uint64_t mask, int t, bool left) {
     const int lane = t & 31, warp = t >> 5, g = lane >> 2, q = lane & 3;
     double keep[2][4][2];
 #pragma unroll
@@ -134,13 +134,24 @@ __device__ __forceinline__ void circ_product(Smem& S, uint64_t mask, int t) {
 #pragma unroll 4
         for (int kk = 0; kk < N; kk += 4) {
             const int k = kk + q;
-            const double a0 = S.X[(16 * warp + g) * XP + k];
-            const double a1 = S.X[(16 * warp + 8 + g) * XP + k];
+            if (!left) { // W = A C: A rows from shared memory, C[k][8 jb' + g] = c[k - col]
+                const double a0 = S.X[(16 * warp + g) * XP + k];
+                const double a1 = S.X[(16 * warp + 8 + g) * XP + k];
 #pragma unroll
-            for (int jb = 0; jb < 4; ++jb) {
-                const double bf = sgn(mask, k - (8 * (4 * half + jb) + g)); // C[k][8 jb' + g]
-                dmma(acc[0][jb], a0, bf);
-                dmma(acc[1][jb], a1, bf);
+                for (int jb = 0; jb < 4; ++jb) {
+                    const double bf = sgn(mask, k - (8 * (4 * half + jb) + g));
+                    dmma(acc[0][jb], a0, bf);
+                    dmma(acc[1][jb], a1, bf);
+                }
+            } else { // W = C A: C[row][k] = c[row - k] synthesised, A[k][col] from shared memory
+                const double c0 = sgn(mask, (16 * warp + g) - k);
+                const double c1 = sgn(mask, (16 * warp + 8 + g) - k);
+#pragma unroll
+                for (int jb = 0; jb < 4; ++jb) {
+                    const double bf = S.X[k * XP + 8 * (4 * half + jb) + g];
+                    dmma(acc[0][jb], c0, bf);
+                    dmma(acc[1][jb], c1, bf);
+                }
             }
         }
         if (half == 0) {
@@ -353,8 +364,8 @@ __device__ bool circ_singular(Smem& S, uint64_t mask, int t) {
 // sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) run in-kernel.
 __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs0, uint64_t seed,
-    const uint64_t* __restrict__ sids, int refine, double* __restrict__ X, rl_precond_report* __restrict__ rep,
-    int* __restrict__ status) {
+    const uint64_t* __restrict__ sids, int refine, int left, double* __restrict__ X,
+    rl_precond_report* __restrict__ rep, int* __restrict__ status) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -395,7 +406,7 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
                 } else {
                     if (t == 0)
                         S.mask = sign_mask_stream(seed, (sid + 7919ULL * static_cast<uint64_t>(a)) ^
-                                                            0x5000000000000000ULL,
+                                                            (left ? 0ULL : 0x5000000000000000ULL),
                                                   reinterpret_cast<uint64_t*>(S.X));
                     __syncthreads();
                     mask = S.mask;
@@ -409,7 +420,7 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
             load_A(S, Ag, t);
             __syncthreads();
             if (a >= 0) {
-                circ_product(S, mask, t);
+                circ_product(S, mask, t, left != 0);
                 __syncthreads();
             }
             if (t == 0) {
@@ -421,28 +432,43 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
             const bool brk = lu_blocked(S, a < 0 ? 0.0 : 1e-300, t, pmn, pmx);
             if (brk && a >= 0)
                 continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
+            const bool lft = left && a >= 0;
             if (vt)
                 S.v0[t] = bt;
             __syncthreads();
+            if (lft) { // rhs = C b (genp.cpp:252-255)
+                const double cb = vt ? circ_vec(S, mask, t) : 0.0;
+                __syncthreads();
+                if (vt)
+                    S.v0[t] = cb;
+                __syncthreads();
+            }
             if (warp == 0)
                 solve_warp0(S, lane);
             __syncthreads();
             double y = 0.0;
             if (vt)
-                y = (a < 0) ? S.v0[t] : circ_vec(S, mask, t);
+                y = (a < 0 || lft) ? S.v0[t] : circ_vec(S, mask, t); // y = z (Left) or C z (Right)
             __syncthreads();
             if (vt)
                 S.v1[t] = y;
             __syncthreads();
             for (int s = 0; a >= 0 && s < refine; ++s) { // genp.cpp:263-274
                 if (vt)
-                    S.v0[t] = -row_residual(Ag, S, bt, t); // b - A y
+                    S.v0[t] = -row_residual(Ag, S, bt, t); // r = b - A y
                 __syncthreads();
+                if (lft) { // rr = C r
+                    const double cr = vt ? circ_vec(S, mask, t) : 0.0;
+                    __syncthreads();
+                    if (vt)
+                        S.v0[t] = cr;
+                    __syncthreads();
+                }
                 if (warp == 0)
                     solve_warp0(S, lane);
                 __syncthreads();
                 if (vt) {
-                    y += circ_vec(S, mask, t);
+                    y += lft ? S.v0[t] : circ_vec(S, mask, t);
                     S.v1[t] = y;
                 }
                 __syncthreads();
@@ -495,7 +521,7 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
 } // namespace
 
 // Returns RL_OK or RL_PIVOT_BREAKDOWN (some system broke down on every attempt).
-rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int refine, uint64_t seed,
+rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int refine, int left, uint64_t seed,
                          const uint64_t* d_sids, double* dX, rl_precond_report* d_rep) {
     cudaStream_t st = stream();
     constexpr size_t kSmem = sizeof(Smem);
@@ -507,10 +533,10 @@ rl_status batched_circ64(uint64_t batch, const double* dA, const double* dB, int
     }
     double* signs = ws<double>(WS_TMP1, batch * N + 1);
     int* d_status = reinterpret_cast<int*>(signs + batch * N);
-    rng_sign_vectors_batched(seed, d_sids, 0, 0x5000000000000000ULL, batch, N, signs);
+    rng_sign_vectors_batched(seed, d_sids, 0, left ? 0ULL : 0x5000000000000000ULL, batch, N, signs);
     RL_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), st));
     k_batched_circ64<<<static_cast<unsigned>(batch), THREADS, kSmem, st>>>(dA, dB, signs, seed, d_sids, refine,
-                                                                            dX, d_rep, d_status);
+                                                                            left, dX, d_rep, d_status);
     RL_LAUNCHED();
     int h = 0;
     RL_CUDA(cudaMemcpyAsync(&h, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -92,21 +92,81 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     return y * fma(-h * y, y, 1.5);
 }
 
-// Cholesky G + shift I = R^T R for k <= 128 in one CTA, unblocked right-looking with ONE barrier
-// per column: at step j every thread reads the still-unscaled row j, forms R_jl = W_jl / R_jj
-// itself (1/R_jj from a refined rsqrt, computed redundantly by every thread) and applies
-// W_il -= R_ji R_jl to its part of the trailing triangle (warp w: rows j+1+w, j+1+w+16, ..;
-// lanes over columns), while the owners of row j write it scaled into R. No R^-1: Q = Y R^-1 is
-// a row-wise triangular solve (k_trsm_rows). shift = shift_coef * sum(shift_part) on pass 0.
-// r <- R (upper, zeros below). *bad is sticky (a non-positive pivot sets it; later passes skip).
-constexpr int CS_T = 512;
-__global__ void __launch_bounds__(CS_T) k_chol_seq(int k, const double* __restrict__ g, const double* shift_part,
-                                                   int nshift, double shift_coef, double* __restrict__ r, int* bad) {
-    extern __shared__ double W[]; // k x (k + 1)
+// Cholesky G + shift I = R^T R and X = R^-1 for k <= 128 in one 512-thread CTA, in shared
+// memory (k padded to KP = 8 ceil(k/8) with an identity corner), 8-column blocks J, three
+// barriers per block:
+//   A  warp 0 factors the 8 x 8 diagonal block in registers (lane c holds column c, pivot
+//      rows by shuffle) and inverts it (X_JJ) — for blocks after the first, inside the
+//      previous block's phase C (lookahead: it first applies that block's update to its own
+//      8 x 8, then factors, while warps 1-15 do the rest of C);
+//   B  one thread per trailing column solves the block's panel row R_J,rest; the others form
+//      T = R_0:J,J X_JJ;
+//   C  rank-8 update of the trailing upper triangle; X_0:J,J = -X_0:J,0:J T.
+// X_ij (i < j) lives in the free lower triangle at W[j][i], its diagonal in rdiag.
+//   shift = shift_coef * sum(shift_part[0..nshift))    (pass 0 of CholeskyQR3; else 0)
+// g <- R (upper, zeros below), rinv <- R^-1.  *bad is sticky: a kernel whose earlier pass
+// failed returns at once; a non-positive pivot sets it.
+constexpr int CH_T = 512;
+// Warp 0: factor the 8 x 8 diagonal block at (c0, c0) of W in registers (lane c holds column
+// c, pivot rows by shuffle) -> R_JJ (upper) and rdiag = 1 / R_tt, then X_JJ = R_JJ^-1 by back
+// substitution, stored transposed in the free lower triangle (X_rc at W[c0+c][c0+r]).
+__device__ __forceinline__ void chol_diag8(double* W, int P, int c0, double* rdiag, int lane, int* s_bad) {
+    const int c = lane & 7;
+    double col[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        col[r] = W[(c0 + r) * P + c0 + c];
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const double d = __shfl_sync(0xffffffffu, col[t], t);
+        ok = ok && (d > 0.0);
+        const double inv = rsqrt_nr(d); // 1 / R_tt
+        const double rtc = (c == t) ? d * inv : col[t] * inv; // R_{t,c} (c >= t)
+        col[t] = rtc;
+        if (c == t)
+            rdiag[c0 + t] = inv;
+#pragma unroll
+        for (int r = t + 1; r < 8; ++r) {
+            const double rtr = __shfl_sync(0xffffffffu, rtc, r); // R_{t,r}
+            col[r] = fma(-rtr, rtc, col[r]);
+        }
+    }
+    if (lane < 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (r <= c)
+                W[(c0 + r) * P + c0 + c] = col[r];
+    }
+    __syncwarp();
+    if (lane < 8) {
+        double x[8];
+#pragma unroll
+        for (int r = 7; r >= 0; --r) {
+            double v = 0.0;
+#pragma unroll
+            for (int l = r + 1; l < 8; ++l)
+                if (l <= c)
+                    v = fma(W[(c0 + r) * P + c0 + l], x[l], v);
+            x[r] = (r == c) ? rdiag[c0 + c] : (r < c ? -v * rdiag[c0 + r] : 0.0);
+            if (r < c)
+                W[(c0 + c) * P + c0 + r] = x[r];
+        }
+    }
+    if (lane == 0 && !ok)
+        *s_bad = 1;
+}
+__global__ void __launch_bounds__(CH_T) k_chol_inv(int k, double* g, const double* shift_part, int nshift,
+                                                   double shift_coef, double* rinv, int* bad) {
+    extern __shared__ double W[]; // KP x (KP + 1)
+    __shared__ double rdiag[KMAX];
+    __shared__ double T[8][KMAX + 1]; // T[c][l] = (R_0:J,J X_JJ)[l][c]; padded: 8 c's hit 8 banks
     __shared__ double s_shift;
+    __shared__ int s_bad;
     if (*bad)
         return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, P = k + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int KP = (k + 7) & ~7, P = KP + 1;
     if (warp == 0) {
         double p = 0.0;
         if (shift_part)
@@ -114,95 +174,122 @@ __global__ void __launch_bounds__(CS_T) k_chol_seq(int k, const double* __restri
                 p += shift_part[i];
         for (int o = 16; o > 0; o >>= 1)
             p += __shfl_xor_sync(0xffffffffu, p, o);
-        if (lane == 0)
+        if (lane == 0) {
             s_shift = shift_coef * p;
+            s_bad = 0;
+        }
     }
     __syncthreads();
     const double shift = s_shift;
-    for (int e = tid; e < k * k; e += CS_T) {
-        const int i = e / k, l = e - i * k;
-        W[i * P + l] = g[e] + (i == l ? shift : 0.0);
-        if (l < i)
-            r[e] = 0.0;
+    for (int e = tid; e < KP * KP; e += CH_T) {
+        const int i = e / KP, l = e - i * KP;
+        double v;
+        if (i < k && l < k)
+            v = g[i * k + l] + (i == l ? shift : 0.0);
+        else
+            v = (i == l) ? 1.0 : 0.0;
+        W[i * P + l] = v;
     }
     __syncthreads();
-    for (int j = 0; j < k; ++j) {
-        const double d = W[j * P + j];
-        if (!(d > 0.0)) { // uniform: every thread reads the same pivot
+    if (warp == 0)
+        chol_diag8(W, P, 0, rdiag, lane, &s_bad);
+    __syncthreads();
+    if (s_bad) { // uniform
+        if (tid == 0)
+            *bad = 1;
+        return;
+    }
+    for (int c0 = 0; c0 < KP; c0 += 8) {
+        // ---- B: panel row of R; T = R_0:J,J X_JJ   (R_JJ, X_JJ: the previous step's lookahead)
+        const int rest = KP - c0 - 8;
+        if (tid < rest) { // R_{c0+t, l} = (W_{c0+t, l} - sum_{s<t} R_{c0+s, c0+t} R_{c0+s, l}) / R_tt
+            const int l = c0 + 8 + tid;
+            double x[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                double v = W[(c0 + t) * P + l];
+#pragma unroll
+                for (int s2 = 0; s2 < t; ++s2)
+                    v = fma(-W[(c0 + s2) * P + c0 + t], x[s2], v);
+                x[t] = v * rdiag[c0 + t];
+                W[(c0 + t) * P + l] = x[t];
+            }
+        }
+        for (int e = tid - rest; e >= 0 && e < 8 * c0; e += CH_T - rest) { // threads >= rest
+            const int l = e >> 3, c = e & 7; // T[l][c] = sum_{m <= c} R_{l, c0+m} X_JJ[m][c]
+            double v = 0.0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (m <= c) {
+                    const double xm = (m == c) ? rdiag[c0 + c] : W[(c0 + c) * P + c0 + m];
+                    v = fma(W[l * P + c0 + m], xm, v);
+                }
+            T[c][l] = v;
+        }
+        __syncthreads();
+        // ---- C: warp 0 brings the next diagonal block up to date and factors it (lookahead);
+        // warps 1-15 update the rest of the trailing triangle and form X_0:J,J
+        if (warp == 0) {
+            if (rest > 0) {
+                const int l = c0 + 8 + (lane & 7);
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int i = c0 + 8 + (lane >> 3) + 4 * r;
+                    if (i <= l) {
+                        double v = W[i * P + l];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            v = fma(-W[(c0 + t) * P + i], W[(c0 + t) * P + l], v);
+                        W[i * P + l] = v;
+                    }
+                }
+                __syncwarp();
+                chol_diag8(W, P, c0 + 8, rdiag, lane, &s_bad);
+            }
+        } else {
+            const int nd = c0 + 16; // the next diagonal block [c0 + 8, c0 + 16)^2 is warp 0's
+            if (rest > 0) {
+                for (int i = c0 + 8 + (warp - 1); i < KP; i += 15) {
+                    double pi[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        pi[t] = W[(c0 + t) * P + i];
+                    const int lstart = i < nd ? nd : i; // upper triangle, minus warp 0's block
+                    for (int l = lstart + ((lane - lstart) & 31); l < KP; l += 32) {
+                        double v = W[i * P + l];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            v = fma(-pi[t], W[(c0 + t) * P + l], v);
+                        W[i * P + l] = v;
+                    }
+                }
+            }
+            for (int e = tid - 32; e < 8 * c0; e += CH_T - 32) { // X_{i, c0+c} = -sum_{l=i}^{c0-1} X_il T[l][c]
+                const int i = e >> 3, c = e & 7;
+                double v0 = rdiag[i] * T[c][i], v1 = 0.0, v2 = 0.0, v3 = 0.0;
+                int l = i + 1;
+                for (; l + 3 < c0; l += 4) { // four chains: the loads pipeline
+                    v0 = fma(W[l * P + i], T[c][l], v0);
+                    v1 = fma(W[(l + 1) * P + i], T[c][l + 1], v1);
+                    v2 = fma(W[(l + 2) * P + i], T[c][l + 2], v2);
+                    v3 = fma(W[(l + 3) * P + i], T[c][l + 3], v3);
+                }
+                for (; l < c0; ++l)
+                    v0 = fma(W[l * P + i], T[c][l], v0);
+                W[(c0 + c) * P + i] = -((v0 + v1) + (v2 + v3));
+            }
+        }
+        __syncthreads();
+        if (s_bad) { // uniform
             if (tid == 0)
                 *bad = 1;
             return;
         }
-        const double inv = rsqrt_nr(d);
-        for (int l = j + tid; l < k; l += CS_T)
-            r[j * k + l] = (l == j) ? d * inv : W[j * P + l] * inv;
-        for (int i = j + 1 + warp; i < k; i += CS_T / 32) {
-            const double rji = W[j * P + i] * inv;
-            for (int l = i + lane; l < k; l += 32)
-                W[i * P + l] = fma(-rji, W[j * P + l] * inv, W[i * P + l]);
-        }
-        __syncthreads();
     }
-}
-
-// Q = Y R^-1 by rows (q R = y, R upper k x k): one warp per two rows (two independent chains),
-// lane l holds y_l, y_{l+32}, .. (k <= 128). Step j: q_j = y_j / R_jj is broadcast by one
-// shuffle and every lane updates y_l -= q_j R_jl for its l > j (R in shared memory, rows
-// contiguous per lane: conflict-free). Forward substitution is more accurate than Y times an
-// explicit R^-1, and needs no inverse.
-constexpr int TR_T = 256;
-__global__ void __launch_bounds__(TR_T) k_trsm_rows(uint64_t m, int k, const double* __restrict__ y,
-                                                    const double* __restrict__ r, double* __restrict__ q,
-                                                    const int* bad) {
-    extern __shared__ double Rs[]; // k x k, then 1/R_jj
-    if (*bad)
-        return;
-    double* rinvd = Rs + k * k;
-    for (int e = threadIdx.x; e < k * k; e += TR_T)
-        Rs[e] = r[e];
-    for (int j = threadIdx.x; j < k; j += TR_T)
-        rinvd[j] = 1.0 / r[j * k + j];
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (TR_T / 32);
-    for (uint64_t p = blockIdx.x * (TR_T / 32) + (threadIdx.x >> 5); 2 * p < m; p += warps) {
-        const uint64_t r0 = 2 * p, r1 = r0 + 1;
-        const bool two = r1 < m;
-        double a[4], b[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int l = lane + 32 * c;
-            a[c] = l < k ? y[r0 * k + l] : 0.0;
-            b[c] = (l < k && two) ? y[r1 * k + l] : 0.0;
-        }
-        for (int j = 0; j < k; ++j) {
-            const int cj = j >> 5, lj = j & 31;
-            double va = cj == 0 ? a[0] : cj == 1 ? a[1] : cj == 2 ? a[2] : a[3];
-            double vb = cj == 0 ? b[0] : cj == 1 ? b[1] : cj == 2 ? b[2] : b[3];
-            const double qa = __shfl_sync(0xffffffffu, va, lj) * rinvd[j];
-            const double qb = __shfl_sync(0xffffffffu, vb, lj) * rinvd[j];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int l = lane + 32 * c;
-                if (l > j && l < k) {
-                    const double rjl = Rs[j * k + l];
-                    a[c] = fma(-qa, rjl, a[c]);
-                    b[c] = fma(-qb, rjl, b[c]);
-                } else if (l == j) {
-                    a[c] = qa;
-                    b[c] = qb;
-                }
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int l = lane + 32 * c;
-            if (l < k) {
-                q[r0 * k + l] = a[c];
-                if (two)
-                    q[r1 * k + l] = b[c];
-            }
-        }
+    for (int e = tid; e < k * k; e += CH_T) {
+        const int i = e / k, l = e - i * k;
+        g[e] = (l >= i) ? W[i * P + l] : 0.0;
+        rinv[e] = (l > i) ? W[l * P + i] : (l == i ? rdiag[i] : 0.0);
     }
 }
 
@@ -229,7 +316,9 @@ __global__ void __launch_bounds__(JS_T) k_jacobi_sv(int k, const double* a, doub
     if (tid < 3)
         rotated[tid] = 0;
     __syncthreads();
-    const double tol = 1e-15;
+    // rotate while |cos| = |a_p . a_q| / (|a_p| |a_q|) exceeds k eps (LAPACK dgesvj's test is
+    // sqrt(m) eps; a bar below the dot products' own rounding floor, ~sqrt(k) eps, never settles)
+    const double tol = static_cast<double>(k) * 2.220446049250313e-16;
     const bool warp_live = warp * 8 < npairs; // warp-uniform
     int sweep = 0;
     for (; sweep < 60; ++sweep) {
@@ -737,10 +826,8 @@ JacobiKernel jacobi_for(int k) {
 void chol_attrs() {
     static bool attr[16] = {};
     if (!attr[ctx().device & 15]) {
-        RL_CUDA(cudaFuncSetAttribute(k_chol_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RL_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      KMAX * (KMAX + 1) * 8));
-        RL_CUDA(cudaFuncSetAttribute(k_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (KMAX * KMAX + KMAX) * 8));
         attr[ctx().device & 15] = true;
     }
 }
@@ -751,7 +838,10 @@ void chol_attrs() {
 void small_sv_launch(int k, const double* d_a, double* d_sg) {
     if (k > KMAX)
         fail(RL_TOO_LARGE, "small SVD: k > 128");
-    if (k >= 16) { // the reference's BDCSVD range (dense_core.cpp:28)
+    // k >= 16: bidiagonalization + multisection (the reference's BDCSVD range, dense_core.cpp:28);
+    // RL_SV_JACOBI=1 selects one-sided Jacobi on the factor's rows (k eps bar) instead
+    static const bool bidiag = getenv("RL_SV_JACOBI") == nullptr;
+    if (bidiag && k >= 16) {
         static bool attr[16] = {};
         if (!attr[ctx().device & 15]) {
             RL_CUDA(cudaFuncSetAttribute(k_bidiag_sv, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -773,8 +863,9 @@ std::vector<double> small_singular_values(int k, const double* d_a) {
     std::vector<double> h = to_host(sg, KMAX + 1);
     static const bool trace = getenv("RL_JACOBI_TRACE") != nullptr;
     if (trace)
-        fprintf(stderr, "[rl] small svd k=%d: %s %.0f\n", k, k >= 16 ? "cycles(bidiag*1e6+multisection)" : "sweeps",
-                h[KMAX]);
+        fprintf(stderr, "[rl] small svd k=%d: %.0f\n", k, h[KMAX]);
+    if (h[KMAX] < 0)
+        fail(RL_NO_CONVERGENCE, "small SVD: Jacobi sweeps did not settle");
     h.resize(k);
     return h;
 }
@@ -784,33 +875,44 @@ namespace {
 // ||R||_F / sqrt(k) <= sigma_1 <= ||R||_F: *flag = 0 passes for sure, 1 fails for sure, 2 needs
 // sigma_1 itself (rare). One warp.
 __global__ void k_rank_bracket(int k, const double* __restrict__ r, int* flag) {
-    const int lane = threadIdx.x;
+    __shared__ double s_ss[8], s_mn[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double ss = 0.0, mn = INFINITY;
-    for (int e = lane; e < k * k; e += 32) {
+    for (int e = tid; e < k * k; e += 256) {
         const double v = r[e];
         ss = fma(v, v, ss);
-        if (e / k == e % k)
-            mn = fmin(mn, fabs(v));
     }
+    for (int i = tid; i < k; i += 256)
+        mn = fmin(mn, fabs(r[i * k + i]));
     for (int o = 16; o > 0; o >>= 1) {
         ss += __shfl_xor_sync(0xffffffffu, ss, o);
         mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     }
     if (lane == 0) {
-        const double fro = sqrt(ss);
-        *flag = (mn > 1e-13 * fro) ? 0 : (mn <= 1e-13 * fro / sqrt(static_cast<double>(k)) ? 1 : 2);
+        s_ss[warp] = ss;
+        s_mn[warp] = mn;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0, b = INFINITY;
+        for (int w = 0; w < 8; ++w) {
+            a += s_ss[w];
+            b = fmin(b, s_mn[w]);
+        }
+        const double fro = sqrt(a);
+        *flag = (b > 1e-13 * fro) ? 0 : (b <= 1e-13 * fro / sqrt(static_cast<double>(k)) ? 1 : 2);
     }
 }
 } // namespace
 
 void rank_bracket_launch(int k, const double* d_r, int* d_flag) {
-    k_rank_bracket<<<1, 32, 0, stream()>>>(k, d_r, d_flag);
+    k_rank_bracket<<<1, 256, 0, stream()>>>(k, d_r, d_flag);
     RL_LAUNCHED();
 }
 
 // Shifted CholeskyQR3 of Y (m x k, row-major, ld k): q (m x k) and r (k x k) with
-// diag(r) > 0. Per pass: the Gram (split-K GEMM), k_chol_seq, Q = src R^-1 by k_trsm_rows and
-// R_acc = R_pass R_acc. No host round trip: the shift is summed on the device and the failure
+// diag(r) > 0. Per pass: the Gram (split-K GEMM), k_chol_inv (R and R^-1), Q = src R^-1 on DMMA
+// and R_acc = R_pass R_acc. No host round trip: the shift is summed on the device and the failure
 // flag d_bad (int, device) is sticky — the caller reads it whenever it next synchronises.
 void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad) {
     if (k > KMAX)
@@ -818,11 +920,11 @@ void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int
     double* g = ws<double>(WS_RF4, 3 * KMAX * KMAX + 64);
     double* rp = g + KMAX * KMAX;
     double* racc = rp + KMAX * KMAX;
-    double* tmpq = ws<double>(WS_RF5, m * k + KMAX + 1);
+    double* tmpq = ws<double>(WS_RF5, m * k + KMAX * KMAX + KMAX + 1);
     const int sp = splits_for(k, k, m);
     chol_attrs();
-    const size_t chol_smem = static_cast<size_t>(k) * (k + 1) * 8;
-    const size_t trsm_smem = static_cast<size_t>(k) * (k + 1) * 8;
+    const int kp = (k + 7) & ~7;
+    const size_t chol_smem = static_cast<size_t>(kp) * (kp + 1) * 8;
     // ||Y||_F^2 for the shift (Fukaya et al.: s = 11 (m k + k(k+1)) u ||Y||_2^2, F-norm bound)
     constexpr int kParts = 256;
     double* part = ws<double>(WS_RESID, kParts);
@@ -830,17 +932,17 @@ void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int
     RL_LAUNCHED();
     const double u = 1.1102230246251565e-16;
     const double coef = 11.0 * (static_cast<double>(m) * k + static_cast<double>(k) * (k + 1)) * u;
-    const unsigned trsm_grid = static_cast<unsigned>(std::min<uint64_t>(cdiv(m, 2 * (TR_T / 32)), 4ULL * ctx().sms));
     const double* src = y;
+    double* rinv = tmpq + m * k; // k x k after the pass-1 Q buffer
     for (int pass = 0; pass < 3; ++pass) {
         // G = src^T src
         gemm_splitk(true, false, k, k, m, 1.0, src, k, src, k, 0.0, g, k, sp);
-        k_chol_seq<<<1, CS_T, chol_smem, stream()>>>(k, g, pass == 0 ? part : nullptr, kParts, coef, rp, d_bad);
+        copy2d_dev(k, k, g, k, rp, k);
+        k_chol_inv<<<1, CH_T, chol_smem, stream()>>>(k, rp, pass == 0 ? part : nullptr, kParts, coef, rinv, d_bad);
         RL_LAUNCHED();
-        // Q_pass = src R_pass^-1
+        // Q_pass = src R_pass^-1 on DMMA
         double* dst = (pass == 1) ? tmpq : q;
-        k_trsm_rows<<<trsm_grid, TR_T, trsm_smem, stream()>>>(m, k, src, rp, dst, d_bad);
-        RL_LAUNCHED();
+        gemm(false, false, m, k, k, 1.0, src, k, rinv, k, 0.0, dst, k);
         // R_acc = R_pass R_acc
         if (pass == 0)
             copy2d_dev(k, k, rp, k, racc, k);

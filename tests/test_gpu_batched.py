@@ -86,3 +86,30 @@ def test_batched_general_kind_fallback_path(rl, oracle):
     for t in range(batch):
         xo, ro, _ = oracle.randomized_genp(A[t], b[t], "gaussian", "right", 0, seed=3, sid=5 + t)
         assert np.abs(x[t] - xo).max() / np.abs(xo).max() < 1e-9
+
+
+@pytest.mark.parametrize("refine", [0, 1])
+def test_batched_left_side_table1_fixtures(rl, golden, oracle, refine):
+    """MulSide::Left in the batched n = 64 kernel (Table 1's side, bench.cpp:127-130: rhs = C b,
+    y = z, refinement r -> C r) on the reference's illblock systems: same accepted attempt and
+    report as the reference, backward error within 2x of the reference's, and agreement with the
+    single-system GPU path on the same system."""
+    A = np.stack([golden[f"illblock64/{t}/A"] for t in range(4)])
+    b = np.stack([golden[f"illblock64/{t}/b"] for t in range(4)])
+    x, reps = rl.randomized_genp_batched(A, b, rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN), rl.MulSide.LEFT,
+                                         refine, 33, np.arange(4, dtype=np.uint64))
+    for t in range(4):
+        y_ref = golden[f"illblock64/{t}/r{refine}/y"]
+        rep_ref = golden[f"illblock64/{t}/r{refine}/report"]
+        assert reps[t].attempt == 0 and reps[t].residual <= 1e-7
+        # the contrast arm (plain GENP of the ill-leading-block system) is catastrophic on both sides;
+        # its exact value is rounding noise amplified by ~1e18 (illblock_system's design)
+        assert (reps[t].raw_residual >= 1.0) == (rep_ref[1] >= 1.0)
+        be = np.linalg.norm(A[t] @ x[t] - b[t]) / (np.linalg.norm(A[t]) * np.linalg.norm(x[t]))
+        be_ref = np.linalg.norm(A[t] @ y_ref - b[t]) / (np.linalg.norm(A[t]) * np.linalg.norm(y_ref))
+        assert be <= max(2 * be_ref, 100 * 2.2e-16)
+        # the single-system GPU path on the same system agrees to rounding
+        xs, rs = rl.randomized_genp(A[t], b[t], rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN), rl.MulSide.LEFT,
+                                    refine, rl.RngStream(33, t))
+        assert rs.attempt == reps[t].attempt
+        assert np.abs(xs - x[t]).max() <= 1e-9 * np.abs(xs).max()
