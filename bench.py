@@ -305,9 +305,9 @@ def hbm_reference_peak(hbm_same_run):
 
 def time_multiplier_apply(torch, rl, dev, dist, tag, A, mult_bytes, hbm_peak):
     """The structured multiplier stage alone (the HBM-bound kernels of config 5): A S with its
-    gather plan (k_sparse_plan + k_sparse_right4), or A H1 H2 (k_hh2_rowdots + k_hh2_apply),
+    gather plan (k_sparse_plan + k_sparse_right4), or A H1 H2 (k_dot_pm1 + k_hh2_onepass: A read once),
     at n = 16384 through the device C-ABI; A (2 GiB) and the output exceed L2, so no flush
-    is needed between calls.  Algorithmic bytes: 2 n^2 8 (sparse) / 3 n^2 8 (pair)."""
+    is needed between calls.  Algorithmic bytes: 2 n^2 8 for both (A read once, A M written once)."""
     n = A.shape[0]
     out = torch.empty_like(A)
     if tag == rl.MultiplierTag.SPARSE_SIGN:
@@ -319,7 +319,7 @@ def time_multiplier_apply(torch, rl, dev, dist, tag, A, mult_bytes, hbm_peak):
         u = torch.from_numpy(rl.rng_draws(rl.RngStream(SEED, 57), "sign", 2 * n)).to(dev)
         u1, u2 = u[:n].contiguous(), u[n:].contiguous()
         fn = lambda: rl.dev_householder_pair_apply_right(u1, u2, A, out)  # noqa: E731
-        kernels = "k_hh2_rowdots + k_hh2_apply"
+        kernels = "k_dot_pm1 + k_hh2_onepass"
     ms, _ = _timed(torch, fn, 3, 20, dist)
     peak, src = hbm_reference_peak(hbm_peak)
     gbs = mult_bytes / (ms * 1e-3) / 1e9

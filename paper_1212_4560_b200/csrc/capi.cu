@@ -45,7 +45,8 @@ int splits_for(uint64_t m, uint64_t n, uint64_t k);
 void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs, const double* a,
                             uint64_t lda, double* out, uint64_t ldo);
 void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
-                         double s12, double* out, uint64_t ldo);
+                         double s12, double* out, uint64_t ldo, const double* s12p = nullptr);
+void dot_pm1_dev(uint64_t n, const double* u1, const double* u2, double* d_out);
 bool circ_fft_supported(uint64_t n);
 bool proto_lowrank_supported(uint64_t m, uint64_t n, uint64_t rho_plus);
 void proto_lowrank_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_plus, double tau, double tau_prime,
@@ -393,14 +394,10 @@ rl_status rl_dev_householder_pair_apply_right(uint64_t n, const double* d_u1, co
                                               const double* d_a, double* d_out) {
     API_BEGIN
     require_positive(n, n, "householder_pair_apply_right");
-    // s12 = u1^T u2: an exact integer for +-1 entries (as randomized_genp's draw computes it)
-    std::vector<double> h1(n), h2(n);
-    download(h1.data(), d_u1, n);
-    download(h2.data(), d_u2, n);
-    double s12 = 0.0;
-    for (uint64_t i = 0; i < n; ++i)
-        s12 += h1[i] * h2[i];
-    hh2_apply_right_dev(n, d_a, n, d_u1, d_u2, s12, d_out, n);
+    // s12 = u1^T u2 on the device (an exact integer for +-1 entries, as randomized_genp's draw has it)
+    double* s12p = ws<double>(WS_FLAGS, 2);
+    dot_pm1_dev(n, d_u1, d_u2, s12p);
+    hh2_apply_right_dev(n, d_a, n, d_u1, d_u2, 0.0, d_out, n, s12p);
     API_END
 }
 

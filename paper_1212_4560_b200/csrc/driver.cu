@@ -29,7 +29,8 @@ void circulant_dense_dev(uint64_t n, const double* c, double* out);
 void rank1_dense_dev(uint64_t n, const double* u, const double* v, double inv_uv, double* out);
 void toeplitz_dense_dev(uint64_t n, const double* g, double* out);
 void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
-                         double s12, double* out, uint64_t ldo);
+                         double s12, double* out, uint64_t ldo, const double* s12p = nullptr);
+void dot_pm1_dev(uint64_t n, const double* u1, const double* u2, double* d_out);
 void hh2_apply_vec_dev(uint64_t n, uint64_t nrhs, const double* u1, const double* u2, const double* y,
                        double* x);
 void sparse_apply_right_dev(uint64_t n, int nnz, const int32_t* rows, const double* signs,

@@ -110,8 +110,8 @@ __global__ void k_hh2_apply(uint64_t n, const double* __restrict__ a, uint64_t l
 // so the row is held on chip. Persistent CTAs (one per SM, 1024 threads): row r arrives in shared
 // memory by one TMA bulk copy (cp.async.bulk + mbarrier), every thread moves its 2K values into
 // registers, thread 0 immediately launches row r + grid into the freed buffer, and the dots,
-// the two-level reduction (warp shuffles, 32 partials in shared memory summed in a fixed order by
-// every thread) and the streaming stores of row r overlap that copy. HBM traffic: A read once,
+// the two-level reduction (warp shuffles, one partial per warp in shared memory summed in a fixed
+// order by every thread) and the streaming stores of row r overlap that copy. HBM traffic: A read once,
 // the output written once = 2 n^2 8 bytes. u1, u2 (+-1) stay in registers for the whole kernel.
 __device__ __forceinline__ uint32_t hh_smem(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -119,10 +119,13 @@ __device__ __forceinline__ uint32_t hh_smem(const void* p) {
 constexpr int HH_THREADS = 1024, HH_K = 8; // 1024 threads x 8 double2 = rows of up to 16384
 __global__ void __launch_bounds__(HH_THREADS, 1)
     k_hh2_onepass(uint64_t n, const double* __restrict__ a, uint64_t lda, const double* __restrict__ u1,
-                  const double* __restrict__ u2, double s12, double c, double* __restrict__ out, uint64_t ldo) {
+                  const double* __restrict__ u2, double s12, const double* __restrict__ s12p, double c,
+                  double* __restrict__ out, uint64_t ldo) {
+    if (s12p)
+        s12 = *s12p;
     extern __shared__ __align__(16) double hh_row[];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ double red1[32], red2[32];
+    __shared__ double red1[HH_THREADS / 32], red2[HH_THREADS / 32];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t nn = static_cast<uint32_t>(n);
     // u1, u2 are +-1 vectors: one sign bit per element (bit 2k + h: element 2(t + k 1024) + h)
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(HH_THREADS, 1)
         __syncthreads();
         double w1 = 0.0, w2 = 0.0;
 #pragma unroll 8
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < HH_THREADS / 32; ++q) {
             w1 += red1[q];
             w2 += red2[q];
         }
@@ -693,8 +696,27 @@ void rank1_dense_dev(uint64_t n, const double* u, const double* v, double inv_uv
 }
 
 // out = A H1 H2 (out may alias a); s12 = u1^T u2 (exact integer, host-computed)
+// u1^T u2 of two +-1 vectors on the device (an exact integer: any summation order gives it)
+__global__ void k_dot_pm1(uint64_t n, const double* __restrict__ u1, const double* __restrict__ u2, double* out) {
+    __shared__ double part[32];
+    double sacc = 0.0;
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x)
+        sacc += u1[i] * u2[i];
+    for (int o = 16; o > 0; o >>= 1)
+        sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if ((threadIdx.x & 31) == 0)
+        part[threadIdx.x >> 5] = sacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (unsigned w = 0; w < blockDim.x / 32; ++w)
+            t += part[w];
+        *out = t;
+    }
+}
+
 void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double* u1, const double* u2,
-                         double s12, double* out, uint64_t ldo) {
+                         double s12, double* out, uint64_t ldo, const double* s12p) {
     if (n <= 2ull * HH_THREADS * HH_K && n % 2 == 0 && lda % 2 == 0 && ldo % 2 == 0 &&
         ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
         const size_t smem = n * sizeof(double);
@@ -705,17 +727,26 @@ void hh2_apply_right_dev(uint64_t n, const double* a, uint64_t lda, const double
             attr[ctx().device & 15] = true;
         }
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, ctx().sms));
-        k_hh2_onepass<<<grid, HH_THREADS, smem, stream()>>>(n, a, lda, u1, u2, s12, 2.0 / static_cast<double>(n),
-                                                            out, ldo);
+        k_hh2_onepass<<<grid, HH_THREADS, smem, stream()>>>(n, a, lda, u1, u2, s12, s12p,
+                                                            2.0 / static_cast<double>(n), out, ldo);
         RL_LAUNCHED();
         return;
     }
     // rows longer than 16384 or unaligned: two passes (row dots, then the rank-2 update)
+    if (s12p) {
+        RL_CUDA(cudaMemcpyAsync(&s12, s12p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+        RL_CUDA(cudaStreamSynchronize(stream()));
+    }
     double* w = ws<double>(WS_SMALL, 2 * n);
     k_hh2_rowdots<<<cdiv(n, 8), 256, 0, stream()>>>(n, a, lda, u1, u2, w, w + n);
     RL_LAUNCHED();
     k_hh2_apply<<<grid_for(n * ((n + 1) / 2), 256), 256, 0, stream()>>>(
         n, a, lda, u1, u2, w, w + n, s12, 2.0 / static_cast<double>(n), out, ldo);
+    RL_LAUNCHED();
+}
+
+void dot_pm1_dev(uint64_t n, const double* u1, const double* u2, double* d_out) {
+    k_dot_pm1<<<1, 1024, 0, stream()>>>(n, u1, u2, d_out);
     RL_LAUNCHED();
 }
 

@@ -185,5 +185,19 @@ g["nr/wide/a"], g["nr/wide/rho"], g["nr/wide/basis"] = wide, np.array([rho]), ba
 g["pt/a"] = R.gaussian_matrix(20, 7, 41, 42)
 g["pt/h2"] = R.power_transform(g["pt/a"], 2)
 
+# --- Table 1 (bench.cpp:107-140 table1_genp, acceptance.cpp:51-73 scale): 100 trials at n = 64,
+# seed 20260825; systems and the reference's samples (rep0.residual, rep1.residual, raw) per trial,
+# each trial exactly table1_genp's run(): illblock_system on (seed, 0x1000000000000 + base),
+# randomized_genp Left refine 0/1 on (seed, 0x2000000000000 + base), base = 64 t (size index 0)
+T1, s1 = 100, 20260825
+As, bs, samp = [], [], []
+for t in range(T1):
+    base = 64 * t
+    At, bt, _ = R.illblock_system(64, s1, 0x1000000000000 + base)
+    _, r0 = R.randomized_genp(At, bt, "circulant_sign", "left", 0, seed=s1, sid=0x2000000000000 + base)
+    _, r1 = R.randomized_genp(At, bt, "circulant_sign", "left", 1, seed=s1, sid=0x2000000000000 + base)
+    As.append(At), bs.append(bt), samp.append([r0[0], r1[0], r0[1]])
+g["t1/A"], g["t1/b"], g["t1/samples"] = np.array(As), np.array(bs), np.array(samp)
+
 np.savez_compressed(os.path.join(OUT, "golden.npz"), **g)
 print("wrote", os.path.join(OUT, "golden.npz"), len(g), "arrays")

@@ -1,5 +1,5 @@
 """Small workloads for ncu captures of the non-DGEMM kernels:
-python tools/prof_kernels.py <c4|c2|hh|sparse|circfft|lu|all> [--time]
+python tools/prof_kernels.py <c4|c2|hh|sparse|circfft|rng|lu|all> [--time]
 Each workload runs the product path once warm and once more (the captured launch); with --time it
 prints the CUDA-event time of the second run instead (no profiler)."""
 import sys
@@ -64,6 +64,10 @@ if which in ("hh", "sparse", "circfft", "all"):
         run("circulant fft apply", lambda: rl.dev_circulant_apply_right(c, A8, o8))
         del A8, o8
     del A, out
+if which in ("rng", "all"):
+    G = torch.empty(8192, 8192, dtype=torch.float64, device=dev)
+    run("gaussian_matrix 8192^2", lambda: rl.dev_gaussian_matrix(G, 0.0, 1.0, rl.RngStream(bench.SEED, 11)))
+    del G
 if which in ("lu", "all"):
     n = 8192
     g = torch.Generator(device=dev).manual_seed(1)
