@@ -461,8 +461,8 @@ rl_status rl_proto_lowrank(uint64_t m, uint64_t n, const double* a, uint64_t rho
         fail(RL_INVALID_ARGUMENT, "approx_basis: rho_plus out of range");
     if (tag == RL_GAUSSIAN && !(sigma > 0.0))
         fail(RL_INVALID_ARGUMENT, "gaussian_matrix: sigma must be positive");
-    if (!proto_lowrank_supported(m, n, rho_plus))
-        fail(RL_TOO_LARGE, "proto_lowrank: the B200 path takes min(m, n) <= 64, max(m, n) <= 256, rho_plus <= 64");
+    if (!proto_lowrank_supported(m, n, rho_plus) && (rho_plus > 64 || rho_plus > n))
+        fail(RL_TOO_LARGE, "proto_lowrank: beyond 64 x 256 the B200 path takes rho_plus <= min(64, n)");
     double* da = upload(WS_H0, a, m * n);
     double* db = ws<double>(WS_H1, n * rho_plus);
     double* dx = ws<double>(WS_H2, m * n);

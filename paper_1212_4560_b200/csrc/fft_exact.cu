@@ -159,6 +159,27 @@ __global__ void k_real_to_complex(uint64_t batch, uint64_t n, uint64_t len, cons
     }
 }
 
+// z[v][i] *= conj(ch[i]): FFT of a cross-correlation with the real generator c
+__global__ void k_corr_mul(uint64_t batch, uint64_t n, const double2* __restrict__ ch, double2* __restrict__ z) {
+    const uint64_t total = batch * n;
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double2 h = ch[e % n];
+        z[e] = cmul_gcc(z[e], make_double2(h.x, -h.y));
+    }
+}
+
+// out[v * ldo + j] = Re z[v][j], j < n_out
+__global__ void k_complex_rows_real(uint64_t batch, uint64_t n, uint64_t n_out, const double2* __restrict__ z,
+                                    double* __restrict__ out, uint64_t ldo) {
+    const uint64_t total = batch * n_out;
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t v = e / n_out, j = e % n_out;
+        out[v * ldo + j] = z[v * n + j].x;
+    }
+}
+
 // fa[i] *= fb[i] (structured.cpp:31-32), fa shared by every vector of fb
 __global__ void k_pointwise(uint64_t batch, uint64_t n, const double2* __restrict__ fa, double2* __restrict__ fb) {
     const uint64_t total = batch * n;
@@ -277,6 +298,33 @@ void fft_exact_dev(uint64_t n, uint64_t batch, const double2* src, double2* dst,
     }
     if (inverse) {
         k_fft_scale<<<grid_for(n * batch, 256), 256, 0, stream()>>>(n * batch, static_cast<double>(n), dst);
+        RL_LAUNCHED();
+    }
+}
+
+// A C for circulants beyond the shared-memory FFT (n > 8192, a power of two): row r of the result
+// is the cyclic cross-correlation of row r of A (its first n_in entries, zero-padded to n) with c,
+// FFT(row) * conj(FFT(c)) through the global-memory passes of fft_exact_dev, in row batches of at
+// most 2^26 complex entries (1 GiB); the first n_out columns are kept (Toeplitz embeddings).
+// O(m n log n) and matrix-free: the dense fallback was a 2 n^3 product.
+void circ_right_fft_large(uint64_t m, uint64_t n, uint64_t n_in, uint64_t n_out, const double* c, const double* a,
+                          uint64_t lda, double* out, uint64_t ldo) {
+    cudaStream_t st = stream();
+    double2* ch = ws<double2>(WS_FFT_C, n);
+    k_real_to_complex<<<grid_for(n, 256), 256, 0, st>>>(1, n, n, c, 1, 0, ch);
+    RL_LAUNCHED();
+    fft_exact_dev(n, 1, ch, ch, 0);
+    const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(m, (1ULL << 26) / n));
+    double2* z = ws<double2>(WS_FFT_X, batch * n);
+    for (uint64_t r0 = 0; r0 < m; r0 += batch) {
+        const uint64_t rows = std::min(batch, m - r0);
+        k_real_to_complex<<<grid_for(rows * n, 256), 256, 0, st>>>(rows, n, n_in, a + r0 * lda, 1, lda, z);
+        RL_LAUNCHED();
+        fft_exact_dev(n, rows, z, z, 0);
+        k_corr_mul<<<grid_for(rows * n, 256), 256, 0, st>>>(rows, n, ch, z);
+        RL_LAUNCHED();
+        fft_exact_dev(n, rows, z, z, 1);
+        k_complex_rows_real<<<grid_for(rows * n_out, 256), 256, 0, st>>>(rows, n, n_out, z, out + r0 * ldo, ldo);
         RL_LAUNCHED();
     }
 }

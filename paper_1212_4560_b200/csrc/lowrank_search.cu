@@ -116,7 +116,8 @@ __device__ void tridiag_extremes(int k, const double* alpha, const double* beta,
 __global__ void __launch_bounds__(ES_T, 1)
     k_extremal_sv(uint64_t m, uint64_t n, const double* __restrict__ a, uint64_t lda, int lanczos, int iters,
                   const double* __restrict__ g0, double* __restrict__ t, double* __restrict__ v, double* __restrict__ w,
-                  double* __restrict__ basis, double* __restrict__ alpha, double* __restrict__ beta, EsOut* out) {
+                  double* __restrict__ basis, double* __restrict__ alpha, double* __restrict__ beta, EsOut* out,
+                  double top_tol) {
     __shared__ double red[ES_T / 32];
     __shared__ double s_lohi[2];
     const int tid = threadIdx.x;
@@ -235,6 +236,12 @@ __global__ void __launch_bounds__(ES_T, 1)
             const bool hi_ok = fabs(hi - prev_hi) <= 1e-4 * fmax(fabs(hi), 1e-300);
             const bool lo_ok = fabs(lo - prev_lo) <= 1e-4 * fmax(fabs(hi), 1e-300);
             settled = hi_ok && lo_ok;
+            // norm2 mode (top_tol > 0): stop once the largest Ritz value has settled
+            if (top_tol > 0.0 && fabs(hi - prev_hi) <= top_tol * fabs(hi)) {
+                closed = true;
+                ++k;
+                break;
+            }
         }
         prev_lo = lo;
         prev_hi = hi;
@@ -277,7 +284,8 @@ void extremal_sv_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, int 
     double* w = v + n;
     double* alpha = w + n;
     double* beta = alpha + kmax + 1;
-    k_extremal_sv<<<1, ES_T, 0, stream()>>>(m, n, a, lda, method, iters, g0, t, v, w, basis, alpha, beta, d_out);
+    k_extremal_sv<<<1, ES_T, 0, stream()>>>(m, n, a, lda, method, iters, g0, t, v, w, basis, alpha, beta, d_out,
+                                            0.0);
     RL_LAUNCHED();
     EsOut h{};
     RL_CUDA(cudaMemcpyAsync(&h, d_out, sizeof(EsOut), cudaMemcpyDeviceToHost, stream()));
@@ -287,6 +295,30 @@ void extremal_sv_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda, int 
                                             : "extremal_sv_estimate: power method did not settle");
     *sv_max = h.sv_max;
     *sv_min = h.sv_min;
+}
+
+// ||A||_2 = sigma_1 of the m x n device matrix (dense::norm2 beyond the one-CTA SVD's sizes): Lanczos
+// on A^T A with full reorthogonalization from a fixed start vector, stopped when the largest Ritz
+// value moves by <= 1e-15 relative (or the Krylov space closes / n steps), then sqrt.
+double norm2_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda) {
+    const uint64_t kmax = std::min<uint64_t>(n, 96);
+    double* g0 = ws<double>(WS_ES0, 2 * n + 2);
+    rng_generate(0x6e6f726d32ULL, n, Draw::Gaussian, 2 * n, 0.0, 1.0, g0);
+    double* sc = ws<double>(WS_ES1, m + 2 * n + 2 * (kmax + 1));
+    double* basis = ws<double>(WS_ES2, kmax * n);
+    EsOut* d_out = reinterpret_cast<EsOut*>(ws<double>(WS_ES3, 4));
+    double* t = sc;
+    double* v = t + m;
+    double* w = v + n;
+    double* alpha = w + n;
+    double* beta = alpha + kmax + 1;
+    k_extremal_sv<<<1, ES_T, 0, stream()>>>(m, n, a, lda, 1, static_cast<int>(kmax), g0, t, v, w, basis, alpha, beta,
+                                            d_out, 1e-15);
+    RL_LAUNCHED();
+    EsOut h{};
+    RL_CUDA(cudaMemcpyAsync(&h, d_out, sizeof(EsOut), cudaMemcpyDeviceToHost, stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+    return h.sv_max;
 }
 
 // cond_probe (lowrank.cpp:350-358)

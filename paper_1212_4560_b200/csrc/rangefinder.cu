@@ -1143,9 +1143,103 @@ bool proto_lowrank_supported(uint64_t m, uint64_t n, uint64_t rho_plus) {
 }
 
 // d_a: m x n on the device.  basis: n x rho_plus (first rho columns valid), approx: m x n.
+double norm2_dev(uint64_t m, uint64_t n, const double* a, uint64_t lda);
+
+// proto_lowrank beyond the one-CTA SVD (min(m, n) > 64 or max(m, n) > 256; rho_plus <= 64 <= n):
+// ||A||_2 and ||A - approx||_2 by Lanczos (norm2_dev), the n x rho_plus sketch's thin SVD as
+// shifted CholeskyQR3 (sketch = Q R) then the one-CTA Jacobi SVD of R with left vectors (the
+// sketch's left vectors are Q U_R), everything else as the small path.
+void proto_lowrank_large_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_plus, double tau,
+                             double tau_prime, int tag, double mu, double sig_g, uint64_t seed, uint64_t sid,
+                             uint64_t* rho_out, double* d_basis, double* d_approx, double* residual, int* ok) {
+    const uint64_t k = rho_plus;
+    double* sc = ws<double>(WS_RF5B, m * k + 3 * n * k + m * n + 3 * k * k + 2 * (m + k) + 64);
+    double* g = sc;                 // m x k
+    double* sk = g + m * k;         // n x k
+    double* qs = sk + n * k;        // n x k
+    double* ab = qs + n * k;        // max(m, n) x k
+    double* diff = ab + n * k;      // m x n
+    double* rs = diff + m * n;      // k x k
+    double* ur = rs + k * k;        // k x k
+    double* scr = ur + k * k;       // k x k
+    double* sg = scr + k * k;       // sigma
+    double* gv = sg + k + 8;        // Toeplitz generators (m + k - 1)
+    if (m > n) // ab holds A T (m x s) below: grow it
+        ab = ws<double>(WS_RF3B, m * k);
+    const double norm_a = norm2_dev(m, n, d_a, n);
+    *rho_out = 0;
+    *residual = 0.0;
+    *ok = 0;
+    RL_CUDA(cudaMemsetAsync(d_approx, 0, m * n * sizeof(double), stream()));
+    RL_CUDA(cudaMemsetAsync(d_basis, 0, n * k * sizeof(double), stream()));
+    if (norm_a == 0.0) {
+        *ok = 1;
+        RL_CUDA(cudaStreamSynchronize(stream()));
+        return;
+    }
+    for (int attempt = 0; attempt <= 3; ++attempt) {
+        const uint64_t ds = sid + 104729ULL * static_cast<uint64_t>(attempt);
+        if (tag == RL_TOEPLITZ_GAUSSIAN) {
+            rng_generate(seed, ds, Draw::Gaussian, m + k - 1, mu, sig_g, gv);
+            k_toeplitz_rect<<<cdiv(m * k, 256), 256, 0, stream()>>>(m, k, gv, g);
+            RL_LAUNCHED();
+        } else {
+            rng_generate(seed, ds, Draw::Gaussian, m * k, mu, sig_g, g);
+        }
+        gemm(true, false, n, k, m, 1.0, d_a, n, g, k, 0.0, sk, k); // A^T G
+        if (!cholqr3(n, static_cast<int>(k), sk, qs, rs))
+            fail(RL_NO_CONVERGENCE, "proto_lowrank: the sketch's QR broke down (numerically rank-deficient beyond "
+                                    "the shifted CholeskyQR3 range)");
+        const std::vector<double> ss = jacobi_svd_dev(k, k, rs, sg, ur, scr);
+        gemm(false, false, n, k, k, 1.0, qs, k, ur, k, 0.0, d_basis, k); // left vectors of the sketch
+        double tau_eff = tau;
+        if (tau_eff <= 0.0) { // the auto rule (lowrank.cpp:132-147)
+            tau_eff = 1e-6;
+            double best_gap = 1.0;
+            for (size_t j = 1; j < ss.size(); ++j) {
+                if (ss[j] >= 1e-3 * ss[0])
+                    continue;
+                const double gap = ss[j] / std::max(ss[j - 1], 1e-300);
+                if (gap < best_gap) {
+                    best_gap = gap;
+                    tau_eff = std::sqrt(std::max(ss[j] * ss[j - 1], 1e-300)) / norm_a;
+                }
+            }
+        }
+        uint64_t s = ss.size();
+        while (s > 0 && ss[s - 1] <= tau_eff * norm_a)
+            --s;
+        if (s == 0) {
+            *rho_out = 0;
+            RL_CUDA(cudaMemsetAsync(d_approx, 0, m * n * sizeof(double), stream()));
+            *residual = 1.0;
+            *ok = 0;
+            continue;
+        }
+        gemm(false, false, m, s, n, 1.0, d_a, n, d_basis, k, 0.0, ab, k);
+        gemm(false, true, m, n, s, 1.0, ab, k, d_basis, k, 0.0, d_approx, n);
+        k_sub<<<cdiv(m * n, 256), 256, 0, stream()>>>(m * n, d_a, d_approx, diff);
+        RL_LAUNCHED();
+        *rho_out = s;
+        *residual = norm2_dev(m, n, diff, n) / norm_a;
+        *ok = *residual <= tau_prime;
+        if (*ok)
+            break;
+    }
+    if (*rho_out < k)
+        for (uint64_t i = 0; i < n; ++i)
+            RL_CUDA(cudaMemsetAsync(d_basis + i * k + *rho_out, 0, (k - *rho_out) * sizeof(double), stream()));
+    RL_CUDA(cudaStreamSynchronize(stream()));
+}
+
 void proto_lowrank_dev(uint64_t m, uint64_t n, const double* d_a, uint64_t rho_plus, double tau, double tau_prime,
                        int tag, double mu, double sig_g, uint64_t seed, uint64_t sid, uint64_t* rho_out,
                        double* d_basis, double* d_approx, double* residual, int* ok) {
+    if (!proto_lowrank_supported(m, n, rho_plus)) {
+        proto_lowrank_large_dev(m, n, d_a, rho_plus, tau, tau_prime, tag, mu, sig_g, seed, sid, rho_out, d_basis,
+                                d_approx, residual, ok);
+        return;
+    }
     double* sc = ws<double>(WS_RF5, 4 * m * n + 2 * n * rho_plus + 2 * m * rho_plus + 2 * (m + n + rho_plus) + 64);
     double* g = sc;                      // m x rho_plus
     double* sk = g + m * rho_plus;       // n x rho_plus

@@ -1186,14 +1186,22 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, in
 
 } // namespace
 
-// true when the FFT path handles n (a power of two, 64 <= n <= 8192)
-bool circ_fft_supported(uint64_t n) { return n >= 64 && n <= CF_MAXN && (n & (n - 1)) == 0; }
+// true when the FFT path handles n: a power of two >= 64 (n <= 8192 in shared memory, larger n
+// through the global-memory passes of circ_right_fft_large)
+bool circ_fft_supported(uint64_t n) { return n >= 64 && (n & (n - 1)) == 0; }
+
+void circ_right_fft_large(uint64_t m, uint64_t n, uint64_t n_in, uint64_t n_out, const double* c, const double* a,
+                          uint64_t lda, double* out, uint64_t ldo);
 
 // out = A C for the circulant with first column c; A, out m x n (out != A)
 namespace {
 // the transform for rows of n_in columns against the length-n circulant c (n a power of two)
 void circ_right_fft_launch(uint64_t m, uint64_t n, uint64_t n_in, uint64_t n_out, const double* c, const double* a,
                            uint64_t lda, double* out, uint64_t ldo) {
+    if (n > static_cast<uint64_t>(CF_MAXN)) {
+        circ_right_fft_large(m, n, n_in, n_out, c, a, lda, out, ldo);
+        return;
+    }
     const size_t smem = (n + n / 8 + 8) * sizeof(double2);
     static bool attr[16] = {};
     if (!attr[ctx().device & 15]) {

@@ -185,6 +185,13 @@ g["nr/wide/a"], g["nr/wide/rho"], g["nr/wide/basis"] = wide, np.array([rho]), ba
 g["pt/a"] = R.gaussian_matrix(20, 7, 41, 42)
 g["pt/h2"] = R.power_transform(g["pt/a"], 2)
 
+# proto_lowrank beyond the one-CTA SVD: a 320 x 320 paper profile (rank 8), rho_plus 12, both kinds
+g["proto320/A"] = R.profile_matrix_paper(320, 8, 41, 60)
+for kind in ("gaussian", "toeplitz_gaussian"):
+    rho, basis, approx, res, ok = R.proto_lowrank(g["proto320/A"], 12, 1e-6, 1e-6, 41, 61, kind=kind)
+    g[f"proto320/{kind}/out"] = np.array([rho, res, float(ok)])
+    g[f"proto320/{kind}/approx"] = approx
+
 # --- Table 1 (bench.cpp:107-140 table1_genp, acceptance.cpp:51-73 scale): 100 trials at n = 64,
 # seed 20260825; systems and the reference's samples (rep0.residual, rep1.residual, raw) per trial,
 # each trial exactly table1_genp's run(): illblock_system on (seed, 0x1000000000000 + base),

@@ -337,11 +337,14 @@ def test_sparse_apply_right_bit_exact(rl, oracle, n):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n", [(64, 64), (255, 256), (1024, 1024), (3, 2048), (8192, 8192), (100, 96)])
+@pytest.mark.parametrize("m,n", [(64, 64), (255, 256), (1024, 1024), (3, 2048), (8192, 8192), (100, 96), (5, 16384),
+                                 (3, 65536)])
 def test_circulant_apply_right_fft(rl, m, n):
     """A C for a circulant multiplier (C(i,j) = c[(i-j) mod n], structured.cpp:54-68) through the
-    FFT path (power-of-two n <= 8192; n = 96 takes the dense fallback) against the dense product
-    in numpy: relative error within 1e-13 (FFT rounding grows like log2 n eps)."""
+    FFT path (power-of-two n: shared-memory transform up to 8192, global-memory passes beyond;
+    n = 96 takes the dense fallback) against the dense product in numpy: relative error within
+    1e-13 up to 8192 (rounding grows like log2 n eps); beyond, the global path's chained twiddles
+    (the reference's own FFT scheme) carry O(n eps), the same order as a dense product's."""
     import torch
     rng = np.random.default_rng(n + m)
     for c in (np.where(rng.random(n) < 0.5, -1.0, 1.0), rng.standard_normal(n)):
@@ -352,7 +355,8 @@ def test_circulant_apply_right_fft(rl, m, n):
         out = torch.empty(m, n, dtype=torch.float64, device=dev)
         rl.dev_circulant_apply_right(torch.from_numpy(c).to(dev), torch.from_numpy(a).to(dev), out)
         got = out.cpu().numpy()
-        assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max() * max(1.0, np.log2(n) / 4)
+        tol = 1e-13 * max(1.0, np.log2(n) / 4) if n <= 8192 else 4 * n * 2.2e-16
+        assert np.abs(got - want).max() <= tol * np.abs(want).max()
 
 
 @pytest.mark.gpu
@@ -414,11 +418,13 @@ def test_randomized_genp_householder_sign(rl, golden, side):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n", [(256, 256), (77, 1000), (33, 999), (5, 257), (4096, 4096), (30, 5000)])
+@pytest.mark.parametrize("m,n", [(256, 256), (77, 1000), (33, 999), (5, 257), (4096, 4096), (30, 5000),
+                                 (4, 12000)])
 def test_toeplitz_apply_right(rl, m, n):
     """A T for a Toeplitz multiplier (T(i,j) = col[i-j] / row[j-i], structured.cpp:70-83) through
     the FFT of its circulant embedding (toeplitz_mul, structured.cpp:156-176; order
-    next_pow2(2n - 1) <= 8192) or the dense fallback (n = 5000), against numpy's dense product."""
+    next_pow2(2n - 1): shared memory up to 8192, global-memory passes beyond — n = 5000, 12000),
+    against numpy's dense product."""
     import torch
     rng = np.random.default_rng(n)
     col, row = rng.standard_normal(n), rng.standard_normal(n)
@@ -431,4 +437,6 @@ def test_toeplitz_apply_right(rl, m, n):
     out = torch.empty(m, n, dtype=torch.float64, device=dev)
     rl.dev_toeplitz_apply_right(torch.from_numpy(col).to(dev), torch.from_numpy(row).to(dev),
                                 torch.from_numpy(a).to(dev), out)
-    assert np.abs(out.cpu().numpy() - want).max() <= 1e-13 * np.abs(want).max() * max(1.0, np.log2(n) / 4)
+    length = 1 << int(np.ceil(np.log2(2 * n - 1)))
+    tol = 1e-13 * max(1.0, np.log2(n) / 4) if length <= 8192 else 4 * length * 2.2e-16
+    assert np.abs(out.cpu().numpy() - want).max() <= tol * np.abs(want).max()

@@ -162,3 +162,20 @@ def test_proto_lowrank(rl, oracle, golden, tau, kind):
     assert np.abs(approx - approx_o).max() <= 1e-12 * np.abs(a).max()
     assert np.abs(basis.T @ basis - np.eye(rho)).max() < 1e-13
     assert abs(res - res_o) <= 0.5 * res_o + 1e-15
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "toeplitz_gaussian"])
+def test_proto_lowrank_beyond_one_cta(rl, golden, kind):
+    """proto_lowrank (lowrank.cpp:108-177) at 320 x 320 (beyond the one-CTA SVD): ||A||_2 and
+    ||A - approx||_2 by Lanczos, the sketch's thin SVD by CholeskyQR3 + Jacobi of R, against the
+    compiled reference's own result on the paper profile (rank 8): same rho and ok, residual within
+    2x, approximations equal to within the residual's scale."""
+    A = golden["proto320/A"]
+    tag = getattr(rl.MultiplierTag, kind.upper())
+    rho, basis, approx, res, ok = rl.proto_lowrank(A, 12, 1e-6, 1e-6, rl.MultiplierKind(tag), rl.RngStream(41, 61))
+    ref = golden[f"proto320/{kind}/out"]
+    assert rho == int(ref[0]) == 8 and ok and bool(ref[2])
+    assert 0.5 * ref[1] <= res <= 2 * ref[1], (res, ref[1])
+    assert np.abs(basis.T @ basis - np.eye(rho)).max() < 1e-12
+    nrm = np.linalg.norm(A, 2)
+    assert np.abs(approx - golden[f"proto320/{kind}/approx"]).max() <= 10 * ref[1] * nrm
