@@ -261,12 +261,15 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t Kfull, double alpha, const 
         return launch<128, 72, 4, 3, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     if (M > 64 && M <= 72)
         return launch<72, 128, 3, 4, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
-    if (N > 64 && z * cdiv(M, 128) * cdiv(N, 64) >= 2ULL * sms && K >= kLongK)
+    if (N > 64 && z * cdiv(M, 128) * cdiv(N, 64) >= 2ULL * sms && K >= kLongK) {
         // two CTAs per SM (128x64 tiles, <= 128 regs): one CTA's prologue / C epilogue
         // overlaps the other's DMMA loop.  Long K: K-tile 32 in 2 stages (217 KB for the two
         // CTAs), half the k-tile barriers of a 16 x 3 ring: A*G 8192^3 33.41 -> 32.76 ms
-        // (DMMA pipe 89.5 -> 91.3% active)
+        // (DMMA pipe 89.5 -> 91.3% active).  (Feeding the padded tiles with per-row TMA bulk
+        // copies, 160 x 256-512 B per stage from one warp, measured 48.7 ms: the copy engine
+        // is not built for that many small transfers.)
         launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    }
     else if (N > 64 && z * cdiv(M, 128) * cdiv(N, 64) >= 2ULL * sms)
         // short K (the LU's trailing updates): K-tile 16 in 3 stages keeps the pipeline full
         // over few k-tiles (7680^2 x 256: 1044 vs 1100 us with the 32 x 2 ring)

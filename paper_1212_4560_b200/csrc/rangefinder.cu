@@ -828,6 +828,7 @@ void chol_attrs() {
     if (!attr[ctx().device & 15]) {
         RL_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      KMAX * (KMAX + 1) * 8));
+
         attr[ctx().device & 15] = true;
     }
 }
