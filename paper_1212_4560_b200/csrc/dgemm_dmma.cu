@@ -14,6 +14,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -215,6 +218,176 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     }
 }
 
+// The long-K full-tile case of A K-major x B N-major (A·G, the big LU updates) fed by the TMA
+// engine: per stage one thread issues six 2-D tensor copies (cp.async.bulk.tensor, SASS UTMALDG)
+// — A as two 128 x 16 boxes, B as four 32 x 16 boxes, 16 doubles = one 128-byte swizzle span
+// each — completing on one mbarrier per stage (expect_tx = the stage's 48 KB). The boxes land
+// with the 128-byte swizzle (16-byte chunk c of line r stored at c ^ (r mod 8)), which keeps the
+// DMMA fragment reads at the minimum two wavefronts for A (8 rows x 4 k) and four for B (4 k x
+// 8 n, a 2-way conflict: DMMA, not shared memory, bounds the loop); the fragment addresses apply
+// the same XOR. The 256 threads issue only fragment loads and DMMAs. Same tile and k order as
+// k_dgemm: bit-identical results.
+__device__ __forceinline__ uint32_t s_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+constexpr int TM_BM = 128, TM_BN = 64, TM_BK = 32;
+constexpr int TM_A_BYTES = TM_BM * TM_BK * 8, TM_B_BYTES = TM_BK * TM_BN * 8;
+constexpr int TM_STAGE = TM_A_BYTES + TM_B_BYTES; // 48 KB
+constexpr int TM_NSTAGE = 2;
+constexpr size_t TM_SMEM = static_cast<size_t>(TM_NSTAGE) * TM_STAGE + 1024; // + alignment slack
+// byte offset of A(r, k) / B(k, n) inside a stage (128-byte swizzle, 16-double boxes)
+__device__ __forceinline__ uint32_t tm_a_off(int r, int k) {
+    return static_cast<uint32_t>((k >> 4) * (TM_BM * 128) + r * 128 + ((((k & 15) >> 1) ^ (r & 7)) << 4) + ((k & 1) << 3));
+}
+__device__ __forceinline__ uint32_t tm_b_off(int k, int n) {
+    return static_cast<uint32_t>(TM_A_BYTES + (n >> 4) * (TM_BK * 128) + k * 128 + ((((n & 15) >> 1) ^ (k & 7)) << 4) +
+                                 ((n & 1) << 3));
+}
+__global__ void __launch_bounds__(256, 2)
+    k_dgemm_tmap(uint64_t M, uint64_t N, uint64_t K, double alpha, const __grid_constant__ CUtensorMap tmA,
+                 const __grid_constant__ CUtensorMap tmB, double beta, double* __restrict__ C, uint64_t ldc) {
+    extern __shared__ __align__(16) unsigned char smem_tm[];
+    __shared__ __align__(8) uint64_t full[TM_NSTAGE];
+    constexpr int WN = 2, WTM = 32, WTN = 32, MF = 4, NF = 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int g = lane >> 2, t = lane & 3;
+    const uint64_t m0 = static_cast<uint64_t>(blockIdx.y) * TM_BM, n0 = static_cast<uint64_t>(blockIdx.x) * TM_BN;
+    const int ktiles = static_cast<int>(K / TM_BK);
+    // 1024-byte aligned stage base (the 128-byte swizzle pattern repeats every 8 lines)
+    const uint32_t base = (s_addr(smem_tm) + 1023u) & ~1023u;
+    unsigned char* gbase = smem_tm + (base - s_addr(smem_tm));
+    if (tid == 0) {
+        for (int s2 = 0; s2 < TM_NSTAGE; ++s2)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&full[s2])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int s2, int kt) { // thread 0
+        const uint32_t mb = s_addr(&full[s2]);
+        const uint32_t st = base + static_cast<uint32_t>(s2 * TM_STAGE);
+        const int k0 = kt * TM_BK;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(TM_STAGE) : "memory");
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                         ::"r"(st + q * TM_BM * 128), "l"(&tmA), "r"(k0 + 16 * q), "r"(static_cast<int>(m0)), "r"(mb)
+                         : "memory");
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                         ::"r"(st + TM_A_BYTES + q * TM_BK * 128), "l"(&tmB), "r"(static_cast<int>(n0) + 16 * q), "r"(k0),
+                           "r"(mb)
+                         : "memory");
+    };
+    double acc[MF][NF][2];
+#pragma unroll
+    for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j)
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (tid == 0)
+        for (int s2 = 0; s2 < TM_NSTAGE - 1 && s2 < ktiles; ++s2)
+            issue(s2, s2);
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int s2 = kt % TM_NSTAGE;
+        {
+            const uint32_t mb = s_addr(&full[s2]), par = static_cast<uint32_t>((kt / TM_NSTAGE) & 1);
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                             " selp.u32 %0, 1, 0, p;\n}"
+                             : "=r"(done)
+                             : "r"(mb), "r"(par)
+                             : "memory");
+        }
+        __syncthreads(); // every warp is done with the stage refilled next (read at kt - 1)
+        const int nk = kt + TM_NSTAGE - 1;
+        if (tid == 0 && nk < ktiles)
+            issue(nk % TM_NSTAGE, nk);
+        const unsigned char* st = gbase + s2 * TM_STAGE;
+#pragma unroll
+        for (int kk = 0; kk < TM_BK; kk += 4) {
+            double af[MF], bf[NF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+                af[i] = *reinterpret_cast<const double*>(st + tm_a_off(wm * WTM + i * 8 + g, kk + t));
+#pragma unroll
+            for (int j = 0; j < NF; ++j)
+                bf[j] = *reinterpret_cast<const double*>(st + tm_b_off(kk + t, wn * WTN + j * 8 + g));
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+#pragma unroll
+                for (int j = 0; j < NF; ++j)
+                    dmma(acc[i][j], af[i], bf[j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < MF; ++i) {
+        const uint64_t row = m0 + wm * WTM + i * 8 + g;
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+            const uint64_t col = n0 + wn * WTN + j * 8 + 2 * t;
+            double* cp = C + row * ldc + col;
+            double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+            if (beta != 0.0) {
+                const double2 o = *reinterpret_cast<const double2*>(cp);
+                v0 = fma(beta, o.x, v0);
+                v1 = fma(beta, o.y, v1);
+            }
+            *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// rows x cols row-major f64 (ld doubles), box box_rows x 16 doubles, 128-byte swizzle
+bool make_tmap(CUtensorMap* tm, const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+    auto enc = tensor_map_encoder();
+    if (!enc)
+        return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {ld * sizeof(double)};
+    const cuuint32_t box[2] = {16, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// true when the TMA kernel took the product
+bool launch_tmap(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda, const double* B,
+                 uint64_t ldb, double beta, double* C, uint64_t ldc) {
+    CUtensorMap ta, tb;
+    if (!make_tmap(&ta, A, M, K, lda, TM_BM) || !make_tmap(&tb, B, K, N, ldb, TM_BK))
+        return false;
+    static bool configured[16] = {};
+    const int dev = ctx().device & 15;
+    if (!configured[dev]) {
+        RL_CUDA(cudaFuncSetAttribute(k_dgemm_tmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(TM_SMEM)));
+        configured[dev] = true;
+    }
+    dim3 grid(cdiv(N, TM_BN), cdiv(M, TM_BM), 1);
+    k_dgemm_tmap<<<grid, 256, TM_SMEM, stream()>>>(M, N, K, alpha, ta, tb, beta, C, ldc);
+    RL_LAUNCHED();
+    return true;
+}
+
 template <int BM, int BN, int WM, int WN, bool AK, bool BKM, int VEC, int NSTAGE, int MINB = 1, int BKT = BK>
 void launch(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda,
             const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, const Split& sp) {
@@ -267,7 +440,14 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t Kfull, double alpha, const 
         // CTAs), half the k-tile barriers of a 16 x 3 ring: A*G 8192^3 33.41 -> 32.76 ms
         // (DMMA pipe 89.5 -> 91.3% active).  (Feeding the padded tiles with per-row TMA bulk
         // copies, 160 x 256-512 B per stage from one warp, measured 48.7 ms: the copy engine
-        // is not built for that many small transfers.)
+        // is not built for that many small transfers.)  Full tiles of A K-major x B N-major go
+        // through 2-D tensor copies with the 128-byte swizzle instead (k_dgemm_tmap);
+        // RL_GEMM_NO_TMA=1 keeps the cp.async ring.
+        static const bool no_tma = getenv("RL_GEMM_NO_TMA") != nullptr;
+        if (AK && !BKM && VEC == 2 && sp.splits == 1 && !no_tma && M % 128 == 0 && N % 64 == 0 && Kfull % 32 == 0 &&
+            ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
+            launch_tmap(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc))
+            return;
         launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     }
     else if (N > 64 && z * cdiv(M, 128) * cdiv(N, 64) >= 2ULL * sms)
