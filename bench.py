@@ -637,7 +637,7 @@ def run_ours(args, dist, rank, world, local_rank):
                 "backward_error_max": bwd, "residual": rep.residual,
                 "attempt_worst_column": rep.attempt, "column_attempts": [c[0] for c in cols],
                 "rng_ms_per_G": round(rng_ms, 3)},
-        "roofline": {"bound": "tensor", "kernel": "k_dgemm (A G, DMMA m8n8k4 f64)",
+        "roofline": {"bound": "tensor", "kernel": "k_dgemm_tmap (A G: TMA tensor copies + DMMA m8n8k4 f64)",
                      "achieved": round(gemm_tf, 3), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
                      "frac": round(gemm_tf / fp64_peak, 4), "traffic": traffic,
                      "peak_source": "same-run FP64 DMMA probe (rl_probe_peaks; MEASURED_PEAKS.json has no fp64)",
