@@ -132,5 +132,40 @@ LowRankResult proto_lowrank(const Matrix& a, std::size_t rho_plus, double tau, d
     return r;
 }
 
+Matrix power_transform(const Matrix& a, unsigned h) {
+    Matrix out(a.rows(), a.cols());
+    check(rl_power_transform(a.rows(), a.cols(), a.data().data(), h, out.data().data()));
+    return out;
+}
+
+SvEstimates extremal_sv_estimate(const Matrix& a, SvMethod method, int iters, rnd::RngStream stream) {
+    SvEstimates e;
+    check(rl_extremal_sv_estimate(a.rows(), a.cols(), a.data().data(), method == SvMethod::Lanczos ? 1 : 0, iters,
+                                  stream.seed, stream.stream_id, &e.sv_max, &e.sv_min));
+    return e;
+}
+
+bool cond_probe(const Matrix& b, double kappa_threshold, SvMethod method, int iters, rnd::RngStream stream) {
+    int pass = 0;
+    check(rl_cond_probe(b.rows(), b.cols(), b.data().data(), kappa_threshold, method == SvMethod::Lanczos ? 1 : 0,
+                        iters, stream.seed, stream.stream_id, &pass));
+    return pass != 0;
+}
+
+NrankResult nrank_search(const Matrix& a, std::size_t rho_minus, std::size_t rho_plus, double kappa_threshold,
+                         SearchPolicy policy, rnd::RngStream stream) {
+    const std::size_t wide = std::max(a.rows(), a.cols());
+    std::vector<double> basis(wide * std::max<std::size_t>(rho_plus, 1), 0.0);
+    uint64_t rho = 0, rows = 0, cols = 0;
+    check(rl_nrank_search(a.rows(), a.cols(), a.data().data(), rho_minus, rho_plus, kappa_threshold,
+                          policy == SearchPolicy::Binary ? 0 : 1, stream.seed, stream.stream_id, &rho, basis.data(),
+                          &rows, &cols));
+    NrankResult r;
+    r.rho = rho;
+    basis.resize(rows * cols);
+    r.basis = Matrix(rows, cols, std::move(basis));
+    return r;
+}
+
 } // namespace lowrank
 } // namespace randla

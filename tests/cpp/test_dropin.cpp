@@ -262,6 +262,30 @@ int main() {
         CHECK(rel_diff(lowrank::project_onto_basis(A, Y, false, dense::Side::Left), A) < 1e-12);
         Matrix Z = lowrank::approx_basis(A, 8, {rnd::MultiplierTag::Gaussian}, lowrank::SpaceSide::RightSpace, {50, 4});
         CHECK(Z.rows() == 60 && Z.cols() == 8);
+        // the rank-search side (test_lowrank.cpp:116-177)
+        for (auto method : {lowrank::SvMethod::Power, lowrank::SvMethod::Lanczos}) {
+            auto est = lowrank::extremal_sv_estimate(Matrix::diagonal(std::vector<double>{5.0, 1.0}), method, 200,
+                                                     rnd::RngStream{41, 15});
+            CHECK(std::abs(est.sv_max - 5.0) < 1e-3 * 5.0);
+            CHECK(std::abs(est.sv_min - 1.0) < 1e-3);
+        }
+        CHECK(lowrank::cond_probe(Matrix::identity(8), 1e6, lowrank::SvMethod::Power, 500, rnd::RngStream{41, 20}));
+        {
+            std::vector<double> sig(8, 1e-10);
+            sig[0] = 1.0;
+            CHECK(!lowrank::cond_probe(Matrix::diagonal(sig), 1e6, lowrank::SvMethod::Power, 500,
+                                       rnd::RngStream{41, 21}));
+        }
+        CHECK(lowrank::nrank_search(Matrix(8, 8), 0, 8, 1e6, lowrank::SearchPolicy::Binary, rnd::RngStream{41, 28}).rho ==
+              0);
+        CHECK(lowrank::nrank_search(Matrix::identity(16), 0, 16, 1e6, lowrank::SearchPolicy::Binary,
+                                    rnd::RngStream{41, 29})
+                  .rho == 16);
+        {
+            Matrix d2 = Matrix::diagonal(std::vector<double>{2.0, 1.0});
+            CHECK(rel_diff(lowrank::power_transform(d2, 0), d2) == 0.0);
+            CHECK(rel_diff(lowrank::power_transform(d2, 1), Matrix::diagonal(std::vector<double>{8.0, 1.0})) < 1e-14);
+        }
         // proto_lowrank (test_lowrank.cpp:72-91): the zero matrix, and a rank-8 matrix recovered
         auto z = lowrank::proto_lowrank(Matrix(4, 4), 2, 1e-8, 1e-6, {rnd::MultiplierTag::Gaussian, 0.0, 1.0},
                                         {41, 9});

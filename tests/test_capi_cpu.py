@@ -41,7 +41,9 @@ def test_cpp_dropin_library_exports_reference_api(rl):
     nm = subprocess.run(["nm", "-DC", "--defined-only", so], capture_output=True, text=True).stdout
     for sym in ("randla::genp::randomized_genp", "randla::genp::genp_factor", "randla::genp::genp_solve",
                 "randla::rnd::gaussian_matrix", "randla::lowrank::approx_basis", "randla::dense::qr_positive",
-                "randla::Matrix::multiply"):
+                "randla::Matrix::multiply", "randla::lowrank::nrank_search", "randla::lowrank::extremal_sv_estimate",
+                "randla::lowrank::cond_probe", "randla::lowrank::power_transform", "randla::lowrank::proto_lowrank",
+                "randla::structured::fft", "randla::structured::toeplitz_mul", "randla::structured::multiply_matrix"):
         assert sym in nm, sym
 
 
