@@ -59,7 +59,7 @@ void toeplitz_dense_dev(uint64_t n, const double* g, double* out);
 void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
                               uint64_t ldo);
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r);
-void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad);
+void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad, bool want_q = true);
 void small_sv_launch(int k, const double* d_a, double* d_sg);
 void rank_bracket_launch(int k, const double* d_r, int* d_flag);
 std::vector<double> small_singular_values(int k, const double* d_a);
@@ -883,7 +883,7 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
     transpose_dev(rho, n, d_b, n, bt, rho);
     double* qb = ws<double>(WS_RF2, n * rho);
     double* rb = ws<double>(WS_RF3B, rho * rho);
-    cholqr3_async(n, static_cast<int>(rho), bt, qb, rb, flags + 2);
+    cholqr3_async(n, static_cast<int>(rho), bt, qb, rb, flags + 2, false); // R only: sigma(B) = sigma(R)
     double* dsg = ws<double>(WS_RF5B, 128 + 1);
     small_sv_launch(static_cast<int>(rho), rb, dsg);
     // one synchronisation: the flags and sigma together

@@ -230,31 +230,61 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
 __device__ __forceinline__ uint32_t s_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-constexpr int TM_BM = 128, TM_BN = 64, TM_BK = 32;
-constexpr int TM_A_BYTES = TM_BM * TM_BK * 8, TM_B_BYTES = TM_BK * TM_BN * 8;
-constexpr int TM_STAGE = TM_A_BYTES + TM_B_BYTES; // 48 KB
-constexpr int TM_NSTAGE = 2;
-constexpr size_t TM_SMEM = static_cast<size_t>(TM_NSTAGE) * TM_STAGE + 1024; // + alignment slack
-// byte offset of A(r, k) / B(k, n) inside a stage (128-byte swizzle, 16-double boxes)
-__device__ __forceinline__ uint32_t tm_a_off(int r, int k) {
-    return static_cast<uint32_t>((k >> 4) * (TM_BM * 128) + r * 128 + ((((k & 15) >> 1) ^ (r & 7)) << 4) + ((k & 1) << 3));
-}
-__device__ __forceinline__ uint32_t tm_b_off(int k, int n) {
-    return static_cast<uint32_t>(TM_A_BYTES + (n >> 4) * (TM_BK * 128) + k * 128 + ((((n & 15) >> 1) ^ (k & 7)) << 4) +
-                                 ((n & 1) << 3));
-}
-__global__ void __launch_bounds__(256, 2)
-    k_dgemm_tmap(uint64_t M, uint64_t N, uint64_t K, double alpha, const __grid_constant__ CUtensorMap tmA,
-                 const __grid_constant__ CUtensorMap tmB, double beta, double* __restrict__ C, uint64_t ldc) {
+constexpr int TM_BK = 32, TM_NSTAGE = 2;
+// Tile geometry of the TMA kernel: BM x BN output tile, K-tile 32, WM x WN warps. A is K-major
+// (boxes BM x 16 along k: A·G, A·H) or M-major (boxes 32 x 16 along m: Q^T A); B is N-major
+// (boxes 32 x 16 along n). Box edges past M / N / K are zero-filled by the copy engine.
+template <int BM, int BN, int WM, int WN, bool AKM>
+struct TmCfg {
+    static constexpr int NT = WM * WN * 32;
+    static constexpr int WTM = BM / WM, WTN = BN / WN, MF = WTM / 8, NF = WTN / 8;
+    static constexpr int A_BYTES = BM * TM_BK * 8, B_BYTES = TM_BK * BN * 8;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr size_t SMEM = static_cast<size_t>(TM_NSTAGE) * STAGE + 1024; // + alignment slack
+    static constexpr int A_BOXES = AKM ? TM_BK / 16 : BM / 16, B_BOXES = BN / 16;
+    static constexpr int A_BOX_BYTES = AKM ? BM * 128 : TM_BK * 128;
+    // byte offsets of A(r, k) / B(k, n) in a stage (128-byte swizzle: chunk c of line l at c ^ (l & 7))
+    __device__ __forceinline__ static uint32_t a_off(int r, int k) {
+        if (AKM)
+            return static_cast<uint32_t>((k >> 4) * A_BOX_BYTES + r * 128 + ((((k & 15) >> 1) ^ (r & 7)) << 4) +
+                                         ((k & 1) << 3));
+        return static_cast<uint32_t>((r >> 4) * A_BOX_BYTES + k * 128 + ((((r & 15) >> 1) ^ (k & 7)) << 4) +
+                                     ((r & 1) << 3));
+    }
+    __device__ __forceinline__ static uint32_t b_off(int k, int n) {
+        return static_cast<uint32_t>(A_BYTES + (n >> 4) * (TM_BK * 128) + k * 128 + ((((n & 15) >> 1) ^ (k & 7)) << 4) +
+                                     ((n & 1) << 3));
+    }
+};
+
+// The TMA-fed DGEMM (A·G, the LU's long trailing updates, A·H, Q^T A): per stage one thread issues
+// the 2-D tensor copies (cp.async.bulk.tensor, SASS UTMALDG) of both operand tiles, 16 doubles =
+// one 128-byte swizzle span per box, completing on one mbarrier per stage (expect_tx = the
+// stage's bytes, zero-filled edges included). The fragment reads apply the swizzle's XOR (the
+// K-major A operand at the minimum two wavefronts, the N- / M-major ones at four: DMMA, not shared
+// memory, bounds the loop). The threads issue only fragment loads and DMMAs. Split-K over
+// blockIdx.z: slice z covers [z kchunk, (z+1) kchunk) (kchunk a multiple of 32) and writes its own
+// C panel (C + z cstride). Same tile and k order as k_dgemm: bit-identical results.
+template <int BM, int BN, int WM, int WN, bool AKM, int MINB>
+__global__ void __launch_bounds__(WM* WN * 32, MINB)
+    k_dgemm_tm(uint64_t M, uint64_t N, uint64_t K, double alpha, const __grid_constant__ CUtensorMap tmA,
+               const __grid_constant__ CUtensorMap tmB, double beta, double* __restrict__ C, uint64_t ldc,
+               uint64_t kchunk, uint64_t cstride) {
+    using T = TmCfg<BM, BN, WM, WN, AKM>;
     extern __shared__ __align__(16) unsigned char smem_tm[];
     __shared__ __align__(8) uint64_t full[TM_NSTAGE];
-    constexpr int WN = 2, WTM = 32, WTN = 32, MF = 4, NF = 4;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int g = lane >> 2, t = lane & 3;
-    const uint64_t m0 = static_cast<uint64_t>(blockIdx.y) * TM_BM, n0 = static_cast<uint64_t>(blockIdx.x) * TM_BN;
-    const int ktiles = static_cast<int>(K / TM_BK);
-    // 1024-byte aligned stage base (the 128-byte swizzle pattern repeats every 8 lines)
+    const int ntn = static_cast<int>((N + BN - 1) / BN);
+    const int ntiles = ntn * static_cast<int>((M + BM - 1) / BM);
+    uint64_t kz0 = 0, kz = K;
+    if (gridDim.z > 1) {
+        kz0 = blockIdx.z * kchunk;
+        kz = kz0 < K ? (K - kz0 < kchunk ? K - kz0 : kchunk) : 0;
+        C += blockIdx.z * cstride;
+    }
+    const int ktiles = static_cast<int>((kz + TM_BK - 1) / TM_BK);
     const uint32_t base = (s_addr(smem_tm) + 1023u) & ~1023u;
     unsigned char* gbase = smem_tm + (base - s_addr(smem_tm));
     if (tid == 0) {
@@ -265,80 +295,105 @@ __global__ void __launch_bounds__(256, 2)
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     }
     __syncthreads();
-    auto issue = [&](int s2, int kt) { // thread 0
+    auto issue = [&](int s2, int kt, int m0, int n0) { // thread 0
         const uint32_t mb = s_addr(&full[s2]);
-        const uint32_t st = base + static_cast<uint32_t>(s2 * TM_STAGE);
-        const int k0 = kt * TM_BK;
+        const uint32_t st = base + static_cast<uint32_t>(s2 * T::STAGE);
+        const int k0 = static_cast<int>(kz0) + kt * TM_BK;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(TM_STAGE) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(T::STAGE) : "memory");
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < T::A_BOXES; ++q) {
+            const int c0 = AKM ? k0 + 16 * q : m0 + 16 * q, c1 = AKM ? m0 : k0;
             asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                         ::"r"(st + q * TM_BM * 128), "l"(&tmA), "r"(k0 + 16 * q), "r"(static_cast<int>(m0)), "r"(mb)
+                         ::"r"(st + q * T::A_BOX_BYTES), "l"(&tmA), "r"(c0), "r"(c1), "r"(mb)
                          : "memory");
+        }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < T::B_BOXES; ++q)
             asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                         ::"r"(st + TM_A_BYTES + q * TM_BK * 128), "l"(&tmB), "r"(static_cast<int>(n0) + 16 * q), "r"(k0),
-                           "r"(mb)
+                         ::"r"(st + T::A_BYTES + q * TM_BK * 128), "l"(&tmB), "r"(n0 + 16 * q), "r"(k0), "r"(mb)
                          : "memory");
     };
-    double acc[MF][NF][2];
-#pragma unroll
-    for (int i = 0; i < MF; ++i)
-#pragma unroll
-        for (int j = 0; j < NF; ++j)
-            acc[i][j][0] = acc[i][j][1] = 0.0;
-    if (tid == 0)
+    // Tiles: one per CTA, or a persistent loop when the grid was capped (the LU's trailing update
+    // leaves SMs to the panel path). `it0` counts the k-tiles this CTA consumed: stage it % 2,
+    // parity (it / 2) & 1 across tiles. The next tile's first stages are issued before the
+    // epilogue: those stages were last read two k-tiles back, before the last loop barrier.
+    int tile = static_cast<int>(blockIdx.x);
+    if (tid == 0 && tile < ntiles)
         for (int s2 = 0; s2 < TM_NSTAGE - 1 && s2 < ktiles; ++s2)
-            issue(s2, s2);
-    for (int kt = 0; kt < ktiles; ++kt) {
-        const int s2 = kt % TM_NSTAGE;
-        {
-            const uint32_t mb = s_addr(&full[s2]), par = static_cast<uint32_t>((kt / TM_NSTAGE) & 1);
-            uint32_t done = 0;
-            while (!done)
-                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                             " selp.u32 %0, 1, 0, p;\n}"
-                             : "=r"(done)
-                             : "r"(mb), "r"(par)
-                             : "memory");
-        }
-        __syncthreads(); // every warp is done with the stage refilled next (read at kt - 1)
-        const int nk = kt + TM_NSTAGE - 1;
-        if (tid == 0 && nk < ktiles)
-            issue(nk % TM_NSTAGE, nk);
-        const unsigned char* st = gbase + s2 * TM_STAGE;
+            issue(s2, s2, (tile / ntn) * BM, (tile % ntn) * BN);
+    int it0 = 0;
+    for (; tile < ntiles; tile += static_cast<int>(gridDim.x)) {
+        const int m0 = (tile / ntn) * BM, n0 = (tile % ntn) * BN;
+        double acc[T::MF][T::NF][2];
 #pragma unroll
-        for (int kk = 0; kk < TM_BK; kk += 4) {
-            double af[MF], bf[NF];
+        for (int i = 0; i < T::MF; ++i)
 #pragma unroll
-            for (int i = 0; i < MF; ++i)
-                af[i] = *reinterpret_cast<const double*>(st + tm_a_off(wm * WTM + i * 8 + g, kk + t));
-#pragma unroll
-            for (int j = 0; j < NF; ++j)
-                bf[j] = *reinterpret_cast<const double*>(st + tm_b_off(kk + t, wn * WTN + j * 8 + g));
-#pragma unroll
-            for (int i = 0; i < MF; ++i)
-#pragma unroll
-                for (int j = 0; j < NF; ++j)
-                    dmma(acc[i][j], af[i], bf[j]);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < MF; ++i) {
-        const uint64_t row = m0 + wm * WTM + i * 8 + g;
-#pragma unroll
-        for (int j = 0; j < NF; ++j) {
-            const uint64_t col = n0 + wn * WTN + j * 8 + 2 * t;
-            double* cp = C + row * ldc + col;
-            double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
-            if (beta != 0.0) {
-                const double2 o = *reinterpret_cast<const double2*>(cp);
-                v0 = fma(beta, o.x, v0);
-                v1 = fma(beta, o.y, v1);
+            for (int j = 0; j < T::NF; ++j)
+                acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kt = 0; kt < ktiles; ++kt) {
+            const int it = it0 + kt, s2 = it % TM_NSTAGE;
+            {
+                const uint32_t mb = s_addr(&full[s2]), par = static_cast<uint32_t>((it / TM_NSTAGE) & 1);
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                                 " selp.u32 %0, 1, 0, p;\n}"
+                                 : "=r"(done)
+                                 : "r"(mb), "r"(par)
+                                 : "memory");
             }
-            *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+            __syncthreads(); // every warp is done with the stage refilled next (read at it - 1)
+            const int nk = kt + TM_NSTAGE - 1;
+            if (tid == 0 && nk < ktiles)
+                issue((it0 + nk) % TM_NSTAGE, nk, m0, n0);
+            const unsigned char* st = gbase + s2 * T::STAGE;
+#pragma unroll
+            for (int kk = 0; kk < TM_BK; kk += 4) {
+                double af[T::MF], bf[T::NF];
+#pragma unroll
+                for (int i = 0; i < T::MF; ++i)
+                    af[i] = *reinterpret_cast<const double*>(st + T::a_off(wm * T::WTM + i * 8 + g, kk + t));
+#pragma unroll
+                for (int j = 0; j < T::NF; ++j)
+                    bf[j] = *reinterpret_cast<const double*>(st + T::b_off(kk + t, wn * T::WTN + j * 8 + g));
+#pragma unroll
+                for (int i = 0; i < T::MF; ++i)
+#pragma unroll
+                    for (int j = 0; j < T::NF; ++j)
+                        dmma(acc[i][j], af[i], bf[j]);
+            }
+        }
+        it0 += ktiles;
+        const int next = tile + static_cast<int>(gridDim.x);
+        if (tid == 0 && next < ntiles)
+            for (int s2 = 0; s2 < TM_NSTAGE - 1 && s2 < ktiles; ++s2)
+                issue((it0 + s2) % TM_NSTAGE, s2, (next / ntn) * BM, (next % ntn) * BN);
+#pragma unroll
+        for (int i = 0; i < T::MF; ++i) {
+            const uint64_t row = static_cast<uint64_t>(m0) + wm * T::WTM + i * 8 + g;
+            if (row >= M)
+                continue;
+#pragma unroll
+            for (int j = 0; j < T::NF; ++j) {
+                const uint64_t col = static_cast<uint64_t>(n0) + wn * T::WTN + j * 8 + 2 * t;
+                if (col >= N)
+                    continue;
+                double* cp = C + row * ldc + col;
+                double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+                if (col + 1 < N) {
+                    if (beta != 0.0) {
+                        const double2 o = *reinterpret_cast<const double2*>(cp);
+                        v0 = fma(beta, o.x, v0);
+                        v1 = fma(beta, o.y, v1);
+                    }
+                    *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+                } else {
+                    if (beta != 0.0)
+                        v0 = fma(beta, cp[0], v0);
+                    cp[0] = v0;
+                }
+            }
         }
     }
 }
@@ -369,21 +424,30 @@ bool make_tmap(CUtensorMap* tm, const double* base, uint64_t rows, uint64_t cols
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// true when the TMA kernel took the product
-bool launch_tmap(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda, const double* B,
-                 uint64_t ldb, double beta, double* C, uint64_t ldc) {
+// true when the TMA kernel took the product. op(A): M x K, K-major (row-major M x K, ld lda) or
+// M-major (A stored K x M, ld lda); B: K x N row-major (ld ldb).
+template <int BM, int BN, int WM, int WN, bool AKM, int MINB>
+bool launch_tm(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda, const double* B,
+               uint64_t ldb, double beta, double* C, uint64_t ldc, const Split& sp) {
+    using T = TmCfg<BM, BN, WM, WN, AKM>;
     CUtensorMap ta, tb;
-    if (!make_tmap(&ta, A, M, K, lda, TM_BM) || !make_tmap(&tb, B, K, N, ldb, TM_BK))
+    const bool ok = AKM ? make_tmap(&ta, A, M, K, lda, BM) : make_tmap(&ta, A, K, M, lda, TM_BK);
+    if (!ok || !make_tmap(&tb, B, K, N, ldb, TM_BK))
         return false;
+    auto kern = k_dgemm_tm<BM, BN, WM, WN, AKM, MINB>;
     static bool configured[16] = {};
     const int dev = ctx().device & 15;
     if (!configured[dev]) {
-        RL_CUDA(cudaFuncSetAttribute(k_dgemm_tmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(TM_SMEM)));
+        RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM)));
         configured[dev] = true;
     }
-    dim3 grid(cdiv(N, TM_BN), cdiv(M, TM_BM), 1);
-    k_dgemm_tmap<<<grid, 256, TM_SMEM, stream()>>>(M, N, K, alpha, ta, tb, beta, C, ldc);
+    // one CTA per tile; ctx().gemm_cta_cap > 0 caps the grid (persistent tile loop)
+    uint64_t tiles = static_cast<uint64_t>(cdiv(N, BN)) * cdiv(M, BM);
+    const int cap = ctx().gemm_cta_cap;
+    if (cap > 0 && tiles > static_cast<uint64_t>(cap))
+        tiles = static_cast<uint64_t>(cap);
+    dim3 grid(static_cast<unsigned>(tiles), 1, sp.splits);
+    kern<<<grid, T::NT, T::SMEM, stream()>>>(M, N, K, alpha, ta, tb, beta, C, ldc, sp.kchunk, sp.cstride);
     RL_LAUNCHED();
     return true;
 }
@@ -430,10 +494,21 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t Kfull, double alpha, const 
     // Gram Y^T Y: both)
     if (M > 64 && M <= 72 && N > 64 && N <= 72)
         return launch<72, 72, 3, 3, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
-    if (N > 64 && N <= 72)
+    // the range finder's skinny products: TMA-fed 128 x 80 (A H) / 80 x 128 (Q^T A) tiles, the
+    // column / row edge past 72 zero-filled by the copy engine (split-K slices of 32-multiples)
+    static const bool no_tma_rf = getenv("RL_GEMM_NO_TMA") != nullptr;
+    const bool tm_ok = !no_tma_rf && VEC == 2 && !BKM && (sp.splits == 1 || sp.kchunk % 32 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+    if (N > 64 && N <= 72) {
+        if (AK && tm_ok && launch_tm<128, 80, 4, 2, true, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp))
+            return;
         return launch<128, 72, 4, 3, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
-    if (M > 64 && M <= 72)
+    }
+    if (M > 64 && M <= 72) {
+        if (!AK && tm_ok && launch_tm<80, 128, 2, 4, false, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp))
+            return;
         return launch<72, 128, 3, 4, AK, BKM, VEC, 3, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
+    }
     if (N > 64 && z * cdiv(M, 128) * cdiv(N, 64) >= 2ULL * sms && K >= kLongK) {
         // two CTAs per SM (128x64 tiles, <= 128 regs): one CTA's prologue / C epilogue
         // overlaps the other's DMMA loop.  Long K: K-tile 32 in 2 stages (217 KB for the two
@@ -441,12 +516,12 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t Kfull, double alpha, const 
         // (DMMA pipe 89.5 -> 91.3% active).  (Feeding the padded tiles with per-row TMA bulk
         // copies, 160 x 256-512 B per stage from one warp, measured 48.7 ms: the copy engine
         // is not built for that many small transfers.)  Full tiles of A K-major x B N-major go
-        // through 2-D tensor copies with the 128-byte swizzle instead (k_dgemm_tmap);
+        // through 2-D tensor copies with the 128-byte swizzle instead (k_dgemm_tm);
         // RL_GEMM_NO_TMA=1 keeps the cp.async ring.
         static const bool no_tma = getenv("RL_GEMM_NO_TMA") != nullptr;
         if (AK && !BKM && VEC == 2 && sp.splits == 1 && !no_tma && M % 128 == 0 && N % 64 == 0 && Kfull % 32 == 0 &&
             ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
-            launch_tmap(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc))
+            launch_tm<128, 64, 4, 2, true, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp))
             return;
         launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     }

@@ -779,6 +779,7 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         }
         RL_CUDA(cudaEventRecord(E_panel, s2));
     };
+    static const int reserve = std::getenv("RL_LU_RESERVE") ? std::atoi(std::getenv("RL_LU_RESERVE")) : 0;
     // RL_LU_TRACE=1: per outer step, time of the panel path (s2) and of the step on s1 (dev)
     static const bool trace = std::getenv("RL_LU_TRACE") != nullptr;
     std::vector<cudaEvent_t> tev;
@@ -811,8 +812,10 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         mark(s2);
         panelW(p);
         mark(s2);
-        // the remaining trailing update runs under the next panel
+        // the remaining trailing update runs under the next panel, on all but `reserve` SMs
+        ctx().gemm_cta_cap = reserve > 0 ? 2 * (ctx().sms - reserve) : 0;
         upd(s1, rest - w2n, rest - w2n, W, at(p + w2n, o), at(o, p + w2n), at(p + w2n, p + w2n));
+        ctx().gemm_cta_cap = 0;
         mark(s1);
     }
     RL_CUDA(cudaStreamWaitEvent(s1, E_panel, 0));

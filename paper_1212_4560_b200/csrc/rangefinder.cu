@@ -156,8 +156,12 @@ __device__ __forceinline__ void chol_diag8(double* W, int P, int c0, double* rdi
     if (lane == 0 && !ok)
         *s_bad = 1;
 }
-__global__ void __launch_bounds__(CH_T) k_chol_inv(int k, double* g, const double* shift_part, int nshift,
-                                                   double shift_coef, double* rinv, int* bad) {
+// G (k x k, read-only) -> R (upper) and R^-1 in shared memory; writes rinv and the accumulated
+// factor racc_out = R (racc_in null) or R racc_in (both upper triangular: CholeskyQR3's
+// R_acc = R_pass R_acc, rows over warps, columns over lanes, ascending l).
+__global__ void __launch_bounds__(CH_T) k_chol_inv(int k, const double* g, const double* shift_part, int nshift,
+                                                   double shift_coef, double* rinv, const double* racc_in,
+                                                   double* racc_out, int* bad) {
     extern __shared__ double W[]; // KP x (KP + 1)
     __shared__ double rdiag[KMAX];
     __shared__ double T[8][KMAX + 1]; // T[c][l] = (R_0:J,J X_JJ)[l][c]; padded: 8 c's hit 8 banks
@@ -288,9 +292,22 @@ __global__ void __launch_bounds__(CH_T) k_chol_inv(int k, double* g, const doubl
     }
     for (int e = tid; e < k * k; e += CH_T) {
         const int i = e / k, l = e - i * k;
-        g[e] = (l >= i) ? W[i * P + l] : 0.0;
         rinv[e] = (l > i) ? W[l * P + i] : (l == i ? rdiag[i] : 0.0);
+        if (!racc_in)
+            racc_out[e] = (l >= i) ? W[i * P + l] : 0.0;
     }
+    if (racc_in)
+        for (int i = warp; i < k; i += CH_T / 32)
+            for (int j = lane; j < k; j += 32) {
+                double v = 0.0;
+                if (j >= i) {
+                    const double* wi = W + i * P;
+#pragma unroll 4
+                    for (int l = i; l <= j; ++l)
+                        v = fma(wi[l], racc_in[static_cast<size_t>(l) * k + j], v);
+                }
+                racc_out[static_cast<size_t>(i) * k + j] = v;
+            }
 }
 
 // Singular values of a k x k matrix (row-major, ld k, k <= 128) by one-sided Jacobi on the
@@ -754,7 +771,8 @@ void gemm_splitk(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double al
         gemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
         return;
     }
-    const uint64_t chunk = ((k + splits - 1) / splits + 15) / 16 * 16;
+    // slices of a multiple of 32 (the TMA kernel's k-tile) so no slice's last tile reaches into the next
+    const uint64_t chunk = ((k + splits - 1) / splits + 31) / 32 * 32;
     const int used = static_cast<int>(cdiv(k, chunk));
     double* parts = ws<double>(WS_RF6, static_cast<uint64_t>(used) * m * n);
     gemm_splitk_parts(ta, tb, m, n, k, a, lda, b, ldb, parts, used, chunk);
@@ -915,12 +933,12 @@ void rank_bracket_launch(int k, const double* d_r, int* d_flag) {
 // diag(r) > 0. Per pass: the Gram (split-K GEMM), k_chol_inv (R and R^-1), Q = src R^-1 on DMMA
 // and R_acc = R_pass R_acc. No host round trip: the shift is summed on the device and the failure
 // flag d_bad (int, device) is sticky — the caller reads it whenever it next synchronises.
-void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad) {
+void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad, bool want_q) {
     if (k > KMAX)
         fail(RL_TOO_LARGE, "qr_positive: more than 128 columns");
     double* g = ws<double>(WS_RF4, 3 * KMAX * KMAX + 64);
-    double* rp = g + KMAX * KMAX;
-    double* racc = rp + KMAX * KMAX;
+    double* racc0 = g + KMAX * KMAX; // R_acc ping-pong (the last pass writes r)
+    double* racc1 = racc0 + KMAX * KMAX;
     double* tmpq = ws<double>(WS_RF5, m * k + KMAX * KMAX + KMAX + 1);
     const int sp = splits_for(k, k, m);
     chol_attrs();
@@ -935,31 +953,29 @@ void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int
     const double coef = 11.0 * (static_cast<double>(m) * k + static_cast<double>(k) * (k + 1)) * u;
     const double* src = y;
     double* rinv = tmpq + m * k; // k x k after the pass-1 Q buffer
+    const double* racc_in = nullptr;
     for (int pass = 0; pass < 3; ++pass) {
         // G = src^T src
         gemm_splitk(true, false, k, k, m, 1.0, src, k, src, k, 0.0, g, k, sp);
-        copy2d_dev(k, k, g, k, rp, k);
-        k_chol_inv<<<1, CH_T, chol_smem, stream()>>>(k, rp, pass == 0 ? part : nullptr, kParts, coef, rinv, d_bad);
+        // R_pass, R_pass^-1 and R_acc = R_pass R_acc in one kernel
+        double* racc_out = pass == 2 ? r : (pass == 0 ? racc0 : racc1);
+        k_chol_inv<<<1, CH_T, chol_smem, stream()>>>(k, g, pass == 0 ? part : nullptr, kParts, coef, rinv, racc_in,
+                                                     racc_out, d_bad);
         RL_LAUNCHED();
-        // Q_pass = src R_pass^-1 on DMMA
+        racc_in = racc_out;
+        // Q_pass = src R_pass^-1 on DMMA (the last pass only when the caller wants Q)
+        if (pass == 2 && !want_q)
+            break;
         double* dst = (pass == 1) ? tmpq : q;
         gemm(false, false, m, k, k, 1.0, src, k, rinv, k, 0.0, dst, k);
-        // R_acc = R_pass R_acc
-        if (pass == 0)
-            copy2d_dev(k, k, rp, k, racc, k);
-        else {
-            gemm(false, false, k, k, k, 1.0, rp, k, racc, k, 0.0, g, k);
-            copy2d_dev(k, k, g, k, racc, k);
-        }
         src = dst;
     }
-    copy2d_dev(k, k, racc, k, r, k);
 }
 
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r) {
     int* d_bad = ws<int>(WS_FLAGS, 4);
     RL_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), stream()));
-    cholqr3_async(m, k, y, q, r, d_bad);
+    cholqr3_async(m, k, y, q, r, d_bad, true);
     int bad = 0;
     RL_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, stream()));
     RL_CUDA(cudaStreamSynchronize(stream()));

@@ -211,12 +211,12 @@ __global__ void k_gen_small(uint64_t eseed, uint64_t nout, GenParams p) {
 // (cta_twist_oop): 65 twist blocks in a row, where one warp per sequence was latency-bound.
 constexpr int kSeqThreads = 320;
 __device__ __forceinline__ void cta_twist_oop(const uint64_t* src, uint64_t* dst, int t);
-__device__ __forceinline__ void cta_sequence(uint64_t (*wb)[kN], uint64_t* seq, int t) {
+__device__ __forceinline__ void cta_sequence(uint64_t (*wb)[kN], uint64_t* seq, int t, int words = kSeqWords) {
     int cur = 0;
-    for (int base = 0; base < kSeqWords; base += kN) {
-        if (t < kN && base + t < kSeqWords)
+    for (int base = 0; base < words; base += kN) {
+        if (t < kN && base + t < words)
             seq[base + t] = wb[cur][t];
-        if (base + kN < kSeqWords)
+        if (base + kN < words)
             cta_twist_oop(wb[cur], wb[cur ^ 1], t);
         cur ^= 1;
     }
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kSeqThreads) k_base_sequence(uint64_t eseed, u
     if (t < 32)
         warp_seed_window(wb[0], eseed, t);
     __syncthreads();
-    cta_sequence(wb, seq, t);
+    cta_sequence(wb, seq, t, kSeqWords + 8); // + 8: from x_8 it is also level-1 window 0's sequence
 }
 __global__ void __launch_bounds__(kSeqThreads) k_window_sequence(const uint64_t* windows, uint64_t* seqs) {
     __shared__ uint64_t wb[2][kN];
@@ -638,18 +638,24 @@ void rng_generate_at(uint64_t seed, uint64_t sid, Draw kind, uint64_t offset, ui
                                      static_cast<int>(kJumpSmem)));
         attr_set[ctx().device & 15] = true;
     }
-    uint64_t* base = ws<uint64_t>(WS_RNG, kSeqWords + nl1 * kN + nl1 * kSeqWords);
-    uint64_t* l1w = base + kSeqWords;
+    uint64_t* base = ws<uint64_t>(WS_RNG, kSeqWords + 8 + nl1 * kN + nl1 * kSeqWords);
+    uint64_t* l1w = base + kSeqWords + 8;
     uint64_t* l1s = l1w + nl1 * kN;
     uint64_t* cw = ws<uint64_t>(WS_RNG2, nchunks * kN);
     k_base_sequence<<<1, kSeqThreads, 0, st>>>(eseed, base);
     RL_LAUNCHED();
-    k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(jt.d_l1, 1ULL << 40, base, true, a_first, 1,
-                                                                        a_first, static_cast<int>(nl1), 1, l1w,
-                                                                        nullptr);
-    RL_LAUNCHED();
-    k_window_sequence<<<static_cast<unsigned>(nl1), kSeqThreads, 0, st>>>(l1w, l1s);
-    RL_LAUNCHED();
+    if (a_first == 0 && nl1 == 1) {
+        // level-1 window 0 is the state at stream position 8, x_8 .. x_319: its word sequence
+        // is the base sequence from x_8 (no level-1 jump, no second sequence)
+        l1s = base + 8;
+    } else {
+        k_jump<<<static_cast<unsigned>(nl1), kJumpThreads, kJumpSmem, st>>>(jt.d_l1, 1ULL << 40, base, true, a_first,
+                                                                            1, a_first, static_cast<int>(nl1), 1, l1w,
+                                                                            nullptr);
+        RL_LAUNCHED();
+        k_window_sequence<<<static_cast<unsigned>(nl1), kSeqThreads, 0, st>>>(l1w, l1s);
+        RL_LAUNCHED();
+    }
     // level-2 jumps for every stride-th chunk, the others by twisting forward.  A draw of at
     // most one wave of chunks jumps to every chunk (the jumps run side by side; forward
     // twisting would add a serial 7-chunk walk).
