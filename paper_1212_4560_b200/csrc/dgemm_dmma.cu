@@ -230,11 +230,11 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
 __device__ __forceinline__ uint32_t s_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-constexpr int TM_BK = 32, TM_NSTAGE = 2;
+constexpr int TM_BK = 32;
 // Tile geometry of the TMA kernel: BM x BN output tile, K-tile 32, WM x WN warps. A is K-major
 // (boxes BM x 16 along k: A·G, A·H) or M-major (boxes 32 x 16 along m: Q^T A); B is N-major
 // (boxes 32 x 16 along n). Box edges past M / N / K are zero-filled by the copy engine.
-template <int BM, int BN, int WM, int WN, bool AKM>
+template <int BM, int BN, int WM, int WN, bool AKM, int TM_NSTAGE>
 struct TmCfg {
     static constexpr int NT = WM * WN * 32;
     static constexpr int WTM = BM / WM, WTN = BN / WN, MF = WTM / 8, NF = WTN / 8;
@@ -265,12 +265,12 @@ struct TmCfg {
 // memory, bounds the loop). The threads issue only fragment loads and DMMAs. Split-K over
 // blockIdx.z: slice z covers [z kchunk, (z+1) kchunk) (kchunk a multiple of 32) and writes its own
 // C panel (C + z cstride). Same tile and k order as k_dgemm: bit-identical results.
-template <int BM, int BN, int WM, int WN, bool AKM, int MINB>
+template <int BM, int BN, int WM, int WN, bool AKM, int MINB, int TM_NSTAGE>
 __global__ void __launch_bounds__(WM* WN * 32, MINB)
     k_dgemm_tm(uint64_t M, uint64_t N, uint64_t K, double alpha, const __grid_constant__ CUtensorMap tmA,
                const __grid_constant__ CUtensorMap tmB, double beta, double* __restrict__ C, uint64_t ldc,
                uint64_t kchunk, uint64_t cstride) {
-    using T = TmCfg<BM, BN, WM, WN, AKM>;
+    using T = TmCfg<BM, BN, WM, WN, AKM, TM_NSTAGE>;
     extern __shared__ __align__(16) unsigned char smem_tm[];
     __shared__ __align__(8) uint64_t full[TM_NSTAGE];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -426,26 +426,23 @@ bool make_tmap(CUtensorMap* tm, const double* base, uint64_t rows, uint64_t cols
 
 // true when the TMA kernel took the product. op(A): M x K, K-major (row-major M x K, ld lda) or
 // M-major (A stored K x M, ld lda); B: K x N row-major (ld ldb).
-template <int BM, int BN, int WM, int WN, bool AKM, int MINB>
+template <int BM, int BN, int WM, int WN, bool AKM, int MINB, int NST = 2>
 bool launch_tm(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda, const double* B,
                uint64_t ldb, double beta, double* C, uint64_t ldc, const Split& sp) {
-    using T = TmCfg<BM, BN, WM, WN, AKM>;
+    using T = TmCfg<BM, BN, WM, WN, AKM, NST>;
     CUtensorMap ta, tb;
     const bool ok = AKM ? make_tmap(&ta, A, M, K, lda, BM) : make_tmap(&ta, A, K, M, lda, TM_BK);
     if (!ok || !make_tmap(&tb, B, K, N, ldb, TM_BK))
         return false;
-    auto kern = k_dgemm_tm<BM, BN, WM, WN, AKM, MINB>;
+    auto kern = k_dgemm_tm<BM, BN, WM, WN, AKM, MINB, NST>;
     static bool configured[16] = {};
     const int dev = ctx().device & 15;
     if (!configured[dev]) {
         RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM)));
         configured[dev] = true;
     }
-    // one CTA per tile; ctx().gemm_cta_cap > 0 caps the grid (persistent tile loop)
-    uint64_t tiles = static_cast<uint64_t>(cdiv(N, BN)) * cdiv(M, BM);
-    const int cap = ctx().gemm_cta_cap;
-    if (cap > 0 && tiles > static_cast<uint64_t>(cap))
-        tiles = static_cast<uint64_t>(cap);
+    // one CTA per tile (the kernel's tile loop also serves grids capped below the tile count)
+    const uint64_t tiles = static_cast<uint64_t>(cdiv(N, BN)) * cdiv(M, BM);
     dim3 grid(static_cast<unsigned>(tiles), 1, sp.splits);
     kern<<<grid, T::NT, T::SMEM, stream()>>>(M, N, K, alpha, ta, tb, beta, C, ldc, sp.kchunk, sp.cstride);
     RL_LAUNCHED();
@@ -519,9 +516,10 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t Kfull, double alpha, const 
         // through 2-D tensor copies with the 128-byte swizzle instead (k_dgemm_tm);
         // RL_GEMM_NO_TMA=1 keeps the cp.async ring.
         static const bool no_tma = getenv("RL_GEMM_NO_TMA") != nullptr;
-        if (AK && !BKM && VEC == 2 && sp.splits == 1 && !no_tma && M % 128 == 0 && N % 64 == 0 && Kfull % 32 == 0 &&
-            ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
-            launch_tm<128, 64, 4, 2, true, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp))
+        const bool tm_full = AK && !BKM && VEC == 2 && sp.splits == 1 && !no_tma && M % 128 == 0 && N % 64 == 0 &&
+                             Kfull % 32 == 0 &&
+                             ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+        if (tm_full && launch_tm<128, 64, 4, 2, true, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp))
             return;
         launch<128, 64, 4, 2, AK, BKM, VEC, 2, 2, 32>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp);
     }

@@ -77,6 +77,15 @@ __device__ __forceinline__ unsigned long long gtimer0() {
     return v;
 }
 #endif
+// RL_LU_TIMELINE=1 (dev aid): %globaltimer of every panel kernel's first start and last end,
+// per 128-step: [diag start, diag end, trsm first start, trsm last end]
+__device__ int g_tl_on;
+__device__ unsigned long long g_tl[64][4];
+__device__ __forceinline__ unsigned long long tl_now() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
 __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t lda, uint64_t n, uint64_t o,
                                                            double floor, double* pivots,
                                                            unsigned long long* breakdown) {
@@ -88,6 +97,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
 #ifdef RL_PANEL_TRACE
     int tsi = 0;
 #endif
+    if (g_tl_on && tid == 0 && o / NB < 64)
+        g_tl[o / NB][0] = tl_now();
     RL_TS_DIAG();
     panel::load_tile_async<NB, NB, PK_THREADS>(W, PT, blk, lda, bs, bs, [](int, int) { return true; });
     panel::cp_async_wait_all();
@@ -198,6 +209,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
     if (tid == 0)
         g_diag_ts[63] = tsi;
 #endif
+    if (g_tl_on && tid == 0 && o / NB < 64)
+        g_tl[o / NB][1] = tl_now();
     if (tid < bs) { // |pivots| and the first step below the floor (genp.cpp:24-26)
         pivots[o + tid] = pabs[tid];
         if (pabs[tid] < floor)
@@ -235,6 +248,8 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
     const bool right = static_cast<int>(blockIdx.x) < nrb;
     const double* diag = a + o * lda + o;
+    if (g_tl_on && tid == 0 && o / NB < 64)
+        atomicMin(&g_tl[o / NB][2], tl_now());
 #ifdef RL_PANEL_TRACE
     const bool tr = (blockIdx.x == 0 || static_cast<int>(blockIdx.x) == nrb) && tid == 0;
     unsigned long long* tsb = g_trsm_ts[right ? 0 : 1];
@@ -350,6 +365,8 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_panel_trsm(double* a, uint64_
                     base[static_cast<uint64_t>(8 * f + 2 * q + e) * lda + row] = x[f][e];
         }
     }
+    if (g_tl_on && tid == 0 && o / NB < 64)
+        atomicMax(&g_tl[o / NB][3], tl_now());
 }
 
 __global__ void k_copy2d(uint64_t rows, uint64_t cols, const double* src, uint64_t lds, double* dst,
@@ -641,8 +658,8 @@ void prep_attrs() {
 
 // Per-thread helper stream (high priority) and events for the panel lookahead.
 struct Lookahead {
-    cudaStream_t s2 = nullptr, s3 = nullptr;
-    cudaEvent_t ev[6] = {};
+    cudaStream_t s2 = nullptr, s3 = nullptr, s4 = nullptr;
+    cudaEvent_t ev[8] = {};
     int device = -1;
 };
 
@@ -653,6 +670,7 @@ Lookahead& lookahead() {
         RL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         RL_CUDA(cudaStreamCreateWithPriority(&la.s2, cudaStreamNonBlocking, hi));
         RL_CUDA(cudaStreamCreateWithPriority(&la.s3, cudaStreamNonBlocking, hi));
+        RL_CUDA(cudaStreamCreateWithPriority(&la.s4, cudaStreamNonBlocking, hi));
         for (auto& e : la.ev)
             RL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         la.device = ctx().device;
@@ -727,8 +745,9 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
     prep_attrs();
     cudaStream_t s1 = stream();
     Lookahead& la = lookahead();
-    cudaStream_t s2 = la.s2, s3 = la.s3;
-    cudaEvent_t E_nd = la.ev[0], E_strips = la.ev[1], E_panel = la.ev[2], E_t1 = la.ev[3], E_s3 = la.ev[4];
+    cudaStream_t s2 = la.s2, s3 = la.s3, s4 = la.s4;
+    cudaEvent_t E_nd = la.ev[0], E_strips = la.ev[1], E_panel = la.ev[2], E_t1 = la.ev[3], E_s3 = la.ev[4],
+                E_s4 = la.ev[5];
     auto at = [&](uint64_t i, uint64_t j) { return a + i * lda + j; };
     const cudaStream_t keep = ctx().stream;
     const uint64_t W = static_cast<uint64_t>(kOuterSteps) * NB; // outer block
@@ -753,33 +772,58 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         }
     };
     // outer panel [o, o + W) on s2 as W / 128 steps: waits E_nd before its first diag LU and
-    // E_strips before its first TRSMs.  After step i (K = 128 from its L and U): the next
-    // step's own 128 x 128 block on s2 (its LU starts next), and on s3 the rest of the panel's
-    // columns (rows below) and the rest of the panel's rows (columns right, up to n), which
-    // the next step's TRSMs wait for.  Rows and columns beyond the panel get their update
-    // later with K = W (the trailing update of the outer step).
+    // E_strips before its first TRSMs.  After step i (K = 128 from its L and U), the rows and
+    // columns of the panel's remaining steps are brought up to date in two parts:
+    //   urgent (s3, the next TRSMs wait for it): the next step's column strip below its block
+    //     and its block row to the right (up to n);
+    //   the rest (s4, beside the next diag LU and TRSMs): the panel's later columns below the
+    //     next block and the panel's later rows right of the panel.  The next step's own-block
+    //     update and urgent strips wait for it (they update the same entries after it).
+    // The next step's own 128 x 128 block is updated on s2 (its LU starts next).  Rows and
+    // columns beyond the panel get their update later with K = W (the trailing update).
     auto panelW = [&](uint64_t o) {
         const uint64_t oe = std::min<uint64_t>(o + W, n);
         RL_CUDA(cudaStreamWaitEvent(s2, E_nd, 0));
         diag(o, s2);
         RL_CUDA(cudaStreamWaitEvent(s2, E_strips, 0));
         trsm(o, s2);
+        bool s4_pending = false;
         for (uint64_t oi = o; oi + NB < oe; oi += NB) {
-            const uint64_t on = oi + NB, wn = std::min<uint64_t>(NB, oe - on);
+            const uint64_t on = oi + NB, wn = std::min<uint64_t>(NB, oe - on), nx = on + wn;
             RL_CUDA(cudaEventRecord(E_t1, s2));
             RL_CUDA(cudaStreamWaitEvent(s3, E_t1, 0));
-            upd(s2, wn, wn, NB, at(on, oi), at(oi, on), at(on, on));                           // own block
-            upd(s3, n - on - wn, oe - on, NB, at(on + wn, oi), at(oi, on), at(on + wn, on));   // panel cols below
-            upd(s3, wn, oe - on - wn, NB, at(on, oi), at(oi, on + wn), at(on, on + wn));       // rest of its rows in panel
-            upd(s3, oe - on, n - oe, NB, at(on, oi), at(oi, oe), at(on, oe));                  // panel rows, right of panel
+            RL_CUDA(cudaStreamWaitEvent(s4, E_t1, 0));
+            if (s4_pending) { // the previous step's remainder covers this step's targets
+                RL_CUDA(cudaStreamWaitEvent(s2, E_s4, 0));
+                RL_CUDA(cudaStreamWaitEvent(s3, E_s4, 0));
+            }
+            upd(s2, wn, wn, NB, at(on, oi), at(oi, on), at(on, on));                    // own block
+            upd(s3, n - nx, wn, NB, at(nx, oi), at(oi, on), at(nx, on));                 // its columns below
+            upd(s3, wn, n - nx, NB, at(on, oi), at(oi, nx), at(on, nx));                 // its rows right
             RL_CUDA(cudaEventRecord(E_s3, s3));
+            upd(s4, n - nx, oe - nx, NB, at(nx, oi), at(oi, nx), at(nx, nx));            // later panel cols below
+            upd(s4, oe - nx, n - oe, NB, at(nx, oi), at(oi, oe), at(nx, oe));            // later panel rows right
+            RL_CUDA(cudaEventRecord(E_s4, s4));
+            s4_pending = true;
             diag(on, s2);
             RL_CUDA(cudaStreamWaitEvent(s2, E_s3, 0));
             trsm(on, s2);
         }
+        if (s4_pending)
+            RL_CUDA(cudaStreamWaitEvent(s2, E_s4, 0));
         RL_CUDA(cudaEventRecord(E_panel, s2));
     };
-    static const int reserve = std::getenv("RL_LU_RESERVE") ? std::atoi(std::getenv("RL_LU_RESERVE")) : 0;
+    static const bool timeline = std::getenv("RL_LU_TIMELINE") != nullptr;
+    if (timeline) {
+        static unsigned long long init[64][4];
+        for (auto& r : init) {
+            r[0] = r[1] = r[3] = 0;
+            r[2] = ~0ULL;
+        }
+        const int on = 1;
+        RL_CUDA(cudaMemcpyToSymbolAsync(g_tl, init, sizeof(init), 0, cudaMemcpyHostToDevice, s1));
+        RL_CUDA(cudaMemcpyToSymbolAsync(g_tl_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, s1));
+    }
     // RL_LU_TRACE=1: per outer step, time of the panel path (s2) and of the step on s1 (dev)
     static const bool trace = std::getenv("RL_LU_TRACE") != nullptr;
     std::vector<cudaEvent_t> tev;
@@ -812,14 +856,26 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         mark(s2);
         panelW(p);
         mark(s2);
-        // the remaining trailing update runs under the next panel, on all but `reserve` SMs
-        ctx().gemm_cta_cap = reserve > 0 ? 2 * (ctx().sms - reserve) : 0;
+        // the remaining trailing update runs under the next panel
         upd(s1, rest - w2n, rest - w2n, W, at(p + w2n, o), at(o, p + w2n), at(p + w2n, p + w2n));
-        ctx().gemm_cta_cap = 0;
         mark(s1);
     }
     RL_CUDA(cudaStreamWaitEvent(s1, E_panel, 0));
     mark(s1);
+    if (timeline) {
+        unsigned long long h[64][4];
+        const int off = 0;
+        RL_CUDA(cudaMemcpyToSymbolAsync(g_tl_on, &off, sizeof(int), 0, cudaMemcpyHostToDevice, s1));
+        RL_CUDA(cudaMemcpyFromSymbolAsync(h, g_tl, sizeof(h), 0, cudaMemcpyDeviceToHost, s1));
+        RL_CUDA(cudaStreamSynchronize(s1));
+        const unsigned long long t0 = h[0][0];
+        const uint64_t steps = std::min<uint64_t>(64, (n + NB - 1) / NB);
+        for (uint64_t i = 0; i < steps; ++i)
+            std::fprintf(stderr, "tl %2llu: diag %8.1f +%6.1f  trsm %8.1f +%6.1f  (gap diag<-prev trsm %6.1f) us\n",
+                         static_cast<unsigned long long>(i), (h[i][0] - t0) * 1e-3, (h[i][1] - h[i][0]) * 1e-3,
+                         h[i][3] ? (h[i][2] - t0) * 1e-3 : 0.0, h[i][3] ? (h[i][3] - h[i][2]) * 1e-3 : 0.0,
+                         i ? ((double)h[i][0] - (double)h[i - 1][3]) * 1e-3 : 0.0);
+    }
     static const bool dtrace = std::getenv("RL_DIAG_TRACE") != nullptr;
     if (dtrace)
         diag_trace_dump();

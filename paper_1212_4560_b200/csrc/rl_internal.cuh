@@ -63,7 +63,6 @@ struct Ctx {
     DevBuf ws[64];                 // named scratch slots (see WS_* below)
     uint64_t launches = 0;
     int sms = 148;
-    int gemm_cta_cap = 0;          // > 0: max CTAs of a TMA GEMM launch (persistent tiles)
     PendingUpload upload;          // set only inside a host-pointer call
 };
 
