@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 #include <vector>
 
@@ -289,13 +290,6 @@ void minmax_fold(const std::vector<double>& p, double* mn, double* mx) {
 
 // max over columns of per-column relative residuals (nrhs = 1: the reference metric);
 // non-finite columns count as +inf when check_finite.
-std::vector<double> residual_cols(uint64_t n, uint64_t nrhs, const double* a, const double* x, const double* b) {
-    double* tmp = ws<double>(WS_RESID, n * nrhs + nrhs);
-    double* out = tmp + n * nrhs;
-    residuals_dev(n, nrhs, a, x, b, tmp, out);
-    return to_host(out, nrhs);
-}
-
 double residual_max(uint64_t n, uint64_t nrhs, const double* a, const double* x, const double* b,
                     bool check_finite) {
     double* tmp = ws<double>(WS_RESID, n * nrhs + nrhs);
@@ -341,39 +335,28 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
     double* sys = ws<double>(WS_SYS, n * n);
     double* tmp = ws<double>(WS_OUT, n * n);
     double* aux = ws<double>(WS_LU_AUX, nblk * 2 * NB * NB);
-    double* vecs = ws<double>(WS_RHS, 4 * n * nrhs + n + 8);
+    double* vecs = ws<double>(WS_RHS, 4 * n * nrhs);
     double* Z = vecs;
     double* Y = Z + n * nrhs;
     double* R = Y + n * nrhs;
     double* D = R + n * nrhs;
-    double* piv = D + n * nrhs;
+    // One host read per attempt: pack = [per-column residuals | |pivots| | breakdown step]
+    double* pack = ws<double>(WS_PACK, nrhs + n + 1);
+    double* piv = pack + nrhs;
     unsigned long long* brk = reinterpret_cast<unsigned long long*>(piv + n);
     cudaStream_t st = stream();
 
-    rl_precond_report rep{};
-    rep.attempt = -1;
-    if (!(flags & 1u)) {
-        // raw-GENP contrast arm (genp.cpp:222-234)
-        wait_upload(A);
-        copy2d_dev(n, n, A, n, sys, n);
-        RL_CUDA(cudaMemsetAsync(brk, 0xff, 8, st));
-        genp_factor_blocked(n, sys, n, 0.0, piv, brk, aux);
-        copy2d_dev(n, nrhs, B, nrhs, Z, nrhs);
-        genp_solve_blocked(n, nrhs, sys, n, aux, Z, nrhs);
-        rep.raw_residual = residual_max(n, nrhs, A, Z, B, true);
-        minmax_fold(to_host(piv, n), &rep.raw_pivot_min, &rep.raw_pivot_max);
-    }
-    rl_precond_report best = rep;
     bool have_best = false;
     rl_status status = RL_OK;
     static const bool debug = std::getenv("RL_DEBUG") != nullptr;
     std::vector<char> col_accepted(nrhs, 0), col_have(nrhs, 0);
     std::vector<double> col_best(nrhs, 0.0), col_pmin(nrhs, 0.0), col_pmax(nrhs, 0.0);
     std::vector<int> col_attempt(nrhs, -1);
-    // Speculative next multiplier: for a dense right-only multiplier, attempt a+1's G is
-    // generated on a side stream while attempt a solves (the wavefront solve leaves most SMs
-    // idle); it is used if attempt a+1 happens, else discarded.  Attempts alternate between
-    // two multiplier slots so the speculation never overwrites the live one.
+    // Speculative multipliers: for a dense right-only multiplier, attempt a+1's G is generated
+    // on a side stream while attempt a solves (the wavefront solve leaves most SMs idle), and
+    // attempt 0's G beside the contrast arm; a speculative draw is used if its attempt
+    // happens, else discarded.  Attempts alternate between two multiplier slots so the
+    // speculation never overwrites the live one.
     const bool speculate = use_right && !use_left && (tag == RL_GAUSSIAN || tag == RL_UNIFORM_PM1);
     struct Spec {
         cudaStream_t s = nullptr;
@@ -389,6 +372,35 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
     }
     int spec_attempt = -1; // attempt whose right multiplier the side stream has generated
     const int mult_slot[2] = {WS_MULT, WS_MULT2};
+    auto spec_draw = [&](int a) { // attempt a's right multiplier on the side stream
+        const uint64_t dn = (sid + 7919ULL * static_cast<uint64_t>(a)) ^ 0x5000000000000000ULL;
+        double* next = ws<double>(mult_slot[a & 1], n * n);
+        RL_CUDA(cudaEventRecord(sp.start, st));
+        RL_CUDA(cudaStreamWaitEvent(sp.s, sp.start, 0));
+        ctx().stream = sp.s;
+        rng_generate(seed, dn, tag == RL_GAUSSIAN ? Draw::Gaussian : Draw::UniformPm1, n * n,
+                     tag == RL_GAUSSIAN ? mu : 0.0, tag == RL_GAUSSIAN ? sigma : 1.0, next);
+        ctx().stream = st;
+        RL_CUDA(cudaEventRecord(sp.done, sp.s));
+        spec_attempt = a;
+    };
+
+    rl_precond_report rep{};
+    rep.attempt = -1;
+    if (speculate && !(flags & 1u))
+        spec_draw(0); // beside the contrast arm
+    if (!(flags & 1u)) {
+        // raw-GENP contrast arm (genp.cpp:222-234)
+        wait_upload(A);
+        copy2d_dev(n, n, A, n, sys, n);
+        RL_CUDA(cudaMemsetAsync(brk, 0xff, 8, st));
+        genp_factor_blocked(n, sys, n, 0.0, piv, brk, aux);
+        copy2d_dev(n, nrhs, B, nrhs, Z, nrhs);
+        genp_solve_blocked(n, nrhs, sys, n, aux, Z, nrhs);
+        rep.raw_residual = residual_max(n, nrhs, A, Z, B, true);
+        minmax_fold(to_host(piv, n), &rep.raw_pivot_min, &rep.raw_pivot_max);
+    }
+    rl_precond_report best = rep;
     for (int attempt = 0; attempt < 8; ++attempt) {
         const uint64_t ds = sid + 7919ULL * static_cast<uint64_t>(attempt);
         rep.attempts_drawn = attempt + 1;
@@ -434,28 +446,10 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
             copy2d_dev(n, nrhs, B, nrhs, Z, nrhs);
         RL_CUDA(cudaMemsetAsync(brk, 0xff, 8, st));
         genp_factor_blocked(n, sys, n, 1e-300, piv, brk, aux);
-        long long hb = -1;
-        RL_CUDA(cudaMemcpyAsync(&hb, brk, 8, cudaMemcpyDeviceToHost, st));
-        RL_CUDA(cudaStreamSynchronize(st));
-        if (hb >= 0) { // PivotBreakdown (genp.cpp:285-288)
-            if (attempt + 1 >= 8 && !have_best) {
-                status = RL_PIVOT_BREAKDOWN;
-                set_error("genp_factor: pivot below floor at step " + std::to_string(hb));
-            }
-            continue;
-        }
-        if (speculate && attempt + 1 < 8) { // next attempt's G beside this attempt's solves
-            const uint64_t dn = (sid + 7919ULL * static_cast<uint64_t>(attempt + 1)) ^ 0x5000000000000000ULL;
-            double* next = ws<double>(mult_slot[(attempt + 1) & 1], n * n);
-            RL_CUDA(cudaEventRecord(sp.start, st));
-            RL_CUDA(cudaStreamWaitEvent(sp.s, sp.start, 0));
-            ctx().stream = sp.s;
-            rng_generate(seed, dn, tag == RL_GAUSSIAN ? Draw::Gaussian : Draw::UniformPm1, n * n,
-                         tag == RL_GAUSSIAN ? mu : 0.0, tag == RL_GAUSSIAN ? sigma : 1.0, next);
-            ctx().stream = st;
-            RL_CUDA(cudaEventRecord(sp.done, sp.s));
-            spec_attempt = attempt + 1;
-        }
+        // The breakdown flag is read with the residuals (one host synchronisation per attempt):
+        // the solves run on a broken factorization too and their results are then discarded.
+        if (speculate && attempt + 1 < 8) // next attempt's G beside this attempt's solves
+            spec_draw(attempt + 1);
         genp_solve_blocked(n, nrhs, sys, n, aux, Z, nrhs);
         if (use_right)
             apply_vec(right, Z, nrhs, Y);
@@ -478,9 +472,23 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
         // Acceptance per right-hand side (genp.cpp:275-282): nrhs columns behave as nrhs
         // independent reference calls sharing the stream — a column keeps the first attempt
         // whose residual is <= 1e-7, else its best attempt.
-        const std::vector<double> res = residual_cols(n, nrhs, A, Y, B);
+        {
+            double* tmpr = ws<double>(WS_RESID, n * nrhs);
+            residuals_dev(n, nrhs, A, Y, B, tmpr, pack);
+        }
+        const std::vector<double> hp = to_host(pack, nrhs + n + 1);
+        long long hb = -1;
+        std::memcpy(&hb, &hp[nrhs + n], 8);
+        if (hb >= 0) { // PivotBreakdown (genp.cpp:285-288)
+            if (attempt + 1 >= 8 && !have_best) {
+                status = RL_PIVOT_BREAKDOWN;
+                set_error("genp_factor: pivot below floor at step " + std::to_string(hb));
+            }
+            continue;
+        }
+        const std::vector<double> res(hp.begin(), hp.begin() + nrhs);
         double pmn = 0.0, pmx = 0.0;
-        minmax_fold(to_host(piv, n), &pmn, &pmx);
+        minmax_fold(std::vector<double>(hp.begin() + nrhs, hp.begin() + nrhs + n), &pmn, &pmx);
         if (debug)
             for (uint64_t j = 0; j < nrhs; ++j)
                 std::fprintf(stderr, "[rl] attempt %d column %llu residual %.3e\n", attempt,
