@@ -150,9 +150,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
         const int rest = NB - c0 - SB;
         if (rest == 0)
             break;
-        // (2) rows below: l_r U_sub = w_r   (x_j = (w_j - sum_{l<j} x_l U_lj) / U_jj)
-        for (int t = tid; t < rest; t += PK_THREADS) {
-            const int r = c0 + SB + t;
+        // (2) rows below: l_r U_sub = w_r   (x_j = (w_j - sum_{l<j} x_l U_lj) / U_jj), threads
+        //     [0, rest); (3) columns right beside it, threads [rest, 2 rest) (disjoint entries)
+        if (tid < rest) {
+            const int r = c0 + SB + tid;
             double x[SB];
 #pragma unroll
             for (int l = 0; l < SB; ++l)
@@ -171,8 +172,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
                 W[r * PT + c0 + l] = x[l];
         }
         // (3) columns right: L_sub y = w  (unit lower)
-        for (int t = tid; t < rest; t += PK_THREADS) {
-            const int c = c0 + SB + t;
+        else if (tid < 2 * rest) {
+            const int c = c0 + SB + (tid - rest);
             double y[SB];
 #pragma unroll
             for (int i = 0; i < SB; ++i)

@@ -30,6 +30,29 @@ def test_gemm_transposes_device(rl):
             assert ((C - ref).abs().max() / ref.abs().max()).item() < 1e-14
 
 
+@pytest.mark.parametrize("m,n,k,ta,beta", [
+    (1000, 72, 768, False, 0.0),   # A H shape: TMA 128 x 80 tile, column edge zero-filled
+    (4096, 72, 2048, False, 0.5),  # full M tiles, beta
+    (72, 1000, 768, True, 0.0),    # Q^T A shape: TMA 80 x 128 tile, M-major A
+    (70, 333, 2048, True, -1.0),   # M < 72, ragged N
+    (1000, 72, 777, False, 0.0),   # odd K: the cp.async kernel
+    (512, 4, 300, False, 0.0),     # <= 8 right-hand sides: the GEMV path
+    (256, 1, 256, False, 1.0),
+])
+def test_gemm_skinny_shapes_device(rl, m, n, k, ta, beta):
+    """The range finder's skinny product shapes (TMA tiles with zero-filled edges) and the GEMV
+    path against torch's fp64 matmul (split-K runs inside the range-finder tests)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = torch.randn(k if ta else m, m if ta else k, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(k, n, dtype=torch.float64, device="cuda", generator=g)
+    C = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
+    ref = ((A.T if ta else A) @ B) + beta * C
+    rl.dev_gemm(A, B, C, beta=beta, trans_a=ta)
+    torch.cuda.synchronize()
+    assert ((C - ref).abs().max() / ref.abs().max()).item() < 1e-14
+
+
 def test_qr_known_answers(rl):
     q, r = rl.qr_positive(np.array([[2.0, 0.0], [0.0, 3.0]]))
     assert np.abs(q - np.eye(2)).max() < 1e-14 and np.abs(r - np.diag([2.0, 3.0])).max() < 1e-14
