@@ -1,78 +1,121 @@
 // K6: batched randomized GENP for small systems (config 2: 4096 x n=64, circulant +-1,
-// MulSide::Right) — semantically the loop bench::table1_genp runs (bench.cpp:117-133) over
-// genp::randomized_genp (genp.cpp:207-291), one stream per system.
+// MulSide::Right; Table 1's MulSide::Left + refine) — semantically the loop
+// bench::table1_genp runs (bench.cpp:117-133) over genp::randomized_genp (genp.cpp:207-291),
+// one stream per system.
 //
-// One 128-thread CTA per system, the 64 x 64 working matrix in shared memory (pitch 68 doubles:
-// conflict-free DMMA fragments).  Per attempt:
-//   * A (64 x 64, L2-resident after the first touch) is staged in shared memory and
-//     W = A C runs on DMMA (warp wp computes rows 16 wp..16 wp+15); the +-1 B fragment
-//     C[k][j] = c[(k - j) mod 64] is synthesised from a 64-bit sign mask.
-//   * No-pivot LU (genp.cpp:20-33) blocked in four 16-column panels: warp 0 factors the
-//     panel in registers (pivot row by shuffles, m = w(i,k) * (1/p), 1/p := 0 for p = 0),
-//     one thread per column solves U12 against the unit L11, all warps update the trailing
-//     square on DMMA — three barriers per panel instead of one per pivot.
-//   * Warp 0 runs the forward / backward substitution on the packed LU (two rows per lane,
-//     shuffle chain; genp.cpp:106-124), then y = C z,
-//     refinement and the residual ||A y - b|| / ||b|| on threads 0..63.
-// The raw-GENP contrast arm is iteration -1 of the same loop (pivot floor 0, no multiplier).  The 8-attempt redraw protocol (stream id + 7919 a, accept
-// <= 1e-7, keep best, genp.cpp:236-290) runs in-kernel.  Exactly singular circulants (a
-// vanishing 64-point DFT coefficient) are pre-screened and skipped; a
-// system that exhausts its attempts is re-run with the exact protocol (pass 1) so the
-// returned best attempt is the reference's.
+// One 64-thread CTA (two warps) per system; every FP64 operation runs on the DFMA pipe (on
+// sm_100a DMMA and DFMA share one FP64 pipe: tools/micro/pipes.cu measures 37.1 TF/s DMMA alone,
+// 34.0 DFMA alone and ~35 mixed, so the design minimises FP64 operations, not DMMA count).
+//   * The working matrix lives in registers, distributed 8 x 8 cyclically: thread (tr, tc) =
+//     (t / 8, t % 8) owns w(tr + 8r, tc + 8c), r, c < 8 — every thread keeps an equal share of
+//     the shrinking trailing matrix until the last block of eight pivots.
+//   * No-pivot LU (genp.cpp:20-33): 64 pivot steps, one barrier each. At step k the owners of
+//     row k and column k publish them (double-buffered, in the idle staging buffer) and the
+//     pivot's owner publishes 1/p; every thread then forms its multipliers m = w(i,k) * (1/p)
+//     (1/p := 0 for p = 0) and updates its own entries with one FMA each; rows / columns at
+//     or left of the pivot are left untouched (predicated FMAs on the boundary block only).
+//   * The multiplier product W = A C (Right) / C A (Left) runs through the FFT, as the
+//     reference's own structured::multiply_matrix does (genp.cpp:158-166, structured.cpp:
+//     178-189): thread t owns row t of A (Right) or column t (Left), packs it as 32 complex
+//     points, runs a register-resident 32-point FFT, the real-FFT split, the pointwise product
+//     with the multiplier's spectrum, the inverse split and the inverse 32-point FFT — about
+//     1.3 K FP64 operations per row against 8 K FMAs for the dense product.
+//   * The packed LU is written once to shared memory for warp 0's substitutions
+//     (genp.cpp:106-124); y = C z, refinement and the residual ||A y - b|| / ||b|| run on all
+//     64 threads.
+// The raw-GENP contrast arm is iteration -1 of the same loop (pivot floor 0, no multiplier).
+// The 8-attempt redraw protocol (stream id + 7919 a, accept <= 1e-7, keep best,
+// genp.cpp:236-290) runs in-kernel.  Exactly singular circulants (a vanishing 64-point DFT
+// coefficient) are pre-screened and skipped; a system that exhausts its
+// attempts is re-run with the exact protocol (pass 1) so the returned best attempt is the
+// reference's.
 #include <cmath>
 
-#include "panel.cuh"
 #include "rl_internal.cuh"
 
 namespace rl {
 
+#ifdef RL_B64_PROF // phase timer for one system (tools/micro/b64_prof.cu); compiled out of the library
+__device__ long long g_b64_prof[32];
+#define B64_MARK(ph)                                                                                \
+    do {                                                                                            \
+        if (threadIdx.x == 0 && blockIdx.x == 0) {                                                  \
+            const long long now_ = clock64();                                                       \
+            g_b64_prof[ph] += now_ - prof_t0;                                                       \
+            prof_t0 = now_;                                                                         \
+        }                                                                                           \
+    } while (0)
+#else
+#define B64_MARK(ph) ((void)0)
+#endif
+
 namespace {
 
 constexpr int N = 64;
-constexpr int THREADS = 128;
-constexpr int XP = N + 4; // shared pitch: 544 B = 32 mod 128 -> conflict-free DMMA fragments
+constexpr int THREADS = 64;
+constexpr int P = 66; // staging pitch (528 B rows: 16-byte aligned, conflict-free 128-bit row reads)
+// LU publication buffer per parity: the pivot row owner-major at pitch 10 (the eight owners'
+// 128-bit reads hit distinct banks), then the pivot column owner-major at pitch 8.
+constexpr int PUB_RP = 10, PUB_C = 8 * PUB_RP, PUB = PUB_C + 64;
 
 struct Smem {
-    double X[N * XP];      // A / W staging, transposed packed LU, LCG scratch
-    double pm[2];          // running |pivot| min / max of the LU
-    double v0[N], v1[N];
-    double2 tw[N];         // DFT twiddles (cos, sin)(2 pi m / 64)
-    double red[4];
-    double rcp[N];         // 1/U_kk
+    double X[N * P]; // A staging / W / packed LU (row-major); sign-stream scratch and DFT twiddles
+    double rcp[N];   // 1/U_kk
+    union {
+        double pub[2 * PUB]; // the LU's row / column publications (two parities x (row, column))
+        struct {
+            double v0[N], v1[N];
+            double2 H[33]; // multiplier spectrum (conj for Right) / 128, bins 0..32
+        };
+    };
+    double red[2];
+    double pm[2];    // |pivot| min / max of the last LU
+    double bsq, best_res;
     uint64_t mask, mask0;
     unsigned bal[2];
     int flag;
     rl_precond_report rp; // the system's report (thread 0), kept out of the register budget
 };
 
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(d[0]), "+d"(d[1])
-                 : "d"(a), "d"(b));
-}
+// (cos, sin)(2 pi j / 64), j < 32 (exact symmetries between entries)
+__constant__ double2 kCS64[32] = {
+    {0x1.0000000000000p+0, 0.0},
+    {0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},
+    {0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3},
+    {0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},
+    {0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},
+    {0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},
+    {0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1},
+    {0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},
+    {0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},
+    {0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},
+    {0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1},
+    {0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},
+    {0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},
+    {0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},
+    {0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1},
+    {0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},
+    {0.0, 0x1.0000000000000p+0},
+    {-0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},
+    {-0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1},
+    {-0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},
+    {-0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},
+    {-0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},
+    {-0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1},
+    {-0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},
+    {-0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},
+    {-0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},
+    {-0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1},
+    {-0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},
+    {-0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},
+    {-0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},
+    {-0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3},
+    {-0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},
+};
 
 __device__ __forceinline__ double sgn(uint64_t mask, int j) { // bit j set <=> c_j = -1
     return ((mask >> (j & 63)) & 1ULL) ? -1.0 : 1.0;
 }
-
-__device__ __forceinline__ double min_fold(double a, double v) { return (v < a) ? v : a; }
-
-// 1/p on the pivot chain: the hardware estimate plus two Newton steps (a few cycles instead of
-// __drcp_rn's correctly rounded sequence); p is warp-uniform, so the rare tiny-|p| fallback
-// does not diverge. 0 -> 0 (the reference's m = 0 for a zero pivot).
-__device__ __forceinline__ double pivot_rcp(double p) {
-    if (p == 0.0)
-        return 0.0;
-    if (!(fabs(p) > 1e-300 && fabs(p) < 1e300))
-        return __drcp_rn(p);
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
-    double e = fma(-p, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-p, r, 1.0);
-    return fma(r, e, r);
-}
-__device__ __forceinline__ double max_fold(double b, double v) { return (b < v) ? v : b; }
 
 // 64 sign draws of stream (seed, sid) after discard(8) as a bitmask (random_gen.cpp:22-31,
 // 55-57).  One thread; only the first phase of the first twist is needed (new[i], i < 72 <
@@ -108,208 +151,332 @@ __device__ uint64_t sign_mask_stream(uint64_t seed, uint64_t sid, uint64_t* scra
     return mask;
 }
 
-__device__ __forceinline__ void load_A(Smem& S, const double* __restrict__ Ag, int t) {
-#pragma unroll 4
-    for (int e = t; e < N * N / 2; e += THREADS) {
-        const double2 v = reinterpret_cast<const double2*>(Ag)[e];
-        const int i = (2 * e) >> 6, j = (2 * e) & 63;
-        *reinterpret_cast<double2*>(S.X + i * XP + j) = v;
-    }
+// ------------------------------------------------------------------ FFT ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// X holds A on entry; on exit X holds W = A C (row-major).  Two passes over the output's
-// column halves (16 accumulators each instead of 32: the kernel's register peak, which sets
-// how many systems share an SM); W goes to registers first, then over A after a barrier.
-__device__ __forceinline__ void circ_product(Smem& S, uint64_t mask, int t, bool left) {
-    const int lane = t & 31, warp = t >> 5, g = lane >> 2, q = lane & 3;
-    double keep[2][4][2];
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-        double acc[2][4][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int jb = 0; jb < 4; ++jb)
-                acc[i][jb][0] = acc[i][jb][1] = 0.0;
-#pragma unroll 4
-        for (int kk = 0; kk < N; kk += 4) {
-            const int k = kk + q;
-            if (!left) { // W = A C: A rows from shared memory, C[k][8 jb' + g] = c[k - col]
-                const double a0 = S.X[(16 * warp + g) * XP + k];
-                const double a1 = S.X[(16 * warp + 8 + g) * XP + k];
-#pragma unroll
-                for (int jb = 0; jb < 4; ++jb) {
-                    const double bf = sgn(mask, k - (8 * (4 * half + jb) + g));
-                    dmma(acc[0][jb], a0, bf);
-                    dmma(acc[1][jb], a1, bf);
-                }
-            } else { // W = C A: C[row][k] = c[row - k] synthesised, A[k][col] from shared memory
-                const double c0 = sgn(mask, (16 * warp + g) - k);
-                const double c1 = sgn(mask, (16 * warp + 8 + g) - k);
-#pragma unroll
-                for (int jb = 0; jb < 4; ++jb) {
-                    const double bf = S.X[k * XP + 8 * (4 * half + jb) + g];
-                    dmma(acc[0][jb], c0, bf);
-                    dmma(acc[1][jb], c1, bf);
-                }
-            }
-        }
-        if (half == 0) {
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int jb = 0; jb < 4; ++jb) {
-                    keep[i][jb][0] = acc[i][jb][0];
-                    keep[i][jb][1] = acc[i][jb][1];
-                }
+__host__ __device__ constexpr int br5(int m) {
+    return ((m & 1) << 4) | ((m & 2) << 2) | (m & 4) | ((m & 8) >> 2) | ((m & 16) >> 4);
+}
+
+// (xr + i xi) *= (cos, -sin)(2 pi j / 64) (forward) or (cos, +sin) (inverse); j < 32 constant
+template <bool INV>
+__device__ __forceinline__ void twiddle(double& xr, double& xi, int j) {
+    if (j == 0)
+        return;
+    if (j == 16) { // -i (forward) / +i (inverse)
+        const double t = xr;
+        if (!INV) {
+            xr = xi;
+            xi = -t;
         } else {
-            __syncthreads(); // every read of A is done
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int jb = 0; jb < 4; ++jb) {
-                    double* row = S.X + (16 * warp + 8 * i + g) * XP + 2 * q;
-                    *reinterpret_cast<double2*>(row + 8 * jb) = make_double2(keep[i][jb][0], keep[i][jb][1]);
-                    *reinterpret_cast<double2*>(row + 8 * (4 + jb)) = make_double2(acc[i][jb][0], acc[i][jb][1]);
-                }
+            xr = -xi;
+            xi = t;
         }
+        return;
+    }
+    const double c = kCS64[j].x, s = INV ? kCS64[j].y : -kCS64[j].y;
+    const double r = fma(xr, c, -xi * s);
+    const double i = fma(xr, s, xi * c);
+    xr = r;
+    xi = i;
+}
+
+// One radix-2 pass of the in-place 32-point FFT on z_k = x[2k] + i x[2k+1] (LEN = butterfly span).
+template <int LEN, bool INV>
+__device__ __forceinline__ void fft_pass(double (&x)[N]) {
+    constexpr int half = LEN / 2;
+#pragma unroll
+    for (int g = 0; g < 32; g += LEN)
+#pragma unroll
+        for (int k = 0; k < half; ++k) {
+            const int a = g + k, b = a + half, j = (64 / LEN) * k;
+            if (!INV) {
+                const double ur = x[2 * a], ui = x[2 * a + 1], vr = x[2 * b], vi = x[2 * b + 1];
+                x[2 * a] = ur + vr;
+                x[2 * a + 1] = ui + vi;
+                double dr = ur - vr, di = ui - vi;
+                twiddle<false>(dr, di, j);
+                x[2 * b] = dr;
+                x[2 * b + 1] = di;
+            } else {
+                double vr = x[2 * b], vi = x[2 * b + 1];
+                twiddle<true>(vr, vi, j);
+                const double ur = x[2 * a], ui = x[2 * a + 1];
+                x[2 * a] = ur + vr;
+                x[2 * a + 1] = ui + vi;
+                x[2 * b] = ur - vr;
+                x[2 * b + 1] = ui - vi;
+            }
+        }
+}
+
+// Forward: decimation in frequency, natural order in, bit-reversed out.  Inverse (unnormalised,
+// +i): decimation in time, bit-reversed in, natural out.
+template <bool INV>
+__device__ __forceinline__ void fft32(double (&x)[N]) {
+    if (!INV) {
+        fft_pass<32, false>(x);
+        fft_pass<16, false>(x);
+        fft_pass<8, false>(x);
+        fft_pass<4, false>(x);
+        fft_pass<2, false>(x);
+    } else {
+        fft_pass<2, true>(x);
+        fft_pass<4, true>(x);
+        fft_pass<8, true>(x);
+        fft_pass<16, true>(x);
+        fft_pass<32, true>(x);
     }
 }
 
-// Blocked no-pivot LU of the 64 x 64 working matrix in S.X (row-major, genp.cpp:20-33 per
-// column step): four 16-column panels.  (a) warp 0 factors the panel rows c0..63 x 16 in
-// registers (two rows per lane, pivot row by shuffles, 1/p := 0 for p = 0), (b) every column
-// right of the panel solves its 16 U entries against the unit L11 (one thread per column),
-// (c) the trailing square is updated on DMMA (K = 16) by all warps.  Three barriers per panel
-// instead of one per pivot.  Returns breakdown (some |p| < floor); pmin/pmax of |pivots|
-// (in pivot order) for every thread; S.rcp = 1/U_kk.
-__device__ __forceinline__ bool lu_blocked(Smem& S, double floor, int t, double& pmin, double& pmax) {
-    const int lane = t & 31, warp = t >> 5;
+__device__ __forceinline__ double2 cmul(double2 p, double2 q) {
+    return make_double2(fma(p.x, q.x, -p.y * q.y), fma(p.x, q.y, p.y * q.x));
+}
+
+// x <- the 64-point circular product of the real vector x with the multiplier whose spectrum
+// (already conjugated for Right, scaled by 1/128) is H[0..32]: IDFT64(DFT64(x) .* H).
+// Packed: Z = FFT32(x_even + i x_odd); X_m = E + W^m O, X_{32-m} = conj(E - W^m O) with
+// E = Z_m + conj Z_{32-m}, O = -i (Z_m - conj Z_{32-m}) (both 2x), W = e^{-2 pi i / 64};
+// Y = X .* H; inverse Z'_m = E' + i O', E' = Y_m + conj Y_{32-m}, O' = (Y_m - conj Y_{32-m}) W^-m,
+// Z'_{32-m} = conj E' + i conj O'; x_even + i x_odd = IFFT32(Z').
+__device__ __forceinline__ void circ_fft64(double (&x)[N], const double2* __restrict__ H) {
+    fft32<false>(x);
+#pragma unroll
+    for (int m = 0; m <= 16; ++m) {
+        const int p = (32 - m) & 31, im = br5(m), ip = br5(p);
+        const double2 zm = make_double2(x[2 * im], x[2 * im + 1]);
+        const double2 zp = make_double2(x[2 * ip], x[2 * ip + 1]);
+        const double2 E = make_double2(zm.x + zp.x, zm.y - zp.y);
+        double2 T = make_double2(zm.y + zp.y, zp.x - zm.x); // O = -i (Z_m - conj Z_p)
+        twiddle<false>(T.x, T.y, m);
+        const double2 ym = cmul(make_double2(E.x + T.x, E.y + T.y), H[m]);
+        const double2 yp = cmul(make_double2(E.x - T.x, T.y - E.y), H[32 - m]);
+        const double2 e2 = make_double2(ym.x + yp.x, ym.y - yp.y);
+        double2 o2 = make_double2(ym.x - yp.x, ym.y + yp.y);
+        twiddle<true>(o2.x, o2.y, m);
+        x[2 * im] = e2.x - o2.y;
+        x[2 * im + 1] = e2.y + o2.x;
+        if (m != 0 && m != 16) {
+            x[2 * ip] = e2.x + o2.y;
+            x[2 * ip + 1] = o2.x - e2.y;
+        }
+    }
+    fft32<true>(x);
+}
+
+// ------------------------------------------------------------------- LU ----
+// 1/p without branches (every thread evaluates it; the pivot's owner publishes it): the
+// hardware estimate plus two Newton steps on p scaled by a power of two into the estimate's
+// range (exact), the scale applied again to the result; 0 -> 0 (the reference's m = 0 for a
+// zero pivot), +-inf -> 0.
+__device__ __forceinline__ double pivot_rcp_nb(double p) {
+    const double ap = fabs(p);
+    const double sc = ap < 0x1p-960 ? 0x1p+600 : (ap > 0x1p+960 ? 0x1p-600 : 1.0);
+    const double q = p * sc;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-q, r, 1.0);
+    r = fma(r, e, r) * sc;
+    return (p == 0.0 || isinf(p)) ? 0.0 : r;
+}
+
+__device__ __forceinline__ void st_if(double* dst, double v, bool pred) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.shared.f64 [%0], %1;\n}" ::"r"(smem_u32(dst)),
+                 "d"(v), "r"(static_cast<int>(pred))
+                 : "memory");
+}
+__device__ __forceinline__ void st2_if(double* dst, double v0, double v1, bool pred) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n @p st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(
+                     smem_u32(dst)),
+                 "d"(v0), "d"(v1), "r"(static_cast<int>(pred))
+                 : "memory");
+}
+
+// Publication for pivot step k = 8K + s (K compile-time, s at run time), owner-major so every
+// owner stores and every reader loads 128-bit pairs: row k as pub[par][tc][c] by the owners
+// (s, tc), column k as pub[par][PUB_C + tr*8 + r] by the owners (tr, s); 1/p into rcp[k].
+// Predicated stores, no branches (a divergent branch costs a reconvergence barrier per step).
+template <int K>
+__device__ __forceinline__ void lu_publish(const double (&w)[8][8], Smem& S, int s, int tr, int tc) {
+    double* ur = S.pub + (s & 1) * PUB + tc * PUB_RP;
+    double* uc = S.pub + (s & 1) * PUB + PUB_C + tr * 8;
+    const bool oc = tc == s, orow = tr == s;
+    st_if(S.rcp + 8 * K + s, pivot_rcp_nb(w[K][K]), oc && orow);
+#pragma unroll
+    for (int r = K & ~1; r < 8; r += 2)
+        st2_if(uc + r, w[r][K], w[r + 1][K], oc);
+#pragma unroll
+    for (int c = K & ~1; c < 8; c += 2)
+        st2_if(ur + c, w[K][c], w[K][c + 1], orow);
+}
+
+// Pivot step k = 8K + s (k-parity PAR = s & 1; LAST: s = 7, the next step opens block K+1).
+// Rows / columns r, c > K are always in the trailing matrix; the block's own row / column K
+// (thread row tr, column tc) leaves it once the step passes tr / tc.  A zero multiplier /
+// pivot-row entry there leaves the finished entries bitwise unchanged (fma(-0, u, w) = w)
+// without per-FMA predicates; the column of multipliers is not written back — column k keeps
+// w(i,k) and L = w(i,k) / p is formed once at the end (lu_store), the same product the update
+// used.  The next step's row / column (KC) are updated and published first, then the rest.
+template <int K, int PAR, bool LAST>
+__device__ __forceinline__ void lu_step(double (&w)[8][8], Smem& S, int s, int tr, int tc) {
+    constexpr int KC = LAST ? K + 1 : K;
+    __syncthreads();
+    const double* ur = S.pub + PAR * PUB + tc * PUB_RP;
+    const double* uc = S.pub + PAR * PUB + PUB_C + tr * 8;
+    const double inv = S.rcp[8 * K + s];
+    double m[8], u[8];
+#pragma unroll
+    for (int r = K & ~1; r < 8; r += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(uc + r);
+        if (r >= K)
+            m[r] = v.x * inv;
+        m[r + 1] = v.y * inv;
+    }
+    m[K] = tr > s ? m[K] : 0.0;
+#pragma unroll
+    for (int c = K & ~1; c < 8; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(ur + c);
+        if (c >= K)
+            u[c] = v.x;
+        u[c + 1] = v.y;
+    }
+    u[K] = tc > s ? u[K] : 0.0;
+    if (KC < 8) {
+#pragma unroll
+        for (int c = K; c < 8; ++c)
+            w[KC][c] = fma(-m[KC], u[c], w[KC][c]);
+#pragma unroll
+        for (int r = K; r < 8; ++r)
+            if (r != KC)
+                w[r][KC] = fma(-m[r], u[KC], w[r][KC]);
+        lu_publish<(KC < 8 ? KC : 7)>(w, S, LAST ? 0 : s + 1, tr, tc);
+    }
+#pragma unroll
+    for (int c = K; c < 8; ++c) {
+        if (c == KC)
+            continue;
+#pragma unroll
+        for (int r = K; r < 8; ++r)
+            if (r != KC)
+                w[r][c] = fma(-m[r], u[c], w[r][c]);
+    }
+}
+
+// The eight pivot steps k = 8K .. 8K+7 of block K; the step index only enters predicates, so
+// one loop body per block and parity (the register indices are compile-time) keeps the code small.
+template <int K>
+__device__ __forceinline__ void lu_block(double (&w)[8][8], Smem& S, int tr, int tc) {
 #pragma unroll 1
-    for (int c0 = 0; c0 < N; c0 += 16) {
-        if (warp == 0) { // (a) the 16 x 16 diagonal block: lane l < 16 holds row c0 + l
-            const bool v = lane < 16;
-            const int r = c0 + (lane & 15);
-            double a[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                a[j] = v ? S.X[r * XP + c0 + j] : 0.0;
-            double mn = S.pm[0], mx = S.pm[1];
-            bool brk = S.flag != 0;
-#pragma unroll
-            for (int kk = 0; kk < 16; ++kk) {
-                const double piv = __shfl_sync(0xffffffffu, a[kk], kk);
-                const double inv = pivot_rcp(piv);
-                if (lane == 0)
-                    S.rcp[c0 + kk] = inv;
-                const double ap = fabs(piv);
-                mn = (c0 + kk == 0) ? ap : min_fold(mn, ap);
-                mx = (c0 + kk == 0) ? ap : max_fold(mx, ap);
-                brk |= ap < floor;
-                const bool below = v && lane > kk;
-                const double m = below ? a[kk] * inv : 0.0;
-                a[kk] = below ? m : a[kk];
-#pragma unroll
-                for (int l = kk + 1; l < 16; ++l)
-                    a[l] = fma(-m, __shfl_sync(0xffffffffu, a[l], kk), a[l]);
-            }
-            if (v)
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    S.X[r * XP + c0 + j] = a[j];
-            if (lane == 0) {
-                S.pm[0] = mn;
-                S.pm[1] = mx;
-                if (brk)
-                    S.flag = 1;
-            }
-        }
-        __syncthreads();
-        const int nc = N - c0 - 16;
-        if (nc == 0)
-            break;
-        // (b) one thread per row below the block (L21 = A21 U11^-1: the same multipliers and
-        // updates, in the same order, as eliminating the rows inside the pivot loop) and one
-        // per column right of it (U12 = L11^-1 A12), warps 0-1 and 2-3
-        if (t < nc) {
-            const int i = c0 + 16 + t;
-            double y[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                y[j] = S.X[i * XP + c0 + j];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const double m = y[k] * S.rcp[c0 + k];
-                y[k] = m;
-#pragma unroll
-                for (int l = k + 1; l < 16; ++l)
-                    y[l] = fma(-m, S.X[(c0 + k) * XP + c0 + l], y[l]);
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                S.X[i * XP + c0 + j] = y[j];
-        } else if (t >= 64 && t - 64 < nc) {
-            const int c = c0 + 16 + (t - 64);
-            double y[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-                y[i] = S.X[(c0 + i) * XP + c];
-#pragma unroll
-            for (int i = 1; i < 16; ++i)
-#pragma unroll
-                for (int k = 0; k < i; ++k)
-                    y[i] = fma(-S.X[(c0 + i) * XP + c0 + k], y[k], y[i]);
-#pragma unroll
-            for (int i = 1; i < 16; ++i)
-                S.X[(c0 + i) * XP + c] = y[i];
-        }
-        __syncthreads();
-        panel::smem_update16(S.X + (c0 + 16) * XP + c0 + 16, XP, S.X + (c0 + 16) * XP + c0, XP,
-                             S.X + c0 * XP + c0 + 16, XP, nc, nc, warp, THREADS / 32, lane);
-        __syncthreads();
+    for (int s = 0; s < 6; s += 2) {
+        lu_step<K, 0, false>(w, S, s, tr, tc);
+        lu_step<K, 1, false>(w, S, s + 1, tr, tc);
     }
-    pmin = S.pm[0];
-    pmax = S.pm[1];
-    return S.flag != 0;
+    lu_step<K, 0, false>(w, S, 6, tr, tc);
+    lu_step<K, 1, true>(w, S, 7, tr, tc);
 }
 
-// warp 0: S.v0 <- U^{-1} L^{-1} S.v0 with the packed LU row-major in X (L_ij = X[i * XP + j]
-// below the diagonal, U on and above). Lane l owns rows l and l + 32; step j reads column j of
-// L or U down the lanes (a 4-way bank conflict at pitch 68, far cheaper than transposing X).
+// No-pivot LU of the register-resident matrix (genp.cpp:20-33): one barrier per pivot step.
+// On exit w holds U on and above the diagonal and w(i,k) (un-normalised) below; S.rcp[k] =
+// 1/U_kk.  S.pub (aliasing the vectors and the spectrum) carries the publications (callers
+// fence before and after).
+__device__ __forceinline__ void lu_regs(double (&w)[8][8], Smem& S, int tr, int tc) {
+    lu_publish<0>(w, S, 0, tr, tc);
+    lu_block<0>(w, S, tr, tc);
+    lu_block<1>(w, S, tr, tc);
+    lu_block<2>(w, S, tr, tc);
+    lu_block<3>(w, S, tr, tc);
+    lu_block<4>(w, S, tr, tc);
+    lu_block<5>(w, S, tr, tc);
+    lu_block<6>(w, S, tr, tc);
+    lu_block<7>(w, S, tr, tc);
+}
+
+// The packed LU into X (row-major): U as factored, L_ij = w(i,j) * (1/U_jj) below the diagonal.
+__device__ __forceinline__ void lu_store(const double (&w)[8][8], Smem& S, int tr, int tc) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const double inv = S.rcp[tc + 8 * c];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            double v = w[r][c];
+            if (r > c || (r == c && tr > tc))
+                v *= inv;
+            S.X[(tr + 8 * r) * P + tc + 8 * c] = v;
+        }
+    }
+}
+
+// Eight substitution steps of warp 0's solve over columns jb .. jb+7 (HI: jb >= 32, the rows
+// l + 32 half), branch-free: the block's L / U entries of the lane's two rows (and the eight
+// 1/U_jj) are loaded first, so each step's chain is one shuffle, (one multiply) and one FMA.
+template <bool HI, bool BACK>
+__device__ __forceinline__ void solve_block8(const Smem& S, int jb, int lane, double& x0, double& x1) {
+    const double* r0 = S.X + lane * P + jb;
+    const double* r1 = S.X + (lane + 32) * P + jb;
+    double a0[8], a1[8], rc[8];
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+        const double2 v0 = *reinterpret_cast<const double2*>(r0 + q);
+        const double2 v1 = *reinterpret_cast<const double2*>(r1 + q);
+        a0[q] = v0.x;
+        a0[q + 1] = v0.y;
+        a1[q] = v1.x;
+        a1[q + 1] = v1.y;
+        if (BACK) {
+            const double2 vr = *reinterpret_cast<const double2*>(S.rcp + jb + q);
+            rc[q] = vr.x;
+            rc[q + 1] = vr.y;
+        }
+    }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+        const int q = BACK ? 7 - qq : qq, j = jb + q;
+        double xj = __shfl_sync(0xffffffffu, HI ? x1 : x0, j & 31);
+        if (BACK)
+            xj *= rc[q];
+        const double f0 = fma(-a0[q], xj, x0), f1 = fma(-a1[q], xj, x1);
+        if (!BACK) { // unit L: rows below j
+            if (!HI)
+                x0 = lane > j ? f0 : x0;
+            x1 = lane + 32 > j ? f1 : x1;
+        } else { // U: row j takes x_j, rows above it are updated
+            if (HI) {
+                x1 = lane + 32 == j ? xj : (lane + 32 < j ? f1 : x1);
+                x0 = f0;
+            } else {
+                x0 = lane == j ? xj : (lane < j ? f0 : x0);
+            }
+        }
+    }
+}
+
+// warp 0: S.v0 <- U^{-1} L^{-1} S.v0 with the packed LU row-major in X (L_ij = X[i * P + j]
+// below the diagonal, U on and above; genp.cpp:106-124).  Lane l owns rows l and l + 32.
 __device__ __forceinline__ void solve_warp0(Smem& S, int lane) {
     double x0 = S.v0[lane], x1 = S.v0[lane + 32];
-    const double* r0 = S.X + lane * XP;
-    const double* r1 = S.X + (lane + 32) * XP;
-#pragma unroll
-    for (int j = 0; j < N; ++j) { // forward, unit L
-        const double yj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
-        if (j < 32 && lane > j)
-            x0 = fma(-r0[j], yj, x0);
-        if (lane + 32 > j)
-            x1 = fma(-r1[j], yj, x1);
-    }
-#pragma unroll
-    for (int j = N - 1; j >= 0; --j) { // backward, U
-        const double xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31) * S.rcp[j];
-        if (j < 32) {
-            if (lane == j)
-                x0 = xj;
-            else if (lane < j)
-                x0 = fma(-r0[j], xj, x0);
-        } else {
-            if (lane + 32 == j)
-                x1 = xj;
-            else if (lane + 32 < j)
-                x1 = fma(-r1[j], xj, x1);
-            x0 = fma(-r0[j], xj, x0);
-        }
-    }
+#pragma unroll 1
+    for (int jb = 0; jb < 32; jb += 8)
+        solve_block8<false, false>(S, jb, lane, x0, x1);
+#pragma unroll 1
+    for (int jb = 32; jb < N; jb += 8)
+        solve_block8<true, false>(S, jb, lane, x0, x1);
+#pragma unroll 1
+    for (int jb = N - 8; jb >= 32; jb -= 8)
+        solve_block8<true, true>(S, jb, lane, x0, x1);
+#pragma unroll 1
+    for (int jb = 24; jb >= 0; jb -= 8)
+        solve_block8<false, true>(S, jb, lane, x0, x1);
     S.v0[lane] = x0;
     S.v0[lane + 32] = x1;
 }
 
-// (C z)_t, z in S.v0 (t < 64)
-__device__ __forceinline__ double circ_vec(const Smem& S, uint64_t mask, int t) {
+// (C z)_t, z in S.v0
+__device__ __forceinline__ double circ_vec(const Smem& S, int t) {
+    const uint64_t mask = S.mask;
     double y = 0.0;
 #pragma unroll 16
     for (int j = 0; j < N; ++j)
@@ -325,176 +492,244 @@ __device__ __forceinline__ double cta_sum(Smem& S, double a, int t) {
     if ((t & 31) == 0)
         S.red[t >> 5] = a;
     __syncthreads();
-    const double s = (S.red[0] + S.red[1]) + (S.red[2] + S.red[3]);
+    const double s = S.red[0] + S.red[1];
     __syncthreads();
     return s;
 }
 
-// (A y)_t - b_t (t < 64), A's row t from global (L2), y in S.v1
-__device__ __forceinline__ double row_residual(const double* __restrict__ Ag, const Smem& S, double bt, int t) {
-    const double2* row = reinterpret_cast<const double2*>(Ag + t * N);
-    double s = 0.0;
-#pragma unroll 8
-    for (int j = 0; j < N / 2; ++j) {
-        const double2 a = row[j];
-        s = fma(a.x, S.v1[2 * j], s);
-        s = fma(a.y, S.v1[2 * j + 1], s);
+// (A y)_t - b_t: A's row t (registers, loaded while the solve runs), y in S.v1; four partial
+// sums keep the FMA chain short
+__device__ __forceinline__ double row_residual(const double (&arow)[N], const Smem& S, double bt) {
+    double p[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+        const double2 y = *reinterpret_cast<const double2*>(S.v1 + j);
+        p[(j >> 1) & 3] = fma(arow[j], y.x, p[(j >> 1) & 3]);
+        p[(j >> 1) & 3] = fma(arow[j + 1], y.y, p[(j >> 1) & 3]);
     }
-    return s - bt;
+    return ((p[0] + p[1]) + (p[2] + p[3])) - bt;
 }
 
-// exact singularity pre-screen: min_k |DFT(c)_k| < 1e-9 (k = 0..32 by conjugate symmetry)
-__device__ bool circ_singular(Smem& S, uint64_t mask, int t) {
+// The multiplier's spectrum: c_hat_m = sum_j c_j e^{-2 pi i jm/64} for m = 0..32 on threads
+// 0..32; H_m = (Right ? conj c_hat_m : c_hat_m) / 128.  Returns (CTA-uniform) whether c is
+// exactly singular: min_m |c_hat_m| < 1e-9 (m = 0..32 covers all bins by conjugate symmetry).
+// The twiddles (cos, sin)(2 pi m / 64) sit in the staging buffer past the sign-stream scratch.
+__device__ bool circ_spectrum(Smem& S, int t, bool left) {
+    const uint64_t mask = S.mask;
+    const double2* tw = reinterpret_cast<const double2*>(S.X + 512);
     bool sing = false;
     if (t <= 32) {
         double re = 0.0, im = 0.0;
 #pragma unroll 8
         for (int j = 0; j < N; ++j) {
-            const double2 w = S.tw[(j * t) & 63];
+            const double2 w = tw[(j * t) & 63];
             const double v = sgn(mask, j);
             re = fma(v, w.x, re);
             im = fma(-v, w.y, im);
         }
         sing = sqrt(re * re + im * im) < 1e-9;
+        S.H[t] = make_double2(re * 0.0078125, (left ? im : -im) * 0.0078125);
     }
     return __syncthreads_or(sing) != 0;
 }
 
 // One CTA per system; the raw arm and the whole redraw protocol (8 attempts on stream
 // sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) run in-kernel.
-__global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
+__global__ void __maxnreg__(248) k_batched_circ64(
     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs0, uint64_t seed,
     const uint64_t* __restrict__ sids, int refine, int left, double* __restrict__ X,
     rl_precond_report* __restrict__ rep, int* __restrict__ status) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const bool vt = t < N;                              // vector-row owner (row t)
     const uint64_t sys = blockIdx.x;
+#ifdef RL_B64_PROF
+    long long prof_t0 = clock64();
+#endif
     const double* Ag = A + sys * N * N;
-    const double bt = vt ? B[sys * N + t] : 0.0;
-    if (vt) {
+    const double* bg = B + sys * N; // b_t is re-read where needed (keeps it out of the registers)
+    {
         const unsigned bal = __ballot_sync(0xffffffffu, signs0[sys * N + t] < 0.0);
         if (lane == 0)
             S.bal[warp] = bal;
-        double s, c;
-        sincospi(static_cast<double>(t) / 32.0, &s, &c);
-        S.tw[t] = make_double2(c, s);
     }
-    __syncthreads();
-    if (t == 0)
-        S.mask0 = (static_cast<uint64_t>(S.bal[1]) << 32) | S.bal[0];
-    const double bsq = cta_sum(S, bt * bt, t);
-    const uint64_t sid = sids[sys];
-    double* xg = X + sys * N;
+    {
+        const double bt = bg[t];
+        const double bsq = cta_sum(S, bt * bt, t);
+        if (t == 0) {
+            S.mask0 = (static_cast<uint64_t>(S.bal[1]) << 32) | S.bal[0];
+            S.bsq = bsq;
+            S.rp = rl_precond_report{};
+            S.rp.attempt = -1;
+        }
+    }
     rl_precond_report& rp = S.rp; // written by thread 0 only
-    if (t == 0) {
-        rp = rl_precond_report{};
-        rp.attempt = -1;
-    }
     int st = RL_PIVOT_BREAKDOWN;
     // pass 0: raw arm (a = -1) + pre-screened protocol; pass 1 (rare): exact protocol
     for (int pass = 0; pass < 2; ++pass) {
         bool have_best = false, skipped = false, accepted = false;
-        double best_res = 0.0;
         for (int a = (pass == 0 ? -1 : 0); a < 8; ++a) {
-            uint64_t mask = 0;
+            double w[8][8];
+            const int tr = t >> 3, tc = t & 7;
             if (a >= 0) {
-                __syncthreads(); // X is free
-                if (a == 0) {
-                    mask = S.mask0;
-                } else {
-                    if (t == 0)
-                        S.mask = sign_mask_stream(seed, (sid + 7919ULL * static_cast<uint64_t>(a)) ^
-                                                            (left ? 0ULL : 0x5000000000000000ULL),
-                                                  reinterpret_cast<uint64_t*>(S.X));
-                    __syncthreads();
-                    mask = S.mask;
+                __syncthreads(); // X, H and the vectors are free
+                if (t == 0)
+                    S.mask = a == 0 ? S.mask0
+                                    : sign_mask_stream(seed, (sids[sys] + 7919ULL * static_cast<uint64_t>(a)) ^
+                                                                 (left ? 0ULL : 0x5000000000000000ULL),
+                                                       reinterpret_cast<uint64_t*>(S.X));
+                {
+                    double sn, cs;
+                    sincospi(static_cast<double>(t) / 32.0, &sn, &cs);
+                    reinterpret_cast<double2*>(S.X + 512)[t] = make_double2(cs, sn);
                 }
-                if (pass == 0 && circ_singular(S, mask, t)) {
+                __syncthreads();
+                B64_MARK(1);
+                const bool sing = circ_spectrum(S, t, left != 0);
+                B64_MARK(2);
+                if (pass == 0 && sing) {
                     skipped = true;
                     continue;
                 }
-            }
-            __syncthreads();
-            load_A(S, Ag, t);
-            __syncthreads();
-            if (a >= 0) {
-                circ_product(S, mask, t, left != 0);
+                // stage A, then W = A C (row t) / C A (column t) through the FFT
+#pragma unroll 4
+                for (int e = t; e < N * N / 2; e += THREADS) {
+                    const double2 v = reinterpret_cast<const double2*>(Ag)[e];
+                    *reinterpret_cast<double2*>(S.X + ((2 * e) >> 6) * P + ((2 * e) & 63)) = v;
+                }
                 __syncthreads();
+                double xr[N];
+                if (!left) {
+#pragma unroll
+                    for (int j = 0; j < N; j += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(S.X + t * P + j);
+                        xr[j] = v.x;
+                        xr[j + 1] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < N; ++k)
+                        xr[k] = S.X[k * P + t];
+                }
+                B64_MARK(3);
+                circ_fft64(xr, S.H);
+                B64_MARK(4);
+                __syncthreads(); // every row / column read
+                if (!left) {
+#pragma unroll
+                    for (int j = 0; j < N; j += 2)
+                        *reinterpret_cast<double2*>(S.X + t * P + j) = make_double2(xr[j], xr[j + 1]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < N; ++k)
+                        S.X[k * P + t] = xr[k];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        w[r][c] = S.X[(tr + 8 * r) * P + tc + 8 * c];
+            } else {
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        w[r][c] = Ag[(tr + 8 * r) * N + tc + 8 * c];
             }
-            if (t == 0) {
-                S.flag = 0;
-                S.pm[0] = S.pm[1] = 0.0;
-            }
+            __syncthreads(); // the spectrum and X's reads are done before the LU publishes
+            B64_MARK(5);
+            lu_regs(w, S, tr, tc);
+            B64_MARK(6);
+            __syncthreads(); // publications consumed
+            lu_store(w, S, tr, tc);
             __syncthreads();
-            double pmn = 0.0, pmx = 0.0;
-            const bool brk = lu_blocked(S, a < 0 ? 0.0 : 1e-300, t, pmn, pmx);
-            if (brk && a >= 0)
+            double arow[N]; // A's row t for the residuals (L2), in flight during the fold and solve
+#pragma unroll
+            for (int j = 0; j < N; j += 2) {
+                const double2 v = reinterpret_cast<const double2*>(Ag + t * N)[j >> 1];
+                arow[j] = v.x;
+                arow[j + 1] = v.y;
+            }
+            if (warp == 0) { // |pivot| min / max (genp.cpp:34-40) and the breakdown test
+                const double p0 = fabs(S.X[lane * (P + 1)]), p1 = fabs(S.X[(lane + 32) * (P + 1)]);
+                const double fl = a < 0 ? 0.0 : 1e-300;
+                const bool brk = __any_sync(0xffffffffu, p0 < fl || p1 < fl);
+                double mn = fmin(p0, p1), mx = fmax(p0, p1);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0) {
+                    const double first = fabs(S.X[0]); // std::min/max keep a NaN first pivot
+                    S.pm[0] = isnan(first) ? first : mn;
+                    S.pm[1] = isnan(first) ? first : mx;
+                    S.flag = brk ? 1 : 0;
+                }
+            }
+            S.v0[t] = bg[t];
+            __syncthreads();
+            B64_MARK(7);
+            if (S.flag && a >= 0)
                 continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
             const bool lft = left && a >= 0;
-            if (vt)
-                S.v0[t] = bt;
-            __syncthreads();
             if (lft) { // rhs = C b (genp.cpp:252-255)
-                const double cb = vt ? circ_vec(S, mask, t) : 0.0;
+                const double cb = circ_vec(S, t);
                 __syncthreads();
-                if (vt)
-                    S.v0[t] = cb;
+                S.v0[t] = cb;
                 __syncthreads();
             }
+            B64_MARK(8);
             if (warp == 0)
                 solve_warp0(S, lane);
             __syncthreads();
-            double y = 0.0;
-            if (vt)
-                y = (a < 0 || lft) ? S.v0[t] : circ_vec(S, mask, t); // y = z (Left) or C z (Right)
+            B64_MARK(9);
+            double y = (a < 0 || lft) ? S.v0[t] : circ_vec(S, t); // y = z (Left) or C z (Right)
             __syncthreads();
-            if (vt)
-                S.v1[t] = y;
+            S.v1[t] = y;
             __syncthreads();
+            B64_MARK(10);
             for (int s = 0; a >= 0 && s < refine; ++s) { // genp.cpp:263-274
-                if (vt)
-                    S.v0[t] = -row_residual(Ag, S, bt, t); // r = b - A y
+                S.v0[t] = -row_residual(arow, S, bg[t]); // r = b - A y
                 __syncthreads();
                 if (lft) { // rr = C r
-                    const double cr = vt ? circ_vec(S, mask, t) : 0.0;
+                    const double cr = circ_vec(S, t);
                     __syncthreads();
-                    if (vt)
-                        S.v0[t] = cr;
+                    S.v0[t] = cr;
                     __syncthreads();
                 }
                 if (warp == 0)
                     solve_warp0(S, lane);
                 __syncthreads();
-                if (vt) {
-                    y += lft ? S.v0[t] : circ_vec(S, mask, t);
-                    S.v1[t] = y;
-                }
+                y += lft ? S.v0[t] : circ_vec(S, t);
+                S.v1[t] = y;
                 __syncthreads();
             }
-            const double e = vt ? row_residual(Ag, S, bt, t) : 0.0;
-            const double res = sqrt(cta_sum(S, e * e, t)) / sqrt(bsq);
+            B64_MARK(11);
+            const double e = row_residual(arow, S, bg[t]);
+            const double res = sqrt(cta_sum(S, e * e, t)) / sqrt(S.bsq);
+            B64_MARK(12);
             if (a < 0) { // contrast arm: non-finite solution -> +inf (genp.cpp:226-231)
-                const int fin = __syncthreads_and(!vt || isfinite(y));
+                const int fin = __syncthreads_and(isfinite(y));
                 if (t == 0) {
                     rp.raw_residual = fin ? res : INFINITY;
-                    rp.raw_pivot_min = pmn;
-                    rp.raw_pivot_max = pmx;
+                    rp.raw_pivot_min = S.pm[0];
+                    rp.raw_pivot_max = S.pm[1];
                 }
                 continue;
             }
             const bool acc = res <= 1e-7;
-            if (acc || !have_best || res < best_res) {
-                if (vt)
-                    xg[t] = y;
+            if (acc || !have_best || res < S.best_res) {
+                X[sys * N + t] = y;
+                __syncthreads(); // every thread has read S.best_res
                 if (t == 0) {
                     rp.residual = res;
-                    rp.pivot_min = pmn;
-                    rp.pivot_max = pmx;
+                    rp.pivot_min = S.pm[0];
+                    rp.pivot_max = S.pm[1];
                     rp.attempt = a;
+                    S.best_res = res;
                 }
-                best_res = res;
                 have_best = true;
             }
             if (t == 0)
@@ -509,6 +744,7 @@ __global__ void __launch_bounds__(THREADS, 6) k_batched_circ64(
         if (accepted || !skipped)
             break;
     }
+    B64_MARK(13);
     if (t == 0) {
         if (rp.attempts_drawn == 0)
             rp.attempts_drawn = 8;
