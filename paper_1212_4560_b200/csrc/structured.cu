@@ -1163,13 +1163,20 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, in
         const bool two = r + 1 < m;
         const double* a0 = a + r * lda;
         const double* a1 = a0 + lda;
-        if (t == 0 && pr + gridDim.x < pairs) { // the next row pair into L2 while this one is transformed
+        // the next row pair into L2 while this one is transformed; the bulk prefetch needs a
+        // 16-byte aligned start and a multiple of 16 bytes: the 16-byte window inside each row
+        // (odd Toeplitz orders / pitches put every other row 8 bytes off)
+        if (t == 0 && pr + gridDim.x < pairs) {
             const double* nx = a + 2 * (pr + gridDim.x) * lda;
             const uint64_t rows = (2 * (pr + gridDim.x) + 1 < m) ? 2 : 1;
-            for (uint64_t q = 0; q < rows; ++q)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + q * lda),
-                             "r"(static_cast<uint32_t>(n_in * sizeof(double)))
-                             : "memory");
+            for (uint64_t q = 0; q < rows; ++q) {
+                const uint64_t b0 = reinterpret_cast<uint64_t>(nx + q * lda);
+                const uint64_t lo = (b0 + 15) & ~15ULL, hi = (b0 + n_in * sizeof(double)) & ~15ULL;
+                if (hi > lo)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
+                                 "r"(static_cast<uint32_t>(hi - lo))
+                                 : "memory");
+            }
         }
         for (int jj = t; jj < n / 8; jj += CF_THREADS)
             cf_dit_first(cz, P, jj, a0, a1, two, n_in);
