@@ -59,7 +59,9 @@ void toeplitz_dense_dev(uint64_t n, const double* g, double* out);
 void circ_apply_right_fft_dev(uint64_t m, uint64_t n, const double* c, const double* a, uint64_t lda, double* out,
                               uint64_t ldo);
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r);
-void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad, bool want_q = true);
+void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad, bool want_q = true,
+                   bool diag_only = false);
+void rank_bracket_diag_launch(int k, const double* d_rdiag, int* d_flag);
 void small_sv_launch(int k, const double* d_a, double* d_sg);
 void rank_bracket_launch(int k, const double* d_r, int* d_flag);
 std::vector<double> small_singular_values(int k, const double* d_a);
@@ -874,8 +876,9 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
     double* dr = ws<double>(WS_RF3, rho * rho);
     int* flags = ws<int>(WS_FLAGS, 4);
     RL_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), stream()));
-    cholqr3_async(m, static_cast<int>(rho), dy, d_q, dr, flags);
-    rank_bracket_launch(static_cast<int>(rho), dr, flags + 1);
+    // only the rank test needs R here: diag(R) and ||R||_F = ||Y||_F (no R_acc products)
+    cholqr3_async(m, static_cast<int>(rho), dy, d_q, dr, flags, true, true);
+    rank_bracket_diag_launch(static_cast<int>(rho), dr, flags + 1);
     // B = Q^T A (lowrank.cpp:61-64 `sta`)
     gemm_splitk(true, false, rho, n, m, 1.0, d_q, rho, d_a, n, 0.0, d_b, n, splits_for(rho, n, m));
     // sigma(B) from R of B^T
@@ -901,7 +904,12 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
         fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient sketch");
     if (hf[1] != 0) {
         bool ok = false;
-        if (hf[1] == 2) {
+        if (hf[1] == 2) { // rare: sigma_1(R) itself — Y is rebuilt and R formed in full
+            rng_generate(seed, sid, Draw::Gaussian, n * rho, 0.0, 1.0, dh);
+            gemm_splitk(false, false, m, rho, n, 1.0, d_a, n, dh, rho, 0.0, dy, rho, splits_for(m, rho, n));
+            double* qtmp = ws<double>(WS_OUT, m * rho);
+            if (!cholqr3(m, static_cast<int>(rho), dy, qtmp, dr))
+                fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient sketch");
             std::vector<double> hr(rho * rho), sr = small_singular_values(static_cast<int>(rho), dr);
             download(hr.data(), dr, rho * rho);
             double min_diag = std::numeric_limits<double>::infinity();

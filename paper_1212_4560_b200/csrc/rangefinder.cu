@@ -161,7 +161,7 @@ __device__ __forceinline__ void chol_diag8(double* W, int P, int c0, double* rdi
 // R_acc = R_pass R_acc, rows over warps, columns over lanes, ascending l).
 __global__ void __launch_bounds__(CH_T) k_chol_inv(int k, const double* g, const double* shift_part, int nshift,
                                                    double shift_coef, double* rinv, const double* racc_in,
-                                                   double* racc_out, int* bad) {
+                                                   double* racc_out, int* bad, int diag_only) {
     extern __shared__ double W[]; // KP x (KP + 1)
     __shared__ double rdiag[KMAX];
     __shared__ double T[8][KMAX + 1]; // T[c][l] = (R_0:J,J X_JJ)[l][c]; padded: 8 c's hit 8 banks
@@ -293,21 +293,46 @@ __global__ void __launch_bounds__(CH_T) k_chol_inv(int k, const double* g, const
     for (int e = tid; e < k * k; e += CH_T) {
         const int i = e / k, l = e - i * k;
         rinv[e] = (l > i) ? W[l * P + i] : (l == i ? rdiag[i] : 0.0);
-        if (!racc_in)
+        if (!racc_in && !diag_only)
             racc_out[e] = (l >= i) ? W[i * P + l] : 0.0;
     }
-    if (racc_in)
-        for (int i = warp; i < k; i += CH_T / 32)
+    if (diag_only) { // only diag(R_acc) = diag(R_pass) .* diag(R_acc_in) (triangular product)
+        for (int i = tid; i < k; i += CH_T)
+            racc_out[i] = racc_in ? W[i * P + i] * racc_in[i] : W[i * P + i];
+        return;
+    }
+    if (racc_in) { // R_acc = R_pass R_acc_in: R_acc_in (upper) transposed into W's lower half, now free
+        __syncthreads(); // X (lower half) and rdiag consumed by the rinv write
+        for (int e = tid; e < k * k; e += CH_T) {
+            const int l = e / k, j = e - l * k;
+            if (j > l)
+                W[j * P + l] = racc_in[e];
+            else if (j == l)
+                rdiag[l] = racc_in[e];
+        }
+        __syncthreads();
+        for (int i = warp; i < k; i += CH_T / 32) { // warp per row i, lane per column j
+            const double* wi = W + i * P;
             for (int j = lane; j < k; j += 32) {
                 double v = 0.0;
-                if (j >= i) {
-                    const double* wi = W + i * P;
-#pragma unroll 4
-                    for (int l = i; l <= j; ++l)
-                        v = fma(wi[l], racc_in[static_cast<size_t>(l) * k + j], v);
+                if (j >= i) { // sum_{l=i..j} R_il Racc_lj: four chains, the diagonal term last
+                    const double* wj = W + j * P;
+                    double v1 = 0.0, v2 = 0.0, v3 = 0.0;
+                    int l = i;
+                    for (; l + 3 < j; l += 4) {
+                        v = fma(wi[l], wj[l], v);
+                        v1 = fma(wi[l + 1], wj[l + 1], v1);
+                        v2 = fma(wi[l + 2], wj[l + 2], v2);
+                        v3 = fma(wi[l + 3], wj[l + 3], v3);
+                    }
+                    for (; l < j; ++l)
+                        v = fma(wi[l], wj[l], v);
+                    v = fma(wi[j], rdiag[j], (v + v1) + (v2 + v3));
                 }
                 racc_out[static_cast<size_t>(i) * k + j] = v;
             }
+        }
+    }
 }
 
 // Singular values of a k x k matrix (row-major, ld k, k <= 128) by one-sided Jacobi on the
@@ -442,7 +467,8 @@ __global__ void __launch_bounds__(JS_T) k_jacobi_sv(int k, const double* a, doub
 //   row k (twisted factorization).  d, e are pre-scaled by a power of two to sigma_max ~ 1.
 //   Each round every unconverged interval gets G = 3 probe points (one thread each);
 //   intervals shrink 4x per round to width 2^-52 sigma_max.
-constexpr int BD_T = 512;
+constexpr int BD_SUB = 4; // threads per reflector dot product (8 per column x 1024 threads measured slower)
+constexpr int BD_T = 512;  // up to 128 columns x 4 threads
 // Row pitch = 4 (mod 16) doubles: a half-warp touching 4 rows x 4 consecutive columns hits
 // 16 distinct 8-byte bank pairs (the updates are shared-memory-bandwidth bound).
 __host__ __device__ constexpr int bd_pitch(int k) { return k + ((4 - k) & 15); }
@@ -525,11 +551,12 @@ __device__ __forceinline__ int tgk_count_below(const double* bb, int k, double x
     const double dm = (q0 == 0.0) ? 1e300 : q1 * rcp_nr(q0);
     return neg + ((dp + dm + x) < 0.0) - k;
 }
-__global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, double* sigma) {
+__global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, double* sigma, int gprobe) {
     extern __shared__ double A[]; // k x bd_pitch(k)
     __shared__ double sq[KMAX], sq2[KMAX], d[KMAX], e[KMAX], bb[2 * KMAX], lo[KMAX], up[KMAX];
     __shared__ int cnt[BD_T];
     __shared__ double s_hi;
+    constexpr int SUB = BD_SUB; // threads per column (left reflector) / row (right reflector)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int P = bd_pitch(k);
     const long long t_start = clock64();
@@ -541,8 +568,8 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
     }
     __syncthreads();
     for (int j = 0; j < k; ++j) {
-        if (j + 1 + warp * 8 < k) { // left reflector of column j (rows j .. k-1), formed by every
-                                     // warp with a column c > j to update
+        if (j + 1 + warp * (32 / SUB) < k) { // left reflector of column j (rows j .. k-1), formed
+                                              // by every warp with a column c > j to update
             const double ts = range_sum(sq, j + 1, k, lane);
             const double x0 = A[j * P + j], ss = fma(x0, x0, ts);
             double alpha = 0.0, tau = 0.0, v0 = x0;
@@ -554,36 +581,37 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
             }
             if (tid == 0)
                 d[j] = alpha;
-            const int c = j + 1 + (tid >> 2), sub = tid & 3;
+            const int c = j + 1 + tid / SUB, sub = tid % SUB;
             const bool on = c < k && tau != 0.0;
-            // rows: sub 0 takes row j (v_j = v0) then j+4, j+8, ...; sub s takes j+s, j+s+4, ...
-            const int i0 = j + sub + (sub == 0 ? 4 : 0);
+            // rows: sub 0 takes row j (v_j = v0) then j+SUB, ...; sub s takes j+s, j+s+SUB, ...
+            const int i0 = j + sub + (sub == 0 ? SUB : 0);
             double s0 = 0.0, s1 = 0.0, ajc = 0.0;
             if (on) {
                 ajc = A[j * P + c];
                 if (sub == 0)
                     s0 = v0 * ajc;
                 int i = i0;
-                for (; i + 4 < k; i += 8) {
+                for (; i + SUB < k; i += 2 * SUB) {
                     s0 = fma(A[i * P + j], A[i * P + c], s0);
-                    s1 = fma(A[(i + 4) * P + j], A[(i + 4) * P + c], s1);
+                    s1 = fma(A[(i + SUB) * P + j], A[(i + SUB) * P + c], s1);
                 }
                 if (i < k)
                     s0 = fma(A[i * P + j], A[i * P + c], s0);
             }
             s0 += s1;
-            s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-            s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+#pragma unroll
+            for (int o = 1; o < SUB; o <<= 1)
+                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
             if (on) {
                 const double w = tau * s0;
                 if (sub == 0)
                     A[j * P + c] = fma(-w, v0, ajc);
                 int i = i0;
-                for (; i + 4 < k; i += 8) { // loads ahead of stores: two independent updates
-                    const double a0 = A[i * P + c], a1 = A[(i + 4) * P + c];
-                    const double v0i = A[i * P + j], v1 = A[(i + 4) * P + j];
+                for (; i + SUB < k; i += 2 * SUB) { // loads ahead of stores: two independent updates
+                    const double a0 = A[i * P + c], a1 = A[(i + SUB) * P + c];
+                    const double v0i = A[i * P + j], v1 = A[(i + SUB) * P + j];
                     A[i * P + c] = fma(-w, v0i, a0);
-                    A[(i + 4) * P + c] = fma(-w, v1, a1);
+                    A[(i + SUB) * P + c] = fma(-w, v1, a1);
                 }
                 if (i < k)
                     A[i * P + c] = fma(-w, A[i * P + j], A[i * P + c]);
@@ -599,8 +627,8 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
         __syncthreads();
         if (j == k - 1)
             break;
-        if (j + 1 + warp * 8 < k) { // right reflector of row j (columns j+1 .. k-1), formed by
-                                     // every warp with a row r > j to update
+        if (j + 1 + warp * (32 / SUB) < k) { // right reflector of row j (columns j+1 .. k-1),
+                                              // formed by every warp with a row r > j to update
             const double ts = range_sum(sq2, j + 2, k, lane);
             const double y0 = A[j * P + j + 1], ss = fma(y0, y0, ts);
             double beta = 0.0, tau = 0.0, u0 = y0;
@@ -613,37 +641,38 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
             if (tid == 0)
                 e[j] = beta;
             const double* urow = A + j * P;
-            const int r = j + 1 + (tid >> 2), sub = tid & 3;
+            const int r = j + 1 + tid / SUB, sub = tid % SUB;
             const bool on = r < k && tau != 0.0;
             double* row = A + (r < k ? r : 0) * P;
-            // columns: sub 0 takes column j+1 (u = u0) then j+5, ...; sub s takes j+1+s, ...
-            const int c0 = j + 1 + sub + (sub == 0 ? 4 : 0);
+            // columns: sub 0 takes column j+1 (u = u0) then j+1+SUB, ...; sub s takes j+1+s, ...
+            const int c0 = j + 1 + sub + (sub == 0 ? SUB : 0);
             double s0 = 0.0, s1 = 0.0, arj = 0.0;
             if (on) {
                 arj = row[j + 1];
                 if (sub == 0)
                     s0 = arj * u0;
                 int c = c0;
-                for (; c + 4 < k; c += 8) {
+                for (; c + SUB < k; c += 2 * SUB) {
                     s0 = fma(row[c], urow[c], s0);
-                    s1 = fma(row[c + 4], urow[c + 4], s1);
+                    s1 = fma(row[c + SUB], urow[c + SUB], s1);
                 }
                 if (c < k)
                     s0 = fma(row[c], urow[c], s0);
             }
             s0 += s1;
-            s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-            s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+#pragma unroll
+            for (int o = 1; o < SUB; o <<= 1)
+                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
             if (on) {
                 const double w = tau * s0;
                 if (sub == 0)
                     row[j + 1] = fma(-w, u0, arj);
                 int c = c0;
-                for (; c + 4 < k; c += 8) {
-                    const double a0 = row[c], a1 = row[c + 4];
-                    const double u0c = urow[c], u1 = urow[c + 4];
+                for (; c + SUB < k; c += 2 * SUB) {
+                    const double a0 = row[c], a1 = row[c + SUB];
+                    const double u0c = urow[c], u1 = urow[c + SUB];
                     row[c] = fma(-w, u0c, a0);
-                    row[c + 4] = fma(-w, u1, a1);
+                    row[c + SUB] = fma(-w, u1, a1);
                 }
                 if (c < k)
                     row[c] = fma(-w, urow[c], row[c]);
@@ -697,7 +726,7 @@ __global__ void __launch_bounds__(BD_T) k_bidiag_sv(int k, const double* a, doub
     }
     __syncthreads();
     // probes per interval: 3 (2 bits a round) keeps the count evaluations off the issue limit
-    const int G = min(3, BD_T / k);
+    const int G = max(1, min(gprobe, BD_T / k));
     for (int round = 0; round < 200; ++round) {
         const int m = tid / G, g = tid - m * G;
         int c = -1;
@@ -867,7 +896,8 @@ void small_sv_launch(int k, const double* d_a, double* d_sg) {
                                          KMAX * bd_pitch(KMAX) * 8));
             attr[ctx().device & 15] = true;
         }
-        k_bidiag_sv<<<1, BD_T, static_cast<size_t>(k) * bd_pitch(k) * 8, stream()>>>(k, d_a, d_sg);
+        static const int gprobe = getenv("RL_BD_PROBES") ? atoi(getenv("RL_BD_PROBES")) : 3; // dev sweeps
+        k_bidiag_sv<<<1, BD_T, static_cast<size_t>(k) * bd_pitch(k) * 8, stream()>>>(k, d_a, d_sg, gprobe);
     } else {
         JacobiKernel kern = jacobi_for(k);
         kern<<<1, JS_T, static_cast<size_t>(k) * k * 8, stream()>>>(k, d_a, d_sg);
@@ -924,6 +954,32 @@ __global__ void k_rank_bracket(int k, const double* __restrict__ r, int* flag) {
 }
 } // namespace
 
+namespace {
+// The same bracket from diag(R) and ||Y||_F^2 = ||R||_F^2 (sum of nparts partials).
+__global__ void k_rank_bracket_diag(int k, const double* __restrict__ rdiag, const double* __restrict__ part,
+                                    int nparts, int* flag) {
+    const int lane = threadIdx.x;
+    double ss = 0.0, mn = INFINITY;
+    for (int e = lane; e < nparts; e += 32)
+        ss += part[e];
+    for (int i = lane; i < k; i += 32)
+        mn = fmin(mn, fabs(rdiag[i]));
+    for (int o = 16; o > 0; o >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0) {
+        const double fro = sqrt(ss);
+        *flag = (mn > 1e-13 * fro) ? 0 : (mn <= 1e-13 * fro / sqrt(static_cast<double>(k)) ? 1 : 2);
+    }
+}
+} // namespace
+
+void rank_bracket_diag_launch(int k, const double* d_rdiag, int* d_flag) {
+    k_rank_bracket_diag<<<1, 32, 0, stream()>>>(k, d_rdiag, ws<double>(WS_RESID, 256), 256, d_flag);
+    RL_LAUNCHED();
+}
+
 void rank_bracket_launch(int k, const double* d_r, int* d_flag) {
     k_rank_bracket<<<1, 256, 0, stream()>>>(k, d_r, d_flag);
     RL_LAUNCHED();
@@ -933,7 +989,10 @@ void rank_bracket_launch(int k, const double* d_r, int* d_flag) {
 // diag(r) > 0. Per pass: the Gram (split-K GEMM), k_chol_inv (R and R^-1), Q = src R^-1 on DMMA
 // and R_acc = R_pass R_acc. No host round trip: the shift is summed on the device and the failure
 // flag d_bad (int, device) is sticky — the caller reads it whenever it next synchronises.
-void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad, bool want_q) {
+// diag_only: r receives only diag(R) (k values) — the R_acc products are skipped (callers that
+// need just the rank test: ||R||_F = ||Y||_F and diag(R) = the product of the passes' diagonals).
+void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int* d_bad, bool want_q,
+                   bool diag_only) {
     if (k > KMAX)
         fail(RL_TOO_LARGE, "qr_positive: more than 128 columns");
     double* g = ws<double>(WS_RF4, 3 * KMAX * KMAX + 64);
@@ -960,7 +1019,7 @@ void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int
         // R_pass, R_pass^-1 and R_acc = R_pass R_acc in one kernel
         double* racc_out = pass == 2 ? r : (pass == 0 ? racc0 : racc1);
         k_chol_inv<<<1, CH_T, chol_smem, stream()>>>(k, g, pass == 0 ? part : nullptr, kParts, coef, rinv, racc_in,
-                                                     racc_out, d_bad);
+                                                     racc_out, d_bad, diag_only ? 1 : 0);
         RL_LAUNCHED();
         racc_in = racc_out;
         // Q_pass = src R_pass^-1 on DMMA (the last pass only when the caller wants Q)
@@ -975,7 +1034,7 @@ void cholqr3_async(uint64_t m, int k, const double* y, double* q, double* r, int
 bool cholqr3(uint64_t m, int k, const double* y, double* q, double* r) {
     int* d_bad = ws<int>(WS_FLAGS, 4);
     RL_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), stream()));
-    cholqr3_async(m, k, y, q, r, d_bad, true);
+    cholqr3_async(m, k, y, q, r, d_bad, true, false);
     int bad = 0;
     RL_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, stream()));
     RL_CUDA(cudaStreamSynchronize(stream()));
