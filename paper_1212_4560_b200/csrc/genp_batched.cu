@@ -61,6 +61,7 @@ constexpr int PUB_RP = 10, PUB_C = 8 * PUB_RP, PUB = PUB_C + 64;
 struct Smem {
     double X[N * P]; // A staging / W / packed LU (row-major); sign-stream scratch and DFT twiddles
     double rcp[N];   // 1/U_kk
+    double pubb[2];  // the forward-substituted right-hand side's pivot entry, per parity
     union {
         double pub[2 * PUB]; // the LU's row / column publications (two parities x (row, column))
         struct {
@@ -268,19 +269,16 @@ __device__ __forceinline__ void circ_fft64(double (&x)[N], const double2* __rest
 
 // ------------------------------------------------------------------- LU ----
 // 1/p without branches (every thread evaluates it; the pivot's owner publishes it): the
-// hardware estimate plus two Newton steps on p scaled by a power of two into the estimate's
-// range (exact), the scale applied again to the result; 0 -> 0 (the reference's m = 0 for a
-// zero pivot), +-inf -> 0.
+// hardware estimate plus two Newton steps, exact to rounding for 2^-1022 <= |p| <= 2^1022;
+// 0 -> 0 (the reference's m = 0 for a zero pivot), +-inf -> 0.  (Subnormal pivots give an
+// infinite reciprocal — the reference's w / p overflows there too.)
 __device__ __forceinline__ double pivot_rcp_nb(double p) {
-    const double ap = fabs(p);
-    const double sc = ap < 0x1p-960 ? 0x1p+600 : (ap > 0x1p+960 ? 0x1p-600 : 1.0);
-    const double q = p * sc;
     double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-    double e = fma(-q, r, 1.0);
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+    double e = fma(-p, r, 1.0);
     r = fma(r, e, r);
-    e = fma(-q, r, 1.0);
-    r = fma(r, e, r) * sc;
+    e = fma(-p, r, 1.0);
+    r = fma(r, e, r);
     return (p == 0.0 || isinf(p)) ? 0.0 : r;
 }
 
@@ -301,11 +299,12 @@ __device__ __forceinline__ void st2_if(double* dst, double v0, double v1, bool p
 // (s, tc), column k as pub[par][PUB_C + tr*8 + r] by the owners (tr, s); 1/p into rcp[k].
 // Predicated stores, no branches (a divergent branch costs a reconvergence barrier per step).
 template <int K>
-__device__ __forceinline__ void lu_publish(const double (&w)[8][8], Smem& S, int s, int tr, int tc) {
+__device__ __forceinline__ void lu_publish(const double (&w)[8][8], double bcur, Smem& S, int s, int tr, int tc) {
     double* ur = S.pub + (s & 1) * PUB + tc * PUB_RP;
     double* uc = S.pub + (s & 1) * PUB + PUB_C + tr * 8;
     const bool oc = tc == s, orow = tr == s;
     st_if(S.rcp + 8 * K + s, pivot_rcp_nb(w[K][K]), oc && orow);
+    st_if(S.pubb + (s & 1), bcur, static_cast<int>(threadIdx.x) == 8 * K + s); // b_k by thread k
 #pragma unroll
     for (int r = K & ~1; r < 8; r += 2)
         st2_if(uc + r, w[r][K], w[r + 1][K], oc);
@@ -322,12 +321,19 @@ __device__ __forceinline__ void lu_publish(const double (&w)[8][8], Smem& S, int
 // w(i,k) and L = w(i,k) / p is formed once at the end (lu_store), the same product the update
 // used.  The next step's row / column (KC) are updated and published first, then the rest.
 template <int K, int PAR, bool LAST>
-__device__ __forceinline__ void lu_step(double (&w)[8][8], Smem& S, int s, int tr, int tc) {
+__device__ __forceinline__ void lu_step(double (&w)[8][8], double& bcur, Smem& S, int s, int tr, int tc) {
     constexpr int KC = LAST ? K + 1 : K;
     __syncthreads();
     const double* ur = S.pub + PAR * PUB + tc * PUB_RP;
     const double* uc = S.pub + PAR * PUB + PUB_C + tr * 8;
     const double inv = S.rcp[8 * K + s];
+    { // forward substitution of the right-hand side alongside (genp.cpp:110-115's order):
+      // thread t holds b_t; rows below the pivot subtract m_t b_k
+        const int t = threadIdx.x, k = 8 * K + s;
+        const double mt = S.pub[PAR * PUB + PUB_C + (t & 7) * 8 + (t >> 3)] * inv;
+        const double f = fma(-mt, S.pubb[PAR], bcur);
+        bcur = t > k ? f : bcur;
+    }
     double m[8], u[8];
 #pragma unroll
     for (int r = K & ~1; r < 8; r += 2) {
@@ -353,7 +359,7 @@ __device__ __forceinline__ void lu_step(double (&w)[8][8], Smem& S, int s, int t
         for (int r = K; r < 8; ++r)
             if (r != KC)
                 w[r][KC] = fma(-m[r], u[KC], w[r][KC]);
-        lu_publish<(KC < 8 ? KC : 7)>(w, S, LAST ? 0 : s + 1, tr, tc);
+        lu_publish<(KC < 8 ? KC : 7)>(w, bcur, S, LAST ? 0 : s + 1, tr, tc);
     }
 #pragma unroll
     for (int c = K; c < 8; ++c) {
@@ -369,30 +375,30 @@ __device__ __forceinline__ void lu_step(double (&w)[8][8], Smem& S, int s, int t
 // The eight pivot steps k = 8K .. 8K+7 of block K; the step index only enters predicates, so
 // one loop body per block and parity (the register indices are compile-time) keeps the code small.
 template <int K>
-__device__ __forceinline__ void lu_block(double (&w)[8][8], Smem& S, int tr, int tc) {
+__device__ __forceinline__ void lu_block(double (&w)[8][8], double& bcur, Smem& S, int tr, int tc) {
 #pragma unroll 1
     for (int s = 0; s < 6; s += 2) {
-        lu_step<K, 0, false>(w, S, s, tr, tc);
-        lu_step<K, 1, false>(w, S, s + 1, tr, tc);
+        lu_step<K, 0, false>(w, bcur, S, s, tr, tc);
+        lu_step<K, 1, false>(w, bcur, S, s + 1, tr, tc);
     }
-    lu_step<K, 0, false>(w, S, 6, tr, tc);
-    lu_step<K, 1, true>(w, S, 7, tr, tc);
+    lu_step<K, 0, false>(w, bcur, S, 6, tr, tc);
+    lu_step<K, 1, true>(w, bcur, S, 7, tr, tc);
 }
 
 // No-pivot LU of the register-resident matrix (genp.cpp:20-33): one barrier per pivot step.
 // On exit w holds U on and above the diagonal and w(i,k) (un-normalised) below; S.rcp[k] =
-// 1/U_kk.  S.pub (aliasing the vectors and the spectrum) carries the publications (callers
-// fence before and after).
-__device__ __forceinline__ void lu_regs(double (&w)[8][8], Smem& S, int tr, int tc) {
-    lu_publish<0>(w, S, 0, tr, tc);
-    lu_block<0>(w, S, tr, tc);
-    lu_block<1>(w, S, tr, tc);
-    lu_block<2>(w, S, tr, tc);
-    lu_block<3>(w, S, tr, tc);
-    lu_block<4>(w, S, tr, tc);
-    lu_block<5>(w, S, tr, tc);
-    lu_block<6>(w, S, tr, tc);
-    lu_block<7>(w, S, tr, tc);
+// 1/U_kk; thread t's bcur (b_t on entry) holds (L^-1 b)_t.  S.pub (aliasing the vectors and
+// the spectrum) carries the publications (callers fence before and after).
+__device__ __forceinline__ void lu_regs(double (&w)[8][8], double& bcur, Smem& S, int tr, int tc) {
+    lu_publish<0>(w, bcur, S, 0, tr, tc);
+    lu_block<0>(w, bcur, S, tr, tc);
+    lu_block<1>(w, bcur, S, tr, tc);
+    lu_block<2>(w, bcur, S, tr, tc);
+    lu_block<3>(w, bcur, S, tr, tc);
+    lu_block<4>(w, bcur, S, tr, tc);
+    lu_block<5>(w, bcur, S, tr, tc);
+    lu_block<6>(w, bcur, S, tr, tc);
+    lu_block<7>(w, bcur, S, tr, tc);
 }
 
 // The packed LU into X (row-major): U as factored, L_ij = w(i,j) * (1/U_jj) below the diagonal.
@@ -454,16 +460,21 @@ __device__ __forceinline__ void solve_block8(const Smem& S, int jb, int lane, do
     }
 }
 
-// warp 0: S.v0 <- U^{-1} L^{-1} S.v0 with the packed LU row-major in X (L_ij = X[i * P + j]
-// below the diagonal, U on and above; genp.cpp:106-124).  Lane l owns rows l and l + 32.
+// warp 0: S.v0 <- U^{-1} L^{-1} S.v0 (FWD) or U^{-1} S.v0 with the packed LU row-major in X
+// (L_ij = X[i * P + j] below the diagonal, U on and above; genp.cpp:106-124).  Lane l owns
+// rows l and l + 32.  (The factorization's own right-hand side is forward-substituted inside
+// the LU; refinement steps run both halves here.)
+template <bool FWD>
 __device__ __forceinline__ void solve_warp0(Smem& S, int lane) {
     double x0 = S.v0[lane], x1 = S.v0[lane + 32];
+    if (FWD) {
 #pragma unroll 1
-    for (int jb = 0; jb < 32; jb += 8)
-        solve_block8<false, false>(S, jb, lane, x0, x1);
+        for (int jb = 0; jb < 32; jb += 8)
+            solve_block8<false, false>(S, jb, lane, x0, x1);
 #pragma unroll 1
-    for (int jb = 32; jb < N; jb += 8)
-        solve_block8<true, false>(S, jb, lane, x0, x1);
+        for (int jb = 32; jb < N; jb += 8)
+            solve_block8<true, false>(S, jb, lane, x0, x1);
+    }
 #pragma unroll 1
     for (int jb = N - 8; jb >= 32; jb -= 8)
         solve_block8<true, true>(S, jb, lane, x0, x1);
@@ -637,9 +648,16 @@ __global__ void __maxnreg__(248) k_batched_circ64(
                     for (int c = 0; c < 8; ++c)
                         w[r][c] = Ag[(tr + 8 * r) * N + tc + 8 * c];
             }
-            __syncthreads(); // the spectrum and X's reads are done before the LU publishes
+            const bool lft = left && a >= 0;
+            double bcur = bg[t]; // the right-hand side, forward-substituted inside the LU
+            if (lft) {           // rhs = C b (genp.cpp:252-255)
+                S.v0[t] = bcur;
+                __syncthreads();
+                bcur = circ_vec(S, t);
+            }
+            __syncthreads(); // the spectrum, X's and v0's reads are done before the LU publishes
             B64_MARK(5);
-            lu_regs(w, S, tr, tc);
+            lu_regs(w, bcur, S, tr, tc);
             B64_MARK(6);
             __syncthreads(); // publications consumed
             lu_store(w, S, tr, tc);
@@ -668,21 +686,14 @@ __global__ void __maxnreg__(248) k_batched_circ64(
                     S.flag = brk ? 1 : 0;
                 }
             }
-            S.v0[t] = bg[t];
+            S.v0[t] = bcur; // L^-1 rhs
             __syncthreads();
             B64_MARK(7);
             if (S.flag && a >= 0)
                 continue; // PivotBreakdown: next attempt (genp.cpp:285-288)
-            const bool lft = left && a >= 0;
-            if (lft) { // rhs = C b (genp.cpp:252-255)
-                const double cb = circ_vec(S, t);
-                __syncthreads();
-                S.v0[t] = cb;
-                __syncthreads();
-            }
             B64_MARK(8);
             if (warp == 0)
-                solve_warp0(S, lane);
+                solve_warp0<false>(S, lane);
             __syncthreads();
             B64_MARK(9);
             double y = (a < 0 || lft) ? S.v0[t] : circ_vec(S, t); // y = z (Left) or C z (Right)
@@ -700,7 +711,7 @@ __global__ void __maxnreg__(248) k_batched_circ64(
                     __syncthreads();
                 }
                 if (warp == 0)
-                    solve_warp0(S, lane);
+                    solve_warp0<true>(S, lane);
                 __syncthreads();
                 y += lft ? S.v0[t] : circ_vec(S, t);
                 S.v1[t] = y;
