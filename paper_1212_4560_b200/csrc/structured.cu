@@ -12,6 +12,7 @@
 //  * NEW sparse +-1 S (nnz per column): (A S)(i,j) = sum_t s_jt A(i, r_jt), a row-tiled
 //    gather (row of A in shared memory, index/sign table from L2): 2 n^2 doubles.
 #include <cstdio>
+#include <cstdlib>
 
 #include "rl_internal.cuh"
 
@@ -1191,6 +1192,292 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_circ_right_fft(uint64_t m, in
     }
 }
 
+
+// ---- n = 8192: register-resident radix 16 x 16 x 32 ----------------------------------------
+// The general kernel above spends ~390 instructions per element (runtime index / twiddle
+// arithmetic in every radix-8 pass, eight shared-memory round trips per transform pair: ncu
+// 112 K warp instructions per row pair, issue-bound at 49%).  For n = 8192 = 16 * 16 * 32 the
+// transform is a three-level four-step FFT whose sub-DFTs run in registers with compile-time
+// twiddles; one table twiddle per element between levels (W^m = hi[m / 64] lo[m % 64],
+// W = e^{-2 pi i / 8192}, sign-folded for m >= 4096):
+//   P1  thread b < 512: x[512 a + b], a < 16 straight from the two rows (coalesced) -> DFT16
+//       over a -> * W^{b c} -> slot (c, b)
+//   P2  thread (c, f): slots (c, 32 e + f), e < 16 -> DFT16 over e -> * W_512^{f g} -> (c, 32 g + f)
+//   P3  thread pair (c, g; gamma): the 32 contiguous slots (c, 32 g + f): a radix-2 step over
+//       f's top bit (each thread its half gamma, * W_32^{beta gamma}) and DFT16 over beta give
+//       X[c + 16 g + 256 (gamma + 2 delta)]; the product with conj(FFT(c)) / n; the adjoint
+//       (inverse DFT16 over delta, the radix-2 recombination with the partner lane by
+//       shuffles) back to the 32 slots
+//   P2', P1'  the adjoints of P2 and P1 (conjugate twiddles, inverse DFT16), P1' storing the
+//       two output rows (coalesced).
+// Shared index i lives at i + (i >> 5): the P3 pairs' 16 groups (33 slots apart) hit distinct
+// bank groups.  Four barriers per row pair, ~30 K warp instructions.
+constexpr int F8_N = 8192, F8_T = 512;
+__device__ __forceinline__ int f8_at(int i) { return i + (i >> 5); }
+
+// (cos, sin)(2 pi j / 64), j < 32
+__constant__ double2 kF8CS[32] = {
+    {0x1.0000000000000p+0, 0.0},
+    {0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},
+    {0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3},
+    {0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},
+    {0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},
+    {0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},
+    {0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1},
+    {0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},
+    {0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},
+    {0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},
+    {0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1},
+    {0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},
+    {0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},
+    {0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},
+    {0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1},
+    {0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},
+    {0.0, 0x1.0000000000000p+0},
+    {-0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},
+    {-0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1},
+    {-0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},
+    {-0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},
+    {-0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},
+    {-0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1},
+    {-0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},
+    {-0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},
+    {-0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},
+    {-0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1},
+    {-0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},
+    {-0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},
+    {-0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},
+    {-0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3},
+    {-0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},
+};
+
+__host__ __device__ constexpr int br4(int m) { return ((m & 1) << 3) | ((m & 2) << 1) | ((m & 4) >> 1) | ((m & 8) >> 3); }
+
+// v *= e^{-+2 pi i j / 64} (INV: +), j < 32 a compile-time constant after unrolling
+template <bool INV>
+__device__ __forceinline__ double2 f8_rot(double2 v, int j) {
+    if (j == 0)
+        return v;
+    if (j == 16)
+        return INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
+    if (j == 8 || j == 24) { // (1 -+ i) / sqrt 2 and its mirror: two roundings
+        constexpr double r = 0.70710678118654752440;
+        const double2 u = INV ? make_double2(v.x - v.y, v.x + v.y) : make_double2(v.x + v.y, v.y - v.x);
+        const double2 e = make_double2(u.x * r, u.y * r);
+        return j == 8 ? e : (INV ? make_double2(-e.y, e.x) : make_double2(e.y, -e.x));
+    }
+    const double c = kF8CS[j].x, sn = INV ? kF8CS[j].y : -kF8CS[j].y;
+    return make_double2(fma(v.x, c, -v.y * sn), fma(v.x, sn, v.y * c));
+}
+
+// In-place 16-point DFT (INV: e^{+}), decimation in frequency: natural order in, X[k] out at
+// v[br4(k)]
+template <bool INV>
+__device__ __forceinline__ void f8_dft16(double2 (&v)[16]) {
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+        const int half = 8 >> st;
+#pragma unroll
+        for (int g = 0; g < 16; g += 2 * half)
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const int a = g + k, b = a + half;
+                const double2 u = v[a], w = v[b];
+                v[a] = cadd(u, w);
+                v[b] = f8_rot<INV>(csub(u, w), (32 / half) * k);
+            }
+    }
+}
+
+struct F8Tw {
+    const double2* lo; // W^j, j < 64
+    const double2* hi; // W^{64 j}, j < 64
+    __device__ __forceinline__ double2 w(int m) const { // W^m, 0 <= m < 8192
+        const double2 r = cmul(hi[(m >> 6) & 63], lo[m & 63]);
+        return (m & 4096) ? make_double2(-r.x, -r.y) : r;
+    }
+};
+
+// chat (natural order) -> P3's thread order: chat_p[512 d + t] = chat[c + 16 g + 256 gam + 512 d]
+// for thread t = 2 (16 c + g) + gam
+__global__ void k_f8_perm(const double2* __restrict__ chat, double2* __restrict__ chat_p) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x; // < 8192
+    const int d = e >> 9, t = e & 511, G = t >> 1, gam = t & 1;
+    chat_p[e] = chat[(G >> 4) + 16 * (G & 15) + 256 * gam + 512 * d];
+}
+
+__global__ void __launch_bounds__(F8_T, 1) k_circ_fft8k(uint64_t m, const double* __restrict__ a, uint64_t lda,
+                                                       const double2* __restrict__ chat, double* __restrict__ out,
+                                                       uint64_t ldo) {
+    extern __shared__ double2 sz[]; // f8_at(8192) slots
+    __shared__ double2 tlo[64], thi[64];
+    const int t = threadIdx.x;
+    if (t < 64) {
+        double sn, cs;
+        sincospi(static_cast<double>(t) / 4096.0, &sn, &cs);
+        tlo[t] = make_double2(cs, -sn);
+        sincospi(static_cast<double>(t) / 64.0, &sn, &cs);
+        thi[t] = make_double2(cs, -sn);
+    }
+    __syncthreads();
+    const F8Tw T{tlo, thi};
+    const uint64_t pairs = (m + 1) / 2;
+    double* sd = reinterpret_cast<double*>(sz); // input staging: row 0 at [0, 8192), row 1 at [8192, 16384)
+    // the row pair pr's two rows into the staging area (cp.async, 16 B each; a missing second
+    // row is zero-filled) — issued under the previous pair's last pass
+    auto stage = [&](uint64_t pr) {
+        const uint64_t r0 = 2 * pr;
+        const double* g0 = a + r0 * lda;
+        const double* g1 = r0 + 1 < m ? g0 + lda : g0;
+        const uint32_t nb1 = r0 + 1 < m ? 16u : 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = 2 * (t + 512 * q);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sd + e)), "l"(g0 + e)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sd + F8_N + e)), "l"(g1 + e),
+                         "r"(nb1)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (t < 2 && pr + gridDim.x < pairs) { // and the pair after it into L2 (16-byte aligned window)
+            const uint64_t nr = 2 * (pr + gridDim.x) + t;
+            if (nr < m) {
+                const uint64_t b0 = reinterpret_cast<uint64_t>(a + nr * lda);
+                const uint64_t lo16 = (b0 + 15) & ~15ULL, hi16 = (b0 + F8_N * sizeof(double)) & ~15ULL;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo16),
+                             "r"(static_cast<uint32_t>(hi16 - lo16))
+                             : "memory");
+            }
+        }
+    };
+    if (blockIdx.x < pairs)
+        stage(blockIdx.x);
+    for (uint64_t pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+        const uint64_t r0 = 2 * pr;
+        const bool two = r0 + 1 < m;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads(); // this pair's rows are staged
+        { // P1: thread b = t
+            double2 v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                v[q] = make_double2(sd[512 * q + t], sd[F8_N + 512 * q + t]);
+            __syncthreads(); // every staged value read before the slots are written
+            f8_dft16<false>(v);
+            // W^{t c}, c = 1.. by repeated products (a few ulps, below the FFT's own error); the
+            // base is re-read each row pair so the power chains stay inside the loop
+            const double2 w1 = T.w(t);
+            double2 wc = w1;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                double2 y = v[br4(c)];
+                if (c) {
+                    y = cmul(y, wc);
+                    wc = cmul(wc, w1);
+                }
+                sz[f8_at(c * 512 + t)] = y;
+            }
+        }
+        __syncthreads();
+        const int c2 = t >> 5, f2 = t & 31, base2 = c2 * 512 + f2;
+        { // P2: thread (c, f)
+            double2 v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                v[e] = sz[f8_at(base2 + 32 * e)];
+            f8_dft16<false>(v);
+            const double2 w2 = T.w(16 * f2);
+            double2 wg = w2; // W_512^{f g}
+#pragma unroll
+            for (int g = 0; g < 16; ++g) {
+                double2 y = v[br4(g)];
+                if (g) {
+                    y = cmul(y, wg);
+                    wg = cmul(wg, w2);
+                }
+                sz[f8_at(base2 + 32 * g)] = y;
+            }
+        }
+        __syncthreads();
+        { // P3: the pair (c, g) = t >> 1, gamma = t & 1
+            const int G = t >> 1, gam = t & 1, c3 = G >> 4, g3 = G & 15, base3 = c3 * 512 + 32 * g3;
+            double2 v[16];
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const double2 u0 = sz[f8_at(base3 + b)], u1 = sz[f8_at(base3 + 16 + b)];
+                double2 s = gam ? csub(u0, u1) : cadd(u0, u1);
+                if (b) {
+                    const double2 r = f8_rot<false>(s, 2 * b); // W_32^b = e^{-2 pi i (2b) / 64}
+                    s = gam ? r : s;
+                }
+                v[b] = s;
+            }
+            __syncwarp();       // the pair's reads of its 32 slots are done before either writes
+            f8_dft16<false>(v); // X[c + 16 g + 256 (gam + 2 d)] at v[br4(d)]
+            double2 y[16];      // natural order in d for the inverse
+#pragma unroll
+            for (int d = 0; d < 16; ++d) // chat in P3's thread order (k_f8_perm): coalesced, L1-resident
+                y[d] = cmul(v[br4(d)], chat[512 * d + t]);
+            f8_dft16<true>(y); // A_gam[f'] at y[br4(f')]
+#pragma unroll
+            for (int q = 0; q < 16; ++q) { // out[16 gam + q] = A0[q] + (-1)^gam conj(W_32^q) A1[q]
+                const double2 mine = y[br4(q)];
+                const double2 other = make_double2(__shfl_xor_sync(0xffffffffu, mine.x, 1),
+                                                   __shfl_xor_sync(0xffffffffu, mine.y, 1));
+                const double2 a0v = gam ? other : mine, a1v = gam ? mine : other;
+                const double2 t1 = f8_rot<true>(a1v, 2 * q); // conj(W_32^q) A1[q]
+                sz[f8_at(base3 + 16 * gam + q)] = gam ? csub(a0v, t1) : cadd(a0v, t1);
+            }
+        }
+        __syncthreads();
+        { // P2': adjoint of P2
+            double2 v[16];
+            const double2 w2 = cconj(T.w(16 * f2));
+            double2 wg = w2;
+#pragma unroll
+            for (int g = 0; g < 16; ++g) {
+                double2 y = sz[f8_at(base2 + 32 * g)];
+                if (g) {
+                    y = cmul(y, wg);
+                    wg = cmul(wg, w2);
+                }
+                v[g] = y;
+            }
+            f8_dft16<true>(v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                sz[f8_at(base2 + 32 * e)] = v[br4(e)];
+        }
+        __syncthreads();
+        { // P1': adjoint of P1, straight to the two output rows
+            double2 v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                v[c] = sz[f8_at(c * 512 + t)];
+            __syncthreads(); // the slots are free: the next pair's rows stream in under this pass
+            if (pr + gridDim.x < pairs)
+                stage(pr + gridDim.x);
+            const double2 w1 = cconj(T.w(t));
+            double2 wc = w1;
+#pragma unroll
+            for (int c = 1; c < 16; ++c) {
+                v[c] = cmul(v[c], wc);
+                wc = cmul(wc, w1);
+            }
+            f8_dft16<true>(v);
+            double* o0 = out + r0 * ldo;
+            double* o1 = o0 + ldo;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const double2 x = v[br4(q)];
+                __stcs(o0 + 512 * q + t, x.x);
+                if (two)
+                    __stcs(o1 + 512 * q + t, x.y);
+            }
+        }
+    }
+}
 } // namespace
 
 // true when the FFT path handles n: a power of two >= 64 (n <= 8192 in shared memory, larger n
@@ -1220,6 +1507,24 @@ void circ_right_fft_launch(uint64_t m, uint64_t n, uint64_t n_in, uint64_t n_out
     double2* chat = ws<double2>(WS_SPLAN, n); // k_sparse_plan's slot: not live at the same time
     k_circ_fft_prep<<<1, CF_THREADS, smem, stream()>>>(static_cast<int>(n), c, chat);
     RL_LAUNCHED();
+    static const bool generic8k = getenv("RL_CIRC_FFT_GENERIC") != nullptr; // dev comparison
+    const bool aligned = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0); // cp.async 16 B
+    if (n == static_cast<uint64_t>(F8_N) && n_in == n && n_out == n && aligned && !generic8k) {
+        const size_t smem8 = static_cast<size_t>(F8_N + F8_N / 32) * sizeof(double2);
+        static bool attr8[16] = {};
+        if (!attr8[ctx().device & 15]) {
+            RL_CUDA(cudaFuncSetAttribute(k_circ_fft8k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem8)));
+            attr8[ctx().device & 15] = true;
+        }
+        const unsigned grid8 = static_cast<unsigned>(std::min<uint64_t>((m + 1) / 2, ctx().sms));
+        double2* chat_p = ws<double2>(WS_FFT_C, F8_N);
+        k_f8_perm<<<F8_N / 256, 256, 0, stream()>>>(chat, chat_p);
+        RL_LAUNCHED();
+        k_circ_fft8k<<<grid8, F8_T, smem8, stream()>>>(m, a, lda, chat_p, out, ldo);
+        RL_LAUNCHED();
+        return;
+    }
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((m + 1) / 2, ctx().sms));
     k_circ_right_fft<<<grid, CF_THREADS, smem, stream()>>>(m, static_cast<int>(n), static_cast<int>(n_in),
                                                            static_cast<int>(n_out), a, lda, chat, out, ldo);

@@ -337,12 +337,13 @@ def test_sparse_apply_right_bit_exact(rl, oracle, n):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n", [(64, 64), (255, 256), (1024, 1024), (3, 2048), (8192, 8192), (100, 96), (5, 16384),
-                                 (3, 65536)])
+@pytest.mark.parametrize("m,n", [(64, 64), (255, 256), (1024, 1024), (3, 2048), (8192, 8192), (301, 8192), (100, 96),
+                                 (5, 16384), (3, 65536)])
 def test_circulant_apply_right_fft(rl, m, n):
     """A C for a circulant multiplier (C(i,j) = c[(i-j) mod n], structured.cpp:54-68) through the
-    FFT path (power-of-two n: shared-memory transform up to 8192, global-memory passes beyond;
-    n = 96 takes the dense fallback) against the dense product in numpy: relative error within
+    FFT path (power-of-two n: shared-memory transform up to 8192 — n = 8192 on the register
+    radix-16/16/32 kernel, an odd row count leaving the last pair's second row empty — global-memory
+    passes beyond; n = 96 takes the dense fallback) against the dense product in numpy: relative error within
     1e-13 up to 8192 (rounding grows like log2 n eps); beyond, the global path's chained twiddles
     (the reference's own FFT scheme) carry O(n eps), the same order as a dense product's."""
     import torch
