@@ -25,6 +25,7 @@ KEYS = {
     "local_store_requests": ("l1tex__t_requests_pipe_lsu_mem_local_op_st.sum", 1),
     "smem_bank_conflicts": ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", 1),
     "sm_clock_ghz": ("smsp__cycles_elapsed.avg.per_second", 1e-9),
+    "warp_instructions": ("smsp__inst_executed.sum", 1),
 }
 STALL = "smsp__average_warps_issue_stalled_"
 
