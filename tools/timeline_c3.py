@@ -26,8 +26,9 @@ t0, t1 = ks[0][0], max(k[1] for k in ks)
 print(f"attempts {rep.attempts_drawn}; span {(t1 - t0) / 1e3:.2f} ms, {len(ks)} device events")
 by = collections.Counter()
 for st, en, nm in ks:
-    by[nm.split("(")[0].replace("void rl::(anonymous namespace)::", "").replace("rl::(anonymous namespace)::", "")[:50]] += en - st
-for nm, us in by.most_common(14):
+    key = nm.replace("void ", "").replace("rl::(anonymous namespace)::", "").replace("rl::", "")
+    by[key.split("(")[0][:60]] += en - st
+for nm, us in by.most_common(20):
     print(f"{us / 1e3:9.3f} ms  {nm}")
 # device-idle time: union of busy intervals
 busy, cur_s, cur_e = 0.0, None, None
@@ -40,3 +41,13 @@ for st, en, _ in ks:
         cur_e = max(cur_e, en)
 busy += cur_e - cur_s
 print(f"device busy {busy / 1e3:.2f} ms of {(t1 - t0) / 1e3:.2f} ms (idle {(t1 - t0 - busy) / 1e3:.2f} ms)")
+# the largest idle gaps (device-wide) with the kernels on either side
+gaps = []
+cur_e, prev = None, None
+for st, en, nm in ks:
+    if cur_e is not None and st > cur_e:
+        gaps.append((st - cur_e, (cur_e - t0) / 1e3, prev, nm))
+    if cur_e is None or en > cur_e:
+        cur_e, prev = en, nm
+for g, at, a_, b_ in sorted(gaps, reverse=True)[:10]:
+    print(f"gap {g:8.1f} us at {at:8.3f} ms: {a_.split('(')[0][-40:]} -> {b_.split('(')[0][-40:]}")
