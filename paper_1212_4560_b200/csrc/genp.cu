@@ -16,6 +16,7 @@
 // Without pivoting the panel is embarrassingly parallel: there is no tall
 // sequential panel factorisation on the critical path.
 #include "panel.cuh"
+#include "reg_lu.cuh"
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -216,6 +217,59 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_diag_lu(double* a, uint64_t l
         pivots[o + tid] = pabs[tid];
         if (pabs[tid] < floor)
             atomicMin(breakdown, static_cast<unsigned long long>(o + tid));
+    }
+}
+
+// Register-resident diagonal-block LU (reg_lu.cuh, G = 16): 256 threads, the 128 x 128 block
+// 16 x 16-cyclic in registers (thread (tr, tc) owns rows tr + 16 r, columns tc + 16 c), 128
+// pivot steps with one barrier each in the reference's right-looking order (genp.cpp:20-33;
+// m = w(i,k) (1/p), 1/p := 0 for p = 0), then L = w(i,k) (1/p) below the diagonal and the packed
+// block back in place.  Rows / columns beyond a ragged last block are the identity.  The
+// shared-memory request (kPanelSmem) keeps GEMM CTAs off the SM, as for the other panel kernels.
+constexpr int DR_THREADS = 256;
+__global__ void __launch_bounds__(DR_THREADS, 1) k_diag_lu_reg(double* a, uint64_t lda, uint64_t n, uint64_t o,
+                                                               double floor, double* pivots,
+                                                               unsigned long long* breakdown) {
+    __shared__ __align__(16) double pub[2 * reglu::Pub<16>::SIZE];
+    __shared__ double rcp[NB];
+    const int t = threadIdx.x, tr = t >> 4, tc = t & 15;
+    const int bs = static_cast<int>((n - o) < NB ? (n - o) : NB);
+    double* blk = a + o * lda + o;
+    if (g_tl_on && t == 0 && o / NB < 64)
+        g_tl[o / NB][0] = tl_now();
+    double w[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int i = tr + 16 * r, j = tc + 16 * c;
+            w[r][c] = (i < bs && j < bs) ? blk[static_cast<uint64_t>(i) * lda + j] : (i == j ? 1.0 : 0.0);
+        }
+    double dummy = 0.0; // (the mbarrier hand-off, reg_lu.cuh MB, measured 31.4 against 30.0 us)
+    reglu::factor<16, false>(w, dummy, reglu::Bufs{pub, rcp, nullptr}, tr, tc);
+    __syncthreads(); // rcp complete
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int j = tc + 16 * c;
+        const double inv = rcp[j];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int i = tr + 16 * r;
+            double v = w[r][c];
+            if (r > c || (r == c && tr > tc))
+                v *= inv;
+            if (i < bs && j < bs)
+                blk[static_cast<uint64_t>(i) * lda + j] = v;
+            if (i == j && i < bs) { // |pivots| and the first step below the floor (genp.cpp:24-26)
+                pivots[o + i] = fabs(v);
+                if (fabs(v) < floor)
+                    atomicMin(breakdown, static_cast<unsigned long long>(o + i));
+            }
+        }
+    }
+    if (g_tl_on && t == 0 && o / NB < 64) {
+        __threadfence();
+        g_tl[o / NB][1] = tl_now();
     }
 }
 
@@ -648,6 +702,8 @@ void prep_attrs() {
                                      static_cast<int>(trsm_smem())));
         RL_CUDA(cudaFuncSetAttribute(k_diag_lu, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(diag_smem())));
+        RL_CUDA(cudaFuncSetAttribute(k_diag_lu_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(diag_smem() - 8 * 1024)));
         RL_CUDA(cudaFuncSetAttribute(k_trsv_wave<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(wave_smem_bytes())));
         RL_CUDA(cudaFuncSetAttribute(k_trsv_wave<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -761,7 +817,12 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         ctx().stream = keep;
     };
     auto diag = [&](uint64_t o, cudaStream_t st) {
-        k_diag_lu<<<1, PK_THREADS, diag_smem(), st>>>(a, lda, n, o, pivot_floor, d_pivots, d_breakdown);
+        static const bool old_diag = std::getenv("RL_DIAG_OLD") != nullptr; // dev comparison
+        if (old_diag)
+            k_diag_lu<<<1, PK_THREADS, diag_smem(), st>>>(a, lda, n, o, pivot_floor, d_pivots, d_breakdown);
+        else
+            k_diag_lu_reg<<<1, DR_THREADS, diag_smem() - 8 * 1024, st>>>(a, lda, n, o, pivot_floor, d_pivots,
+                                                                          d_breakdown);
         RL_LAUNCHED();
     };
     auto trsm = [&](uint64_t o, cudaStream_t st) {

@@ -31,6 +31,7 @@
 // reference's.
 #include <cmath>
 
+#include "reg_lu.cuh"
 #include "rl_internal.cuh"
 
 namespace rl {
@@ -56,7 +57,7 @@ constexpr int THREADS = 64;
 constexpr int P = 66; // staging pitch (528 B rows: 16-byte aligned, conflict-free 128-bit row reads)
 // LU publication buffer per parity: the pivot row owner-major at pitch 10 (the eight owners'
 // 128-bit reads hit distinct banks), then the pivot column owner-major at pitch 8.
-constexpr int PUB_RP = 10, PUB_C = 8 * PUB_RP, PUB = PUB_C + 64;
+constexpr int PUB = reglu::Pub<8>::SIZE;
 
 struct Smem {
     double X[N * P]; // A staging / W / packed LU (row-major); sign-stream scratch and DFT twiddles
@@ -268,137 +269,10 @@ __device__ __forceinline__ void circ_fft64(double (&x)[N], const double2* __rest
 }
 
 // ------------------------------------------------------------------- LU ----
-// 1/p without branches (every thread evaluates it; the pivot's owner publishes it): the
-// hardware estimate plus two Newton steps, exact to rounding for 2^-1022 <= |p| <= 2^1022;
-// 0 -> 0 (the reference's m = 0 for a zero pivot), +-inf -> 0.  (Subnormal pivots give an
-// infinite reciprocal — the reference's w / p overflows there too.)
-__device__ __forceinline__ double pivot_rcp_nb(double p) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
-    double e = fma(-p, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-p, r, 1.0);
-    r = fma(r, e, r);
-    return (p == 0.0 || isinf(p)) ? 0.0 : r;
-}
-
-__device__ __forceinline__ void st_if(double* dst, double v, bool pred) {
-    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.shared.f64 [%0], %1;\n}" ::"r"(smem_u32(dst)),
-                 "d"(v), "r"(static_cast<int>(pred))
-                 : "memory");
-}
-__device__ __forceinline__ void st2_if(double* dst, double v0, double v1, bool pred) {
-    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n @p st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(
-                     smem_u32(dst)),
-                 "d"(v0), "d"(v1), "r"(static_cast<int>(pred))
-                 : "memory");
-}
-
-// Publication for pivot step k = 8K + s (K compile-time, s at run time), owner-major so every
-// owner stores and every reader loads 128-bit pairs: row k as pub[par][tc][c] by the owners
-// (s, tc), column k as pub[par][PUB_C + tr*8 + r] by the owners (tr, s); 1/p into rcp[k].
-// Predicated stores, no branches (a divergent branch costs a reconvergence barrier per step).
-template <int K>
-__device__ __forceinline__ void lu_publish(const double (&w)[8][8], double bcur, Smem& S, int s, int tr, int tc) {
-    double* ur = S.pub + (s & 1) * PUB + tc * PUB_RP;
-    double* uc = S.pub + (s & 1) * PUB + PUB_C + tr * 8;
-    const bool oc = tc == s, orow = tr == s;
-    st_if(S.rcp + 8 * K + s, pivot_rcp_nb(w[K][K]), oc && orow);
-    st_if(S.pubb + (s & 1), bcur, static_cast<int>(threadIdx.x) == 8 * K + s); // b_k by thread k
-#pragma unroll
-    for (int r = K & ~1; r < 8; r += 2)
-        st2_if(uc + r, w[r][K], w[r + 1][K], oc);
-#pragma unroll
-    for (int c = K & ~1; c < 8; c += 2)
-        st2_if(ur + c, w[K][c], w[K][c + 1], orow);
-}
-
-// Pivot step k = 8K + s (k-parity PAR = s & 1; LAST: s = 7, the next step opens block K+1).
-// Rows / columns r, c > K are always in the trailing matrix; the block's own row / column K
-// (thread row tr, column tc) leaves it once the step passes tr / tc.  A zero multiplier /
-// pivot-row entry there leaves the finished entries bitwise unchanged (fma(-0, u, w) = w)
-// without per-FMA predicates; the column of multipliers is not written back — column k keeps
-// w(i,k) and L = w(i,k) / p is formed once at the end (lu_store), the same product the update
-// used.  The next step's row / column (KC) are updated and published first, then the rest.
-template <int K, int PAR, bool LAST>
-__device__ __forceinline__ void lu_step(double (&w)[8][8], double& bcur, Smem& S, int s, int tr, int tc) {
-    constexpr int KC = LAST ? K + 1 : K;
-    __syncthreads();
-    const double* ur = S.pub + PAR * PUB + tc * PUB_RP;
-    const double* uc = S.pub + PAR * PUB + PUB_C + tr * 8;
-    const double inv = S.rcp[8 * K + s];
-    { // forward substitution of the right-hand side alongside (genp.cpp:110-115's order):
-      // thread t holds b_t; rows below the pivot subtract m_t b_k
-        const int t = threadIdx.x, k = 8 * K + s;
-        const double mt = S.pub[PAR * PUB + PUB_C + (t & 7) * 8 + (t >> 3)] * inv;
-        const double f = fma(-mt, S.pubb[PAR], bcur);
-        bcur = t > k ? f : bcur;
-    }
-    double m[8], u[8];
-#pragma unroll
-    for (int r = K & ~1; r < 8; r += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(uc + r);
-        if (r >= K)
-            m[r] = v.x * inv;
-        m[r + 1] = v.y * inv;
-    }
-    m[K] = tr > s ? m[K] : 0.0;
-#pragma unroll
-    for (int c = K & ~1; c < 8; c += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(ur + c);
-        if (c >= K)
-            u[c] = v.x;
-        u[c + 1] = v.y;
-    }
-    u[K] = tc > s ? u[K] : 0.0;
-    if (KC < 8) {
-#pragma unroll
-        for (int c = K; c < 8; ++c)
-            w[KC][c] = fma(-m[KC], u[c], w[KC][c]);
-#pragma unroll
-        for (int r = K; r < 8; ++r)
-            if (r != KC)
-                w[r][KC] = fma(-m[r], u[KC], w[r][KC]);
-        lu_publish<(KC < 8 ? KC : 7)>(w, bcur, S, LAST ? 0 : s + 1, tr, tc);
-    }
-#pragma unroll
-    for (int c = K; c < 8; ++c) {
-        if (c == KC)
-            continue;
-#pragma unroll
-        for (int r = K; r < 8; ++r)
-            if (r != KC)
-                w[r][c] = fma(-m[r], u[c], w[r][c]);
-    }
-}
-
-// The eight pivot steps k = 8K .. 8K+7 of block K; the step index only enters predicates, so
-// one loop body per block and parity (the register indices are compile-time) keeps the code small.
-template <int K>
-__device__ __forceinline__ void lu_block(double (&w)[8][8], double& bcur, Smem& S, int tr, int tc) {
-#pragma unroll 1
-    for (int s = 0; s < 6; s += 2) {
-        lu_step<K, 0, false>(w, bcur, S, s, tr, tc);
-        lu_step<K, 1, false>(w, bcur, S, s + 1, tr, tc);
-    }
-    lu_step<K, 0, false>(w, bcur, S, 6, tr, tc);
-    lu_step<K, 1, true>(w, bcur, S, 7, tr, tc);
-}
-
-// No-pivot LU of the register-resident matrix (genp.cpp:20-33): one barrier per pivot step.
-// On exit w holds U on and above the diagonal and w(i,k) (un-normalised) below; S.rcp[k] =
-// 1/U_kk; thread t's bcur (b_t on entry) holds (L^-1 b)_t.  S.pub (aliasing the vectors and
-// the spectrum) carries the publications (callers fence before and after).
+// The factorization itself is reglu::factor<8, true> (reg_lu.cuh): 64 pivot steps, one
+// barrier each, the right-hand side forward-substituted alongside.
 __device__ __forceinline__ void lu_regs(double (&w)[8][8], double& bcur, Smem& S, int tr, int tc) {
-    lu_publish<0>(w, bcur, S, 0, tr, tc);
-    lu_block<0>(w, bcur, S, tr, tc);
-    lu_block<1>(w, bcur, S, tr, tc);
-    lu_block<2>(w, bcur, S, tr, tc);
-    lu_block<3>(w, bcur, S, tr, tc);
-    lu_block<4>(w, bcur, S, tr, tc);
-    lu_block<5>(w, bcur, S, tr, tc);
-    lu_block<6>(w, bcur, S, tr, tc);
-    lu_block<7>(w, bcur, S, tr, tc);
+    reglu::factor<8, true>(w, bcur, reglu::Bufs{S.pub, S.rcp, S.pubb}, tr, tc);
 }
 
 // The packed LU into X (row-major): U as factored, L_ij = w(i,j) * (1/U_jj) below the diagonal.
