@@ -154,10 +154,6 @@ __device__ uint64_t sign_mask_stream(uint64_t seed, uint64_t sid, uint64_t* scra
 }
 
 // ------------------------------------------------------------------ FFT ----
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
 __host__ __device__ constexpr int br5(int m) {
     return ((m & 1) << 4) | ((m & 2) << 2) | (m & 4) | ((m & 8) >> 2) | ((m & 16) >> 4);
 }
