@@ -817,8 +817,12 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
         ctx().stream = keep;
     };
     auto diag = [&](uint64_t o, cudaStream_t st) {
-        static const bool old_diag = std::getenv("RL_DIAG_OLD") != nullptr; // dev comparison
-        if (old_diag)
+        // RL_DIAG_REG=1 (dev): the register kernel — 30 against 32 us per block, but its rounding
+        // moves config 3's accepted attempts, which sit inside the reference's own 1-ulp band
+        // (agreement with the oracle 6/16 columns against 11/16; the oracle agrees with itself
+        // under a 1-ulp perturbation in 7/16), and the step then needs three draws, not two
+        static const bool reg_diag = std::getenv("RL_DIAG_REG") != nullptr;
+        if (!reg_diag)
             k_diag_lu<<<1, PK_THREADS, diag_smem(), st>>>(a, lda, n, o, pivot_floor, d_pivots, d_breakdown);
         else
             k_diag_lu_reg<<<1, DR_THREADS, diag_smem() - 8 * 1024, st>>>(a, lda, n, o, pivot_floor, d_pivots,
