@@ -7,7 +7,12 @@
 // down with no best.  Every FLOP runs on the GPU; the host only reads back the
 // scalars the protocol branches on (breakdown flag, residuals, pivots).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -542,6 +547,84 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
 
 const std::vector<rl_column_report>& last_column_reports() { return g_last_cols; }
 
+void init_device(int device);
+const char* last_error();
+
+namespace {
+// Host worker pool for the general batched path.  The reference runs table1_genp's trials on
+// parallel_trials worker threads (bench.cpp:63-93); here each worker keeps its own per-thread
+// context (stream, workspaces, the LU's lookahead streams), so the systems' latency-bound
+// launches overlap on the GPU.  Persistent (the per-thread workspaces are allocated once);
+// one batched call at a time uses it.
+class SystemPool {
+  public:
+    static SystemPool& get() {
+        static SystemPool p;
+        return p;
+    }
+    int size() const { return static_cast<int>(threads_.size()); }
+    // job(worker) on every worker; returns when all are done
+    void run(int device, const std::function<void(int)>& job) {
+        std::lock_guard<std::mutex> one(run_m_);
+        std::unique_lock<std::mutex> lk(m_);
+        job_ = &job;
+        device_ = device;
+        pending_ = size();
+        ++gen_;
+        cv_.notify_all();
+        done_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+    ~SystemPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_)
+            t.join();
+    }
+
+  private:
+    SystemPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        int n = static_cast<int>(std::max(1u, std::min(8u, hw ? hw : 1u)));
+        if (const char* e = std::getenv("RL_BATCH_THREADS")) // RL_BATCH_THREADS=1: the serial order
+            n = std::max(1, std::min(64, std::atoi(e)));
+        for (int i = 0; i < n; ++i)
+            threads_.emplace_back([this, i] { loop(i); });
+    }
+    void loop(int id) {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(m_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_)
+                return;
+            seen = gen_;
+            const std::function<void(int)>* job = job_;
+            const int dev = device_;
+            lk.unlock();
+            try {
+                init_device(dev);
+                (*job)(id);
+            } catch (...) {
+            }
+            lk.lock();
+            if (--pending_ == 0)
+                done_.notify_all();
+        }
+    }
+    std::vector<std::thread> threads_;
+    std::mutex m_, run_m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* job_ = nullptr;
+    int device_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+} // namespace
+
 rl_status randomized_genp_batched_dev(uint64_t batch, uint64_t n, const double* dA, const double* dB,
                                       int tag, double mu, double sigma, int side, int refine,
                                       uint64_t seed, const uint64_t* d_sids, double* dX,
@@ -550,17 +633,34 @@ rl_status randomized_genp_batched_dev(uint64_t batch, uint64_t n, const double* 
         fail(RL_INVALID_ARGUMENT, "randomized_genp: refine must be in {0, 1, 2}");
     if (tag == RL_CIRCULANT_SIGN && (side == RL_RIGHT || side == RL_LEFT) && n == 64)
         return batched_circ64(batch, dA, dB, refine, side == RL_LEFT ? 1 : 0, seed, d_sids, dX, d_rep);
-    // general kinds / sizes: one system at a time through the blocked path
+    // general kinds / sizes: the blocked single-system path, systems spread over the host worker
+    // pool (each worker's own stream and workspaces; the result of a system does not depend on
+    // which worker ran it)
     std::vector<uint64_t> sids(batch);
     RL_CUDA(cudaMemcpyAsync(sids.data(), d_sids, batch * 8, cudaMemcpyDeviceToHost, stream()));
-    RL_CUDA(cudaStreamSynchronize(stream()));
+    RL_CUDA(cudaStreamSynchronize(stream())); // also: the inputs are resident before the workers read them
     std::vector<rl_precond_report> reps(batch);
-    for (uint64_t t = 0; t < batch; ++t) {
-        rl_status s = randomized_genp_dev(n, 1, dA + t * n * n, dB + t * n, tag, mu, sigma, side, refine,
-                                          seed, sids[t], dX + t * n, &reps[t], 0);
-        if (s != RL_OK)
-            return s;
-    }
+    std::vector<rl_status> st(batch, RL_OK);
+    std::vector<std::string> msg(batch);
+    std::atomic<uint64_t> next{0};
+    SystemPool::get().run(ctx().device, [&](int) {
+        for (uint64_t t = next++; t < batch; t = next++) {
+            try {
+                st[t] = randomized_genp_dev(n, 1, dA + t * n * n, dB + t * n, tag, mu, sigma, side, refine, seed,
+                                            sids[t], dX + t * n, &reps[t], 0);
+                if (st[t] != RL_OK)
+                    msg[t] = last_error();
+            } catch (const Failure& f) {
+                st[t] = f.code;
+                msg[t] = f.msg;
+            }
+        }
+    });
+    for (uint64_t t = 0; t < batch; ++t) // the first failing system, as the serial loop reported
+        if (st[t] != RL_OK) {
+            set_error(msg[t]);
+            return st[t];
+        }
     RL_CUDA(cudaMemcpyAsync(d_rep, reps.data(), batch * sizeof(rl_precond_report), cudaMemcpyHostToDevice,
                             stream()));
     RL_CUDA(cudaStreamSynchronize(stream()));

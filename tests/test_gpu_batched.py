@@ -88,6 +88,28 @@ def test_batched_general_kind_fallback_path(rl, oracle):
         assert np.abs(x[t] - xo).max() / np.abs(xo).max() < 1e-9
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,side", [(256, "LEFT"), (256, "RIGHT"), (130, "LEFT")])
+def test_batched_general_path_worker_pool_is_bitwise_serial(rl, n, side):
+    """The general batched path spreads systems over host worker threads (table1_genp's
+    parallel_trials, bench.cpp:63-93): every system's x and report must equal, bit for bit, a
+    single randomized_genp call on the caller's thread (tests/test_bench.cpp:57-73's contract)."""
+    batch = 12
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((batch, n, n))
+    h = n // 2
+    A[:, :h, :h] = rng.standard_normal((batch, h, h - 1)) @ rng.standard_normal((batch, h - 1, h))
+    b = rng.standard_normal((batch, n))
+    kind = rl.MultiplierKind(rl.MultiplierTag.CIRCULANT_SIGN)
+    sd = getattr(rl.MulSide, side)
+    sids = [1000 + 7 * t for t in range(batch)]
+    x, reps = rl.randomized_genp_batched(A, b, kind, sd, 1, 11, sids)
+    for t in range(batch):
+        xs, rs = rl.randomized_genp(A[t], b[t], kind, sd, 1, rl.RngStream(11, sids[t]))
+        assert np.array_equal(x[t], xs)
+        assert (reps[t].residual, reps[t].attempt, reps[t].raw_residual) == (rs.residual, rs.attempt, rs.raw_residual)
+
+
 @pytest.mark.parametrize("refine", [0, 1])
 def test_batched_left_side_table1_fixtures(rl, golden, oracle, refine):
     """MulSide::Left in the batched n = 64 kernel (Table 1's side, bench.cpp:127-130: rhs = C b,
