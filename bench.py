@@ -257,6 +257,8 @@ def run_config1(torch, rl, dev, dist, args, fp64_peak):
     bwd = float(((A @ x - b).norm() / (A.norm() * x.norm())).item())
     # the same solve from host buffers through the public host-pointer call
     hA, hb, hx = A.cpu().numpy(), b.cpu().numpy().ravel(), np.empty(n)
+    for _ in range(max(args.warmup, 3)):  # the host path's own warm-up (its contrast-arm helper thread)
+        rl.randomized_genp(hA, hb, kind, rl.MulSide.RIGHT, 0, st)
     t0 = time.perf_counter()
     reps = max(args.steps, 20)
     for _ in range(reps):

@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
+#include <exception>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -321,6 +322,72 @@ double residual_max(uint64_t n, uint64_t nrhs, const double* a, const double* x,
 
 } // namespace
 
+void init_device(int device);
+
+namespace {
+// One persistent helper thread per calling thread: randomized_genp's raw-GENP contrast arm runs
+// on it (its own stream, workspaces and LU streams) while the calling thread draws, applies
+// and factors the attempts — the two factorizations are independent and both latency-bound at
+// small n.
+class AsyncWorker {
+  public:
+    AsyncWorker() : th_([this] { loop(); }) {}
+    ~AsyncWorker() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    void submit(std::function<void()> f) {
+        std::lock_guard<std::mutex> lk(m_);
+        job_ = std::move(f);
+        has_ = true;
+        done_ = false;
+        cv_.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return done_; });
+    }
+
+  private:
+    void loop() {
+        std::unique_lock<std::mutex> lk(m_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || has_; });
+            if (stop_ && !has_)
+                return;
+            std::function<void()> job = std::move(job_);
+            has_ = false;
+            lk.unlock();
+            job();
+            lk.lock();
+            done_ = true;
+            cv_.notify_all();
+        }
+    }
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::function<void()> job_;
+    bool has_ = false, done_ = true, stop_ = false;
+    std::thread th_;
+};
+AsyncWorker& contrast_worker() {
+    static thread_local AsyncWorker w;
+    return w;
+}
+// joins the helper on every exit path (the job references the caller's locals)
+struct JoinGuard {
+    AsyncWorker* w = nullptr;
+    ~JoinGuard() {
+        if (w)
+            w->wait();
+    }
+};
+} // namespace
+
 // Per-column outcome of this thread's last randomized_genp_dev call (rl_last_column_reports).
 thread_local std::vector<rl_column_report> g_last_cols;
 
@@ -394,16 +461,52 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
     rep.attempt = -1;
     if (speculate && !(flags & 1u))
         spec_draw(0); // beside the contrast arm
-    if (!(flags & 1u)) {
-        // raw-GENP contrast arm (genp.cpp:222-234)
+    // raw-GENP contrast arm (genp.cpp:222-234) on the helper thread, concurrently with the attempts
+    struct RawArm {
+        double res = 0.0, pmin = 0.0, pmax = 0.0;
+        std::exception_ptr err;
+    } raw;
+    JoinGuard join;
+    static const bool raw_serial = std::getenv("RL_RAW_SERIAL") != nullptr; // dev comparison
+    if (!(flags & 1u) && raw_serial) {
         wait_upload(A);
         copy2d_dev(n, n, A, n, sys, n);
         RL_CUDA(cudaMemsetAsync(brk, 0xff, 8, st));
         genp_factor_blocked(n, sys, n, 0.0, piv, brk, aux);
         copy2d_dev(n, nrhs, B, nrhs, Z, nrhs);
         genp_solve_blocked(n, nrhs, sys, n, aux, Z, nrhs);
-        rep.raw_residual = residual_max(n, nrhs, A, Z, B, true);
-        minmax_fold(to_host(piv, n), &rep.raw_pivot_min, &rep.raw_pivot_max);
+        raw.res = residual_max(n, nrhs, A, Z, B, true);
+        minmax_fold(to_host(piv, n), &raw.pmin, &raw.pmax);
+    }
+    if (!(flags & 1u) && !raw_serial) {
+        wait_upload(A); // A and B are resident on this stream before the helper reads them
+        static thread_local cudaEvent_t ev_in = nullptr;
+        if (!ev_in)
+            RL_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        RL_CUDA(cudaEventRecord(ev_in, st));
+        const int dev = ctx().device;
+        const cudaEvent_t e_in = ev_in;
+        contrast_worker().submit([&raw, dev, e_in, n, nrhs, A, B, nblk] {
+            try {
+                init_device(dev);
+                RL_CUDA(cudaStreamWaitEvent(stream(), e_in, 0));
+                double* rs = ws<double>(WS_SYS, n * n);
+                double* raux = ws<double>(WS_LU_AUX, nblk * 2 * NB * NB);
+                double* rz = ws<double>(WS_RHS, n * nrhs);
+                double* rpiv = ws<double>(WS_PACK, n + 1);
+                unsigned long long* rbrk = reinterpret_cast<unsigned long long*>(rpiv + n);
+                copy2d_dev(n, n, A, n, rs, n);
+                RL_CUDA(cudaMemsetAsync(rbrk, 0xff, 8, stream()));
+                genp_factor_blocked(n, rs, n, 0.0, rpiv, rbrk, raux);
+                copy2d_dev(n, nrhs, B, nrhs, rz, nrhs);
+                genp_solve_blocked(n, nrhs, rs, n, raux, rz, nrhs);
+                raw.res = residual_max(n, nrhs, A, rz, B, true);
+                minmax_fold(to_host(rpiv, n), &raw.pmin, &raw.pmax);
+            } catch (...) {
+                raw.err = std::current_exception();
+            }
+        });
+        join.w = &contrast_worker();
     }
     rl_precond_report best = rep;
     for (int attempt = 0; attempt < 8; ++attempt) {
@@ -537,6 +640,17 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
         best = rep;
         status = RL_OK;
     }
+    if (join.w) {
+        join.w->wait();
+        join.w = nullptr;
+        if (raw.err)
+            std::rethrow_exception(raw.err);
+    }
+    if (!(flags & 1u)) { // the contrast arm's report fields
+        best.raw_residual = raw.res;
+        best.raw_pivot_min = raw.pmin;
+        best.raw_pivot_max = raw.pmax;
+    }
     if (status == RL_OK && report) {
         best.attempts_drawn = rep.attempts_drawn;
         *report = best;
@@ -547,7 +661,6 @@ rl_status randomized_genp_dev(uint64_t n, uint64_t nrhs, const double* A, const 
 
 const std::vector<rl_column_report>& last_column_reports() { return g_last_cols; }
 
-void init_device(int device);
 const char* last_error();
 
 namespace {
