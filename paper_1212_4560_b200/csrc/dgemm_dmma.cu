@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+} // namespace
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -423,6 +425,8 @@ bool make_tmap(CUtensorMap* tm, const double* base, uint64_t rows, uint64_t cols
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+namespace {
 
 // true when the TMA kernel took the product. op(A): M x K, K-major (row-major M x K, ld lda) or
 // M-major (A stored K x M, ld lda); B: K x N row-major (ld ldb).

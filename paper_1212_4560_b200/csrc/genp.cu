@@ -972,14 +972,354 @@ void genp_factor_dev(uint64_t n, double* a, uint64_t lda, double pivot_floor, do
 // Kept for the C-ABI signature (the solves need no precomputed block inverses).
 void genp_block_inverses(uint64_t, const double*, uint64_t, double*) {}
 
+// One right-hand side, n <= 512: both substitutions in one warp (genp.cpp:106-124: the row-j
+// update x_i -= L_ij x_j in ascending j, then x_i -= U_ij x_j in descending j and x_i / U_ii).
+// Lane l keeps rows l + 32 q (q < NQ = n / 32 rounded up); the columns are swept in blocks of
+// four (below).  The coefficients arrive as panels of W = 256 / NQ columns (rows from the
+// panel's 32-row group down for L, rows 0.. for U) by TMA — two 256 x 16 boxes per panel, 128-byte
+// swizzle (a lane's 128-bit read of its row's column pair and the quarter-warp's eight rows hit
+// distinct banks), zero fill past n — into a 3-stage ring two panels ahead, so the warp never
+// waits on L2 and no thread spends instructions on staging.
+constexpr int SW_MAXN = 512, SW_STAGES = 3;
+constexpr uint32_t SW_BOX = 256 * 128;    // one box: 256 rows x 16 doubles
+constexpr uint32_t SW_STAGE = 2 * SW_BOX; // one panel
+__host__ __device__ constexpr size_t sweep_smem_bytes() {
+    return 1024 + static_cast<size_t>(SW_STAGES) * SW_STAGE + SW_MAXN * sizeof(double2);
+}
+
+__device__ __forceinline__ uint32_t sw_saddr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Byte offset of element (i, c) of a panel whose boxes start at row r0 (c even: the pair c, c+1).
+// NQ = 8: the two boxes are columns 0-15 / 16-31; NQ = 16: rows r0.. / r0+256.. of 16 columns.
+template <int NQ>
+struct SweepGeo {
+    static constexpr int W = 256 / NQ;
+    __device__ static uint32_t off(int i, int c, int r0) {
+        const int rr = i - r0;
+        const int bx = NQ == 8 ? (c >> 4) : (rr >> 8);
+        const int r = NQ == 8 ? rr : (rr & 255), cc = c & 15;
+        return static_cast<uint32_t>(bx) * SW_BOX + static_cast<uint32_t>(r) * 128u +
+               static_cast<uint32_t>((((cc >> 1) ^ (r & 7)) << 4) | ((cc & 1) << 3));
+    }
+    // the same for the lane's own row lane + 32 q, qrel = q minus the panel's first register
+    // (a constant once the q loop is unrolled): the row part folds into an immediate, the
+    // swizzle is lane & 7
+    __device__ static uint32_t lane_off(int qrel, int lane, int c) {
+        const int bxr = NQ == 8 ? 0 : qrel >> 3, rq = NQ == 8 ? qrel : qrel & 7;
+        const int cc = c & 15;
+        return static_cast<uint32_t>((NQ == 8 ? (c >> 4) : bxr)) * SW_BOX + static_cast<uint32_t>(lane + 32 * rq) * 128u +
+               static_cast<uint32_t>((((cc >> 1) ^ (lane & 7)) << 4) | ((cc & 1) << 3));
+    }
+};
+
+// x / U_jj as the reference divides.  Fast path: the reciprocal's quotient plus one residual
+// correction — correctly rounded when the reciprocal is (Markstein) and nothing under- or
+// overflows; a flag (integer ops, off the dependency chain) marks any step outside that range
+// and the caller re-runs the pass with the division itself.  x and U_jj are warp-uniform.
+template <bool EXACT>
+__device__ __forceinline__ double sweep_div(double x, double2 d, unsigned& bad) {
+    if (EXACT)
+        return x / d.x;
+    double q = x * d.y;
+    q = fma(fma(-q, d.x, x), d.y, q);
+    const int hx = __double2hiint(x) & 0x7fffffff;
+    const unsigned eq = (__double2hiint(q) >> 20) & 0x7ff, ex = static_cast<unsigned>(hx) >> 20,
+                   er = (__double2hiint(d.y) >> 20) & 0x7ff;
+    const unsigned zx = (hx | __double2loint(x)) == 0;
+    bad |= static_cast<unsigned>(er - 128u > 1792u) |
+           ((zx ^ 1u) & (static_cast<unsigned>(eq - 128u > 1792u) | static_cast<unsigned>(ex - 128u > 1792u)));
+    return q;
+}
+
+// One column step (ragged panel edges): x_j from its owner lane, then every row in reach.
+template <bool LOWER, bool EXACT, int NQ, int QP>
+__device__ __forceinline__ void sweep_col(const unsigned char* pb, int r0, const double2* dg, double (&x)[NQ], int j0,
+                                          int jj, int lane, unsigned& bad) {
+    using G = SweepGeo<NQ>;
+    const int j = j0 + jj, src = j & 31;
+    double xj = __shfl_sync(0xffffffffu, x[QP], src);
+    if (!LOWER) {
+        xj = sweep_div<EXACT>(xj, dg[j], bad);
+        x[QP] = lane == src ? xj : x[QP];
+    }
+#pragma unroll
+    for (int q = LOWER ? QP : 0; q < (LOWER ? NQ : QP + 1); ++q) {
+        const int i = lane + 32 * q;
+        const double f = fma(-*reinterpret_cast<const double*>(pb + G::lane_off(LOWER ? q - QP : q, lane, jj)),
+                             xj, x[q]);
+        x[q] = (q != QP || (LOWER ? i > j : i < j)) ? f : x[q];
+    }
+}
+
+// Four column steps at once: the four x_j leave their owner lanes by four independent shuffles
+// and every lane finishes them redundantly through the 4 x 4 triangle (broadcast coefficient
+// reads) — the same operations, in the same order, as four single steps, with one shuffle
+// latency on the chain instead of four.  Then every row takes the four updates (two 128-bit
+// coefficient loads); rows of other registers than QP are all inside the triangle's reach
+// (below the block for L, above for U), so only register QP needs the per-row selects.  Rows
+// past n hold garbage that never reaches a valid row.
+template <bool LOWER, bool EXACT, int NQ, int QP>
+__device__ __forceinline__ void sweep_block4(const unsigned char* pb, int r0, const double2* dg, double (&x)[NQ],
+                                             int j0, int jb, int lane, unsigned& bad) {
+    using G = SweepGeo<NQ>;
+    // L: columns jb, jb+1, jb+2, jb+3 in that order; U: jb+3, jb+2, jb+1, jb
+    const int base = j0 + jb, s0 = base & 31;
+    auto coef = [&](int i, int c) { return *reinterpret_cast<const double*>(pb + G::off(i, c, r0)); };
+    double v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+        v[t] = __shfl_sync(0xffffffffu, x[QP], s0 + t);
+    double xs[4]; // xs[t] = final x_{base + t}
+    if (LOWER) {
+        xs[0] = v[0];
+#pragma unroll
+        for (int t = 1; t < 4; ++t) {
+            double a = v[t];
+#pragma unroll
+            for (int u = 0; u < t; ++u)
+                a = fma(-coef(base + t, jb + u), xs[u], a);
+            xs[t] = a;
+        }
+    } else {
+        xs[3] = sweep_div<EXACT>(v[3], dg[base + 3], bad);
+#pragma unroll
+        for (int t = 2; t >= 0; --t) {
+            double a = v[t];
+#pragma unroll
+            for (int u = 3; u > t; --u)
+                a = fma(-coef(base + t, jb + u), xs[u], a);
+            xs[t] = sweep_div<EXACT>(a, dg[base + t], bad);
+        }
+    }
+#pragma unroll
+    for (int q = LOWER ? QP : 0; q < (LOWER ? NQ : QP + 1); ++q) {
+        const int i = lane + 32 * q;
+        const double2 c01 = *reinterpret_cast<const double2*>(pb + G::lane_off(LOWER ? q - QP : q, lane, jb));
+        const double2 c23 =
+            *reinterpret_cast<const double2*>(pb + G::lane_off(LOWER ? q - QP : q, lane, jb + 2));
+        const double c[4] = {c01.x, c01.y, c23.x, c23.y};
+        double y = x[q];
+        if (q != QP) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int u = LOWER ? t : 3 - t;
+                y = fma(-c[u], xs[u], y);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int u = LOWER ? t : 3 - t;
+                const double f = fma(-c[u], xs[u], y);
+                y = (LOWER ? i > base + u : i < base + u) ? f : y;
+            }
+            if (!LOWER)
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    y = lane == s0 + t ? xs[t] : y;
+        }
+        x[q] = y;
+    }
+}
+
+// The steps of one panel; QP = the register holding the panel's rows, resolved by recursion so
+// every x[] index is a compile-time constant (x stays in registers).
+template <bool LOWER, bool EXACT, int NQ, int QP>
+__device__ __forceinline__ void sweep_panel(const unsigned char* pb, int r0, const double2* dg, double (&x)[NQ],
+                                            int j0, int cols, int lane, unsigned& bad) {
+    if constexpr (QP < NQ) {
+        if ((j0 >> 5) != QP) {
+            sweep_panel<LOWER, EXACT, NQ, QP + 1>(pb, r0, dg, x, j0, cols, lane, bad);
+            return;
+        }
+        if (LOWER) {
+            int jj = 0;
+#pragma unroll 1
+            for (; jj + 4 <= cols; jj += 4)
+                sweep_block4<true, EXACT, NQ, QP>(pb, r0, dg, x, j0, jj, lane, bad);
+#pragma unroll 1
+            for (; jj < cols; ++jj)
+                sweep_col<true, EXACT, NQ, QP>(pb, r0, dg, x, j0, jj, lane, bad);
+        } else {
+            int jj = cols - 1;
+#pragma unroll 1
+            for (; (jj + 1) & 3; --jj) // a ragged panel edge first: the blocks stay 4-aligned
+                sweep_col<false, EXACT, NQ, QP>(pb, r0, dg, x, j0, jj, lane, bad);
+#pragma unroll 1
+            for (; jj >= 3; jj -= 4)
+                sweep_block4<false, EXACT, NQ, QP>(pb, r0, dg, x, j0, jj - 3, lane, bad);
+        }
+    }
+}
+
+// RL_SWEEP_TRACE=1 (dev): per panel %globaltimer stamps: data ready / sweep end
+__device__ unsigned long long g_sweep_ts[3][64][2];
+
+// Panel sequence: 0..np-1 the L panels in order, then the U panels from the last, repeated for
+// an exact re-run of the U pass.
+template <int NQ>
+struct SweepRing {
+    const CUtensorMap* tm;
+    unsigned char* buf;
+    uint64_t* full;
+    int np, lane;
+    __device__ void panel(int seq, bool& lower, int& p) const {
+        lower = seq < np;
+        p = lower ? seq : np - 1 - (seq - np) % np;
+    }
+    __device__ int row0(bool lower, int p) const { return lower ? ((SweepGeo<NQ>::W * p) & ~31) : 0; }
+    __device__ void issue(int seq, int limit) const { // lane 0
+        if (lane != 0 || seq >= limit)
+            return;
+        bool lower;
+        int p;
+        panel(seq, lower, p);
+        const int j0 = SweepGeo<NQ>::W * p, r0 = row0(lower, p), st = seq % SW_STAGES;
+        const uint32_t mb = sw_saddr(&full[st]), dst = sw_saddr(buf) + st * SW_STAGE;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(SW_STAGE) : "memory");
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx) {
+            const int c = NQ == 8 ? j0 + 16 * bx : j0, r = NQ == 8 ? r0 : r0 + 256 * bx;
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                    dst + bx * SW_BOX),
+                "l"(tm), "r"(c), "r"(r), "r"(mb)
+                : "memory");
+        }
+    }
+    __device__ const unsigned char* wait(int seq) const {
+        const int st = seq % SW_STAGES;
+        const uint32_t mb = sw_saddr(&full[st]), par = (seq / SW_STAGES) & 1;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                         " selp.u32 %0, 1, 0, p;\n}"
+                         : "=r"(done)
+                         : "r"(mb), "r"(par)
+                         : "memory");
+        return buf + st * SW_STAGE;
+    }
+};
+
+template <bool LOWER, bool EXACT, int NQ>
+__device__ __forceinline__ void sweep_pass(const SweepRing<NQ>& R, int seq0, int limit, int n, const double2* dg,
+                                           double (&x)[NQ], int lane, unsigned& bad, int trace) {
+    constexpr int W = SweepGeo<NQ>::W;
+#pragma unroll 1
+    for (int it = 0; it < R.np; ++it) {
+        const int seq = seq0 + it;
+        const unsigned char* pb = R.wait(seq);
+        if (trace && lane == 0 && it < 64)
+            g_sweep_ts[seq / R.np][it][0] = gtimer();
+        __syncwarp();
+        R.issue(seq + SW_STAGES - 1, limit); // into the stage the previous panel freed
+        bool lower;
+        int p;
+        R.panel(seq, lower, p);
+        const int j0 = W * p;
+        sweep_panel<LOWER, EXACT, NQ, 0>(pb, R.row0(lower, p), dg, x, j0, min(W, n - j0), lane, bad);
+        if (trace && lane == 0 && it < 64)
+            g_sweep_ts[seq / R.np][it][1] = gtimer();
+    }
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(32, 1) k_trsv_sweep1(const __grid_constant__ CUtensorMap tm,
+                                                       const double* __restrict__ lu, uint64_t lda, int n, double* b,
+                                                       uint64_t ldb, int trace) {
+    extern __shared__ __align__(16) unsigned char swm[];
+    __shared__ __align__(8) uint64_t full[SW_STAGES];
+    const int lane = threadIdx.x;
+    unsigned char* buf = swm + (((sw_saddr(swm) + 1023u) & ~1023u) - sw_saddr(swm));
+    double2* dg = reinterpret_cast<double2*>(buf + SW_STAGES * SW_STAGE); // {U_ii, 1 / U_ii}
+    const int np = (n + SweepGeo<NQ>::W - 1) / SweepGeo<NQ>::W;
+    const SweepRing<NQ> R{&tm, buf, full, np, lane};
+    if (lane == 0) {
+        for (int s2 = 0; s2 < SW_STAGES; ++s2)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sw_saddr(&full[s2])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm) : "memory");
+    }
+    __syncwarp();
+    for (int s2 = 0; s2 < SW_STAGES - 1; ++s2)
+        R.issue(s2, 2 * np);
+    for (int i = lane; i < n; i += 32) {
+        const double u = lu[static_cast<uint64_t>(i) * lda + i];
+        dg[i] = make_double2(u, 1.0 / u);
+    }
+    double x[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int i = lane + 32 * q;
+        x[q] = i < n ? b[static_cast<uint64_t>(i) * ldb] : 0.0;
+    }
+    __syncwarp();
+    unsigned bad = 0;
+    sweep_pass<true, false, NQ>(R, 0, 2 * np, n, dg, x, lane, bad, trace);
+    double y[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+        y[q] = x[q];
+    sweep_pass<false, false, NQ>(R, np, 2 * np, n, dg, x, lane, bad, trace);
+    if (__any_sync(0xffffffffu, bad)) { // a quotient outside the fast path's range: divide
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            x[q] = y[q];
+        __syncwarp();
+        for (int s2 = 0; s2 < SW_STAGES - 1; ++s2)
+            R.issue(2 * np + s2, 3 * np);
+        sweep_pass<false, true, NQ>(R, 2 * np, 3 * np, n, dg, x, lane, bad, trace);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int i = lane + 32 * q;
+        if (i < n)
+            b[static_cast<uint64_t>(i) * ldb] = x[q];
+    }
+}
+
 // Forward (unit L) then backward (U) substitution (genp.cpp:106-124) as two wavefront
 // launches per slice of <= 32 right-hand sides; b (n x nrhs, ldb) is overwritten by the
-// solution.
+// solution (one right-hand side with n <= 512: the one-CTA sweep).
 void genp_solve_blocked(uint64_t n, uint64_t nrhs, const double* lu, uint64_t lda, const double* aux,
                         double* b, uint64_t ldb) {
     (void)aux;
     prep_attrs();
     cudaStream_t st = stream();
+    static const bool no_sweep = std::getenv("RL_NO_SWEEP1") != nullptr; // dev comparison
+    CUtensorMap tm;
+    if (nrhs == 1 && n <= static_cast<uint64_t>(SW_MAXN) && !no_sweep &&
+        make_tmap(&tm, lu, n, n, lda, 256)) { // one small system: one warp
+        static bool attr[16] = {};
+        if (!attr[ctx().device & 15]) {
+            RL_CUDA(cudaFuncSetAttribute(k_trsv_sweep1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sweep_smem_bytes())));
+            RL_CUDA(cudaFuncSetAttribute(k_trsv_sweep1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sweep_smem_bytes())));
+            attr[ctx().device & 15] = true;
+        }
+        const int nn = static_cast<int>(n);
+        static const bool strace = std::getenv("RL_SWEEP_TRACE") != nullptr;
+        if (n <= 256)
+            k_trsv_sweep1<8><<<1, 32, sweep_smem_bytes(), st>>>(tm, lu, lda, nn, b, ldb, strace);
+        else
+            k_trsv_sweep1<16><<<1, 32, sweep_smem_bytes(), st>>>(tm, lu, lda, nn, b, ldb, strace);
+        RL_LAUNCHED();
+        if (strace) {
+            static unsigned long long h[3][64][2];
+            RL_CUDA(cudaMemcpyFromSymbolAsync(h, g_sweep_ts, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+            RL_CUDA(cudaStreamSynchronize(st));
+            const int np = static_cast<int>((n + (n <= 256 ? 31 : 15)) / (n <= 256 ? 32 : 16));
+            const unsigned long long t0 = h[0][0][0];
+            for (int d = 0; d < 2; ++d)
+                for (int i = 0; i < np && i < 64; ++i)
+                    std::fprintf(stderr, "sweep %s panel %2d: ready %7.2f end %7.2f us\n", d ? "U" : "L", i,
+                                 (h[d][i][0] - t0) * 1e-3, (h[d][i][1] - t0) * 1e-3);
+        }
+        return;
+    }
     const uint64_t nblk = (n + NB - 1) / NB;
     int* sync = ws<int>(WS_WAVE, 2 * (nblk + 1));
     static const bool trace = std::getenv("RL_WAVE_TRACE") != nullptr;

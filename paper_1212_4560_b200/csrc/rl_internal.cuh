@@ -2,6 +2,7 @@
 // launch accounting.  Not part of the C-ABI.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -125,6 +126,11 @@ struct GenpAux {
 void genp_factor_dev(uint64_t n, double* a, uint64_t lda, double pivot_floor, double* d_pivots,
                      int64_t* d_breakdown);
 // Multi-RHS solve with the packed LU: B (n x nrhs, ld = ldb) overwritten by X.
+// rows x cols row-major f64 (ld doubles) as a TMA tensor map: box box_rows x 16 doubles, 128-byte
+// swizzle, zero fill past the edges (dgemm_dmma.cu); false when the driver entry is missing or
+// the layout is not TMA-addressable (base / ld not 16-byte aligned)
+bool make_tmap(CUtensorMap* tm, const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
+
 void genp_solve_dev(uint64_t n, uint64_t nrhs, const double* lu, uint64_t lda, double* b,
                     uint64_t ldb);
 

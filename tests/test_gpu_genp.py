@@ -119,6 +119,21 @@ def test_ragged_sizes_vs_oracle(rl, oracle, n):
         assert rel(X[:, j], oracle.genp_solve_packed(w, B[:, j])) < 1e-12
 
 
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 64, 100, 255, 256, 257, 511, 512, 513, 777, 1024, 1025])
+def test_single_rhs_solve_vs_oracle(rl, oracle, n):
+    """One right-hand side with n <= 1024 takes the one-CTA column sweep (both substitutions in
+    one launch, panels of 32 columns staged ahead); n = 1025 the wavefront.  Both against the
+    reference's row-order substitution, plus run-to-run bit identity."""
+    rng = np.random.default_rng(1000 + n)
+    a = rng.standard_normal((n, n)) + 2 * np.sqrt(n) * np.eye(n)
+    f = rl.genp_factor(a)
+    _, _, _, w = oracle.genp_factor(a)
+    b = rng.standard_normal(n)
+    y = rl.genp_solve(f, b)
+    assert rel(y, oracle.genp_solve_packed(w, b)) < 1e-12
+    assert np.array_equal(y, rl.genp_solve(f, b))
+
+
 @pytest.mark.parametrize("kind,refine", [("gaussian", 0), ("gaussian", 1), ("circulant_sign", 0),
                                          ("circulant_sign", 1), ("uniform_pm1", 0)])
 def test_config1_parity(rl, oracle, golden, kind, refine):
