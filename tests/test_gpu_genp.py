@@ -134,6 +134,26 @@ def test_single_rhs_solve_vs_oracle(rl, oracle, n):
     assert np.array_equal(y, rl.genp_solve(f, b))
 
 
+@pytest.mark.parametrize("scale", [1e-300, 1e300, 0.0])
+def test_single_rhs_solve_extreme_scales(rl, oracle, scale):
+    """The sweep's fast quotient (reciprocal + one residual correction) is exact only away from
+    under/overflow; right-hand sides near the ends of the exponent range set its range flag and
+    the U pass re-runs with the division itself — results still the reference's (zero b: x = 0
+    without the re-run)."""
+    n = 200
+    rng = np.random.default_rng(77)
+    a = rng.standard_normal((n, n)) + 2 * np.sqrt(n) * np.eye(n)
+    f = rl.genp_factor(a)
+    _, _, _, w = oracle.genp_factor(a)
+    b = rng.standard_normal(n) * scale
+    y = rl.genp_solve(f, b)
+    yo = oracle.genp_solve_packed(w, b)
+    if scale == 0.0:
+        assert np.array_equal(y, np.zeros(n))
+    else:
+        assert np.all(np.isfinite(y)) and rel(y, yo) < 1e-12
+
+
 @pytest.mark.parametrize("kind,refine", [("gaussian", 0), ("gaussian", 1), ("circulant_sign", 0),
                                          ("circulant_sign", 1), ("uniform_pm1", 0)])
 def test_config1_parity(rl, oracle, golden, kind, refine):

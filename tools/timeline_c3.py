@@ -51,3 +51,6 @@ for st, en, nm in ks:
         cur_e, prev = en, nm
 for g, at, a_, b_ in sorted(gaps, reverse=True)[:10]:
     print(f"gap {g:8.1f} us at {at:8.3f} ms: {a_.split('(')[0][-40:]} -> {b_.split('(')[0][-40:]}")
+if len(sys.argv) > 1 and sys.argv[1] == "head":  # the first device events in order
+    for st, en, nm in ks[:12]:
+        print(f"{(st - t0) / 1e3:9.3f} {(en - t0) / 1e3:9.3f} ms  {nm.replace('(anonymous namespace)::', '')[:70]}")
