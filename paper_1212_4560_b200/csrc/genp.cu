@@ -803,6 +803,8 @@ void genp_factor_blocked(uint64_t n, double* a, uint64_t lda, double pivot_floor
     cudaStream_t s1 = stream();
     Lookahead& la = lookahead();
     cudaStream_t s2 = la.s2, s3 = la.s3, s4 = la.s4;
+    if (n <= static_cast<uint64_t>(kOuterSteps) * NB) // one outer panel: nothing to overlap, and
+        s2 = s3 = s4 = s1;                           // each cross-stream hop costs ~5 us
     cudaEvent_t E_nd = la.ev[0], E_strips = la.ev[1], E_panel = la.ev[2], E_t1 = la.ev[3], E_s3 = la.ev[4],
                 E_s4 = la.ev[5];
     auto at = [&](uint64_t i, uint64_t j) { return a + i * lda + j; };
