@@ -871,7 +871,12 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
     double* dh = ws<double>(WS_RF1, n * rho);
     rng_generate(seed, sid, Draw::Gaussian, n * rho, 0.0, 1.0, dh);
     double* dy = ws<double>(WS_RF2, m * rho);
-    gemm_splitk(false, false, m, rho, n, 1.0, d_a, n, dh, rho, 0.0, dy, rho, splits_for(m, rho, n));
+    // both GEMM operands K-major: H^T (rho x n) and, below, Q^T (rho x m) let the TMA kernel
+    // load the 72-wide operand as one box per 16 k (same k order, same bits as the N-/M-major
+    // forms)
+    double* dht = ws<double>(WS_RF7, n * rho);
+    transpose_dev(n, rho, dh, rho, dht, n);
+    gemm_splitk(false, true, m, rho, n, 1.0, d_a, n, dht, n, 0.0, dy, rho, splits_for(m, rho, n));
     // [Q, R] = qr_positive(Y), its rank test bracketed on the device (k_rank_bracket)
     double* dr = ws<double>(WS_RF3, rho * rho);
     int* flags = ws<int>(WS_FLAGS, 4);
@@ -880,7 +885,9 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
     cholqr3_async(m, static_cast<int>(rho), dy, d_q, dr, flags, true, true);
     rank_bracket_diag_launch(static_cast<int>(rho), dr, flags + 1);
     // B = Q^T A (lowrank.cpp:61-64 `sta`)
-    gemm_splitk(true, false, rho, n, m, 1.0, d_q, rho, d_a, n, 0.0, d_b, n, splits_for(rho, n, m));
+    double* dqt = ws<double>(WS_RF8, m * rho);
+    transpose_dev(m, rho, d_q, rho, dqt, m);
+    gemm_splitk(false, false, rho, n, m, 1.0, dqt, m, d_a, n, 0.0, d_b, n, splits_for(rho, n, m));
     // sigma(B) from R of B^T
     double* bt = ws<double>(WS_RF1, n * rho);
     transpose_dev(rho, n, d_b, n, bt, rho);
@@ -906,7 +913,8 @@ rl_status rl_dev_range_finder(uint64_t m, uint64_t n, const double* d_a, uint64_
         bool ok = false;
         if (hf[1] == 2) { // rare: sigma_1(R) itself — Y is rebuilt and R formed in full
             rng_generate(seed, sid, Draw::Gaussian, n * rho, 0.0, 1.0, dh);
-            gemm_splitk(false, false, m, rho, n, 1.0, d_a, n, dh, rho, 0.0, dy, rho, splits_for(m, rho, n));
+            transpose_dev(n, rho, dh, rho, dht, n); // the same product as the first Y
+            gemm_splitk(false, true, m, rho, n, 1.0, d_a, n, dht, n, 0.0, dy, rho, splits_for(m, rho, n));
             double* qtmp = ws<double>(WS_OUT, m * rho);
             if (!cholqr3(m, static_cast<int>(rho), dy, qtmp, dr))
                 fail(RL_RANK_DEFICIENT, "qr_positive: numerically rank-deficient sketch");

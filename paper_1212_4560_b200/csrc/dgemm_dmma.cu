@@ -234,15 +234,17 @@ constexpr int TM_BK = 32;
 // Tile geometry of the TMA kernel: BM x BN output tile, K-tile 32, WM x WN warps. A is K-major
 // (boxes BM x 16 along k: A·G, A·H) or M-major (boxes 32 x 16 along m: Q^T A); B is N-major
 // (boxes 32 x 16 along n). Box edges past M / N / K are zero-filled by the copy engine.
-template <int BM, int BN, int WM, int WN, bool AKM, int TM_NSTAGE>
+template <int BM, int BN, int WM, int WN, bool AKM, bool BKMJ, int TM_NSTAGE>
 struct TmCfg {
     static constexpr int NT = WM * WN * 32;
     static constexpr int WTM = BM / WM, WTN = BN / WN, MF = WTM / 8, NF = WTN / 8;
     static constexpr int A_BYTES = BM * TM_BK * 8, B_BYTES = TM_BK * BN * 8;
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr size_t SMEM = static_cast<size_t>(TM_NSTAGE) * STAGE + 1024; // + alignment slack
-    static constexpr int A_BOXES = AKM ? TM_BK / 16 : BM / 16, B_BOXES = BN / 16;
-    static constexpr int A_BOX_BYTES = AKM ? BM * 128 : TM_BK * 128;
+    static constexpr int A_BOXES = AKM ? TM_BK / 16 : BM / 16, B_BOXES = BKMJ ? TM_BK / 16 : BN / 16;
+    static constexpr int A_BOX_BYTES = AKM ? BM * 128 : TM_BK * 128, B_BOX_BYTES = BKMJ ? BN * 128 : TM_BK * 128;
+    // every box starts on a 1024-byte swizzle-pattern boundary
+    static_assert(A_BYTES % 1024 == 0 && A_BOX_BYTES % 1024 == 0 && B_BOX_BYTES % 1024 == 0, "box alignment");
     // byte offsets of A(r, k) / B(k, n) in a stage (128-byte swizzle: chunk c of line l at c ^ (l & 7))
     __device__ __forceinline__ static uint32_t a_off(int r, int k) {
         if (AKM)
@@ -252,6 +254,9 @@ struct TmCfg {
                                      ((r & 1) << 3));
     }
     __device__ __forceinline__ static uint32_t b_off(int k, int n) {
+        if (BKMJ) // B stored N x K (K-major): the same box geometry as a K-major A
+            return static_cast<uint32_t>(A_BYTES + (k >> 4) * B_BOX_BYTES + n * 128 +
+                                         ((((k & 15) >> 1) ^ (n & 7)) << 4) + ((k & 1) << 3));
         return static_cast<uint32_t>(A_BYTES + (n >> 4) * (TM_BK * 128) + k * 128 + ((((n & 15) >> 1) ^ (k & 7)) << 4) +
                                      ((n & 1) << 3));
     }
@@ -265,12 +270,12 @@ struct TmCfg {
 // memory, bounds the loop). The threads issue only fragment loads and DMMAs. Split-K over
 // blockIdx.z: slice z covers [z kchunk, (z+1) kchunk) (kchunk a multiple of 32) and writes its own
 // C panel (C + z cstride). Same tile and k order as k_dgemm: bit-identical results.
-template <int BM, int BN, int WM, int WN, bool AKM, int MINB, int TM_NSTAGE>
+template <int BM, int BN, int WM, int WN, bool AKM, bool BKMJ, int MINB, int TM_NSTAGE>
 __global__ void __launch_bounds__(WM* WN * 32, MINB)
     k_dgemm_tm(uint64_t M, uint64_t N, uint64_t K, double alpha, const __grid_constant__ CUtensorMap tmA,
                const __grid_constant__ CUtensorMap tmB, double beta, double* __restrict__ C, uint64_t ldc,
                uint64_t kchunk, uint64_t cstride) {
-    using T = TmCfg<BM, BN, WM, WN, AKM, TM_NSTAGE>;
+    using T = TmCfg<BM, BN, WM, WN, AKM, BKMJ, TM_NSTAGE>;
     extern __shared__ __align__(16) unsigned char smem_tm[];
     __shared__ __align__(8) uint64_t full[TM_NSTAGE];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -309,10 +314,12 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
                          : "memory");
         }
 #pragma unroll
-        for (int q = 0; q < T::B_BOXES; ++q)
+        for (int q = 0; q < T::B_BOXES; ++q) {
+            const int c0 = BKMJ ? k0 + 16 * q : n0 + 16 * q, c1 = BKMJ ? n0 : k0;
             asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                         ::"r"(st + T::A_BYTES + q * TM_BK * 128), "l"(&tmB), "r"(n0 + 16 * q), "r"(k0), "r"(mb)
+                         ::"r"(st + T::A_BYTES + q * T::B_BOX_BYTES), "l"(&tmB), "r"(c0), "r"(c1), "r"(mb)
                          : "memory");
+        }
     };
     // Tiles: one per CTA, or a persistent loop when the grid was capped (the LU's trailing update
     // leaves SMs to the panel path). `it0` counts the k-tiles this CTA consumed: stage it % 2,
@@ -430,15 +437,15 @@ namespace {
 
 // true when the TMA kernel took the product. op(A): M x K, K-major (row-major M x K, ld lda) or
 // M-major (A stored K x M, ld lda); B: K x N row-major (ld ldb).
-template <int BM, int BN, int WM, int WN, bool AKM, int MINB, int NST = 2>
+template <int BM, int BN, int WM, int WN, bool AKM, int MINB, int NST = 2, bool BKMJ = false>
 bool launch_tm(uint64_t M, uint64_t N, uint64_t K, double alpha, const double* A, uint64_t lda, const double* B,
                uint64_t ldb, double beta, double* C, uint64_t ldc, const Split& sp) {
-    using T = TmCfg<BM, BN, WM, WN, AKM, NST>;
+    using T = TmCfg<BM, BN, WM, WN, AKM, BKMJ, NST>;
     CUtensorMap ta, tb;
     const bool ok = AKM ? make_tmap(&ta, A, M, K, lda, BM) : make_tmap(&ta, A, K, M, lda, TM_BK);
-    if (!ok || !make_tmap(&tb, B, K, N, ldb, TM_BK))
+    if (!ok || !(BKMJ ? make_tmap(&tb, B, N, K, ldb, BN) : make_tmap(&tb, B, K, N, ldb, TM_BK)))
         return false;
-    auto kern = k_dgemm_tm<BM, BN, WM, WN, AKM, MINB, NST>;
+    auto kern = k_dgemm_tm<BM, BN, WM, WN, AKM, BKMJ, MINB, NST>;
     static bool configured[16] = {};
     const int dev = ctx().device & 15;
     if (!configured[dev]) {
@@ -498,6 +505,22 @@ void dispatch_shape(uint64_t M, uint64_t N, uint64_t Kfull, double alpha, const 
     // the range finder's skinny products: TMA-fed 128 x 80 (A H) / 80 x 128 (Q^T A) tiles, the
     // column / row edge past 72 zero-filled by the copy engine (split-K slices of 32-multiples)
     static const bool no_tma_rf = getenv("RL_GEMM_NO_TMA") != nullptr;
+    // both operands K-major (A H with H^T stored rho x n; Q^T A with Q^T stored rho x m): the
+    // 72-wide operand is ONE 72 x 16 box per 16 k (no padding to 80) and its fragment reads hit
+    // the two-wavefront minimum like A's
+    const bool tm_kk = !no_tma_rf && VEC == 2 && AK && (sp.splits == 1 || sp.kchunk % 32 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+    // A H: 128 x 72 tiles (8 warps, 2 per SM; 128 row tiles x 2 K slices at m = 16384: each
+    // busy SM at the DMMA probe's rate, 20 SMs idle).  Measured and not kept: 112 x 72 tiles of
+    // 7 warps (147 x 2 CTAs fill the GPU, but 7 warps load the four SM sub-partitions unevenly:
+    // 334 us against 297) and 64 x 72 tiles of 4 warps at 3 CTAs per SM (2.9 waves of 5 K
+    // slices: 302 us).  Q^T A: 72 x 128 tiles (32 column tiles x 9 slices = 288 of 296 slots).
+    if (BKM && N > 64 && N <= 72 && N % 2 == 0 && tm_kk &&
+        launch_tm<128, 72, 8, 1, true, 2, 2, true>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp))
+        return;
+    if (!BKM && M > 64 && M <= 72 && N > 72 && tm_kk &&
+        launch_tm<72, 128, 1, 8, true, 2, 2>(M, N, Kfull, alpha, A, lda, B, ldb, beta, C, ldc, sp))
+        return;
     const bool tm_ok = !no_tma_rf && VEC == 2 && !BKM && (sp.splits == 1 || sp.kchunk % 32 == 0) &&
                        ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
     if (N > 64 && N <= 72) {

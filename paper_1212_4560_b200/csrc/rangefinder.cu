@@ -74,6 +74,31 @@ __global__ void k_splitk_reduce(uint64_t m, uint64_t n, int splits, const double
     }
 }
 
+// Even n / ldc, < 2^32 outputs: two adjacent outputs per thread (16-byte loads and stores),
+// 32-bit index arithmetic (the 64-bit e / n of the general kernel dominated A H's 9.4 MB
+// reduction); the same summation order as k_splitk_reduce.
+__global__ void k_splitk_reduce2(uint32_t n, uint32_t total, int splits, const double* __restrict__ parts,
+                                 double alpha, double beta, double* __restrict__ c, uint32_t ldc) {
+    const uint32_t e = 2u * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (e >= total)
+        return;
+    double2 s = make_double2(0.0, 0.0);
+    for (int p = 0; p < splits; ++p) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(parts + static_cast<uint64_t>(p) * total + e));
+        s.x += v.x;
+        s.y += v.y;
+    }
+    const uint32_t i = e / n, j = e - i * n;
+    double2* cp = reinterpret_cast<double2*>(c + static_cast<uint64_t>(i) * ldc + j);
+    double2 v = make_double2(alpha * s.x, alpha * s.y);
+    if (beta != 0.0) {
+        const double2 o = *cp;
+        v.x = fma(beta, o.x, v.x);
+        v.y = fma(beta, o.y, v.y);
+    }
+    *cp = v;
+}
+
 // Reciprocal and reciprocal square root from the SFU seed plus two Newton steps (a few ulp;
 // no IEEE slow path): the Jacobi rotation only needs c^2 + s^2 = 1 to rounding level.
 __device__ __forceinline__ double rcp_nr(double x) {
@@ -807,6 +832,11 @@ void gemm_splitk(bool ta, bool tb, uint64_t m, uint64_t n, uint64_t k, double al
     gemm_splitk_parts(ta, tb, m, n, k, a, lda, b, ldb, parts, used, chunk);
     if (m * n * 32 <= 4ULL * 1024 * 1024 && used >= 32)
         k_splitk_reduce_warp<<<cdiv(m * n * 32, 256), 256, 0, stream()>>>(m, n, used, parts, alpha, beta, c, ldc);
+    else if (n % 2 == 0 && ldc % 2 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0 && m * n < (1ULL << 32) &&
+             ldc < (1ULL << 32))
+        k_splitk_reduce2<<<cdiv(m * n / 2, 256), 256, 0, stream()>>>(static_cast<uint32_t>(n),
+                                                                     static_cast<uint32_t>(m * n), used, parts,
+                                                                     alpha, beta, c, static_cast<uint32_t>(ldc));
     else
         k_splitk_reduce<<<cdiv(m * n, 256), 256, 0, stream()>>>(m, n, used, parts, alpha, beta, c, ldc);
     RL_LAUNCHED();

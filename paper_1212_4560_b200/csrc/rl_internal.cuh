@@ -76,7 +76,7 @@ enum WsSlot {
     WS_RNG2, WS_SMALL, WS_LU_AUX, WS_BATCH, WS_RF1, WS_RF2, WS_RF3, WS_LVEC, WS_RESID, WS_RF4,
     WS_RF5, WS_RF6, WS_H0, WS_H1, WS_H2, WS_H3, WS_WAVE, WS_MULT2, WS_RNG3, WS_RNG4, WS_SPLAN, WS_T1, WS_T2,
     WS_FFT_GEN, WS_FFT_C, WS_FFT_X, WS_FFT_TMP, WS_FFT_OUT, WS_FFT_FLAG, WS_FLAGS, WS_RF3B, WS_RF5B,
-    WS_ES0, WS_ES1, WS_ES2, WS_ES3, WS_ES4, WS_ES5, WS_PACK
+    WS_ES0, WS_ES1, WS_ES2, WS_ES3, WS_ES4, WS_ES5, WS_PACK, WS_RF7, WS_RF8
 };
 
 Ctx& ctx();          // thread-local context (initialises the device on first use)
