@@ -416,7 +416,10 @@ __device__ bool circ_spectrum(Smem& S, int t, bool left) {
 
 // One CTA per system; the raw arm and the whole redraw protocol (8 attempts on stream
 // sid + 7919 a, right multiplier from stream ^ 0x5000000000000000) run in-kernel.
-__global__ void __maxnreg__(248) k_batched_circ64(
+#ifndef RL_B64_MAXREG
+#define RL_B64_MAXREG 248
+#endif
+__global__ void __maxnreg__(RL_B64_MAXREG) k_batched_circ64(
     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ signs0, uint64_t seed,
     const uint64_t* __restrict__ sids, int refine, int left, double* __restrict__ X,
     rl_precond_report* __restrict__ rep, int* __restrict__ status) {
