@@ -18,8 +18,10 @@ cap sparseplan  sparse  "k_sparse_plan"     1
 cap circfft     circfft "k_circ_fft8k"      1
 cap cholinv     c4      "k_chol_inv"        6
 cap bidiag      c4      "k_bidiag_sv"       2
-cap rf_dgemm    c4      "k_dgemm_tm<128, 80"   1
+cap rf_dgemm    c4      "k_dgemm_tm<128, 72"   1
+cap rf_dgemm_qta c4     "k_dgemm_tm<72, 128"   1
 cap gen_chunks  rng     "k_gen_chunks"      1
 cap diag_lu     lu      "k_diag_lu"         64
 cap panel_trsm  lu      "k_panel_trsm"      64
 cap trsv_wave   lu      "k_trsv_wave"       2
+cap lu_dgemm    lu      "k_dgemm_tm<128, 64"   2
